@@ -1,0 +1,122 @@
+/* sqf_trainer.h — C ABI of the B200 training step, the drop-in for the
+ * reference's Trainer (seqforge include/seqforge/trainer.hpp:80-125). The
+ * reference is a C++ library with no FFI of its own; these entries are what a
+ * binding of its Trainer would call (see INTEGRATION.md for the C++ adapter
+ * and the ctypes stub). Status convention: 0 ok, 1 "data exhausted"
+ * (train_one), negative = error class of the reference's taxonomy
+ * (common.hpp:11-34) with the message in sqf_last_error():
+ *   -1 ConfigError -2 ShapeError -3 BoundsError -4 CapacityError
+ *   -5 IntegrityError -6 DivergenceError -7 RegistryError -8 IoError
+ *   -10 DeviceError (CUDA/NCCL) -9 other
+ */
+#ifndef SQF_TRAINER_H
+#define SQF_TRAINER_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* StepStats (trainer.hpp:57-66) */
+typedef struct sqf_step_stats {
+  int64_t step;
+  double loss;     /* summed over tokens, unnormalised, unscaled */
+  double nll;
+  int64_t ntokens;
+  int64_t ncorrect;
+  double lr;
+  int32_t skipped; /* fp16 overflow: scaler updated, nothing else */
+  int32_t _pad;
+  double scale;    /* loss scale used (0 when not in fp16) */
+} sqf_step_stats;
+
+const char* sqf_last_error(void);
+
+/* NCCL unique id (128 bytes) for multi-process data parallelism; rank 0
+ * creates it and the launcher broadcasts it (torch.distributed store). */
+int sqf_nccl_unique_id(void* out128);
+
+/* Trainer(cfg, task) (trainer.hpp:84-85, trainer.cpp:89-142).
+ * arch + raw user overrides resolve like Registry::resolve_architecture
+ * (registry.cpp:96-110). With npairs > 0 the in-memory corpus (eos-terminated
+ * id sequences, concatenated) is the task; otherwise cfg["task"] is made
+ * through the registry ("synthetic"). rank/world: this process's place in
+ * the data-parallel group (world 1 = single GPU; nccl_id ignored). */
+void* sqf_trainer_create(const char* arch, const char* const* keys, const char* const* vals, int n,
+                         const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
+                         const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab,
+                         int rank, int world, const void* nccl_id);
+void sqf_trainer_free(void* t);
+
+/* Trainer::train_one (trainer.cpp:204-208): 0 ok, 1 exhausted */
+int sqf_trainer_train_one(void* t, sqf_step_stats* out);
+/* Trainer::train_step (trainer.cpp:210-273): sub[w][a] given as corpus-index
+ * member lists, counts[w*accum + a] members each, concatenated. */
+int sqf_trainer_train_step(void* t, const int32_t* members, const int32_t* counts, sqf_step_stats* out);
+/* Trainer::evaluate (trainer.cpp:275-289) over the trainer's own corpus
+ * subset given by corpus indices (teacher-forced, fp32 master). */
+int sqf_trainer_evaluate(void* t, const int32_t* corpus_idx, int n, double* loss, double* nll,
+                         int64_t* ntokens, int64_t* ncorrect);
+
+int64_t sqf_trainer_num_params(void* t);
+/* fp32 master in the reference's canonical manifest order */
+int sqf_trainer_params(void* t, float* out);
+int sqf_trainer_set_params(void* t, const float* in); /* then rebroadcast() */
+/* last step's reduced gradient (before unscale / 1/ntokens), canonical order */
+int sqf_trainer_last_grads(void* t, float* out);
+int sqf_trainer_manifest_size(void* t);
+int sqf_trainer_manifest_entry(void* t, int i, char* name, int cap, int64_t* offset, int64_t* numel,
+                               int64_t* device_offset);
+int sqf_trainer_adam_state(void* t, float* m, float* v, int64_t* step_count); /* canonical order */
+int sqf_trainer_scaler(void* t, double* scale, int64_t* successes);
+int sqf_trainer_progress(void* t, int64_t* step, int32_t* epoch, int32_t* cursor, int32_t* nbatches);
+int sqf_trainer_set_injector(void* t, const int64_t* steps, int n); /* set_overflow_injector */
+int sqf_trainer_restore(void* t, int64_t step, int32_t epoch, int32_t cursor, double scale,
+                        int64_t successes);
+/* our kernel launches during the last train_step, and its device time (ms) */
+int64_t sqf_trainer_kernel_launches(void* t);
+float sqf_trainer_last_step_ms(void* t);
+/* CUDA stream the trainer launches on (cudaStream_t) */
+void* sqf_trainer_stream(void* t);
+
+/* ---------------- host-side boundary pieces (no GPU needed) --------------- */
+/* synthetic WMT-shaped corpus; two-call protocol: pass
+ * null id buffers to get total lengths in *src_total / *tgt_total */
+int sqf_synthetic_corpus(int npairs, int src_vocab, int tgt_vocab, double zipf_s, uint64_t seed,
+                         int32_t* src_len, int32_t* tgt_len, int32_t* src_ids, int32_t* tgt_ids,
+                         int64_t* src_total, int64_t* tgt_total);
+void* sqf_corpus_create(int npairs, const int32_t* src_len, const int32_t* tgt_len,
+                        const int32_t* src_ids, const int32_t* tgt_ids);
+void sqf_corpus_free(void* c);
+/* make_batches (data.cpp:115-161) */
+int sqf_make_batches(void* corpus, int64_t max_tokens, int max_sentences, uint64_t seed,
+                     int32_t* nbatches, int32_t* sizes, int32_t* members);
+/* shuffle_epoch (data.cpp:163-170) */
+int sqf_shuffle_epoch(int nbatches, uint64_t seed, int epoch, int32_t* order);
+/* make_minibatch (data.cpp:172-219): dims = {rows, src_width, tgt_width} */
+int sqf_make_minibatch(void* corpus, const int32_t* members, int n, int32_t* dims, int32_t* source,
+                       int32_t* target_in, int32_t* target_out, int32_t* src_lens, int32_t* tgt_lens,
+                       int64_t* ntokens);
+/* Trainer::split_batch (trainer.cpp:186-202): member counts per group g = w*A+a */
+int sqf_split_counts(int rows, int workers, int accum, int32_t* counts);
+/* bucket_gradients (trainer.cpp:50-73) */
+int sqf_bucket_gradients(const int64_t* sizes, int n, int64_t threshold, int32_t* nbuckets,
+                         int64_t* starts, int64_t* ends);
+/* model layout + initial parameters on the host (model.cpp:74-150):
+ * canonical-order params (cap >= num params) and the manifest count */
+int sqf_model_init(const char* arch, const char* const* keys, const char* const* vals, int n,
+                   float* params, int64_t cap, int64_t* num_params, int* manifest_size);
+/* LossScaler policy (trainer.cpp:21-48) over an overflow sequence */
+int sqf_scaler_run(double init, int64_t window, double mn, double mx, const uint8_t* overflow, int n,
+                   double* scales, int32_t* diverged_at);
+/* learning-rate schedules (optim.cpp:97-137) by registry name */
+int sqf_schedule_lr(const char* name, double base, int64_t warmup, double init, double eta_min,
+                    int64_t period, double t_mult, int64_t step, double* out);
+/* binary16 RNE round trip (fp16.cpp:22-76) */
+float sqf_quantize_fp16(float x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SQF_TRAINER_H */

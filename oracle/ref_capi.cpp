@@ -1,0 +1,574 @@
+// TEST INFRASTRUCTURE ONLY — never linked into, loaded by or called from the
+// product path. This file is a thin C-ABI shim over the *unmodified* C++
+// reference (seqforge, /root/reference/proj) so Python tests can use the
+// reference itself as the parity oracle. It is compiled together with the
+// reference's own sources by oracle/Makefile into oracle/_ref/libseqforge_ref.so.
+//
+// Every entry point forwards to the reference's public API; the only logic
+// here is marshalling (flat arrays <-> SequencePair/MiniBatch) and mapping
+// the reference's exception taxonomy (common.hpp:11-34) onto status codes.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "seqforge/common.hpp"
+#include "seqforge/criterions.hpp"
+#include "seqforge/data.hpp"
+#include "seqforge/fp16.hpp"
+#include "seqforge/model.hpp"
+#include "seqforge/optim.hpp"
+#include "seqforge/registry.hpp"
+#include "seqforge/rng.hpp"
+#include "seqforge/tape.hpp"
+#include "seqforge/trainer.hpp"
+
+using namespace seqforge;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const ConfigError*>(&e)) return -1;
+  if (dynamic_cast<const ShapeError*>(&e)) return -2;
+  if (dynamic_cast<const BoundsError*>(&e)) return -3;
+  if (dynamic_cast<const CapacityError*>(&e)) return -4;
+  if (dynamic_cast<const IntegrityError*>(&e)) return -5;
+  if (dynamic_cast<const DivergenceError*>(&e)) return -6;
+  if (dynamic_cast<const RegistryError*>(&e)) return -7;
+  if (dynamic_cast<const IoError*>(&e)) return -8;
+  return -9;
+}
+
+#define GUARD(...)                      \
+  try {                                 \
+    __VA_ARGS__;                        \
+    return 0;                           \
+  } catch (const std::exception& e) {   \
+    return fail(e);                     \
+  }
+
+// Named architectures used by BASELINE.json's configs, registered over the
+// reference's pre-norm `transformer` through its public
+// Registry::register_architecture (registry.cpp:76-94).
+void register_bench_archs(Registry& r) {
+  auto add = [&](const char* name, int64_t d, int64_t h, int64_t L, int64_t f) {
+    ArchitectureDef a;
+    a.name = name;
+    a.base_model = "transformer";
+    a.overrides = {{"d_model", d},   {"heads", h},          {"enc_layers", L},
+                   {"dec_layers", L}, {"d_ffn", f},         {"max_positions", int64_t{256}},
+                   {"share_embeddings", false}};
+    r.register_architecture(std::move(a), "sqf-oracle");
+  };
+  add("transformer_base_defaults", 64, 4, 2, 128);
+  add("transformer_iwslt_de_en", 512, 4, 6, 1024);
+  add("transformer_wmt_en_de", 512, 8, 6, 2048);
+  add("transformer_vaswani_wmt_en_de_big", 1024, 16, 6, 4096);
+}
+
+Registry& oracle_registry() {
+  static Registry reg = [] {
+    Registry r;
+    register_builtins(r);
+    register_bench_archs(r);
+    return r;
+  }();
+  return reg;
+}
+
+Dictionary synthetic_dict(int vocab) {
+  Dictionary d;
+  for (int i = Dictionary::kNumReserved; i < vocab; ++i) d.add_symbol("w" + std::to_string(i), 1);
+  return d;
+}
+
+struct Corpus {
+  std::vector<SequencePair> pairs;
+};
+
+class MemTask : public TaskBase {
+ public:
+  MemTask(const Corpus& c, int sv, int tv)
+      : pairs_(c.pairs), src_(synthetic_dict(sv)), tgt_(synthetic_dict(tv)) {}
+  const Dictionary& source_dict() const override { return src_; }
+  const Dictionary& target_dict() const override { return tgt_; }
+  const std::vector<SequencePair>& train_pairs() const override { return pairs_; }
+
+ private:
+  std::vector<SequencePair> pairs_;
+  Dictionary src_, tgt_;
+};
+
+struct TrainerBox {
+  Config cfg;
+  std::unique_ptr<Trainer> tr;
+  std::vector<int64_t> inject;
+};
+
+struct StatsC {
+  int64_t step;
+  double loss;
+  double nll;
+  int64_t ntokens;
+  int64_t ncorrect;
+  double lr;
+  int32_t skipped;
+  int32_t _pad;
+  double scale;
+};
+
+void fill(StatsC* o, const StepStats& s) {
+  o->step = s.step;
+  o->loss = s.loss;
+  o->nll = s.nll;
+  o->ntokens = s.ntokens;
+  o->ncorrect = s.ncorrect;
+  o->lr = s.lr;
+  o->skipped = s.skipped ? 1 : 0;
+  o->_pad = 0;
+  o->scale = s.scale;
+}
+
+void copy_minibatch(const MiniBatch& b, int32_t* dims, int32_t* source, int32_t* target_in,
+                    int32_t* target_out, int32_t* src_lens, int32_t* tgt_lens, int64_t* ntokens) {
+  dims[0] = b.rows;
+  dims[1] = b.src_width;
+  dims[2] = b.tgt_width;
+  if (source) std::memcpy(source, b.source.data(), b.source.size() * 4);
+  if (target_in) std::memcpy(target_in, b.target_in.data(), b.target_in.size() * 4);
+  if (target_out) std::memcpy(target_out, b.target_out.data(), b.target_out.size() * 4);
+  if (src_lens) std::memcpy(src_lens, b.src_lens.data(), b.src_lens.size() * 4);
+  if (tgt_lens) std::memcpy(tgt_lens, b.tgt_lens.data(), b.tgt_lens.size() * 4);
+  if (ntokens) *ntokens = b.ntokens;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sqfref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- numerics
+float sqfref_quantize_fp16(float x) { return quantize_fp16(x); }
+uint16_t sqfref_f32_to_f16_bits(float x) { return f32_to_f16_bits(x); }
+float sqfref_f16_bits_to_f32(uint16_t h) { return f16_bits_to_f32(h); }
+void sqfref_quantize_many(float* x, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) x[i] = quantize_fp16(x[i]);
+}
+
+void sqfref_rng_u64(uint64_t seed, uint64_t stream, uint64_t counter, int n, uint64_t* out) {
+  RngStream r(seed, stream, counter);
+  for (int i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+void sqfref_rng_double(uint64_t seed, uint64_t stream, uint64_t counter, int n, double* out) {
+  RngStream r(seed, stream, counter);
+  for (int i = 0; i < n; ++i) out[i] = r.next_double();
+}
+void sqfref_rng_normal(uint64_t seed, uint64_t stream, uint64_t counter, int n, double* out) {
+  RngStream r(seed, stream, counter);
+  for (int i = 0; i < n; ++i) out[i] = r.next_normal();
+}
+void sqfref_rng_below(uint64_t seed, uint64_t stream, uint64_t counter, uint64_t bound, int n,
+                      uint64_t* out) {
+  RngStream r(seed, stream, counter);
+  for (int i = 0; i < n; ++i) out[i] = r.next_below(bound);
+}
+void sqfref_positional_row(int pos, int d, float* out) { positional_row(pos, d, out); }
+
+// ---------------------------------------------------------------- corpus / data
+void* sqfref_corpus_create(int npairs, const int32_t* src_len, const int32_t* tgt_len,
+                           const int32_t* src_ids, const int32_t* tgt_ids) {
+  auto* c = new Corpus;
+  c->pairs.resize(static_cast<size_t>(npairs));
+  int64_t so = 0, to = 0;
+  for (int i = 0; i < npairs; ++i) {
+    auto& p = c->pairs[static_cast<size_t>(i)];
+    p.source.assign(src_ids + so, src_ids + so + src_len[i]);
+    p.target.assign(tgt_ids + to, tgt_ids + to + tgt_len[i]);
+    p.corpus_index = i;
+    so += src_len[i];
+    to += tgt_len[i];
+  }
+  return c;
+}
+void sqfref_corpus_free(void* c) { delete static_cast<Corpus*>(c); }
+
+// make_batches (data.cpp:115-161): returns batch count; sizes/members are
+// written into caller buffers of capacity npairs.
+int sqfref_make_batches(void* corpus, int64_t max_tokens, int max_sentences, uint64_t seed,
+                        int32_t* nbatches, int32_t* sizes, int32_t* members) {
+  GUARD({
+    auto* c = static_cast<Corpus*>(corpus);
+    EpochPlan p = make_batches(c->pairs, max_tokens,
+                               max_sentences > 0 ? std::optional<int>(max_sentences) : std::nullopt,
+                               seed);
+    *nbatches = static_cast<int32_t>(p.batches.size());
+    int64_t k = 0;
+    for (size_t b = 0; b < p.batches.size(); ++b) {
+      sizes[b] = static_cast<int32_t>(p.batches[b].size());
+      for (int m : p.batches[b]) members[k++] = m;
+    }
+  })
+}
+
+// shuffle_epoch (data.cpp:163-170) for a plan with `nbatches` batches
+int sqfref_shuffle_epoch(int nbatches, uint64_t seed, int epoch, int32_t* order) {
+  GUARD({
+    EpochPlan p;
+    p.batches.resize(static_cast<size_t>(nbatches));
+    p.shuffle_seed = seed;
+    std::vector<int> o = shuffle_epoch(p, epoch);
+    for (size_t i = 0; i < o.size(); ++i) order[i] = o[i];
+  })
+}
+
+// make_minibatch (data.cpp:172-219); dims = {rows, src_width, tgt_width}
+int sqfref_make_minibatch(void* corpus, const int32_t* members, int n, int32_t* dims,
+                          int32_t* source, int32_t* target_in, int32_t* target_out,
+                          int32_t* src_lens, int32_t* tgt_lens, int64_t* ntokens) {
+  GUARD({
+    auto* c = static_cast<Corpus*>(corpus);
+    std::vector<int> m(members, members + n);
+    MiniBatch b = make_minibatch(c->pairs, m);
+    copy_minibatch(b, dims, source, target_in, target_out, src_lens, tgt_lens, ntokens);
+  })
+}
+
+int sqfref_bucket_gradients(const int64_t* sizes, int n, int64_t threshold, int32_t* nbuckets,
+                            int64_t* starts, int64_t* ends) {
+  GUARD({
+    std::vector<int64_t> s(sizes, sizes + n);
+    auto b = bucket_gradients(s, threshold);
+    *nbuckets = static_cast<int32_t>(b.size());
+    for (size_t i = 0; i < b.size(); ++i) {
+      starts[i] = b[i].start;
+      ends[i] = b[i].end;
+    }
+  })
+}
+
+// ---------------------------------------------------------------- schedules / optimizer / scaler
+int sqfref_inverse_sqrt(double base, int64_t warmup, double init, int64_t step, double* out) {
+  GUARD({ *out = InverseSqrtSchedule(base, warmup, init).lr(step); })
+}
+int sqfref_cosine_restart(double base, double eta_min, int64_t period, double t_mult, int64_t step,
+                          double* out) {
+  GUARD({ *out = CosineRestartSchedule(base, eta_min, period, t_mult).lr(step); })
+}
+
+// Adam (optim.cpp:48-66): one apply with moments/step restored from the caller
+int sqfref_adam(float* params, const float* grads, int64_t n, float* m, float* v, int64_t t,
+                double lr, double b1, double b2, double eps) {
+  GUARD({
+    AdamOptimizer opt(n, b1, b2, eps);
+    opt.load_state_blobs({{"adam.m", std::vector<float>(m, m + n)},
+                          {"adam.v", std::vector<float>(v, v + n)}});
+    opt.set_step_count(t);
+    opt.apply(std::span<float>(params, static_cast<size_t>(n)),
+              std::span<const float>(grads, static_cast<size_t>(n)), lr);
+    auto blobs = opt.state_blobs();
+    std::memcpy(m, blobs[0].second.data(), static_cast<size_t>(n) * 4);
+    std::memcpy(v, blobs[1].second.data(), static_cast<size_t>(n) * 4);
+  })
+}
+
+// LossScaler (trainer.cpp:21-48) driven by an overflow sequence; returns the
+// index of the update that diverged in *diverged_at (-1 if none)
+int sqfref_scaler_run(double init, int64_t window, double mn, double mx, const uint8_t* overflow,
+                      int n, double* scales, int32_t* diverged_at) {
+  GUARD({
+    LossScaler s(init, window, mn, mx);
+    *diverged_at = -1;
+    for (int i = 0; i < n; ++i) {
+      try {
+        s.update(overflow[i] != 0);
+      } catch (const DivergenceError&) {
+        *diverged_at = i;
+        return 0;
+      }
+      scales[i] = s.scale();
+    }
+  })
+}
+
+// ---------------------------------------------------------------- single tape ops
+// softmax_xent (tape.cpp:151-168, 259-290, 481-502) with backward seeded by
+// `seed` on active rows (tape.cpp:506-516).
+int sqfref_xent(const float* logits, int rows, int vocab, const int32_t* gold,
+                const uint8_t* active, float eps, int fp16, float seed, float* loss_rows,
+                float* nll_rows, uint8_t* correct, float* dlogits) {
+  GUARD({
+    std::vector<float> none;
+    Tape tape{std::span<const float>(none.data(), 0), fp16 ? DType::F16E : DType::F32};
+    int l = tape.leaf(Tensor({rows, vocab}, std::vector<float>(logits, logits + int64_t(rows) * vocab)));
+    int x = tape.softmax_xent(l, std::vector<int>(gold, gold + rows),
+                              std::vector<uint8_t>(active, active + rows), eps);
+    const TapeNode& n = tape.node(x);
+    for (int r = 0; r < rows; ++r) {
+      loss_rows[r] = n.out.data()[r];
+      nll_rows[r] = n.nll[static_cast<size_t>(r)];
+      correct[r] = n.correct[static_cast<size_t>(r)];
+    }
+    if (dlogits) {
+      std::vector<float> pg;
+      tape.backward(x, seed, pg);
+      std::memcpy(dlogits, tape.node(l).grad.data(), sizeof(float) * size_t(rows) * vocab);
+    }
+  })
+}
+
+// layer_norm (tape.cpp:96-107, 211-222, 383-418): forward + backward_from(dy)
+int sqfref_layer_norm(const float* x, int rows, int d, const float* gamma, const float* beta,
+                      int fp16, const float* dy, float* y, float* dx, float* dgamma,
+                      float* dbeta) {
+  GUARD({
+    std::vector<float> p(gamma, gamma + d);
+    p.insert(p.end(), beta, beta + d);
+    Tape tape{p, fp16 ? DType::F16E : DType::F32};
+    int in = tape.leaf(Tensor({rows, d}, std::vector<float>(x, x + int64_t(rows) * d)));
+    int o = tape.layer_norm(in, ParamRef{0, 1, d}, ParamRef{d, 1, d});
+    std::memcpy(y, tape.out(o).data(), sizeof(float) * size_t(rows) * d);
+    if (dy) {
+      std::vector<float> pg(static_cast<size_t>(2 * d), 0.0f);
+      Tensor g({rows, d}, std::vector<float>(dy, dy + int64_t(rows) * d));
+      tape.backward_from(o, g, pg);
+      std::memcpy(dx, tape.node(in).grad.data(), sizeof(float) * size_t(rows) * d);
+      std::memcpy(dgamma, pg.data(), sizeof(float) * d);
+      std::memcpy(dbeta, pg.data() + d, sizeof(float) * d);
+    }
+  })
+}
+
+// attention (tape.cpp:123-149, 229-258, 426-480)
+int sqfref_attention(const float* q, int rq, const float* k, const float* v, int rk, int d,
+                     int heads, const int32_t* key_base, const int32_t* key_len, int fp16,
+                     const float* dout, float* out, float* dq, float* dk, float* dv) {
+  GUARD({
+    std::vector<float> none;
+    Tape tape{std::span<const float>(none.data(), 0), fp16 ? DType::F16E : DType::F32};
+    int iq = tape.leaf(Tensor({rq, d}, std::vector<float>(q, q + int64_t(rq) * d)));
+    int ik = tape.leaf(Tensor({rk, d}, std::vector<float>(k, k + int64_t(rk) * d)));
+    int iv = tape.leaf(Tensor({rk, d}, std::vector<float>(v, v + int64_t(rk) * d)));
+    int o = tape.attention(iq, ik, iv, heads, std::vector<int>(key_base, key_base + rq),
+                           std::vector<int>(key_len, key_len + rq));
+    std::memcpy(out, tape.out(o).data(), sizeof(float) * size_t(rq) * d);
+    if (dout) {
+      std::vector<float> pg;
+      Tensor g({rq, d}, std::vector<float>(dout, dout + int64_t(rq) * d));
+      tape.backward_from(o, g, pg);
+      std::memcpy(dq, tape.node(iq).grad.data(), sizeof(float) * size_t(rq) * d);
+      std::memcpy(dk, tape.node(ik).grad.data(), sizeof(float) * size_t(rk) * d);
+      std::memcpy(dv, tape.node(iv).grad.data(), sizeof(float) * size_t(rk) * d);
+    }
+  })
+}
+
+// matmul_nt (+ add_bias when bias != null), tape.cpp:46-67, 182-197, 324-358
+int sqfref_linear(const float* x, int rows, int in_dim, const float* w, const float* bias,
+                  int out_dim, int fp16, const float* dy, float* y, float* dx, float* dw,
+                  float* db) {
+  GUARD({
+    std::vector<float> p(w, w + int64_t(out_dim) * in_dim);
+    if (bias) p.insert(p.end(), bias, bias + out_dim);
+    Tape tape{p, fp16 ? DType::F16E : DType::F32};
+    int in = tape.leaf(Tensor({rows, in_dim}, std::vector<float>(x, x + int64_t(rows) * in_dim)));
+    int o = tape.matmul_nt(in, ParamRef{0, out_dim, in_dim});
+    if (bias) o = tape.add_bias(o, ParamRef{int64_t(out_dim) * in_dim, 1, out_dim});
+    std::memcpy(y, tape.out(o).data(), sizeof(float) * size_t(rows) * out_dim);
+    if (dy) {
+      std::vector<float> pg(p.size(), 0.0f);
+      Tensor g({rows, out_dim}, std::vector<float>(dy, dy + int64_t(rows) * out_dim));
+      tape.backward_from(o, g, pg);
+      std::memcpy(dx, tape.node(in).grad.data(), sizeof(float) * size_t(rows) * in_dim);
+      std::memcpy(dw, pg.data(), sizeof(float) * size_t(out_dim) * in_dim);
+      if (bias) std::memcpy(db, pg.data() + int64_t(out_dim) * in_dim, sizeof(float) * out_dim);
+    }
+  })
+}
+
+// ---------------------------------------------------------------- trainer
+// arch + raw user overrides resolved exactly as Registry::resolve_architecture
+// (registry.cpp:96-110); the task is the in-memory corpus (trainer.hpp:84-85).
+void* sqfref_trainer_create(const char* arch, const char** keys, const char** vals, int n,
+                            void* corpus, int src_vocab, int tgt_vocab) {
+  try {
+    std::vector<std::pair<std::string, std::string>> user;
+    for (int i = 0; i < n; ++i) user.emplace_back(keys[i], vals[i]);
+    auto box = std::make_unique<TrainerBox>();
+    box->cfg = oracle_registry().resolve_architecture(arch, user);
+    auto task = std::make_unique<MemTask>(*static_cast<Corpus*>(corpus), src_vocab, tgt_vocab);
+    box->tr = std::make_unique<Trainer>(box->cfg, std::move(task), oracle_registry());
+    return box.release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+void sqfref_trainer_free(void* h) { delete static_cast<TrainerBox*>(h); }
+
+int sqfref_trainer_set_injector(void* h, const int64_t* steps, int n) {
+  GUARD({
+    auto* b = static_cast<TrainerBox*>(h);
+    b->inject.assign(steps, steps + n);
+    std::vector<int64_t> s = b->inject;
+    b->tr->set_overflow_injector([s](int64_t step) {
+      for (int64_t x : s)
+        if (x == step) return true;
+      return false;
+    });
+  })
+}
+
+// returns 1 when the data stream is exhausted (trainer.cpp:204-208)
+int sqfref_trainer_train_one(void* h, StatsC* out) {
+  try {
+    auto st = static_cast<TrainerBox*>(h)->tr->train_one();
+    if (!st) return 1;
+    fill(out, *st);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// explicit dispatch (trainer.cpp:210-273): counts[w*A+a] members each
+int sqfref_trainer_train_step(void* h, void* corpus, const int32_t* members, const int32_t* counts,
+                              int workers, int accum, StatsC* out) {
+  GUARD({
+    auto* c = static_cast<Corpus*>(corpus);
+    std::vector<std::vector<MiniBatch>> sub(static_cast<size_t>(workers));
+    int64_t k = 0;
+    for (int w = 0; w < workers; ++w)
+      for (int a = 0; a < accum; ++a) {
+        int cnt = counts[w * accum + a];
+        std::vector<int> m(members + k, members + k + cnt);
+        k += cnt;
+        if (cnt == 0) {
+          sub[static_cast<size_t>(w)].push_back(MiniBatch{});
+        } else {
+          sub[static_cast<size_t>(w)].push_back(make_minibatch(c->pairs, m));
+        }
+      }
+    fill(out, static_cast<TrainerBox*>(h)->tr->train_step(sub));
+  })
+}
+
+int64_t sqfref_trainer_num_params(void* h) { return static_cast<TrainerBox*>(h)->tr->model().num_params(); }
+int sqfref_trainer_params(void* h, float* out) {
+  GUARD({
+    auto p = static_cast<TrainerBox*>(h)->tr->model().params();
+    std::memcpy(out, p.data(), p.size() * 4);
+  })
+}
+int sqfref_trainer_set_params(void* h, const float* in) {
+  GUARD({
+    auto* b = static_cast<TrainerBox*>(h);
+    auto p = b->tr->model().params();
+    std::memcpy(p.data(), in, p.size() * 4);
+    b->tr->rebroadcast();
+  })
+}
+int sqfref_trainer_replica_params(void* h, int w, float* out) {
+  GUARD({
+    auto p = static_cast<TrainerBox*>(h)->tr->replica(w).params();
+    std::memcpy(out, p.data(), p.size() * 4);
+  })
+}
+int sqfref_trainer_manifest_size(void* h) {
+  return static_cast<int>(static_cast<TrainerBox*>(h)->tr->model().manifest().size());
+}
+int sqfref_trainer_manifest_entry(void* h, int i, char* name, int cap, int64_t* offset,
+                                  int64_t* numel) {
+  GUARD({
+    const auto& e = static_cast<TrainerBox*>(h)->tr->model().manifest().at(static_cast<size_t>(i));
+    std::snprintf(name, static_cast<size_t>(cap), "%s", e.name.c_str());
+    *offset = e.offset;
+    *numel = e.numel;
+  })
+}
+int sqfref_trainer_adam_state(void* h, float* m, float* v, int64_t* t) {
+  GUARD({
+    auto& opt = static_cast<TrainerBox*>(h)->tr->optimizer();
+    for (auto& [name, data] : opt.state_blobs()) {
+      if (name == "adam.m") std::memcpy(m, data.data(), data.size() * 4);
+      if (name == "adam.v") std::memcpy(v, data.data(), data.size() * 4);
+    }
+    *t = opt.step_count();
+  })
+}
+int sqfref_trainer_scaler(void* h, double* scale, int64_t* good) {
+  GUARD({
+    const auto& s = static_cast<TrainerBox*>(h)->tr->scaler();
+    *scale = s.scale();
+    *good = s.successes();
+  })
+}
+int sqfref_trainer_progress(void* h, int64_t* step, int32_t* epoch, int32_t* cursor,
+                            int32_t* nbatches) {
+  GUARD({
+    auto* t = static_cast<TrainerBox*>(h)->tr.get();
+    *step = t->step();
+    *epoch = t->epoch();
+    *cursor = t->cursor();
+    *nbatches = t->batches_per_epoch();
+  })
+}
+int sqfref_trainer_buckets(void* h, int32_t* n, int64_t* starts, int64_t* ends) {
+  GUARD({
+    const auto& b = static_cast<TrainerBox*>(h)->tr->buckets();
+    *n = static_cast<int32_t>(b.size());
+    if (starts)
+      for (size_t i = 0; i < b.size(); ++i) {
+        starts[i] = b[i].start;
+        ends[i] = b[i].end;
+      }
+  })
+}
+
+// One sub-batch forward+backward on the (shadow of the) master parameters,
+// restated from train_step's inner body (trainer.cpp:223-240) with the
+// reference's own Tape/criterion: fills grad (caller-zeroed or accumulated).
+int sqfref_trainer_subbatch_grad(void* h, void* corpus, const int32_t* members, int n, float seed,
+                                 float* grad, StatsC* out) {
+  GUARD({
+    auto* b = static_cast<TrainerBox*>(h);
+    auto* c = static_cast<Corpus*>(corpus);
+    Trainer& t = *b->tr;
+    std::unique_ptr<ModelBase> rep = t.model().clone();
+    if (t.fp16()) {
+      auto p = rep->params();
+      for (float& x : p) x = quantize_fp16(x);
+    }
+    auto crit = oracle_registry().make_criterion(b->cfg.get_str("criterion"), b->cfg);
+    MiniBatch mb = make_minibatch(c->pairs, std::vector<int>(members, members + n));
+    Tape tape{rep->params(), t.fp16() ? DType::F16E : DType::F32};
+    CriterionOutput co = crit->compute(*rep, mb, tape);
+    tape.backward(co.loss_node, seed,
+                  std::span<float>(grad, static_cast<size_t>(rep->num_params())));
+    StepStats s;
+    s.loss = co.loss;
+    s.nll = co.nll;
+    s.ntokens = co.ntokens;
+    s.ncorrect = co.ncorrect;
+    fill(out, s);
+  })
+}
+
+// Trainer::evaluate (trainer.cpp:275-289) over a corpus
+int sqfref_trainer_evaluate(void* h, void* corpus, double* loss, double* nll, int64_t* ntokens,
+                            int64_t* ncorrect) {
+  GUARD({
+    EvalStats e = static_cast<TrainerBox*>(h)->tr->evaluate(static_cast<Corpus*>(corpus)->pairs);
+    *loss = e.loss;
+    *nll = e.nll;
+    *ntokens = e.ntokens;
+    *ncorrect = e.ncorrect;
+  })
+}
+
+}  // extern "C"

@@ -1,0 +1,301 @@
+"""B200-native mixed-precision data-parallel Transformer training step.
+
+Python face of the C-ABI library (include/sqf_trainer.h, include/sqf_kernels.h).
+It mirrors the seqforge reference's Trainer surface (trainer.hpp:80-125): same
+config keys, registry names, StepStats, train_one / train_step / evaluate,
+overflow injector, scaler, progress. All compute runs in the native library's
+sm_100a kernels; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+
+__all__ = ["Corpus", "Trainer", "synthetic_corpus", "make_batches", "shuffle_epoch", "make_minibatch",
+           "split_counts", "bucket_gradients", "model_init", "scaler_run", "schedule_lr", "quantize_fp16",
+           "nccl_unique_id", "NativeError", "BOS", "PAD", "EOS", "UNK"]
+
+BOS, PAD, EOS, UNK = 0, 1, 2, 3
+NativeError = L.NativeError
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class Corpus:
+    """Eos-terminated id sequences, concatenated (SequencePair list, data.hpp:50-54)."""
+    src_len: np.ndarray
+    tgt_len: np.ndarray
+    src_ids: np.ndarray
+    tgt_ids: np.ndarray
+
+    @property
+    def npairs(self) -> int:
+        return int(self.src_len.shape[0])
+
+    @classmethod
+    def from_pairs(cls, pairs):
+        sl = np.array([len(s) for s, _ in pairs], np.int32)
+        tl = np.array([len(t) for _, t in pairs], np.int32)
+        si = np.array([x for s, _ in pairs for x in s], np.int32)
+        ti = np.array([x for _, t in pairs for x in t], np.int32)
+        return cls(sl, tl, si, ti)
+
+    def pair(self, i: int):
+        so = int(self.src_len[:i].sum())
+        to = int(self.tgt_len[:i].sum())
+        return (self.src_ids[so:so + self.src_len[i]].tolist(), self.tgt_ids[to:to + self.tgt_len[i]].tolist())
+
+    def handle(self):
+        return L.sqf_corpus_create(self.npairs, _ptr(self.src_len), _ptr(self.tgt_len), _ptr(self.src_ids),
+                                   _ptr(self.tgt_ids))
+
+
+def synthetic_corpus(npairs: int, src_vocab: int, tgt_vocab: int, zipf_s: float = 1.1, seed: int = 1) -> Corpus:
+    """SURVEY §8(d) generator: lengths clamp(round(exp(3.1+0.6z)),1,200), ids Zipf(s) over [4, V)."""
+    sl = np.zeros(npairs, np.int32)
+    tl = np.zeros(npairs, np.int32)
+    st, tt = C.c_int64(), C.c_int64()
+    L.check(L.sqf_synthetic_corpus(npairs, src_vocab, tgt_vocab, zipf_s, seed, _ptr(sl), _ptr(tl), None, None,
+                                   C.byref(st), C.byref(tt)))
+    si = np.zeros(st.value, np.int32)
+    ti = np.zeros(tt.value, np.int32)
+    L.check(L.sqf_synthetic_corpus(npairs, src_vocab, tgt_vocab, zipf_s, seed, _ptr(sl), _ptr(tl), _ptr(si), _ptr(ti),
+                                   C.byref(st), C.byref(tt)))
+    return Corpus(sl, tl, si, ti)
+
+
+def make_batches(corpus: Corpus, max_tokens: int, max_sentences: int = 0, seed: int = 1):
+    h = corpus.handle()
+    try:
+        n = C.c_int32()
+        sizes = np.zeros(max(1, corpus.npairs), np.int32)
+        members = np.zeros(max(1, corpus.npairs), np.int32)
+        L.check(L.sqf_make_batches(h, max_tokens, max_sentences, seed, C.byref(n), _ptr(sizes), _ptr(members)))
+        out, k = [], 0
+        for b in range(n.value):
+            out.append(members[k:k + sizes[b]].tolist())
+            k += sizes[b]
+        return out
+    finally:
+        L.sqf_corpus_free(h)
+
+
+def shuffle_epoch(nbatches: int, seed: int, epoch: int):
+    order = np.zeros(max(1, nbatches), np.int32)
+    L.check(L.sqf_shuffle_epoch(nbatches, seed, epoch, _ptr(order)))
+    return order[:nbatches].tolist()
+
+
+def make_minibatch(corpus: Corpus, members):
+    h = corpus.handle()
+    try:
+        m = np.asarray(members, np.int32)
+        maxw = int(max(corpus.src_len.max(), corpus.tgt_len.max())) if corpus.npairs else 1
+        cap = max(1, len(m) * maxw)
+        dims = np.zeros(3, np.int32)
+        src, tin, tout = (np.zeros(cap, np.int32) for _ in range(3))
+        sl, tl = np.zeros(max(1, len(m)), np.int32), np.zeros(max(1, len(m)), np.int32)
+        nt = C.c_int64()
+        L.check(L.sqf_make_minibatch(h, _ptr(m), len(m), _ptr(dims), _ptr(src), _ptr(tin), _ptr(tout), _ptr(sl),
+                                     _ptr(tl), C.byref(nt)))
+        r, s, t = (int(x) for x in dims)
+        return {"rows": r, "src_width": s, "tgt_width": t, "source": src[:r * s].reshape(r, s),
+                "target_in": tin[:r * t].reshape(r, t), "target_out": tout[:r * t].reshape(r, t),
+                "src_lens": sl[:r].copy(), "tgt_lens": tl[:r].copy(), "ntokens": nt.value}
+    finally:
+        L.sqf_corpus_free(h)
+
+
+def split_counts(rows: int, workers: int, accum: int):
+    c = np.zeros(workers * accum, np.int32)
+    L.check(L.sqf_split_counts(rows, workers, accum, _ptr(c)))
+    return c.tolist()
+
+
+def bucket_gradients(sizes, threshold: int):
+    s = np.asarray(sizes, np.int64)
+    n = C.c_int32()
+    st = np.zeros(len(s) + 1, np.int64)
+    en = np.zeros(len(s) + 1, np.int64)
+    L.check(L.sqf_bucket_gradients(_ptr(s), len(s), threshold, C.byref(n), _ptr(st), _ptr(en)))
+    return list(zip(st[:n.value].tolist(), en[:n.value].tolist()))
+
+
+def _kv(overrides):
+    keys = [str(k) for k in overrides]
+    vals = [str(v).lower() if isinstance(v, bool) else str(v) for v in overrides.values()]
+    return L.cstrs(keys), L.cstrs(vals), len(keys)
+
+
+def model_init(arch: str, overrides: dict):
+    """Initial canonical-order parameters of the model (host, model.cpp:135-150)."""
+    k, v, n = _kv(overrides)
+    num = C.c_int64()
+    ms = C.c_int()
+    L.check(L.sqf_model_init(arch.encode(), k, v, n, None, 0, C.byref(num), C.byref(ms)))
+    out = np.zeros(num.value, np.float32)
+    L.check(L.sqf_model_init(arch.encode(), k, v, n, _ptr(out), num.value, C.byref(num), C.byref(ms)))
+    return out
+
+
+def scaler_run(init, window, mn, mx, overflow):
+    ov = np.asarray(overflow, np.uint8)
+    sc = np.zeros(max(1, len(ov)), np.float64)
+    d = C.c_int32()
+    L.check(L.sqf_scaler_run(init, window, mn, mx, _ptr(ov), len(ov), _ptr(sc), C.byref(d)))
+    return sc[:len(ov)].tolist(), d.value
+
+
+def schedule_lr(name, step, lr=5e-4, warmup=400, warmup_init_lr=0.0, eta_min=0.0, period=1000, t_mult=1.0):
+    out = C.c_double()
+    L.check(L.sqf_schedule_lr(name.encode(), lr, warmup, warmup_init_lr, eta_min, period, t_mult, step,
+                              C.byref(out)))
+    return out.value
+
+
+def quantize_fp16(x: float) -> float:
+    return float(L.sqf_quantize_fp16(x))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    L.check(L.sqf_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+@dataclass
+class EvalStats:
+    loss: float
+    nll: float
+    ntokens: int
+    ncorrect: int
+
+
+class Trainer:
+    """Drop-in for the reference's Trainer (trainer.hpp:80-125) on B200.
+
+    ``arch`` + ``overrides`` resolve like Registry::resolve_architecture; pass a
+    ``corpus`` for an in-memory task (the reference's task-injecting ctor) or set
+    ``task=synthetic`` in the overrides. ``rank``/``world``/``nccl_id`` place this
+    process in the data-parallel group (one process per GPU).
+    """
+
+    def __init__(self, arch: str, overrides: dict | None = None, corpus: Corpus | None = None,
+                 src_vocab: int = 0, tgt_vocab: int = 0, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None):
+        overrides = dict(overrides or {})
+        self.overrides = overrides
+        k, v, n = _kv(overrides)
+        self.corpus = corpus
+        idbuf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        if corpus is not None:
+            h = L.sqf_trainer_create(arch.encode(), k, v, n, _ptr(corpus.src_len), _ptr(corpus.tgt_len),
+                                     _ptr(corpus.src_ids), _ptr(corpus.tgt_ids), corpus.npairs, src_vocab,
+                                     tgt_vocab, rank, world, idbuf)
+        else:
+            h = L.sqf_trainer_create(arch.encode(), k, v, n, None, None, None, None, 0, 0, 0, rank, world, idbuf)
+        if not h:
+            raise L.NativeError(-9, (L.sqf_last_error() or b"").decode())
+        self._h = h
+        self.workers = int(overrides.get("workers", 1))
+        self.accum = int(overrides.get("accum", 1))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.sqf_trainer_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # ---- the hot path
+    def train_one(self):
+        st = L.StepStats()
+        r = L.check(L.sqf_trainer_train_one(self._h, C.byref(st)))
+        return None if r == 1 else st.as_dict()
+
+    def train_step(self, sub):
+        """sub[w][a] = list of corpus indices (reference train_step(sub[W][A]))."""
+        counts = np.array([len(m) for row in sub for m in row], np.int32)
+        members = np.array([x for row in sub for m in row for x in m] or [0], np.int32)
+        st = L.StepStats()
+        L.check(L.sqf_trainer_train_step(self._h, _ptr(members), _ptr(counts), C.byref(st)))
+        return st.as_dict()
+
+    def evaluate(self, corpus_idx) -> EvalStats:
+        idx = np.asarray(corpus_idx, np.int32)
+        loss, nll, nt, nc = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+        L.check(L.sqf_trainer_evaluate(self._h, _ptr(idx), len(idx), C.byref(loss), C.byref(nll), C.byref(nt),
+                                       C.byref(nc)))
+        return EvalStats(loss.value, nll.value, nt.value, nc.value)
+
+    # ---- state
+    @property
+    def num_params(self) -> int:
+        return int(L.sqf_trainer_num_params(self._h))
+
+    def params(self) -> np.ndarray:
+        out = np.zeros(self.num_params, np.float32)
+        L.check(L.sqf_trainer_params(self._h, _ptr(out)))
+        return out
+
+    def set_params(self, p: np.ndarray):
+        p = np.ascontiguousarray(p, np.float32)
+        L.check(L.sqf_trainer_set_params(self._h, _ptr(p)))
+
+    def last_grads(self) -> np.ndarray:
+        out = np.zeros(self.num_params, np.float32)
+        L.check(L.sqf_trainer_last_grads(self._h, _ptr(out)))
+        return out
+
+    def manifest(self):
+        out = []
+        buf = C.create_string_buffer(256)
+        for i in range(L.sqf_trainer_manifest_size(self._h)):
+            off, num, doff = C.c_int64(), C.c_int64(), C.c_int64()
+            L.check(L.sqf_trainer_manifest_entry(self._h, i, buf, 256, C.byref(off), C.byref(num), C.byref(doff)))
+            out.append((buf.value.decode(), off.value, num.value, doff.value))
+        return out
+
+    def adam_state(self):
+        m = np.zeros(self.num_params, np.float32)
+        v = np.zeros(self.num_params, np.float32)
+        t = C.c_int64()
+        L.check(L.sqf_trainer_adam_state(self._h, _ptr(m), _ptr(v), C.byref(t)))
+        return m, v, t.value
+
+    def scaler(self):
+        s, g = C.c_double(), C.c_int64()
+        L.check(L.sqf_trainer_scaler(self._h, C.byref(s), C.byref(g)))
+        return s.value, g.value
+
+    def progress(self):
+        s, e, c, n = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+        L.check(L.sqf_trainer_progress(self._h, C.byref(s), C.byref(e), C.byref(c), C.byref(n)))
+        return {"step": s.value, "epoch": e.value, "cursor": c.value, "batches_per_epoch": n.value}
+
+    def set_overflow_injector(self, steps):
+        a = np.asarray(list(steps) or [0], np.int64)
+        L.check(L.sqf_trainer_set_injector(self._h, _ptr(a), len(list(steps))))
+
+    def restore(self, step, epoch, cursor, scale=0.0, successes=0):
+        L.check(L.sqf_trainer_restore(self._h, step, epoch, cursor, scale, successes))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(L.sqf_trainer_kernel_launches(self._h))
+
+    @property
+    def last_step_ms(self) -> float:
+        return float(L.sqf_trainer_last_step_ms(self._h))
+
+    @property
+    def stream(self) -> int:
+        return int(L.sqf_trainer_stream(self._h) or 0)

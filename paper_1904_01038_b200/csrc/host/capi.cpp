@@ -1,0 +1,399 @@
+// C ABI (include/sqf_trainer.h) over the host trainer. Exceptions never cross
+// the boundary: they become the reference's error classes as status codes.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../../include/sqf_trainer.h"
+#include "nccl_dyn.hpp"
+#include "trainer.hpp"
+
+namespace sqf {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const ConfigError*>(&e)) return -1;
+  if (dynamic_cast<const ShapeError*>(&e)) return -2;
+  if (dynamic_cast<const BoundsError*>(&e)) return -3;
+  if (dynamic_cast<const CapacityError*>(&e)) return -4;
+  if (dynamic_cast<const IntegrityError*>(&e)) return -5;
+  if (dynamic_cast<const DivergenceError*>(&e)) return -6;
+  if (dynamic_cast<const RegistryError*>(&e)) return -7;
+  if (dynamic_cast<const IoError*>(&e)) return -8;
+  if (dynamic_cast<const DeviceError*>(&e)) return -10;
+  return -9;
+}
+
+#define SQF_GUARD(...)                \
+  try {                               \
+    __VA_ARGS__;                      \
+    return 0;                         \
+  } catch (const std::exception& e) { \
+    return fail(e);                   \
+  }
+
+struct Corpus {
+  std::vector<SequencePair> pairs;
+};
+
+std::vector<SequencePair> unpack_pairs(int npairs, const int32_t* sl, const int32_t* tl, const int32_t* si,
+                                       const int32_t* ti) {
+  std::vector<SequencePair> out(static_cast<size_t>(npairs));
+  int64_t so = 0, to = 0;
+  for (int i = 0; i < npairs; ++i) {
+    out[size_t(i)].source.assign(si + so, si + so + sl[i]);
+    out[size_t(i)].target.assign(ti + to, ti + to + tl[i]);
+    out[size_t(i)].corpus_index = i;
+    so += sl[i];
+    to += tl[i];
+  }
+  return out;
+}
+
+class MemoryTask : public TaskBase {
+ public:
+  MemoryTask(std::vector<SequencePair> p, int sv, int tv) : pairs_(std::move(p)), sv_(sv), tv_(tv) {}
+  int source_vocab() const override { return sv_; }
+  int target_vocab() const override { return tv_; }
+  const std::vector<SequencePair>& train_pairs() const override { return pairs_; }
+
+ private:
+  std::vector<SequencePair> pairs_;
+  int sv_, tv_;
+};
+
+std::vector<std::pair<std::string, std::string>> user_kv(const char* const* k, const char* const* v, int n) {
+  std::vector<std::pair<std::string, std::string>> out;
+  for (int i = 0; i < n; ++i) out.emplace_back(k[i], v[i]);
+  return out;
+}
+
+void fill(sqf_step_stats* o, const StepStats& s) {
+  o->step = s.step;
+  o->loss = s.loss;
+  o->nll = s.nll;
+  o->ntokens = s.ntokens;
+  o->ncorrect = s.ncorrect;
+  o->lr = s.lr;
+  o->skipped = s.skipped ? 1 : 0;
+  o->_pad = 0;
+  o->scale = s.scale;
+}
+
+Trainer* T(void* t) { return static_cast<Trainer*>(t); }
+
+}  // namespace
+}  // namespace sqf
+
+using namespace sqf;
+
+extern "C" {
+
+const char* sqf_last_error(void) { return g_err.c_str(); }
+
+int sqf_nccl_unique_id(void* out128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (NcclApi::get().GetUniqueId(&id) != ncclSuccess) {
+    g_err = "ncclGetUniqueId failed";
+    return -10;
+  }
+  std::memcpy(out128, &id, 128);
+  return 0;
+}
+
+void* sqf_trainer_create(const char* arch, const char* const* keys, const char* const* vals, int n,
+                         const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
+                         const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab, int rank, int world,
+                         const void* nccl_id) {
+  try {
+    const Registry& reg = global_registry();
+    Config cfg = reg.resolve_architecture(arch, user_kv(keys, vals, n));
+    std::unique_ptr<TaskBase> task;
+    if (npairs > 0)
+      task = std::make_unique<MemoryTask>(unpack_pairs(npairs, src_len, tgt_len, src_ids, tgt_ids), src_vocab,
+                                          tgt_vocab);
+    ncclUniqueId id;
+    if (nccl_id) std::memcpy(&id, nccl_id, sizeof id);
+    return new Trainer(cfg, reg, std::move(task), rank, world, nccl_id ? &id : nullptr);
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void sqf_trainer_free(void* t) { delete T(t); }
+
+int sqf_trainer_train_one(void* t, sqf_step_stats* out) {
+  try {
+    auto st = T(t)->train_one();
+    if (!st) return 1;
+    fill(out, *st);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int sqf_trainer_train_step(void* t, const int32_t* members, const int32_t* counts, sqf_step_stats* out) {
+  SQF_GUARD({
+    Trainer& tr = *T(t);
+    const auto& pairs = tr.task().train_pairs();
+    std::vector<std::vector<MiniBatch>> sub(size_t(tr.workers()));
+    int64_t k = 0;
+    for (int w = 0; w < tr.workers(); ++w)
+      for (int a = 0; a < tr.accum(); ++a) {
+        const int c = counts[w * tr.accum() + a];
+        std::vector<int> m(members + k, members + k + c);
+        k += c;
+        sub[size_t(w)].push_back(c == 0 ? MiniBatch{} : make_minibatch(pairs, m));
+      }
+    fill(out, tr.train_step(sub));
+  })
+}
+
+int sqf_trainer_evaluate(void* t, const int32_t* idx, int n, double* loss, double* nll, int64_t* ntokens,
+                         int64_t* ncorrect) {
+  SQF_GUARD({
+    Trainer& tr = *T(t);
+    const auto& pairs = tr.task().train_pairs();
+    std::vector<SequencePair> sel;
+    for (int i = 0; i < n; ++i) {
+      SequencePair p = pairs.at(size_t(idx[i]));
+      p.corpus_index = i;
+      sel.push_back(std::move(p));
+    }
+    EvalStats e = tr.evaluate(sel);
+    *loss = e.loss;
+    *nll = e.nll;
+    *ntokens = e.ntokens;
+    *ncorrect = e.ncorrect;
+  })
+}
+
+int64_t sqf_trainer_num_params(void* t) { return T(t)->model().num_params(); }
+
+int sqf_trainer_params(void* t, float* out) {
+  SQF_GUARD({
+    T(t)->pull_params();
+    auto p = T(t)->model().params();
+    std::memcpy(out, p.data(), p.size() * 4);
+  })
+}
+
+int sqf_trainer_set_params(void* t, const float* in) {
+  SQF_GUARD({
+    auto p = T(t)->model().params();
+    std::memcpy(p.data(), in, p.size() * 4);
+    T(t)->push_params();
+  })
+}
+
+int sqf_trainer_last_grads(void* t, float* out) {
+  SQF_GUARD({
+    auto g = T(t)->reduced_grads();
+    std::memcpy(out, g.data(), g.size() * 4);
+  })
+}
+
+int sqf_trainer_manifest_size(void* t) { return int(T(t)->model().manifest().size()); }
+
+int sqf_trainer_manifest_entry(void* t, int i, char* name, int cap, int64_t* offset, int64_t* numel,
+                               int64_t* device_offset) {
+  SQF_GUARD({
+    const auto& e = T(t)->model().manifest().at(size_t(i));
+    std::snprintf(name, size_t(cap), "%s", e.name.c_str());
+    *offset = e.offset;
+    *numel = e.numel;
+    *device_offset = e.device_offset;
+  })
+}
+
+int sqf_trainer_adam_state(void* t, float* m, float* v, int64_t* step_count) {
+  SQF_GUARD({
+    Trainer& tr = *T(t);
+    for (auto& [name, data] : tr.optimizer().state_blobs()) {
+      std::vector<float> canon(data.size());
+      tr.model().to_canonical_order(data, canon);
+      if (name == "adam.m") std::memcpy(m, canon.data(), canon.size() * 4);
+      if (name == "adam.v") std::memcpy(v, canon.data(), canon.size() * 4);
+    }
+    *step_count = tr.optimizer().step_count();
+  })
+}
+
+int sqf_trainer_scaler(void* t, double* scale, int64_t* successes) {
+  SQF_GUARD({
+    const LossScaler& s = T(t)->scaler();
+    *scale = s.scale();
+    *successes = s.successes();
+  })
+}
+
+int sqf_trainer_progress(void* t, int64_t* step, int32_t* epoch, int32_t* cursor, int32_t* nbatches) {
+  SQF_GUARD({
+    *step = T(t)->step();
+    *epoch = T(t)->epoch();
+    *cursor = T(t)->cursor();
+    *nbatches = T(t)->batches_per_epoch();
+  })
+}
+
+int sqf_trainer_set_injector(void* t, const int64_t* steps, int n) {
+  SQF_GUARD({
+    std::vector<int64_t> s(steps, steps + n);
+    T(t)->set_overflow_injector([s](int64_t step) { return std::find(s.begin(), s.end(), step) != s.end(); });
+  })
+}
+
+int sqf_trainer_restore(void* t, int64_t step, int32_t epoch, int32_t cursor, double scale, int64_t successes) {
+  SQF_GUARD({
+    T(t)->restore_progress(step, epoch, cursor);
+    if (T(t)->fp16()) T(t)->restore_scaler(scale, successes);
+  })
+}
+
+int64_t sqf_trainer_kernel_launches(void* t) { return T(t)->kernel_launches(); }
+float sqf_trainer_last_step_ms(void* t) { return T(t)->last_step_ms(); }
+void* sqf_trainer_stream(void* t) { return static_cast<void*>(T(t)->stream()); }
+
+// ---------------------------------------------------------------- host-only
+int sqf_synthetic_corpus(int npairs, int src_vocab, int tgt_vocab, double zipf_s, uint64_t seed, int32_t* src_len,
+                         int32_t* tgt_len, int32_t* src_ids, int32_t* tgt_ids, int64_t* src_total,
+                         int64_t* tgt_total) {
+  SQF_GUARD({
+    auto pairs = synthetic_corpus(npairs, src_vocab, tgt_vocab, zipf_s, seed);
+    int64_t so = 0, to = 0;
+    for (int i = 0; i < npairs; ++i) {
+      const auto& p = pairs[size_t(i)];
+      if (src_len) src_len[i] = int32_t(p.source.size());
+      if (tgt_len) tgt_len[i] = int32_t(p.target.size());
+      if (src_ids) std::copy(p.source.begin(), p.source.end(), src_ids + so);
+      if (tgt_ids) std::copy(p.target.begin(), p.target.end(), tgt_ids + to);
+      so += int64_t(p.source.size());
+      to += int64_t(p.target.size());
+    }
+    *src_total = so;
+    *tgt_total = to;
+  })
+}
+
+void* sqf_corpus_create(int npairs, const int32_t* sl, const int32_t* tl, const int32_t* si, const int32_t* ti) {
+  auto* c = new Corpus;
+  c->pairs = unpack_pairs(npairs, sl, tl, si, ti);
+  return c;
+}
+void sqf_corpus_free(void* c) { delete static_cast<Corpus*>(c); }
+
+int sqf_make_batches(void* corpus, int64_t max_tokens, int max_sentences, uint64_t seed, int32_t* nbatches,
+                     int32_t* sizes, int32_t* members) {
+  SQF_GUARD({
+    const auto& pairs = static_cast<Corpus*>(corpus)->pairs;
+    EpochPlan p = make_batches(pairs, max_tokens, max_sentences > 0 ? std::optional<int>(max_sentences) : std::nullopt,
+                               seed);
+    *nbatches = int32_t(p.batches.size());
+    int64_t k = 0;
+    for (size_t b = 0; b < p.batches.size(); ++b) {
+      sizes[b] = int32_t(p.batches[b].size());
+      for (int m : p.batches[b]) members[k++] = m;
+    }
+  })
+}
+
+int sqf_shuffle_epoch(int nbatches, uint64_t seed, int epoch, int32_t* order) {
+  SQF_GUARD({
+    EpochPlan p;
+    p.batches.resize(size_t(nbatches));
+    p.shuffle_seed = seed;
+    auto o = shuffle_epoch(p, epoch);
+    std::copy(o.begin(), o.end(), order);
+  })
+}
+
+int sqf_make_minibatch(void* corpus, const int32_t* members, int n, int32_t* dims, int32_t* source,
+                       int32_t* target_in, int32_t* target_out, int32_t* src_lens, int32_t* tgt_lens,
+                       int64_t* ntokens) {
+  SQF_GUARD({
+    MiniBatch b = make_minibatch(static_cast<Corpus*>(corpus)->pairs, std::vector<int>(members, members + n));
+    dims[0] = b.rows;
+    dims[1] = b.src_width;
+    dims[2] = b.tgt_width;
+    if (source) std::copy(b.source.begin(), b.source.end(), source);
+    if (target_in) std::copy(b.target_in.begin(), b.target_in.end(), target_in);
+    if (target_out) std::copy(b.target_out.begin(), b.target_out.end(), target_out);
+    if (src_lens) std::copy(b.src_lens.begin(), b.src_lens.end(), src_lens);
+    if (tgt_lens) std::copy(b.tgt_lens.begin(), b.tgt_lens.end(), tgt_lens);
+    if (ntokens) *ntokens = b.ntokens;
+  })
+}
+
+int sqf_split_counts(int rows, int workers, int accum, int32_t* counts) {
+  SQF_GUARD({
+    const int groups = workers * accum;
+    if (groups < 1) throw ConfigError("split: workers and accum must be at least 1");
+    for (int g = 0; g < groups; ++g) counts[g] = rows / groups + (g < rows % groups ? 1 : 0);
+  })
+}
+
+int sqf_bucket_gradients(const int64_t* sizes, int n, int64_t threshold, int32_t* nbuckets, int64_t* starts,
+                         int64_t* ends) {
+  SQF_GUARD({
+    auto b = bucket_gradients(std::vector<int64_t>(sizes, sizes + n), threshold);
+    *nbuckets = int32_t(b.size());
+    for (size_t i = 0; i < b.size(); ++i) {
+      starts[i] = b[i].start;
+      ends[i] = b[i].end;
+    }
+  })
+}
+
+int sqf_model_init(const char* arch, const char* const* keys, const char* const* vals, int n, float* params,
+                   int64_t cap, int64_t* num_params, int* manifest_size) {
+  SQF_GUARD({
+    const Registry& reg = global_registry();
+    Config cfg = reg.resolve_architecture(arch, user_kv(keys, vals, n));
+    auto m = reg.make_model(reg.architecture(cfg.get_str("arch")).base_model, cfg,
+                            uint64_t(cfg.get_int("seed")));
+    *num_params = m->num_params();
+    *manifest_size = int(m->manifest().size());
+    if (params && cap >= m->num_params()) std::memcpy(params, m->params().data(), size_t(m->num_params()) * 4);
+  })
+}
+
+int sqf_scaler_run(double init, int64_t window, double mn, double mx, const uint8_t* overflow, int n,
+                   double* scales, int32_t* diverged_at) {
+  SQF_GUARD({
+    LossScaler s(init, window, mn, mx);
+    *diverged_at = -1;
+    for (int i = 0; i < n; ++i) {
+      try {
+        s.update(overflow[i] != 0);
+      } catch (const DivergenceError&) {
+        *diverged_at = i;
+        return 0;
+      }
+      scales[i] = s.scale();
+    }
+  })
+}
+
+int sqf_schedule_lr(const char* name, double base, int64_t warmup, double init, double eta_min, int64_t period,
+                    double t_mult, int64_t step, double* out) {
+  SQF_GUARD({
+    Config c = engine_default_config();
+    c.set_user("lr", base);
+    c.set_user("warmup", warmup);
+    c.set_user("warmup_init_lr", init);
+    c.set_user("eta_min", eta_min);
+    c.set_user("cosine_period", period);
+    c.set_user("cosine_t_mult", t_mult);
+    *out = global_registry().make_scheduler(name, c)->lr(step);
+  })
+}
+
+float sqf_quantize_fp16(float x) { return quantize_fp16(x); }
+
+}  // extern "C"

@@ -1,0 +1,411 @@
+#include "device_tape.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+
+namespace sqf {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void sfk_check(int status, const char* what) {
+  if (status != SFK_OK) throw DeviceError(std::string(what) + " failed: " + sfk_last_error());
+}
+
+// ------------------------------------------------------------------ arena
+Arena::~Arena() {
+  for (auto& c : chunks_) cudaFree(c.base);
+}
+
+void* Arena::alloc(size_t bytes) {
+  bytes = (bytes + 255) & ~size_t(255);
+  while (cur_ < chunks_.size() && chunks_[cur_].used + bytes > chunks_[cur_].size) ++cur_;
+  if (cur_ == chunks_.size()) {
+    size_t sz = std::max(bytes, size_t(256) << 20);
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, sz), "arena cudaMalloc");
+    chunks_.push_back({static_cast<char*>(p), sz, 0});
+  }
+  Chunk& c = chunks_[cur_];
+  void* out = c.base + c.used;
+  c.used += bytes;
+  return out;
+}
+
+void Arena::reset() {
+  for (auto& c : chunks_) c.used = 0;
+  cur_ = 0;
+}
+
+size_t Arena::capacity() const {
+  size_t s = 0;
+  for (const auto& c : chunks_) s += c.size;
+  return s;
+}
+
+// ------------------------------------------------------------------ batch packing
+namespace {
+// recording-order segments for the embedding backward: unique ids ascending,
+// each with its rows in ascending (= recording) order
+void build_segments(const std::vector<int>& ids, std::vector<int32_t>& uniq, std::vector<int32_t>& off,
+                    std::vector<int32_t>& rows) {
+  std::vector<int32_t> order(ids.size());
+  for (size_t i = 0; i < ids.size(); ++i) order[i] = int32_t(i);
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return ids[a] < ids[b]; });
+  uniq.clear();
+  off.clear();
+  rows.assign(order.begin(), order.end());
+  for (size_t i = 0; i < order.size(); ++i) {
+    if (i == 0 || ids[order[i]] != ids[order[i - 1]]) {
+      uniq.push_back(ids[order[i]]);
+      off.push_back(int32_t(i));
+    }
+  }
+  off.push_back(int32_t(order.size()));
+}
+}  // namespace
+
+PackedBatch PackedBatch::pack(const MiniBatch& b) {
+  PackedBatch p;
+  p.rows = b.rows;
+  p.src_width = b.src_width;
+  p.tgt_width = b.tgt_width;
+  p.ntokens = b.ntokens;
+  std::vector<int32_t> su, so, sr, tu, to, tr;
+  build_segments(b.source, su, so, sr);
+  build_segments(b.target_in, tu, to, tr);
+  auto put = [&](const auto& v) {
+    const size_t at = p.blob.size();
+    p.blob.insert(p.blob.end(), v.begin(), v.end());
+    // keep every section 16-byte aligned
+    while (p.blob.size() % 4) p.blob.push_back(0);
+    return at;
+  };
+  p.off_source = put(b.source);
+  p.off_tin = put(b.target_in);
+  p.off_tout = put(b.target_out);
+  p.off_slens = put(b.src_lens);
+  p.off_su = put(su);
+  p.off_so = put(so);
+  p.off_sr = put(sr);
+  p.off_tu = put(tu);
+  p.off_to = put(to);
+  p.off_tr = put(tr);
+  p.n_su = int(su.size());
+  p.n_tu = int(tu.size());
+  return p;
+}
+
+DeviceBatch PackedBatch::bind(const int32_t* d) const {
+  DeviceBatch b;
+  b.rows = rows;
+  b.src_width = src_width;
+  b.tgt_width = tgt_width;
+  b.ntokens = ntokens;
+  b.source = d + off_source;
+  b.target_in = d + off_tin;
+  b.target_out = d + off_tout;
+  b.src_lens = d + off_slens;
+  b.src_segs = {d + off_su, d + off_so, d + off_sr, n_su};
+  b.tgt_segs = {d + off_tu, d + off_to, d + off_tr, n_tu};
+  return b;
+}
+
+// ------------------------------------------------------------------ tape
+DeviceTape::DeviceTape(Arena& arena, const DeviceParams& params, int dtype, cudaStream_t stream)
+    : arena_(arena), params_(params), dtype_(dtype), esize_(dtype == SFK_F32 ? 4 : 2), stream_(stream) {}
+
+int DeviceTape::embedding(ParamRef table, const int32_t* ids, int rows, int width, float scale, const float* pe,
+                          const DeviceBatch::Segs& segs) {
+  Node n;
+  n.kind = Kind::Embedding;
+  n.p0 = table;
+  n.ids = ids;
+  n.rows = rows;
+  n.cols = table.cols;
+  n.width = width;
+  n.scale = scale;
+  n.segs = segs;
+  n.out = alloc_elems(int64_t(rows) * n.cols);
+  sfk_check(sfk_embed_fwd(dtype_, ids, rows, width, n.cols, pptr(table), pe, scale, n.out, stream_), "embed_fwd");
+  ++launches_;
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
+int DeviceTape::layer_norm(int x, ParamRef gamma, ParamRef beta) {
+  const Node& in = nodes_[x];
+  if (gamma.cols != in.cols || beta.cols != in.cols) throw ShapeError("layer_norm: affine parameter length mismatch");
+  Node n;
+  n.kind = Kind::LayerNorm;
+  n.in0 = x;
+  n.p0 = gamma;
+  n.p1 = beta;
+  n.rows = in.rows;
+  n.cols = in.cols;
+  n.out = alloc_elems(int64_t(n.rows) * n.cols);
+  n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * 8));
+  sfk_check(sfk_layernorm_fwd(dtype_, in.out, n.rows, n.cols, pptr(gamma), pptr(beta), n.out, n.stats, stream_),
+            "layernorm_fwd");
+  ++launches_;
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
+void DeviceTape::gemm(int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
+                      bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias, const void* res, int64_t ldr,
+                      const void* mask, int64_t ldm) {
+  sfk_gemm_args g{};
+  g.m = m;
+  g.n = n;
+  g.k = k;
+  g.dtype = dtype_;
+  g.a = a;
+  g.lda = lda;
+  g.a_kmajor = a_kmajor;
+  g.b = b;
+  g.ldb = ldb;
+  g.b_kmajor = b_kmajor;
+  g.c = c;
+  g.ldc = ldc;
+  g.bias = bias;
+  g.res = res;
+  g.ldr = ldr;
+  g.mask = mask;
+  g.ldm = ldm;
+  g.flags = flags;
+  sfk_check(sfk_gemm(&g, stream_), "gemm");
+  ++launches_;
+}
+
+int DeviceTape::linear(int x, ParamRef w, const ParamRef* bias, bool relu, int residual) {
+  const Node& in = nodes_[x];
+  if (in.cols != w.cols) throw ShapeError("matmul_nt: inner dimension mismatch");
+  if (bias && (bias->cols != w.rows || bias->rows != 1)) throw ShapeError("add_bias: bias length mismatch");
+  Node n;
+  n.kind = Kind::Linear;
+  n.in0 = x;
+  n.in1 = residual;
+  n.p0 = w;
+  if (bias) n.p1 = *bias;
+  n.has_bias = bias != nullptr;
+  n.relu = relu;
+  n.rows = in.rows;
+  n.cols = w.rows;
+  if (residual >= 0 && (nodes_[residual].rows != n.rows || nodes_[residual].cols != n.cols))
+    throw ShapeError("add: shape mismatch");
+  n.out = alloc_elems(int64_t(n.rows) * n.cols);
+  int flags = SFK_EPI_PREROUND;
+  if (bias) flags |= SFK_EPI_BIAS;
+  if (relu) flags |= SFK_EPI_RELU;
+  if (residual >= 0) flags |= SFK_EPI_RESIDUAL;
+  gemm(n.rows, n.cols, in.cols, in.out, in.cols, true, pptr(w), w.cols, true, n.out, n.cols, flags,
+       bias ? pptr(*bias) : nullptr, residual >= 0 ? nodes_[residual].out : nullptr, n.cols);
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
+int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
+                          int k_width, bool causal, const int32_t* k_len) {
+  if (heads <= 0 || d % heads != 0) throw ShapeError("attention: d_model not divisible by heads");
+  const Node& qn = nodes_[q];
+  const Node& kn = nodes_[kv];
+  if (qn.rows != batch * q_width || kn.rows != batch * k_width) throw ShapeError("attention: span layout mismatch");
+  Node n;
+  n.kind = Kind::Attention;
+  n.in0 = q;
+  n.in1 = kv;
+  n.q_col = q_col;
+  n.k_col = k_col;
+  n.v_col = v_col;
+  n.heads = heads;
+  n.batch = batch;
+  n.q_width = q_width;
+  n.k_width = k_width;
+  n.causal = causal;
+  n.k_len = k_len;
+  n.rows = qn.rows;
+  n.cols = d;
+  n.out = alloc_elems(int64_t(n.rows) * d);
+  n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * heads * 8));
+  sfk_attn_args a{};
+  a.dtype = dtype_;
+  a.batch = batch;
+  a.q_width = q_width;
+  a.k_width = k_width;
+  a.heads = heads;
+  a.dh = d / heads;
+  a.causal = causal;
+  a.k_len = k_len;
+  a.q = static_cast<const char*>(qn.out) + q_col * esize_;
+  a.ldq = qn.cols;
+  a.k = static_cast<const char*>(kn.out) + k_col * esize_;
+  a.ldk = kn.cols;
+  a.v = static_cast<const char*>(kn.out) + v_col * esize_;
+  a.ldv = kn.cols;
+  a.o = n.out;
+  a.ldo = d;
+  a.stats = n.stats;
+  sfk_check(sfk_attention_fwd(&a, stream_), "attention_fwd");
+  ++launches_;
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
+int DeviceTape::softmax_xent(int logits, const int32_t* gold, float epsilon) {
+  if (epsilon < 0.f || epsilon >= 1.f) throw ConfigError("softmax_xent: epsilon must be in [0, 1)");
+  Node n;
+  n.kind = Kind::Xent;
+  n.in0 = logits;
+  n.gold = gold;
+  n.eps = epsilon;
+  n.rows = nodes_[logits].rows;
+  n.cols = 1;
+  n.row_out = static_cast<float*>(arena_.alloc(size_t(n.rows) * 16));
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
+std::pair<void*, bool> DeviceTape::grad_of(int id) {
+  Node& n = nodes_[id];
+  if (n.grad) return {n.grad, false};
+  n.grad = alloc_elems(int64_t(n.rows) * n.cols);
+  return {n.grad, true};
+}
+
+void DeviceTape::run_xent(Node& n, float seed, bool with_grad, double* stats_acc) {
+  Node& lg = nodes_[n.in0];
+  // the logits buffer becomes its own gradient (dlogits written in place)
+  sfk_check(sfk_xent_fwd_bwd(dtype_, lg.out, lg.rows, lg.cols, lg.cols, n.gold, kPad, n.eps, seed,
+                             with_grad ? lg.out : nullptr, n.row_out, stream_),
+            "xent");
+  sfk_check(sfk_xent_reduce(n.row_out, n.rows, stats_acc, stream_), "xent_reduce");
+  launches_ += 2;
+  if (with_grad) lg.grad = lg.out;
+}
+
+void DeviceTape::finish(int loss_node, double* stats_acc) {
+  Node& n = nodes_.at(loss_node);
+  if (n.kind != Kind::Xent) throw ShapeError("finish: loss node must be a softmax_xent node");
+  run_xent(n, 0.f, false, stats_acc);
+}
+
+void DeviceTape::backward(int loss_node, float seed, double* stats_acc) {
+  if (loss_node < 0 || loss_node >= int(nodes_.size())) throw BoundsError("backward: bad node id");
+  Node& n = nodes_[loss_node];
+  if (n.kind != Kind::Xent) throw ShapeError("backward: loss node must be a softmax_xent node");
+  run_xent(n, seed, true, stats_acc);
+  for (int i = loss_node - 1; i >= 0; --i) backward_node(i);
+}
+
+void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out) {
+  const int max_parts = 64;
+  float* part = static_cast<float*>(arena_.alloc(size_t(max_parts) * cols * 4));
+  int nparts = 0;
+  sfk_check(sfk_colsum_partial(dtype_, dy, rows, cols, ld, part, &nparts, stream_), "colsum_partial");
+  sfk_check(sfk_colsum_finish(dtype_, part, nparts, cols, out, stream_), "colsum_finish");
+  launches_ += 2;
+}
+
+void DeviceTape::backward_node(int id) {
+  Node& n = nodes_[id];
+  if (!n.grad) return;  // no consumer contributed (e.g. unused branch)
+  switch (n.kind) {
+    case Kind::Xent:
+      return;
+    case Kind::Embedding: {
+      sfk_check(sfk_embed_bwd(dtype_, n.segs.uniq, n.segs.off, n.segs.rows, n.segs.n, n.cols, n.grad, n.scale,
+                              gptr(n.p0), stream_),
+                "embed_bwd");
+      ++launches_;
+      return;
+    }
+    case Kind::LayerNorm: {
+      const Node& in = nodes_[n.in0];
+      auto [dx, fresh] = grad_of(n.in0);
+      const int max_parts = 296;
+      float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
+      int nparts = 0;
+      sfk_check(sfk_layernorm_bwd(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx, fresh ? 0 : 1,
+                                  part, &nparts, stream_),
+                "layernorm_bwd");
+      sfk_check(sfk_colsum_finish(dtype_, part, nparts, n.cols, gptr(n.p0), stream_),
+                "ln dgamma");
+      sfk_check(sfk_colsum_finish(dtype_, part + size_t(nparts) * n.cols, nparts, n.cols, gptr(n.p1), stream_),
+                "ln dbeta");
+      launches_ += 3;
+      return;
+    }
+    case Kind::Linear: {
+      const Node& in = nodes_[n.in0];
+      void* dy = n.grad;
+      // residual add: the residual input receives dy unchanged; alias when fresh
+      if (n.in1 >= 0) {
+        Node& r = nodes_[n.in1];
+        if (!r.grad) {
+          r.grad = dy;
+        } else {
+          throw ShapeError("linear: residual input already has a gradient (unsupported fan-out)");
+        }
+      }
+      if (n.has_bias) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
+      // dgrad into the input; a relu input gets the masked (pre-activation) grad
+      Node& inm = nodes_[n.in0];
+      auto [dx, fresh] = grad_of(n.in0);
+      int flags = fresh ? 0 : SFK_EPI_ACCUM;
+      const void* mask = nullptr;
+      if (inm.kind == Kind::Linear && inm.relu) {
+        if (!fresh) throw ShapeError("linear: relu output with several consumers is unsupported");
+        flags = SFK_EPI_MASK;
+        mask = inm.out;
+        inm.grad_masked = true;
+      }
+      gemm(n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols, flags, nullptr,
+           nullptr, 0, mask, in.cols);
+      // wgrad: dW += dy^T x
+      gemm(n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0), n.p0.cols, SFK_EPI_ACCUM);
+      return;
+    }
+    case Kind::Attention: {
+      const Node& qn = nodes_[n.in0];
+      const Node& kn = nodes_[n.in1];
+      auto [dq, fq] = grad_of(n.in0);
+      auto [dkv, fkv] = grad_of(n.in1);
+      if (!fq || (!fkv && n.in0 != n.in1))
+        throw ShapeError("attention: q/k/v inputs must not have other consumers");
+      sfk_attn_args a{};
+      a.dtype = dtype_;
+      a.batch = n.batch;
+      a.q_width = n.q_width;
+      a.k_width = n.k_width;
+      a.heads = n.heads;
+      a.dh = n.cols / n.heads;
+      a.causal = n.causal;
+      a.k_len = n.k_len;
+      a.q = static_cast<const char*>(qn.out) + n.q_col * esize_;
+      a.ldq = qn.cols;
+      a.k = static_cast<const char*>(kn.out) + n.k_col * esize_;
+      a.ldk = kn.cols;
+      a.v = static_cast<const char*>(kn.out) + n.v_col * esize_;
+      a.ldv = kn.cols;
+      a.o = n.out;
+      a.ldo = n.cols;
+      a.stats = n.stats;
+      a.dout = n.grad;
+      a.lddo = n.cols;
+      a.dq = static_cast<char*>(dq) + n.q_col * esize_;
+      a.lddq = qn.cols;
+      a.dk = static_cast<char*>(dkv) + n.k_col * esize_;
+      a.lddk = kn.cols;
+      a.dv = static_cast<char*>(dkv) + n.v_col * esize_;
+      a.lddv = kn.cols;
+      a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
+      sfk_check(sfk_attention_bwd(&a, stream_), "attention_bwd");
+      launches_ += 2;
+      return;
+    }
+  }
+}
+
+}  // namespace sqf

@@ -1,0 +1,157 @@
+// Device tape: records the forward of one sub-batch as sm_100a kernel launches
+// and replays the exact reverse order for backward, mirroring the reference's
+// Tape contract (tape.hpp:63-108): node outputs are kept for backward,
+// activation gradients accumulate per node, parameter gradients accumulate
+// into a caller-owned flat buffer that the tape never zeroes (the basis of
+// `accum`/update_freq delayed updates).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../../include/sqf_kernels.h"
+#include "plugins.hpp"
+
+namespace sqf {
+
+void cuda_check(cudaError_t e, const char* what);
+void sfk_check(int status, const char* what);
+
+// Bump allocator over a few large cudaMalloc chunks; reset() once per
+// sub-batch. Allocation order is deterministic so steady state never grows.
+class Arena {
+ public:
+  ~Arena();
+  void* alloc(size_t bytes);
+  void reset();
+  size_t capacity() const;
+
+ private:
+  struct Chunk {
+    char* base;
+    size_t size, used;
+  };
+  std::vector<Chunk> chunks_;
+  size_t cur_ = 0;
+};
+
+// One sub-batch resident on the device (ids, lengths, embedding-backward segments).
+struct DeviceBatch {
+  int rows = 0, src_width = 0, tgt_width = 0;
+  int64_t ntokens = 0;
+  const int32_t* source = nullptr;      // rows x S
+  const int32_t* target_in = nullptr;   // rows x T
+  const int32_t* target_out = nullptr;  // rows x T
+  const int32_t* src_lens = nullptr;    // rows
+  struct Segs {
+    const int32_t* uniq = nullptr;
+    const int32_t* off = nullptr;
+    const int32_t* rows = nullptr;
+    int n = 0;
+  } src_segs, tgt_segs;
+};
+
+// Host-side packing of a MiniBatch into one int32 blob (uploaded with a single
+// cudaMemcpyAsync); returns the element count. bind() turns a device copy of
+// the blob into a DeviceBatch.
+struct PackedBatch {
+  std::vector<int32_t> blob;
+  int rows = 0, src_width = 0, tgt_width = 0;
+  int64_t ntokens = 0;
+  size_t off_source = 0, off_tin = 0, off_tout = 0, off_slens = 0;
+  size_t off_su = 0, off_so = 0, off_sr = 0, off_tu = 0, off_to = 0, off_tr = 0;
+  int n_su = 0, n_tu = 0;
+  static PackedBatch pack(const MiniBatch& b);
+  DeviceBatch bind(const int32_t* dev_blob) const;
+};
+
+struct DeviceParams {
+  float* master = nullptr;   // fp32 master (device order)
+  void* compute = nullptr;   // parameters the kernels read (== master in fp32 mode)
+  void* grad = nullptr;      // flat gradient accumulator (caller owned)
+  int64_t n = 0;
+};
+
+class DeviceTape {
+ public:
+  enum class Kind { Embedding, LayerNorm, Linear, Attention, Xent };
+
+  DeviceTape(Arena& arena, const DeviceParams& params, int dtype, cudaStream_t stream);
+
+  // a8: out = q(q(E[ids]) * scale) + q(pe[pos]) ; rows = batch*width
+  int embedding(ParamRef table, const int32_t* ids, int rows, int width, float scale, const float* pe,
+                const DeviceBatch::Segs& segs);
+  // a14
+  int layer_norm(int x, ParamRef gamma, ParamRef beta);
+  // a9 (+a11 bias, a12 relu, a13 residual add): y = [res +] [relu](x W^T [+ b])
+  int linear(int x, ParamRef w, const ParamRef* bias, bool relu, int residual = -1);
+  // a16: q/k/v are column slices [q_col, q_col+d) of node q and [k_col..), [v_col..) of node kv
+  int attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
+                int k_width, bool causal, const int32_t* k_len);
+  // a18: records the loss node; stats are produced when backward()/finish() runs
+  int softmax_xent(int logits, const int32_t* gold, float epsilon);
+
+  // Seeds d(loss_row) = seed on active rows (tape.cpp:506-516), runs the fused
+  // xent fwd+bwd and sweeps nodes in exact reverse order.
+  void backward(int loss_node, float seed, double* stats_acc);
+  // forward-only loss statistics (evaluate)
+  void finish(int loss_node, double* stats_acc);
+
+  int dtype() const { return dtype_; }
+  size_t size() const { return nodes_.size(); }
+  int rows(int id) const { return nodes_[id].rows; }
+  int cols(int id) const { return nodes_[id].cols; }
+  const void* out(int id) const { return nodes_[id].out; }
+  // number of our kernels launched so far (bench evidence)
+  int64_t launches() const { return launches_; }
+
+ private:
+  struct Node {
+    Kind kind;
+    int in0 = -1, in1 = -1, in2 = -1;
+    ParamRef p0{}, p1{};
+    bool has_bias = false, relu = false, causal = false;
+    int rows = 0, cols = 0;
+    void* out = nullptr;
+    void* grad = nullptr;
+    bool grad_masked = false;  // relu node: grad already holds d(pre-activation)
+    float* stats = nullptr;    // LN: (mean,rstd); attention: (max,1/sum)
+    // embedding
+    const int32_t* ids = nullptr;
+    int width = 0;
+    float scale = 1.f;
+    DeviceBatch::Segs segs;
+    // attention
+    int q_col = 0, k_col = 0, v_col = 0, heads = 0, batch = 0, q_width = 0, k_width = 0;
+    const int32_t* k_len = nullptr;
+    // xent
+    const int32_t* gold = nullptr;
+    float eps = 0.f;
+    float* row_out = nullptr;
+  };
+
+  Arena& arena_;
+  DeviceParams params_;
+  int dtype_;
+  size_t esize_;
+  cudaStream_t stream_;
+  std::vector<Node> nodes_;
+  int64_t launches_ = 0;
+
+  void* alloc_elems(int64_t n) { return arena_.alloc(size_t(n) * esize_); }
+  void* pptr(const ParamRef& p) const { return static_cast<char*>(params_.compute) + p.offset * esize_; }
+  void* gptr(const ParamRef& p) const { return static_cast<char*>(params_.grad) + p.offset * esize_; }
+  // gradient buffer of node `id`: returns {ptr, fresh}; allocates on first use
+  std::pair<void*, bool> grad_of(int id);
+  void backward_node(int id);
+  void run_xent(Node& n, float seed, bool with_grad, double* stats_acc);
+  void gemm(int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
+            bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias = nullptr, const void* res = nullptr,
+            int64_t ldr = 0, const void* mask = nullptr, int64_t ldm = 0);
+  void bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out);
+};
+
+}  // namespace sqf

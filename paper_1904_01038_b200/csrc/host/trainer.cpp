@@ -1,0 +1,376 @@
+#include "trainer.hpp"
+
+#include "nccl_dyn.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace sqf {
+
+void set_model_position_table(ModelBase& m, const float* dev);
+
+namespace {
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw DeviceError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
+}
+ncclDataType_t nccl_type(int dtype) {
+  return dtype == SFK_F32 ? ncclFloat32 : dtype == SFK_F16 ? ncclFloat16 : ncclBfloat16;
+}
+}  // namespace
+
+Trainer::Trainer(const Config& cfg, const Registry& reg, std::unique_ptr<TaskBase> task, int rank, int world,
+                 const ncclUniqueId* nccl_id)
+    : cfg_(cfg), task_(std::move(task)), rank_(rank), world_(world) {
+  if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw ConfigError("trainer: bad rank/world");
+  if (!task_) task_ = reg.make_task(cfg_.get_str("task"), cfg_);
+  if (world_ > 1) {
+    if (!nccl_id) throw ConfigError("trainer: world > 1 needs an NCCL unique id");
+    nccl_check(NcclApi::get().CommInitRank(&comm_, world_, *nccl_id, rank_), "ncclCommInitRank");
+  }
+  init(reg);
+}
+
+Trainer::~Trainer() {
+  if (comm_) NcclApi::get().CommDestroy(comm_);
+  cudaFree(master_);
+  if (compute_ != master_) cudaFree(compute_);
+  for (void* g : grads_) cudaFree(g);
+  cudaFree(pe_);
+  cudaFree(stats_dev_);
+  cudaFree(flag_dev_);
+  cudaFree(blob_dev_);
+  cudaFreeHost(blob_host_);
+  cudaFreeHost(readback_host_);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Trainer::init(const Registry& reg) {
+  workers_ = int(cfg_.get_int("workers"));
+  accum_ = int(cfg_.get_int("accum"));
+  if (workers_ < 1 || accum_ < 1) throw ConfigError("trainer: workers and accum must be at least 1");
+  if (workers_ % world_ != 0) throw ConfigError("trainer: workers must be a multiple of the process count");
+  local_ = workers_ / world_;
+  fp16_ = cfg_.get_bool("fp16");
+  bf16_ = cfg_.get_bool("bf16");
+  if (fp16_ && bf16_) throw ConfigError("trainer: fp16 and bf16 are exclusive");
+  dtype_ = fp16_ ? SFK_F16 : bf16_ ? SFK_BF16 : SFK_F32;
+  max_epochs_ = int(cfg_.get_int("max_epochs"));
+  if (max_epochs_ < 1) throw ConfigError("trainer: max_epochs must be at least 1");
+  seed_ = uint64_t(cfg_.get_int("seed"));
+  const std::string dispatch = cfg_.get_str("dispatch");
+  if (dispatch != "split" && dispatch != "deal") throw ConfigError("trainer: dispatch must be split or deal");
+  deal_ = dispatch == "deal";
+
+  if (cfg_.get_int("src_vocab") == 0) cfg_.set_user("src_vocab", int64_t(task_->source_vocab()));
+  if (cfg_.get_int("tgt_vocab") == 0) cfg_.set_user("tgt_vocab", int64_t(task_->target_vocab()));
+
+  model_ = reg.make_model(reg.architecture(cfg_.get_str("arch")).base_model, cfg_, seed_);
+  criterion_ = reg.make_criterion(cfg_.get_str("criterion"), cfg_);
+  optimizer_ = reg.make_optimizer(cfg_.get_str("optimizer"), cfg_, model_->num_params());
+  scheduler_ = reg.make_scheduler(cfg_.get_str("scheduler"), cfg_);
+  if (fp16_)
+    scaler_ = std::make_unique<LossScaler>(cfg_.get_real("fp16_init_scale"), cfg_.get_int("fp16_scale_window"),
+                                           cfg_.get_real("fp16_min_scale"), cfg_.get_real("fp16_max_scale"));
+
+  // buckets over the device order (sizes of manifest entries sorted by device offset)
+  std::vector<std::pair<int64_t, int64_t>> dev;
+  for (const auto& e : model_->manifest()) dev.emplace_back(e.device_offset, e.numel);
+  std::sort(dev.begin(), dev.end());
+  std::vector<int64_t> sizes;
+  for (auto& p : dev) sizes.push_back(p.second);
+  buckets_ = bucket_gradients(sizes, cfg_.get_int("bucket_threshold"));
+
+  const int64_t ms = cfg_.get_int("max_sentences");
+  // deal dispatch packs at the per-replica budget; split packs one global batch
+  plan_ = make_batches(task_->train_pairs(), cfg_.get_int("max_tokens"),
+                       ms > 0 ? std::optional<int>(int(ms)) : std::nullopt, seed_);
+  epoch_ = 1;
+  pos_ = 0;
+  order_ = plan_.batches.empty() ? std::vector<int>{} : shuffle_epoch(plan_, 1);
+
+  // device state
+  n_ = model_->num_params();
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaEventCreate(&ev0_), "event");
+  cuda_check(cudaEventCreate(&ev1_), "event");
+  cuda_check(cudaMalloc(&master_, size_t(n_) * 4), "master");
+  if (dtype_ == SFK_F32) {
+    compute_ = master_;
+  } else {
+    cuda_check(cudaMalloc(&compute_, size_t(n_) * 2), "shadow");
+  }
+  for (int i = 0; i < local_; ++i) {
+    void* g = nullptr;
+    cuda_check(cudaMalloc(&g, size_t(n_) * esize()), "grads");
+    grads_.push_back(g);
+  }
+  const std::vector<float> pe = model_->position_table();
+  if (!pe.empty()) {
+    cuda_check(cudaMalloc(&pe_, pe.size() * 4), "pe");
+    cuda_check(cudaMemcpy(pe_, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice), "pe upload");
+    set_model_position_table(*model_, pe_);
+  }
+  cuda_check(cudaMalloc(&stats_dev_, 4 * sizeof(double)), "stats");
+  cuda_check(cudaMalloc(&flag_dev_, 16), "flag");
+  cuda_check(cudaMallocHost(&readback_host_, 64), "readback");
+  push_params();
+}
+
+const LossScaler& Trainer::scaler() const {
+  if (!scaler_) throw ConfigError("trainer: loss scaler exists only in fp16 mode");
+  return *scaler_;
+}
+
+void Trainer::push_params() {
+  std::vector<float> dev(static_cast<size_t>(n_));
+  model_->to_device_order(model_->params(), dev);
+  cuda_check(cudaMemcpy(master_, dev.data(), size_t(n_) * 4, cudaMemcpyHostToDevice), "params upload");
+  rebroadcast();
+}
+
+void Trainer::rebroadcast() {
+  // trainer.cpp:149-156: replicas = quantised master; every rank holds the same
+  // master (identical reduced grads -> identical updates), so no traffic
+  if (compute_ != master_) sfk_check(sfk_cast(master_, compute_, dtype_, n_, stream_), "rebroadcast");
+  cuda_check(cudaStreamSynchronize(stream_), "rebroadcast sync");
+}
+
+void Trainer::pull_params() {
+  std::vector<float> dev(static_cast<size_t>(n_));
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  cuda_check(cudaMemcpy(dev.data(), master_, size_t(n_) * 4, cudaMemcpyDeviceToHost), "params download");
+  model_->to_canonical_order(dev, model_->params());
+}
+
+std::vector<float> Trainer::reduced_grads() {
+  std::vector<float> devf(static_cast<size_t>(n_));
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (dtype_ == SFK_F32) {
+    cuda_check(cudaMemcpy(devf.data(), grads_[0], size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
+  } else {
+    float* tmp = nullptr;
+    cuda_check(cudaMalloc(&tmp, size_t(n_) * 4), "grads tmp");
+    sfk_check(sfk_convert(dtype_, grads_[0], SFK_F32, tmp, n_, stream_), "grads convert");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    cuda_check(cudaMemcpy(devf.data(), tmp, size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
+    cudaFree(tmp);
+  }
+  std::vector<float> out(static_cast<size_t>(n_));
+  model_->to_canonical_order(devf, out);
+  return out;
+}
+
+void Trainer::restore_progress(int64_t step, int epoch, int cursor) {
+  if (step < 0 || epoch < 1 || cursor < 0 || cursor > int(plan_.batches.size()))
+    throw IntegrityError("trainer: restored progress out of range");
+  step_ = step;
+  epoch_ = epoch;
+  pos_ = cursor;
+  order_ = plan_.batches.empty() ? std::vector<int>{} : shuffle_epoch(plan_, epoch_);
+}
+
+void Trainer::restore_scaler(double scale, int64_t successes) {
+  if (!scaler_) throw IntegrityError("trainer: scaler state present but fp16 is off");
+  scaler_->restore(scale, successes);
+}
+
+std::optional<MiniBatch> Trainer::next_batch() {
+  // trainer.cpp:173-184
+  if (plan_.batches.empty()) return std::nullopt;
+  if (pos_ >= int(order_.size())) {
+    if (epoch_ >= max_epochs_) return std::nullopt;
+    ++epoch_;
+    order_ = shuffle_epoch(plan_, epoch_);
+    pos_ = 0;
+  }
+  const std::vector<int>& members = plan_.batches[size_t(order_[size_t(pos_)])];
+  ++pos_;
+  return make_minibatch(task_->train_pairs(), members);
+}
+
+std::optional<StepStats> Trainer::train_one() {
+  if (!deal_) {
+    std::optional<MiniBatch> b = next_batch();
+    if (!b) return std::nullopt;
+    return train_step(split_batch(task_->train_pairs(), *b, workers_, accum_));
+  }
+  // deal: W*A consecutive per-replica batches of the shuffled plan (fairseq
+  // semantics); replayable on the reference through its train_step
+  std::vector<std::vector<MiniBatch>> sub(static_cast<size_t>(workers_));
+  for (int w = 0; w < workers_; ++w)
+    for (int a = 0; a < accum_; ++a) {
+      std::optional<MiniBatch> b = next_batch();
+      if (!b) {
+        if (w == 0 && a == 0) return std::nullopt;
+        sub[size_t(w)].push_back(MiniBatch{});
+      } else {
+        sub[size_t(w)].push_back(std::move(*b));
+      }
+    }
+  return train_step(sub);
+}
+
+void Trainer::upload(const std::vector<PackedBatch>& packs, std::vector<DeviceBatch>& out) {
+  size_t total = 0;
+  for (const auto& p : packs) total += p.blob.size();
+  if (total == 0) return;
+  if (total > blob_host_cap_) {
+    cudaFreeHost(blob_host_);
+    blob_host_cap_ = total * 2;
+    cuda_check(cudaMallocHost(&blob_host_, blob_host_cap_ * 4), "pinned staging");
+  }
+  if (total > blob_cap_) {
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    cudaFree(blob_dev_);
+    blob_cap_ = total * 2;
+    cuda_check(cudaMalloc(&blob_dev_, blob_cap_ * 4), "batch blob");
+  }
+  size_t at = 0;
+  out.clear();
+  for (const auto& p : packs) {
+    std::memcpy(blob_host_ + at, p.blob.data(), p.blob.size() * 4);
+    out.push_back(p.bind(blob_dev_ + at));
+    at += p.blob.size();
+  }
+  cuda_check(cudaMemcpyAsync(blob_dev_, blob_host_, total * 4, cudaMemcpyHostToDevice, stream_), "batch H2D");
+}
+
+void Trainer::allreduce_grads() {
+  if (world_ <= 1) return;
+  // bucketed all-reduce over NVLink, buckets in reverse device order (the
+  // order backward completes them); same sum on every rank, so every rank
+  // then runs the identical update (no rebroadcast traffic)
+  nccl_check(NcclApi::get().GroupStart(), "group");
+  for (const auto& b : buckets_)
+    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grads_[0]) + b.start * esize(),
+                             static_cast<char*>(grads_[0]) + b.start * esize(), size_t(b.end - b.start),
+                             nccl_type(dtype_), ncclSum, comm_, stream_),
+               "allreduce grads");
+  nccl_check(NcclApi::get().AllReduce(stats_dev_, stats_dev_, 4, ncclFloat64, ncclSum, comm_, stream_), "allreduce stats");
+  nccl_check(NcclApi::get().GroupEnd(), "group");
+}
+
+StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
+  if (int(sub.size()) != workers_) throw ShapeError("train_step: need one sub-batch list per replica");
+  for (const auto& l : sub)
+    if (int(l.size()) != accum_) throw ShapeError("train_step: every replica takes exactly accum sub-batches");
+  const double scale = fp16_ ? scaler_->scale() : 1.0;
+  StepStats stats;
+  stats.step = step_ + 1;
+  if (fp16_) stats.scale = scale;
+  for (const auto& l : sub)
+    for (const auto& b : l) stats.ntokens += b.ntokens;  // == sum of active target rows
+  if (stats.ntokens == 0) throw ShapeError("train_step: zero target tokens in the minibatch");
+
+  // pack + upload this rank's sub-batches in one copy
+  std::vector<PackedBatch> packs;
+  std::vector<std::pair<int, int>> which;
+  for (int lw = 0; lw < local_; ++lw) {
+    const int w = rank_ * local_ + lw;
+    for (int a = 0; a < accum_; ++a) {
+      const MiniBatch& b = sub[size_t(w)][size_t(a)];
+      if (b.rows == 0) continue;
+      packs.push_back(PackedBatch::pack(b));
+      which.emplace_back(lw, a);
+    }
+  }
+  std::vector<DeviceBatch> dev;
+  cuda_check(cudaEventRecord(ev0_, stream_), "event");
+  upload(packs, dev);
+  cuda_check(cudaMemsetAsync(stats_dev_, 0, 4 * sizeof(double), stream_), "stats zero");
+  cuda_check(cudaMemsetAsync(flag_dev_, 0, 4, stream_), "flag zero");
+  for (int lw = 0; lw < local_; ++lw)
+    cuda_check(cudaMemsetAsync(grads_[size_t(lw)], 0, size_t(n_) * esize(), stream_), "grad zero");
+  launches_ = 0;
+  for (size_t i = 0; i < dev.size(); ++i) {
+    const int lw = which[i].first, a = which[i].second;
+    const int w = rank_ * local_ + lw;
+    model_->set_train_step(step_ * workers_ * accum_ + int64_t(w) * accum_ + a);
+    arena_.reset();
+    DeviceTape tape(arena_, DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
+    CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
+    // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
+    tape.backward(out.loss_node, float(scale), stats_dev_);
+    launches_ += tape.launches();
+  }
+  // in-process replicas fold in index order with re-rounding (trainer.cpp:75-87)
+  for (int lw = 1; lw < local_; ++lw) {
+    sfk_check(sfk_accumulate(dtype_, grads_[0], grads_[size_t(lw)], n_, stream_), "replica fold");
+    ++launches_;
+  }
+  allreduce_grads();
+  sfk_check(sfk_nonfinite(dtype_, grads_[0], n_, flag_dev_, stream_), "overflow check");
+  ++launches_;
+
+  const bool injected = fp16_ && injector_ && injector_(stats.step);
+  const double lr = scheduler_->lr(stats.step);
+  const int64_t t_before = optimizer_->step_count();
+  if (!injected) {
+    GradPrep prep;
+    prep.scale = float(scale);
+    prep.unscale = fp16_;
+    prep.ntokens = float(stats.ntokens);
+    prep.skip = flag_dev_;
+    optimizer_->apply(master_, compute_ == master_ ? nullptr : compute_, dtype_, grads_[0], dtype_, n_, lr, prep,
+                      stream_);
+    ++launches_;
+  }
+  char* rb = static_cast<char*>(readback_host_);
+  cuda_check(cudaMemcpyAsync(rb, stats_dev_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_), "stats D2H");
+  cuda_check(cudaMemcpyAsync(rb + 32, flag_dev_, 4, cudaMemcpyDeviceToHost, stream_), "flag D2H");
+  cuda_check(cudaEventRecord(ev1_, stream_), "event");
+  cuda_check(cudaStreamSynchronize(stream_), "step sync");
+  cudaEventElapsedTime(&last_ms_, ev0_, ev1_);
+  const double* st = reinterpret_cast<const double*>(rb);
+  const int32_t flag = *reinterpret_cast<const int32_t*>(rb + 32);
+  stats.loss = st[0];
+  stats.nll = st[1];
+  stats.ncorrect = int64_t(st[3]);
+
+  if (fp16_) {
+    if (flag || injected) {
+      if (!injected) optimizer_->set_step_count(t_before);  // device update was predicated off
+      stats.skipped = true;
+      scaler_->update(true);  // may raise DivergenceError at the floor
+      return stats;
+    }
+  } else if (flag) {
+    optimizer_->set_step_count(t_before);
+    throw DivergenceError("optimizer: non-finite gradient");
+  }
+  stats.lr = lr;
+  step_ = stats.step;
+  if (fp16_) scaler_->update(false);
+  return stats;
+}
+
+EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
+  // trainer.cpp:275-289: teacher-forced scoring on the fp32 master
+  EvalStats out;
+  if (pairs.empty()) return out;
+  EpochPlan plan = make_batches(pairs, cfg_.get_int("max_tokens"), std::nullopt, 0);
+  cuda_check(cudaMemsetAsync(stats_dev_, 0, 4 * sizeof(double), stream_), "stats zero");
+  for (const auto& members : plan.batches) {
+    MiniBatch b = make_minibatch(pairs, members);
+    std::vector<PackedBatch> packs{PackedBatch::pack(b)};
+    std::vector<DeviceBatch> dev;
+    upload(packs, dev);
+    arena_.reset();
+    DeviceTape tape(arena_, DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    CriterionOutput c = criterion_->compute(*model_, dev[0], tape);
+    tape.finish(c.loss_node, stats_dev_);
+    cuda_check(cudaStreamSynchronize(stream_), "eval sync");  // staging buffer reuse
+  }
+  double st[4];
+  cuda_check(cudaMemcpy(st, stats_dev_, sizeof st, cudaMemcpyDeviceToHost), "eval D2H");
+  out.loss = st[0];
+  out.nll = st[1];
+  out.ntokens = int64_t(st[2]);
+  out.ncorrect = int64_t(st[3]);
+  return out;
+}
+
+}  // namespace sqf

@@ -1,0 +1,129 @@
+// B200 data-parallel trainer with the reference's Trainer contract
+// (include/seqforge/trainer.hpp:80-125, src/trainer.cpp:89-289): W replicas x A
+// accumulation, loss-scale seeding of backward, bucketed all-reduce, overflow
+// skip + scaler policy, unscale, / global ntokens, optimizer, rebroadcast.
+//
+// Replica placement: one process per GPU (rank r of `world`), each owning
+// workers/world logical replicas. Within a process the replicas run one after
+// another on its GPU and fold in index order (trainer.cpp:75-87); across
+// processes gradients are summed by bucketed NCCL all-reduce over NVLink.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <functional>
+#include <memory>
+#include <optional>
+
+#include "device_tape.hpp"
+#include "plugins.hpp"
+
+namespace sqf {
+
+struct StepStats {
+  int64_t step = 0;
+  double loss = 0.0, nll = 0.0;
+  int64_t ntokens = 0, ncorrect = 0;
+  double lr = 0.0;
+  bool skipped = false;
+  double scale = 0.0;
+};
+
+struct EvalStats {
+  double loss = 0.0, nll = 0.0;
+  int64_t ntokens = 0, ncorrect = 0;
+};
+
+class Trainer {
+ public:
+  // task == nullptr: the task is made through the registry from cfg["task"]
+  Trainer(const Config& cfg, const Registry& reg, std::unique_ptr<TaskBase> task, int rank = 0, int world = 1,
+          const ncclUniqueId* nccl_id = nullptr);
+  ~Trainer();
+
+  std::optional<StepStats> train_one();
+  StepStats train_step(const std::vector<std::vector<MiniBatch>>& sub);
+  EvalStats evaluate(const std::vector<SequencePair>& pairs);
+
+  int64_t step() const { return step_; }
+  int epoch() const { return epoch_; }
+  int cursor() const { return pos_; }
+  int batches_per_epoch() const { return int(plan_.batches.size()); }
+  int workers() const { return workers_; }
+  int accum() const { return accum_; }
+  bool fp16() const { return fp16_; }
+  const Config& config() const { return cfg_; }
+  ModelBase& model() { return *model_; }
+  OptimizerBase& optimizer() { return *optimizer_; }
+  TaskBase& task() { return *task_; }
+  const LossScaler& scaler() const;
+  const std::vector<GradientBucket>& buckets() const { return buckets_; }
+
+  // host <-> device parameter sync (canonical order)
+  void pull_params();                       // device master -> model().params()
+  void push_params();                       // model().params() -> device master, then rebroadcast
+  void rebroadcast();
+  std::vector<float> reduced_grads();       // last step's reduced gradient, canonical order, as float
+  void restore_progress(int64_t step, int epoch, int cursor);
+  void restore_scaler(double scale, int64_t successes);
+  void set_overflow_injector(std::function<bool(int64_t)> f) { injector_ = std::move(f); }
+
+  int64_t kernel_launches() const { return launches_; }
+  int dtype() const { return dtype_; }
+  cudaStream_t stream() const { return stream_; }
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  // timing hook: events recorded on the compute stream around the last step
+  float last_step_ms() const { return last_ms_; }
+
+ private:
+  Config cfg_;
+  std::unique_ptr<TaskBase> task_;
+  std::unique_ptr<ModelBase> model_;
+  std::unique_ptr<CriterionBase> criterion_;
+  std::unique_ptr<OptimizerBase> optimizer_;
+  std::unique_ptr<SchedulerBase> scheduler_;
+  std::unique_ptr<LossScaler> scaler_;
+
+  int workers_ = 1, accum_ = 1, max_epochs_ = 1;
+  bool fp16_ = false, bf16_ = false, deal_ = false;
+  int dtype_ = SFK_F32;
+  uint64_t seed_ = 1;
+  int rank_ = 0, world_ = 1, local_ = 1;
+
+  // device state (device parameter order)
+  int64_t n_ = 0;
+  float* master_ = nullptr;
+  void* compute_ = nullptr;        // == master_ in fp32 mode
+  std::vector<void*> grads_;       // one per local replica, compute dtype
+  float* pe_ = nullptr;
+  double* stats_dev_ = nullptr;    // loss, nll, ntokens, ncorrect
+  int32_t* flag_dev_ = nullptr;
+  int32_t* blob_dev_ = nullptr;
+  size_t blob_cap_ = 0;
+  int32_t* blob_host_ = nullptr;   // pinned staging
+  size_t blob_host_cap_ = 0;
+  void* readback_host_ = nullptr;  // pinned: stats + flag
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+  Arena arena_;
+
+  std::vector<GradientBucket> buckets_;
+  EpochPlan plan_;
+  int epoch_ = 1, pos_ = 0;
+  std::vector<int> order_;
+  int64_t step_ = 0;
+  std::function<bool(int64_t)> injector_;
+  int64_t launches_ = 0;
+  float last_ms_ = 0.f;
+
+  void init(const Registry& reg);
+  std::optional<MiniBatch> next_batch();
+  size_t esize() const { return dtype_ == SFK_F32 ? 4 : 2; }
+  void upload(const std::vector<PackedBatch>& packs, std::vector<DeviceBatch>& out);
+  void allreduce_grads();
+};
+
+}  // namespace sqf

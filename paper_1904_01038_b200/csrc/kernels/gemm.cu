@@ -1,0 +1,526 @@
+// GEMM family for Tape::matmul_nt forward / dgrad / wgrad (reference
+// tape.cpp:182-189, 324-346; kernels.cpp:9-16) with the fused epilogues of
+// add_bias / relu / residual add / relu-backward / gradient accumulation.
+//
+// fp16/bf16: a persistent warp-specialised tcgen05 kernel for sm_100a.
+//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (mbarriers)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN,
+//               K=16 per instruction, fp32 accumulators in TMEM, 2 buffers)
+//   warps 2..5  epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+// Operand majors are handled by the UMMA descriptors (K-major or MN-major
+// canonical SW128 layouts), so dgrad and wgrad read activations in place with
+// no transposes.
+// fp32: a SIMT kernel (true fp32 FMA, no TF32) for the reference's fp32 mode.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace sfk {
+
+// ------------------------------------------------------------------ epilogue
+struct Epi {
+  void* c;
+  int64_t ldc;
+  const void* bias;
+  const void* res;
+  int64_t ldr;
+  const void* mask;
+  int64_t ldm;
+  int flags;
+};
+
+template <typename T>
+__device__ __forceinline__ float epi_value(const Epi& e, int64_t row, int col, float acc) {
+  using N = Num<T>;
+  float v = acc;
+  if (e.flags & SFK_EPI_ACCUM) {
+    // gradient accumulation: q(old + acc), one rounding (tape.cpp:296-299)
+    return N::rnd(N::ld(static_cast<const T*>(e.c) + row * e.ldc + col) + v);
+  }
+  if (e.flags & SFK_EPI_PREROUND) v = N::rnd(v);
+  if (e.flags & SFK_EPI_BIAS) v = N::rnd(v + N::ld(static_cast<const T*>(e.bias) + col));
+  if (e.flags & SFK_EPI_RELU) v = v > 0.0f ? v : 0.0f;
+  if (e.flags & SFK_EPI_MASK) v = N::ld(static_cast<const T*>(e.mask) + row * e.ldm + col) > 0.0f ? N::rnd(v) : 0.0f;
+  if (e.flags & SFK_EPI_RESIDUAL) v = N::rnd(N::ld(static_cast<const T*>(e.res) + row * e.ldr + col) + v);
+  return v;
+}
+
+// ------------------------------------------------------------------ SIMT fp32
+namespace simt {
+constexpr int TM = 64, TN = 64, TK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(256) gemm_simt(const T* __restrict__ a, int64_t sa_i, int64_t sa_k,
+                                                 const T* __restrict__ b, int64_t sb_j, int64_t sb_k,
+                                                 Epi e, int M, int N, int K) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int i = tid; i < TM * TK; i += 256) {
+      const int mi = i / TK, ki = i % TK;
+      const int gm = m0 + mi, gk = k0 + ki;
+      As[ki][mi] = (gm < M && gk < K) ? Num<T>::ld(a + gm * sa_i + gk * sa_k) : 0.0f;
+      const int gn = n0 + mi;
+      Bs[ki][mi] = (gn < N && gk < K) ? Num<T>::ld(b + gn * sb_j + gk * sb_k) : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) av[r] = As[kk][ty * 4 + r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gm = m0 + ty * 4 + r;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int gn = n0 + tx * 4 + c;
+      if (gn >= N) continue;
+      const float v = epi_value<T>(e, gm, gn, acc[r][c]);
+      Num<T>::st(static_cast<T*>(e.c) + int64_t(gm) * e.ldc + gn, v);
+    }
+  }
+}
+}  // namespace simt
+
+// ------------------------------------------------------------------ tcgen05
+namespace tc {
+constexpr int BM = 128, BK = 64, kThreads = 192;
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(saddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(saddr(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bits
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (Blackwell)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <typename T>
+struct Pack;
+template <>
+struct Pack<__half> {
+  static __device__ __forceinline__ uint32_t two(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack(uint32_t u) {
+    __half2 h = *reinterpret_cast<__half2*>(&u);
+    return __half22float2(h);
+  }
+};
+template <>
+struct Pack<__nv_bfloat16> {
+  static __device__ __forceinline__ uint32_t two(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack(uint32_t u) {
+    __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&u);
+    return __bfloat1622float2(h);
+  }
+};
+
+// 32 consecutive accumulators of one row -> fused epilogue -> global
+template <typename T>
+__device__ __forceinline__ void epilogue_row32(const Epi& e, int64_t row, int col0, int N, const uint32_t (&r)[32],
+                                               bool vec_ok) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  T* out = static_cast<T*>(e.c) + row * e.ldc + col0;
+  if (vec_ok && col0 + 32 <= N) {
+    // all side inputs share the 16B alignment checked on the host
+    if (e.flags == SFK_EPI_ACCUM) {
+      uint4* po = reinterpret_cast<uint4*>(out);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 old = po[q];
+        uint32_t w[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 o = Pack<T>::unpack(w[j]);
+          w[j] = Pack<T>::two(o.x + v[q * 8 + 2 * j], o.y + v[q * 8 + 2 * j + 1]);
+        }
+        po[q] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      return;
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = epi_value<T>(e, row, col0 + i, v[i]);
+    uint4* po = reinterpret_cast<uint4*>(out);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      po[q] = make_uint4(Pack<T>::two(v[q * 8 + 0], v[q * 8 + 1]), Pack<T>::two(v[q * 8 + 2], v[q * 8 + 3]),
+                         Pack<T>::two(v[q * 8 + 4], v[q * 8 + 5]), Pack<T>::two(v[q * 8 + 6], v[q * 8 + 7]));
+    }
+    return;
+  }
+  for (int i = 0; i < 32 && col0 + i < N; ++i) Num<T>::st(out + i, epi_value<T>(e, row, col0 + i, v[i]));
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int BN, bool A_MN, bool B_MN, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Epi e, int M,
+            int N, int K, int vec_ok) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], C::STAGE);
+          uint8_t* a_dst = smem + s * C::STAGE;
+          uint8_t* b_dst = a_dst + C::A_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(&ta, &full[s], a_dst, k0, m0);
+          } else {
+            tma_load_2d(&ta, &full[s], a_dst, m0, k0);
+            tma_load_2d(&ta, &full[s], a_dst + 8192, m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(&tb, &full[s], b_dst, k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(&tb, &full[s], b_dst + j * 8192, n0 + 64 * j, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // instruction descriptor: D=f32, A/B = f16|bf16, majors, N>>3, M>>4
+      const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(A_MN) << 15) |
+                             (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+      int it = 0, t = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+        const int buf = t & 1;
+        mbar_wait(&tempty[buf], ((t >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          fence_after();
+          const uint32_t a_addr = saddr(smem + s * C::STAGE);
+          const uint32_t b_addr = a_addr + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 32 B inside the swizzled 128 B row; MN-major:
+            // advance 16 K-rows (2 KB) to the next pair of 8-row groups
+            const uint64_t ad = A_MN ? smem_desc(a_addr + k * 2048, 8192, 1024) : smem_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(b_addr + k * 2048, 8192, 1024) : smem_desc(b_addr + k * 32, 16, 1024);
+            umma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row_in_tile = quarter * 32 + lane;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+      const int buf = t & 1;
+      const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+      mbar_wait(&tfull[buf], (t >> 1) & 1);
+      fence_after();
+      const int64_t row = m0 + row_in_tile;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + buf * BN + ch * 32, r);
+        if (row < M && n0 + ch * 32 < N) epilogue_row32<T>(e, row, n0 + ch * 32, N, r, vec_ok != 0);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D map over a row-major [rows x cols] matrix with leading dimension ld,
+// box {64 (inner), box_rows}, 128B swizzle, OOB -> zero
+bool make_map(CUtensorMap* map, int dtype, const void* base, int64_t cols, int64_t rows, int64_t ld,
+              int box_rows) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(map, dtype == SFK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms_cached() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, typename T>
+int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
+  using C = Cfg<BN>;
+  CUtensorMap ta, tb;
+  // A: K-major [m][k] -> map cols=k rows=m, box rows 128; MN-major [k][m] -> cols=m rows=k, box 64x64
+  bool ok = A_MN ? make_map(&ta, g->dtype, g->a, g->m, g->k, g->lda, 64)
+                 : make_map(&ta, g->dtype, g->a, g->k, g->m, g->lda, BM);
+  ok = ok && (B_MN ? make_map(&tb, g->dtype, g->b, g->n, g->k, g->ldb, 64)
+                   : make_map(&tb, g->dtype, g->b, g->k, g->n, g->ldb, BN));
+  if (!ok) {
+    set_error("sfk_gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
+    return SFK_EINVAL;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_tc<BN, A_MN, B_MN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+        cudaSuccess)
+      return check_launch("sfk_gemm: smem attribute");
+    attr_set = true;
+  }
+  const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
+  const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
+  gemm_tc<BN, A_MN, B_MN, T><<<grid, kThreads, C::SMEM, s>>>(ta, tb, e, g->m, g->n, g->k, vec_ok ? 1 : 0);
+  return check_launch("sfk_gemm(tcgen05)");
+}
+
+// tile width by wave efficiency (tiles / (waves * SMs)); wider wins ties
+int pick_bn(int m, int n) {
+  const int sms = num_sms_cached();
+  int best = 256;
+  double best_eff = -1;
+  for (int bn : {256, 128, 64}) {
+    const long tiles = long((m + BM - 1) / BM) * ((n + bn - 1) / bn);
+    const long waves = (tiles + sms - 1) / sms;
+    double eff = double(tiles) / double(waves * sms);
+    eff *= (bn == 256 ? 1.0 : bn == 128 ? 0.97 : 0.80);  // smem-bandwidth penalty of narrow tiles
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+template <typename T>
+int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
+  const int bn = pick_bn(g->m, g->n);
+  const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
+#define SFK_TC(BNV)                                                    \
+  switch (layout) {                                                    \
+    case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s);      \
+    case 1: return launch<BNV, false, true, T>(g, e, vec_ok, s);       \
+    case 3: return launch<BNV, true, true, T>(g, e, vec_ok, s);        \
+    default: return launch<BNV, true, false, T>(g, e, vec_ok, s);      \
+  }
+  if (bn == 256) { SFK_TC(256) }
+  if (bn == 128) { SFK_TC(128) }
+  SFK_TC(64)
+#undef SFK_TC
+}
+}  // namespace tc
+
+}  // namespace sfk
+
+extern "C" int sfk_gemm(const sfk_gemm_args* g, void* stream) {
+  using namespace sfk;
+  if (!g || g->m < 0 || g->n < 0 || g->k < 0 || !g->c) {
+    set_error("sfk_gemm: bad arguments");
+    return SFK_EINVAL;
+  }
+  if (g->m == 0 || g->n == 0) return SFK_OK;
+  Epi e{g->c, g->ldc, g->bias, g->res, g->ldr, g->mask, g->ldm, g->flags};
+  if (((g->flags & SFK_EPI_BIAS) && !g->bias) || ((g->flags & SFK_EPI_RESIDUAL) && !g->res) ||
+      ((g->flags & SFK_EPI_MASK) && !g->mask)) {
+    set_error("sfk_gemm: epilogue input missing");
+    return SFK_EINVAL;
+  }
+  cudaStream_t s = as_stream(stream);
+  if (g->k == 0) {
+    set_error("sfk_gemm: k == 0");
+    return SFK_EINVAL;
+  }
+  if (g->dtype == SFK_F32 || g->force_simt) {
+    const int64_t sa_i = g->a_kmajor ? g->lda : 1, sa_k = g->a_kmajor ? 1 : g->lda;
+    const int64_t sb_j = g->b_kmajor ? g->ldb : 1, sb_k = g->b_kmajor ? 1 : g->ldb;
+    dim3 grid((g->n + simt::TN - 1) / simt::TN, (g->m + simt::TM - 1) / simt::TM);
+    SFK_DISPATCH(g->dtype, T,
+                 simt::gemm_simt<T><<<grid, 256, 0, s>>>(static_cast<const T*>(g->a), sa_i, sa_k,
+                                                         static_cast<const T*>(g->b), sb_j, sb_k, e, g->m, g->n,
+                                                         g->k));
+    return check_launch("sfk_gemm(simt)");
+  }
+  // TMA: 16-byte aligned bases and leading dimensions
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  if (!al16(g->a) || !al16(g->b) || (g->lda % 8) || (g->ldb % 8)) {
+    set_error("sfk_gemm: tensor-core path needs 16-byte aligned operands and ld % 8 == 0");
+    return SFK_EINVAL;
+  }
+  const bool vec_ok = al16(g->c) && (g->ldc % 8 == 0) &&
+                      (!(g->flags & SFK_EPI_RESIDUAL) || (al16(g->res) && g->ldr % 8 == 0)) &&
+                      (!(g->flags & SFK_EPI_MASK) || (al16(g->mask) && g->ldm % 8 == 0)) &&
+                      (!(g->flags & SFK_EPI_BIAS) || al16(g->bias));
+  if (g->dtype == SFK_F16) return tc::dispatch<__half>(g, e, vec_ok, s);
+  if (g->dtype == SFK_BF16) return tc::dispatch<__nv_bfloat16>(g, e, vec_ok, s);
+  set_error("sfk_gemm: bad dtype");
+  return SFK_EINVAL;
+}

@@ -1,0 +1,136 @@
+// Optimizer-side kernels: overflow check (trainer.cpp:247-253), fused
+// unscale + 1/ntokens + Adam (trainer.cpp:260-268, optim.cpp:48-66) with the
+// fp16 shadow rebroadcast (trainer.cpp:149-156), SGD, casts.
+// Adam runs in double exactly as the reference (double m/v/update math, fp32
+// storage), so given identical gradients the update is bit-identical.
+#include "common.cuh"
+
+namespace sfk {
+
+template <typename T>
+__global__ void nonfinite_k(const T* __restrict__ g, int64_t n, int32_t* flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    bad |= !isfinite(Num<T>::ld(g + i));
+  bad = __syncthreads_or(bad);
+  if (bad && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+template <typename G, typename S>
+__global__ void adam_k(float* __restrict__ master, S* __restrict__ shadow, const G* __restrict__ grad,
+                       float* __restrict__ m, float* __restrict__ v, int64_t n, double lr, double b1, double b2,
+                       double eps, double bc1, double bc2, float scale, int unscale, float ntok,
+                       const int32_t* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float gf = Num<G>::ld(grad + i);
+    if (unscale) gf = __fdiv_rn(gf, scale);
+    gf = __fdiv_rn(gf, ntok);
+    const double g = gf;
+    // explicit _rn ops: no FMA contraction, same evaluation order as optim.cpp:53-56
+    const double mm = __dadd_rn(__dmul_rn(b1, double(m[i])), __dmul_rn(1.0 - b1, g));
+    const double vv = __dadd_rn(__dmul_rn(b2, double(v[i])), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
+    const float mf = float(mm), vf = float(vv);
+    m[i] = mf;
+    v[i] = vf;
+    const double mhat = __ddiv_rn(double(mf), bc1);
+    const double vhat = __ddiv_rn(double(vf), bc2);
+    const float p = float(__dsub_rn(double(master[i]), __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps))));
+    master[i] = p;
+    if (shadow) Num<S>::st(shadow + i, p);
+  }
+}
+
+template <typename G, typename S>
+__global__ void sgd_k(float* __restrict__ master, S* __restrict__ shadow, const G* __restrict__ grad, int64_t n,
+                      double lr, float scale, int unscale, float ntok, const int32_t* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    float gf = Num<G>::ld(grad + i);
+    if (unscale) gf = __fdiv_rn(gf, scale);
+    gf = __fdiv_rn(gf, ntok);
+    const float p = float(__dsub_rn(double(master[i]), __dmul_rn(lr, double(gf))));
+    master[i] = p;
+    if (shadow) Num<S>::st(shadow + i, p);
+  }
+}
+
+template <typename S, typename D>
+__global__ void convert_k(const S* __restrict__ src, D* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    Num<D>::st(dst + i, Num<S>::ld(src + i));
+}
+
+template <typename T>
+__global__ void accumulate_k(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    Num<T>::st(dst + i, __fadd_rn(Num<T>::ld(dst + i), Num<T>::ld(src + i)));
+}
+
+inline int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  const int cap = 148 * 16;
+  return int(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace sfk
+
+using namespace sfk;
+
+extern "C" int sfk_nonfinite(int dtype, const void* g, int64_t n, int32_t* flag, void* stream) {
+  if (n == 0) return SFK_OK;
+  SFK_DISPATCH(dtype, T,
+               nonfinite_k<T><<<grid_for(n), 256, 0, as_stream(stream)>>>(static_cast<const T*>(g), n, flag));
+  return check_launch("sfk_nonfinite");
+}
+
+#define SFK_DISPATCH2(gd, G, sd, S, ...)                    \
+  SFK_DISPATCH(gd, G, {                                     \
+    switch (sd) {                                           \
+      case SFK_F32: { using S = float; __VA_ARGS__; break; } \
+      case SFK_F16: { using S = __half; __VA_ARGS__; break; } \
+      case SFK_BF16: { using S = __nv_bfloat16; __VA_ARGS__; break; } \
+      default: set_error("bad shadow dtype"); return SFK_EINVAL; \
+    }                                                       \
+  })
+
+extern "C" int sfk_adam(int grad_dtype, float* master, void* shadow, int shadow_dtype, const void* grad, float* m,
+                        float* v, int64_t n, double lr, double b1, double b2, double eps, double bc1, double bc2,
+                        float scale, int unscale, float ntokens, const int32_t* skip, void* stream) {
+  if (n == 0) return SFK_OK;
+  SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
+                adam_k<G, S><<<grid_for(n), 256, 0, as_stream(stream)>>>(
+                    master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n, lr, b1, b2, eps, bc1, bc2,
+                    scale, unscale, ntokens, skip));
+  return check_launch("sfk_adam");
+}
+
+extern "C" int sfk_sgd(int grad_dtype, float* master, void* shadow, int shadow_dtype, const void* grad, int64_t n,
+                       double lr, float scale, int unscale, float ntokens, const int32_t* skip, void* stream) {
+  if (n == 0) return SFK_OK;
+  SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
+                sgd_k<G, S><<<grid_for(n), 256, 0, as_stream(stream)>>>(master, static_cast<S*>(shadow),
+                                                                        static_cast<const G*>(grad), n, lr, scale,
+                                                                        unscale, ntokens, skip));
+  return check_launch("sfk_sgd");
+}
+
+extern "C" int sfk_cast(const float* src, void* dst, int dst_dtype, int64_t n, void* stream) {
+  return sfk_convert(SFK_F32, src, dst_dtype, dst, n, stream);
+}
+
+extern "C" int sfk_convert(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream) {
+  if (n == 0) return SFK_OK;
+  SFK_DISPATCH2(src_dtype, S, dst_dtype, D,
+                convert_k<S, D><<<grid_for(n), 256, 0, as_stream(stream)>>>(static_cast<const S*>(src),
+                                                                            static_cast<D*>(dst), n));
+  return check_launch("sfk_convert");
+}
+
+extern "C" int sfk_accumulate(int dtype, void* dst, const void* src, int64_t n, void* stream) {
+  if (n == 0) return SFK_OK;
+  SFK_DISPATCH(dtype, T,
+               accumulate_k<T><<<grid_for(n), 256, 0, as_stream(stream)>>>(static_cast<T*>(dst),
+                                                                          static_cast<const T*>(src), n));
+  return check_launch("sfk_accumulate");
+}

@@ -1,0 +1,253 @@
+"""GPU parity of each sm_100a kernel through the C ABI (include/sqf_kernels.h)
+against the reference oracle (the seqforge tape ops, oracle/_ref) or, for the
+GEMM, an fp64 product of the same (rounded) operands. Tolerances are stated
+per test; integer/index outputs are compared exactly."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def L():
+    from paper_1904_01038_b200 import _lib
+    return _lib
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+TDT = {0: torch.float32, 1: torch.float16, 2: torch.bfloat16}
+
+
+def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=False, with_c=None):
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    td = TDT[dtype]
+    A = (torch.randn(m, k, device="cuda", generator=g) * 0.5).to(td)  # logical A(i,k)
+    B = (torch.randn(n, k, device="cuda", generator=g) * 0.5).to(td)  # logical B(j,k)
+    a_store = A.contiguous() if a_kmajor else A.t().contiguous()
+    b_store = B.contiguous() if b_kmajor else B.t().contiguous()
+    bias = (torch.randn(n, device="cuda", generator=g)).to(td)
+    res = (torch.randn(m, n, device="cuda", generator=g)).to(td)
+    mask = (torch.randn(m, n, device="cuda", generator=g)).to(td)
+    c = with_c.clone() if with_c is not None else torch.randn(m, n, device="cuda", generator=g).to(td)
+    c0 = c.clone()
+    args = lib.GemmArgs(m=m, n=n, k=k, dtype=dtype, a=ptr(a_store), lda=a_store.shape[1], a_kmajor=int(a_kmajor),
+                        b=ptr(b_store), ldb=b_store.shape[1], b_kmajor=int(b_kmajor), c=ptr(c), ldc=n,
+                        bias=ptr(bias), res=ptr(res), ldr=n, mask=ptr(mask), ldm=n, flags=flags,
+                        force_simt=int(force_simt))
+    lib.check(lib.sfk_gemm(C.byref(args), stream()), kernel=True)
+    torch.cuda.synchronize()
+    acc = (A.double() @ B.double().t()).float()
+    q = (lambda x: x.to(td).float()) if dtype != 0 else (lambda x: x)
+    v = acc
+    if flags & lib.EPI_ACCUM:
+        v = q(c0.float() + acc)
+    else:
+        if flags & lib.EPI_PREROUND:
+            v = q(v)
+        if flags & lib.EPI_BIAS:
+            v = q(v + bias.float())
+        if flags & lib.EPI_RELU:
+            v = torch.clamp_min(v, 0)
+        if flags & lib.EPI_MASK:
+            v = torch.where(mask.float() > 0, q(v), torch.zeros_like(v))
+        if flags & lib.EPI_RESIDUAL:
+            v = q(res.float() + v)
+    return c.float(), q(v)
+
+
+@pytest.mark.parametrize("dtype", [1, 2])
+@pytest.mark.parametrize("layout", [(True, True), (True, False), (False, False), (False, True)])
+@pytest.mark.parametrize("shape", [(128, 256, 64), (200, 320, 96), (1000, 72, 520), (4096, 3072, 1024),
+                                   (3584, 1024, 4096), (17, 24, 16)])
+def test_gemm_tc_layouts(dtype, layout, shape):
+    m, n, k = shape
+    got, want = run_gemm(m, n, k, dtype, *layout)
+    tol = 4e-3 if dtype == 1 else 2e-2
+    torch.testing.assert_close(got, want, rtol=tol, atol=tol * max(1.0, k ** 0.5 * 0.25))
+
+
+@pytest.mark.parametrize("flags", [1 | 2, 1 | 2 | 4, 1 | 2 | 16, 8, 32, 1 | 2 | 4 | 16])
+def test_gemm_tc_epilogues(flags):
+    got, want = run_gemm(300, 200, 128, 1, True, flags != 32, flags)
+    torch.testing.assert_close(got, want, rtol=4e-3, atol=8e-3)
+
+
+@pytest.mark.parametrize("layout", [(True, True), (True, False), (False, False)])
+def test_gemm_simt_fp32(layout):
+    got, want = run_gemm(133, 70, 95, 0, *layout, flags=1 | 2 | 16)
+    torch.testing.assert_close(got, want, rtol=1e-5, atol=1e-5)
+
+
+def test_gemm_rejects_misaligned_tc_operands():
+    lib = L()
+    a = torch.zeros(64, 30, dtype=torch.float16, device="cuda")
+    c = torch.zeros(64, 64, dtype=torch.float16, device="cuda")
+    args = lib.GemmArgs(m=64, n=64, k=30, dtype=1, a=ptr(a), lda=30, a_kmajor=1, b=ptr(a), ldb=30, b_kmajor=1,
+                        c=ptr(c), ldc=64)
+    assert lib.sfk_gemm(C.byref(args), stream()) == -1
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("rows,vocab,eps", [(7, 11, 0.1), (64, 1000, 0.1), (33, 32768, 0.1), (20, 10000, 0.0)])
+def test_xent_matches_reference(fp16, rows, vocab, eps):
+    lib = L()
+    rng = np.random.default_rng(rows)
+    lg = (rng.standard_normal((rows, vocab)) * 3).astype(np.float32)
+    if fp16:
+        lg = ref.quantize_array(lg)
+    gold = rng.integers(0, vocab, rows).astype(np.int32)
+    gold[::5] = 1  # pad rows
+    seed = 256.0 if fp16 else 1.0
+    loss, nll, corr, dl = ref.xent(lg, gold, eps, fp16, seed)
+    dt = 1 if fp16 else 0
+    t = torch.tensor(lg, device="cuda").to(TDT[dt])
+    g = torch.tensor(gold, device="cuda")
+    rows_out = torch.zeros(rows, 4, device="cuda")
+    acc = torch.zeros(4, dtype=torch.float64, device="cuda")
+    lib.check(lib.sfk_xent_fwd_bwd(dt, ptr(t), rows, vocab, vocab, ptr(g), 1, eps, seed, ptr(t), ptr(rows_out),
+                                   stream()), kernel=True)
+    lib.check(lib.sfk_xent_reduce(ptr(rows_out), rows, ptr(acc), stream()), kernel=True)
+    torch.cuda.synchronize()
+    ro = rows_out.cpu().numpy()
+    active = gold != 1
+    np.testing.assert_array_equal(ro[:, 3], active.astype(np.float32))
+    np.testing.assert_array_equal(ro[:, 2], corr.astype(np.float32))  # argmax (first max) exact
+    np.testing.assert_allclose(ro[:, 1], nll, rtol=2e-6, atol=2e-5)
+    np.testing.assert_allclose(ro[:, 0], loss, rtol=1e-3 if fp16 else 2e-6, atol=2e-5)
+    np.testing.assert_allclose(t.float().cpu().numpy(), dl, rtol=1e-3 if fp16 else 1e-5, atol=1e-6 * seed)
+    a = acc.cpu().numpy()
+    assert a[2] == active.sum() and a[3] == corr.sum()
+    np.testing.assert_allclose(a[0], float(loss.astype(np.float64).sum()), rtol=1e-3 if fp16 else 1e-6)
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("rows,d", [(5, 16), (300, 512), (129, 1024), (64, 64)])
+def test_layernorm_matches_reference(fp16, rows, d):
+    lib = L()
+    rng = np.random.default_rng(d)
+    x = (rng.standard_normal((rows, d)) * 2 + 0.5).astype(np.float32)
+    gm = (1 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    bt = (0.1 * rng.standard_normal(d)).astype(np.float32)
+    dy = rng.standard_normal((rows, d)).astype(np.float32)
+    if fp16:
+        x, gm, bt, dy = (ref.quantize_array(a) for a in (x, gm, bt, dy))
+    y, dx, dg, db = ref.layer_norm(x, gm, bt, dy, fp16)
+    dt = 1 if fp16 else 0
+    T = lambda a: torch.tensor(a, device="cuda").to(TDT[dt])  # noqa: E731
+    tx, tg, tb, tdy = T(x), T(gm), T(bt), T(dy)
+    ty = torch.zeros_like(tx)
+    stats = torch.zeros(rows, 2, device="cuda")
+    lib.check(lib.sfk_layernorm_fwd(dt, ptr(tx), rows, d, ptr(tg), ptr(tb), ptr(ty), ptr(stats), stream()), True)
+    tdx = torch.zeros_like(tx)
+    part = torch.zeros(2 * 296 * d, device="cuda")
+    npart = C.c_int()
+    lib.check(lib.sfk_layernorm_bwd(dt, ptr(tx), ptr(tdy), rows, d, ptr(tg), ptr(stats), ptr(tdx), 0, ptr(part),
+                                    C.byref(npart), stream()), True)
+    dgt = torch.zeros(d, device="cuda").to(TDT[dt])
+    dbt = torch.zeros(d, device="cuda").to(TDT[dt])
+    lib.check(lib.sfk_colsum_finish(dt, ptr(part), npart.value, d, ptr(dgt), stream()), True)
+    lib.check(lib.sfk_colsum_finish(dt, C.c_void_p(part.data_ptr() + 4 * npart.value * d), npart.value, d,
+                                    ptr(dbt), stream()), True)
+    torch.cuda.synchronize()
+    rt = 2e-3 if fp16 else 1e-5
+    np.testing.assert_allclose(ty.float().cpu().numpy(), y, rtol=rt, atol=rt)
+    np.testing.assert_allclose(tdx.float().cpu().numpy(), dx, rtol=rt * 5, atol=rt * 5)
+    np.testing.assert_allclose(dgt.float().cpu().numpy(), dg, rtol=rt * 5, atol=rt * 5 * rows ** 0.5)
+    np.testing.assert_allclose(dbt.float().cpu().numpy(), db, rtol=rt * 5, atol=rt * 5 * rows ** 0.5)
+
+
+def _spans(batch, qw, kw, lens, causal):
+    kb, kl = [], []
+    for b in range(batch):
+        for t in range(qw):
+            kb.append(b * kw)
+            kl.append(t + 1 if causal else lens[b])
+    return kb, kl
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+@pytest.mark.parametrize("batch,qw,kw,heads,dh,causal", [(3, 7, 7, 2, 8, False), (2, 9, 9, 4, 16, True),
+                                                        (4, 6, 11, 8, 64, False), (2, 40, 40, 4, 128, True),
+                                                        (3, 25, 31, 16, 64, False)])
+def test_attention_matches_reference(fp16, batch, qw, kw, heads, dh, causal):
+    lib = L()
+    rng = np.random.default_rng(qw * kw)
+    d = heads * dh
+    lens = rng.integers(1, kw + 1, batch).astype(np.int32)
+    q = rng.standard_normal((batch * qw, d)).astype(np.float32)
+    k = rng.standard_normal((batch * kw, d)).astype(np.float32)
+    v = rng.standard_normal((batch * kw, d)).astype(np.float32)
+    do = rng.standard_normal((batch * qw, d)).astype(np.float32)
+    if fp16:
+        q, k, v, do = (ref.quantize_array(a) for a in (q, k, v, do))
+    kb, kl = _spans(batch, qw, kw, lens, causal)
+    out, dq, dk, dv = ref.attention(q, k, v, heads, kb, kl, do, fp16)
+    dt = 1 if fp16 else 0
+    T = lambda a: torch.tensor(a, device="cuda").to(TDT[dt])  # noqa: E731
+    tq, tk, tv, tdo = T(q), T(k), T(v), T(do)
+    to, tdq, tdk, tdv = (torch.zeros_like(x) for x in (tq, tk, tk, tv))
+    to = torch.zeros_like(tq)
+    tdq = torch.zeros_like(tq)
+    stats = torch.zeros(batch * qw * heads, 2, device="cuda")
+    scratch = torch.zeros(batch * qw * heads, device="cuda")
+    tl = torch.tensor(lens, device="cuda")
+    a = lib.AttnArgs(dtype=dt, batch=batch, q_width=qw, k_width=kw, heads=heads, dh=dh, causal=int(causal),
+                     k_len=ptr(tl), q=ptr(tq), ldq=d, k=ptr(tk), ldk=d, v=ptr(tv), ldv=d, o=ptr(to), ldo=d,
+                     stats=ptr(stats), dout=ptr(tdo), lddo=d, dq=ptr(tdq), lddq=d, dk=ptr(tdk), lddk=d,
+                     dv=ptr(tdv), lddv=d, scratch=ptr(scratch))
+    lib.check(lib.sfk_attention_fwd(C.byref(a), stream()), True)
+    lib.check(lib.sfk_attention_bwd(C.byref(a), stream()), True)
+    torch.cuda.synchronize()
+    rt = 4e-3 if fp16 else 2e-5
+    for got, want in ((to, out), (tdq, dq), (tdk, dk), (tdv, dv)):
+        np.testing.assert_allclose(got.float().cpu().numpy(), want, rtol=rt, atol=rt * 4)
+
+
+def test_adam_bit_exact_with_reference():
+    lib = L()
+    rng = np.random.default_rng(3)
+    n = 10000
+    p = rng.standard_normal(n).astype(np.float32)
+    g = ref.quantize_array(rng.standard_normal(n).astype(np.float32) * 512)
+    m = (rng.standard_normal(n) * 0.01).astype(np.float32)
+    v = (rng.random(n) * 0.01).astype(np.float32)
+    scale, ntok, lr, t = 512.0, 3333.0, 7e-4, 5
+    g_pre = ((g / np.float32(scale)).astype(np.float32) / np.float32(ntok)).astype(np.float32)
+    want_p, want_m, want_v = ref.adam(p, g_pre, m, v, t - 1, lr)
+    tp, tm, tv = (torch.tensor(a, device="cuda") for a in (p, m, v))
+    tg = torch.tensor(g, device="cuda").half()
+    sh = torch.zeros(n, dtype=torch.float16, device="cuda")
+    bc1, bc2 = 1 - 0.9 ** t, 1 - 0.98 ** t
+    lib.check(lib.sfk_adam(1, ptr(tp), ptr(sh), 1, ptr(tg), ptr(tm), ptr(tv), n, lr, 0.9, 0.98, 1e-8, bc1, bc2,
+                           scale, 1, ntok, None, stream()), True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(tp.cpu().numpy().view(np.uint32), want_p.view(np.uint32))
+    np.testing.assert_array_equal(tm.cpu().numpy().view(np.uint32), want_m.view(np.uint32))
+    np.testing.assert_array_equal(tv.cpu().numpy().view(np.uint32), want_v.view(np.uint32))
+    np.testing.assert_array_equal(sh.float().cpu().numpy(), ref.quantize_array(want_p))
+
+
+def test_nonfinite_flag():
+    lib = L()
+    g = torch.zeros(1 << 20, dtype=torch.float16, device="cuda")
+    flag = torch.zeros(4, dtype=torch.int32, device="cuda")
+    lib.check(lib.sfk_nonfinite(1, ptr(g), g.numel(), ptr(flag), stream()), True)
+    torch.cuda.synchronize()
+    assert flag[0].item() == 0
+    g[777777] = float("inf")
+    lib.check(lib.sfk_nonfinite(1, ptr(g), g.numel(), ptr(flag), stream()), True)
+    torch.cuda.synchronize()
+    assert flag[0].item() == 1
