@@ -79,6 +79,12 @@ int64_t sqf_trainer_kernel_launches(void* t);
 float sqf_trainer_last_step_ms(void* t);
 /* CUDA stream the trainer launches on (cudaStream_t) */
 void* sqf_trainer_stream(void* t);
+/* per-launch CUDA-event profiling of the following steps (on = 1) and its
+ * accumulated per-class totals: class 0..9 = gemm_fwd, gemm_dgrad,
+ * gemm_wgrad, attn_fwd, attn_bwd, layernorm, xent, embed, bias_grad, optim.
+ * Returns the class name, or NULL past the last class. */
+int sqf_trainer_set_profile(void* t, int on);
+const char* sqf_trainer_profile(void* t, int cls, double* ms, double* flops, double* bytes, int64_t* launches);
 
 /* ---------------- host-side boundary pieces (no GPU needed) --------------- */
 /* synthetic WMT-shaped corpus; two-call protocol: pass

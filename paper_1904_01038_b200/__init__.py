@@ -299,3 +299,17 @@ class Trainer:
     @property
     def stream(self) -> int:
         return int(L.sqf_trainer_stream(self._h) or 0)
+
+    def set_profile(self, on: bool = True):
+        L.check(L.sqf_trainer_set_profile(self._h, int(on)))
+
+    def profile(self):
+        """Per kernel class: {name: (ms, flops, bytes, launches)} accumulated since set_profile."""
+        out = {}
+        for c in range(64):
+            ms, fl, by, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+            name = L.sqf_trainer_profile(self._h, c, C.byref(ms), C.byref(fl), C.byref(by), C.byref(n))
+            if not name:
+                break
+            out[name.decode()] = (ms.value, fl.value, by.value, n.value)
+        return out

@@ -109,6 +109,8 @@ sqf_trainer_restore = _sig("sqf_trainer_restore", C.c_int, vp, i64, i32, i32, f6
 sqf_trainer_kernel_launches = _sig("sqf_trainer_kernel_launches", i64, vp)
 sqf_trainer_last_step_ms = _sig("sqf_trainer_last_step_ms", f32, vp)
 sqf_trainer_stream = _sig("sqf_trainer_stream", vp, vp)
+sqf_trainer_set_profile = _sig("sqf_trainer_set_profile", C.c_int, vp, C.c_int)
+sqf_trainer_profile = _sig("sqf_trainer_profile", cp, vp, C.c_int, P(f64), P(f64), P(f64), P(i64))
 
 # ---- host boundary pieces
 sqf_synthetic_corpus = _sig("sqf_synthetic_corpus", C.c_int, C.c_int, C.c_int, C.c_int, f64, u64, vp, vp, vp, vp,

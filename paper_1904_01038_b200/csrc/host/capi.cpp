@@ -260,6 +260,18 @@ int64_t sqf_trainer_kernel_launches(void* t) { return T(t)->kernel_launches(); }
 float sqf_trainer_last_step_ms(void* t) { return T(t)->last_step_ms(); }
 void* sqf_trainer_stream(void* t) { return static_cast<void*>(T(t)->stream()); }
 
+int sqf_trainer_set_profile(void* t, int on) { SQF_GUARD(T(t)->set_profile(on != 0)) }
+
+const char* sqf_trainer_profile(void* t, int cls, double* ms, double* flops, double* bytes, int64_t* launches) {
+  Profiler* p = T(t)->profiler();
+  if (cls < 0 || cls >= Profiler::kCats) return nullptr;
+  *ms = p ? p->ms[cls] : 0.0;
+  *flops = p ? p->flops[cls] : 0.0;
+  *bytes = p ? p->bytes[cls] : 0.0;
+  *launches = p ? p->count[cls] : 0;
+  return Profiler::name(cls);
+}
+
 // ---------------------------------------------------------------- host-only
 int sqf_synthetic_corpus(int npairs, int src_vocab, int tgt_vocab, double zipf_s, uint64_t seed, int32_t* src_len,
                          int32_t* tgt_len, int32_t* src_ids, int32_t* tgt_ids, int64_t* src_total,

@@ -2,7 +2,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <map>
 
 namespace sqf {
 
@@ -44,6 +43,51 @@ size_t Arena::capacity() const {
   return s;
 }
 
+// ------------------------------------------------------------------ profiler
+const char* Profiler::name(int c) {
+  static const char* n[] = {"gemm_fwd", "gemm_dgrad", "gemm_wgrad", "attn_fwd", "attn_bwd",
+                            "layernorm", "xent", "embed", "bias_grad", "optim"};
+  return c >= 0 && c < kCats ? n[c] : "?";
+}
+Profiler::~Profiler() {
+  for (auto e : pool_) cudaEventDestroy(e);
+}
+cudaEvent_t Profiler::get() {
+  if (next_ == pool_.size()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "profiler event");
+    pool_.push_back(e);
+  }
+  return pool_[next_++];
+}
+void Profiler::begin(cudaStream_t s) {
+  open_ = get();
+  cuda_check(cudaEventRecord(open_, s), "profiler record");
+}
+void Profiler::end(cudaStream_t s, int cat, double fl, double by) {
+  cudaEvent_t b = get();
+  cuda_check(cudaEventRecord(b, s), "profiler record");
+  pending_.push_back({open_, b, cat, fl, by});
+}
+void Profiler::collect() {
+  for (const Rec& r : pending_) {
+    cuda_check(cudaEventSynchronize(r.b), "profiler sync");
+    float t = 0.f;
+    cuda_check(cudaEventElapsedTime(&t, r.a, r.b), "profiler elapsed");
+    ms[r.cat] += t;
+    flops[r.cat] += r.flops;
+    bytes[r.cat] += r.bytes;
+    count[r.cat] += 1;
+  }
+  pending_.clear();
+  next_ = 0;
+}
+void Profiler::reset() {
+  pending_.clear();
+  next_ = 0;
+  for (int c = 0; c < kCats; ++c) ms[c] = flops[c] = bytes[c] = 0, count[c] = 0;
+}
+
 // ------------------------------------------------------------------ batch packing
 namespace {
 // recording-order segments for the embedding backward: unique ids ascending,
@@ -78,8 +122,7 @@ PackedBatch PackedBatch::pack(const MiniBatch& b) {
   auto put = [&](const auto& v) {
     const size_t at = p.blob.size();
     p.blob.insert(p.blob.end(), v.begin(), v.end());
-    // keep every section 16-byte aligned
-    while (p.blob.size() % 4) p.blob.push_back(0);
+    while (p.blob.size() % 4) p.blob.push_back(0);  // 16-byte aligned sections
     return at;
   };
   p.off_source = put(b.source);
@@ -128,7 +171,9 @@ int DeviceTape::embedding(ParamRef table, const int32_t* ids, int rows, int widt
   n.scale = scale;
   n.segs = segs;
   n.out = alloc_elems(int64_t(rows) * n.cols);
+  pbegin();
   sfk_check(sfk_embed_fwd(dtype_, ids, rows, width, n.cols, pptr(table), pe, scale, n.out, stream_), "embed_fwd");
+  pend(Profiler::Embed, 0, double(rows) * n.cols * (2.0 * esize_ + 4));
   ++launches_;
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
@@ -146,16 +191,18 @@ int DeviceTape::layer_norm(int x, ParamRef gamma, ParamRef beta) {
   n.cols = in.cols;
   n.out = alloc_elems(int64_t(n.rows) * n.cols);
   n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * 8));
+  pbegin();
   sfk_check(sfk_layernorm_fwd(dtype_, in.out, n.rows, n.cols, pptr(gamma), pptr(beta), n.out, n.stats, stream_),
             "layernorm_fwd");
+  pend(Profiler::LayerNorm, 0, double(n.rows) * (2.0 * n.cols * esize_ + 8));
   ++launches_;
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
 }
 
-void DeviceTape::gemm(int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
-                      bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias, const void* res, int64_t ldr,
-                      const void* mask, int64_t ldm) {
+void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b,
+                      int64_t ldb, bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias, const void* res,
+                      int64_t ldr, const void* mask, int64_t ldm) {
   sfk_gemm_args g{};
   g.m = m;
   g.n = n;
@@ -175,7 +222,9 @@ void DeviceTape::gemm(int m, int n, int k, const void* a, int64_t lda, bool a_km
   g.mask = mask;
   g.ldm = ldm;
   g.flags = flags;
+  pbegin();
   sfk_check(sfk_gemm(&g, stream_), "gemm");
+  pend(cat, 2.0 * m * n * k, double(esize_) * (double(m) * k + double(n) * k + double(m) * n));
   ++launches_;
 }
 
@@ -200,11 +249,19 @@ int DeviceTape::linear(int x, ParamRef w, const ParamRef* bias, bool relu, int r
   if (bias) flags |= SFK_EPI_BIAS;
   if (relu) flags |= SFK_EPI_RELU;
   if (residual >= 0) flags |= SFK_EPI_RESIDUAL;
-  gemm(n.rows, n.cols, in.cols, in.out, in.cols, true, pptr(w), w.cols, true, n.out, n.cols, flags,
+  gemm(Profiler::GemmFwd, n.rows, n.cols, in.cols, in.out, in.cols, true, pptr(w), w.cols, true, n.out, n.cols, flags,
        bias ? pptr(*bias) : nullptr, residual >= 0 ? nodes_[residual].out : nullptr, n.cols);
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
 }
+
+namespace {
+double attn_flops(int batch, int qw, int kw, const int32_t* /*k_len device*/, int d, bool causal, bool bwd) {
+  // padded-span upper bound: every query row of sentence b against its key span
+  const double pairs = causal ? double(batch) * qw * (qw + 1) / 2.0 : double(batch) * qw * kw;
+  return (bwd ? 8.0 : 4.0) * pairs * d;
+}
+}  // namespace
 
 int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
                           int k_width, bool causal, const int32_t* k_len) {
@@ -247,7 +304,10 @@ int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d,
   a.o = n.out;
   a.ldo = d;
   a.stats = n.stats;
+  pbegin();
   sfk_check(sfk_attention_fwd(&a, stream_), "attention_fwd");
+  pend(Profiler::AttnFwd, attn_flops(batch, q_width, k_width, k_len, d, causal, false),
+       double(esize_) * d * (2.0 * n.rows + 2.0 * kn.rows));
   ++launches_;
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
@@ -277,10 +337,12 @@ std::pair<void*, bool> DeviceTape::grad_of(int id) {
 void DeviceTape::run_xent(Node& n, float seed, bool with_grad, double* stats_acc) {
   Node& lg = nodes_[n.in0];
   // the logits buffer becomes its own gradient (dlogits written in place)
+  pbegin();
   sfk_check(sfk_xent_fwd_bwd(dtype_, lg.out, lg.rows, lg.cols, lg.cols, n.gold, kPad, n.eps, seed,
                              with_grad ? lg.out : nullptr, n.row_out, stream_),
             "xent");
   sfk_check(sfk_xent_reduce(n.row_out, n.rows, stats_acc, stream_), "xent_reduce");
+  pend(Profiler::Xent, 0, double(lg.rows) * lg.cols * esize_ * (with_grad ? 2.0 : 1.0));
   launches_ += 2;
   if (with_grad) lg.grad = lg.out;
 }
@@ -303,8 +365,10 @@ void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void*
   const int max_parts = 64;
   float* part = static_cast<float*>(arena_.alloc(size_t(max_parts) * cols * 4));
   int nparts = 0;
+  pbegin();
   sfk_check(sfk_colsum_partial(dtype_, dy, rows, cols, ld, part, &nparts, stream_), "colsum_partial");
   sfk_check(sfk_colsum_finish(dtype_, part, nparts, cols, out, stream_), "colsum_finish");
+  pend(Profiler::BiasGrad, 0, double(rows) * cols * esize_);
   launches_ += 2;
 }
 
@@ -315,9 +379,11 @@ void DeviceTape::backward_node(int id) {
     case Kind::Xent:
       return;
     case Kind::Embedding: {
+      pbegin();
       sfk_check(sfk_embed_bwd(dtype_, n.segs.uniq, n.segs.off, n.segs.rows, n.segs.n, n.cols, n.grad, n.scale,
                               gptr(n.p0), stream_),
                 "embed_bwd");
+      pend(Profiler::Embed, 0, double(n.rows) * n.cols * esize_ + 2.0 * n.segs.n * n.cols * esize_);
       ++launches_;
       return;
     }
@@ -327,13 +393,14 @@ void DeviceTape::backward_node(int id) {
       const int max_parts = 296;
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
       int nparts = 0;
+      pbegin();
       sfk_check(sfk_layernorm_bwd(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx, fresh ? 0 : 1,
                                   part, &nparts, stream_),
                 "layernorm_bwd");
-      sfk_check(sfk_colsum_finish(dtype_, part, nparts, n.cols, gptr(n.p0), stream_),
-                "ln dgamma");
+      sfk_check(sfk_colsum_finish(dtype_, part, nparts, n.cols, gptr(n.p0), stream_), "ln dgamma");
       sfk_check(sfk_colsum_finish(dtype_, part + size_t(nparts) * n.cols, nparts, n.cols, gptr(n.p1), stream_),
                 "ln dbeta");
+      pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
       launches_ += 3;
       return;
     }
@@ -343,11 +410,8 @@ void DeviceTape::backward_node(int id) {
       // residual add: the residual input receives dy unchanged; alias when fresh
       if (n.in1 >= 0) {
         Node& r = nodes_[n.in1];
-        if (!r.grad) {
-          r.grad = dy;
-        } else {
-          throw ShapeError("linear: residual input already has a gradient (unsupported fan-out)");
-        }
+        if (r.grad) throw ShapeError("linear: residual input already has a gradient (unsupported fan-out)");
+        r.grad = dy;
       }
       if (n.has_bias) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
       // dgrad into the input; a relu input gets the masked (pre-activation) grad
@@ -361,10 +425,11 @@ void DeviceTape::backward_node(int id) {
         mask = inm.out;
         inm.grad_masked = true;
       }
-      gemm(n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols, flags, nullptr,
-           nullptr, 0, mask, in.cols);
+      gemm(Profiler::GemmDgrad, n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols,
+           flags, nullptr, nullptr, 0, mask, in.cols);
       // wgrad: dW += dy^T x
-      gemm(n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0), n.p0.cols, SFK_EPI_ACCUM);
+      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
+           n.p0.cols, SFK_EPI_ACCUM);
       return;
     }
     case Kind::Attention: {
@@ -372,8 +437,7 @@ void DeviceTape::backward_node(int id) {
       const Node& kn = nodes_[n.in1];
       auto [dq, fq] = grad_of(n.in0);
       auto [dkv, fkv] = grad_of(n.in1);
-      if (!fq || (!fkv && n.in0 != n.in1))
-        throw ShapeError("attention: q/k/v inputs must not have other consumers");
+      if (!fq || (!fkv && n.in0 != n.in1)) throw ShapeError("attention: q/k/v inputs must not have other consumers");
       sfk_attn_args a{};
       a.dtype = dtype_;
       a.batch = n.batch;
@@ -401,7 +465,10 @@ void DeviceTape::backward_node(int id) {
       a.dv = static_cast<char*>(dkv) + n.v_col * esize_;
       a.lddv = kn.cols;
       a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
+      pbegin();
       sfk_check(sfk_attention_bwd(&a, stream_), "attention_bwd");
+      pend(Profiler::AttnBwd, attn_flops(n.batch, n.q_width, n.k_width, n.k_len, n.cols, n.causal, true),
+           double(esize_) * n.cols * (4.0 * n.rows + 4.0 * kn.rows));
       launches_ += 2;
       return;
     }

@@ -68,6 +68,35 @@ struct PackedBatch {
   DeviceBatch bind(const int32_t* dev_blob) const;
 };
 
+// Optional per-launch CUDA-event timing (bench/profiling pass only): every
+// launch the tape issues is bracketed by an event pair on the tape's stream
+// and attributed to a kernel class with its algorithmic flops and bytes.
+class Profiler {
+ public:
+  enum Cat { GemmFwd, GemmDgrad, GemmWgrad, AttnFwd, AttnBwd, LayerNorm, Xent, Embed, BiasGrad, Optim, kCats };
+  static const char* name(int c);
+  ~Profiler();
+  void begin(cudaStream_t s);
+  void end(cudaStream_t s, int cat, double flops, double bytes);
+  // resolves all pending events (synchronises)
+  void collect();
+  void reset();
+  double ms[kCats] = {}, flops[kCats] = {}, bytes[kCats] = {};
+  int64_t count[kCats] = {};
+
+ private:
+  struct Rec {
+    cudaEvent_t a, b;
+    int cat;
+    double flops, bytes;
+  };
+  std::vector<cudaEvent_t> pool_;
+  size_t next_ = 0;
+  std::vector<Rec> pending_;
+  cudaEvent_t open_ = nullptr;
+  cudaEvent_t get();
+};
+
 struct DeviceParams {
   float* master = nullptr;   // fp32 master (device order)
   void* compute = nullptr;   // parameters the kernels read (== master in fp32 mode)
@@ -107,6 +136,7 @@ class DeviceTape {
   const void* out(int id) const { return nodes_[id].out; }
   // number of our kernels launched so far (bench evidence)
   int64_t launches() const { return launches_; }
+  void set_profiler(Profiler* p) { prof_ = p; }
 
  private:
   struct Node {
@@ -140,6 +170,13 @@ class DeviceTape {
   cudaStream_t stream_;
   std::vector<Node> nodes_;
   int64_t launches_ = 0;
+  Profiler* prof_ = nullptr;
+  void pbegin() {
+    if (prof_) prof_->begin(stream_);
+  }
+  void pend(int cat, double flops, double bytes) {
+    if (prof_) prof_->end(stream_, cat, flops, bytes);
+  }
 
   void* alloc_elems(int64_t n) { return arena_.alloc(size_t(n) * esize_); }
   void* pptr(const ParamRef& p) const { return static_cast<char*>(params_.compute) + p.offset * esize_; }
@@ -148,7 +185,7 @@ class DeviceTape {
   std::pair<void*, bool> grad_of(int id);
   void backward_node(int id);
   void run_xent(Node& n, float seed, bool with_grad, double* stats_acc);
-  void gemm(int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
+  void gemm(int cat, int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
             bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias = nullptr, const void* res = nullptr,
             int64_t ldr = 0, const void* mask = nullptr, int64_t ldm = 0);
   void bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out);

