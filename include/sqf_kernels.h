@@ -71,6 +71,7 @@ typedef struct sfk_gemm_args {
   const void* mask; int64_t ldm;  /* [m x n]        (SFK_EPI_MASK)     */
   int flags;
   int force_simt;                 /* testing: run the SIMT kernel for any dtype */
+  int tile_n;                     /* tuning: force the tcgen05 tile width (64/128/256), 0 = auto */
 } sfk_gemm_args;
 
 int sfk_gemm(const sfk_gemm_args* g, void* stream);
@@ -107,6 +108,14 @@ int sfk_layernorm_bwd(int dtype, const void* x, const void* dy, int rows, int d,
                       const void* gamma, const float* stats, void* dx, int accumulate,
                       float* part, int* nparts, void* stream);
 
+/* Complete LN backward: dx as above plus dgamma = q(dgamma + sum dy*xh),
+ * dbeta = q(dbeta + sum dy), the column partials folded in a fixed order
+ * (deterministic) by one fold kernel for both vectors.
+ * part: >= 2*296*d floats scratch; counter: reserved (may be NULL). */
+int sfk_layernorm_bwd_fused(int dtype, const void* x, const void* dy, int rows, int d,
+                            const void* gamma, const float* stats, void* dx, int accumulate,
+                            float* part, int32_t* counter, void* dgamma, void* dbeta, void* stream);
+
 /* ------------------------------------------- column sums (bias grad, a11)
  * tape.cpp:347-358: db = q(db + sum_rows dy). Two deterministic passes:
  * sfk_colsum_partial writes part[nblk][n]; sfk_colsum_finish folds nblk
@@ -115,6 +124,10 @@ int sfk_colsum_partial(int dtype, const void* x, int rows, int n, int64_t ld,
                        float* part, int* nparts, void* stream);
 int sfk_colsum_finish(int dtype, const float* part, int nparts, int n, void* out,
                       void* stream);
+/* Both passes in one call: out = q(out + sum_rows x). part: >= 64*n floats
+ * scratch; counters: reserved (may be NULL). */
+int sfk_colsum(int dtype, const void* x, int rows, int n, int64_t ld, float* part,
+               int32_t* counters, void* out, void* stream);
 
 /* --------------------------------------------------- attention (a16/a17)
  * Multi-head attention over ragged per-sentence key spans (tape.cpp:229-258,

@@ -364,12 +364,10 @@ void DeviceTape::backward(int loss_node, float seed, double* stats_acc) {
 void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out) {
   const int max_parts = 64;
   float* part = static_cast<float*>(arena_.alloc(size_t(max_parts) * cols * 4));
-  int nparts = 0;
   pbegin();
-  sfk_check(sfk_colsum_partial(dtype_, dy, rows, cols, ld, part, &nparts, stream_), "colsum_partial");
-  sfk_check(sfk_colsum_finish(dtype_, part, nparts, cols, out, stream_), "colsum_finish");
+  sfk_check(sfk_colsum(dtype_, dy, rows, cols, ld, part, counters((cols + 1023) / 1024), out, stream_), "colsum");
   pend(Profiler::BiasGrad, 0, double(rows) * cols * esize_);
-  launches_ += 2;
+  launches_ += 1;
 }
 
 void DeviceTape::backward_node(int id) {
@@ -392,16 +390,12 @@ void DeviceTape::backward_node(int id) {
       auto [dx, fresh] = grad_of(n.in0);
       const int max_parts = 296;
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
-      int nparts = 0;
       pbegin();
-      sfk_check(sfk_layernorm_bwd(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx, fresh ? 0 : 1,
-                                  part, &nparts, stream_),
+      sfk_check(sfk_layernorm_bwd_fused(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx,
+                                        fresh ? 0 : 1, part, counters(1), gptr(n.p0), gptr(n.p1), stream_),
                 "layernorm_bwd");
-      sfk_check(sfk_colsum_finish(dtype_, part, nparts, n.cols, gptr(n.p0), stream_), "ln dgamma");
-      sfk_check(sfk_colsum_finish(dtype_, part + size_t(nparts) * n.cols, nparts, n.cols, gptr(n.p1), stream_),
-                "ln dbeta");
       pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
-      launches_ += 3;
+      launches_ += 1;
       return;
     }
     case Kind::Linear: {

@@ -137,6 +137,13 @@ class DeviceTape {
   // number of our kernels launched so far (bench evidence)
   int64_t launches() const { return launches_; }
   void set_profiler(Profiler* p) { prof_ = p; }
+  // pool of zeroed int32 counters for single-launch deterministic reductions
+  // (each user re-arms its slots to 0); handed out round-robin
+  void set_counters(int32_t* base, int64_t n, int64_t* cursor) {
+    ctr_base_ = base;
+    ctr_n_ = n;
+    ctr_cursor_ = cursor;
+  }
 
  private:
   struct Node {
@@ -171,6 +178,16 @@ class DeviceTape {
   std::vector<Node> nodes_;
   int64_t launches_ = 0;
   Profiler* prof_ = nullptr;
+  int32_t* ctr_base_ = nullptr;
+  int64_t ctr_n_ = 0;
+  int64_t* ctr_cursor_ = nullptr;
+  int32_t* counters(int k) {
+    if (!ctr_base_ || k > ctr_n_) throw DeviceError("device tape: no counter pool");
+    if (*ctr_cursor_ + k > ctr_n_) *ctr_cursor_ = 0;
+    int32_t* p = ctr_base_ + *ctr_cursor_;
+    *ctr_cursor_ += k;
+    return p;
+  }
   void pbegin() {
     if (prof_) prof_->begin(stream_);
   }

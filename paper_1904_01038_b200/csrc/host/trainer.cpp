@@ -39,6 +39,7 @@ Trainer::~Trainer() {
   cudaFree(pe_);
   cudaFree(stats_dev_);
   cudaFree(flag_dev_);
+  cudaFree(counters_);
   cudaFree(blob_dev_);
   cudaFreeHost(blob_host_);
   cudaFreeHost(readback_host_);
@@ -115,6 +116,8 @@ void Trainer::init(const Registry& reg) {
   }
   cuda_check(cudaMalloc(&stats_dev_, 4 * sizeof(double)), "stats");
   cuda_check(cudaMalloc(&flag_dev_, 16), "flag");
+  cuda_check(cudaMalloc(&counters_, size_t(kCounters) * 4), "counters");
+  cuda_check(cudaMemset(counters_, 0, size_t(kCounters) * 4), "counters");
   cuda_check(cudaMallocHost(&readback_host_, 64), "readback");
   push_params();
 }
@@ -292,6 +295,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     arena_.reset();
     DeviceTape tape(arena_, DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
     tape.set_profiler(prof_.get());
+    tape.set_counters(counters_, kCounters, &counter_cursor_);
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
     tape.backward(out.loss_node, float(scale), stats_dev_);
@@ -365,6 +369,7 @@ EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
     upload(packs, dev);
     arena_.reset();
     DeviceTape tape(arena_, DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    tape.set_counters(counters_, kCounters, &counter_cursor_);
     CriterionOutput c = criterion_->compute(*model_, dev[0], tape);
     tape.finish(c.loss_node, stats_dev_);
     cuda_check(cudaStreamSynchronize(stream_), "eval sync");  // staging buffer reuse

@@ -106,6 +106,9 @@ class Trainer {
   float* pe_ = nullptr;
   double* stats_dev_ = nullptr;    // loss, nll, ntokens, ncorrect
   int32_t* flag_dev_ = nullptr;
+  int32_t* counters_ = nullptr;    // zeroed pool for single-launch reductions
+  int64_t counter_cursor_ = 0;
+  static constexpr int64_t kCounters = 1 << 16;
   int32_t* blob_dev_ = nullptr;
   size_t blob_cap_ = 0;
   int32_t* blob_host_ = nullptr;   // pinned staging

@@ -221,6 +221,10 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_kv_k(P p, const T* __restrict
 }  // namespace attn
 }  // namespace sfk
 
+namespace sfk {
+int attention_mma(const sfk_attn_args* s, bool bwd, cudaStream_t st);
+}
+
 using namespace sfk;
 
 static int check_attn(const sfk_attn_args* a) {
@@ -234,6 +238,9 @@ static int check_attn(const sfk_attn_args* a) {
 
 extern "C" int sfk_attention_fwd(const sfk_attn_args* a, void* stream) {
   if (int e = check_attn(a)) return e;
+  if (a->batch * a->q_width == 0) return SFK_OK;
+  // fp16/bf16: tensor-core flash kernel; fp32 parity mode: exact SIMT kernel below
+  if (a->dtype != SFK_F32) return attention_mma(a, false, as_stream(stream));
   attn::P p{a->batch, a->q_width, a->k_width, a->heads, a->dh, a->causal, a->k_len, 1.0f / sqrtf(float(a->dh))};
   const int64_t warps = int64_t(a->batch) * a->q_width * a->heads;
   if (warps == 0) return SFK_OK;
@@ -249,6 +256,8 @@ extern "C" int sfk_attention_fwd(const sfk_attn_args* a, void* stream) {
 
 extern "C" int sfk_attention_bwd(const sfk_attn_args* a, void* stream) {
   if (int e = check_attn(a)) return e;
+  if (a->batch * a->q_width == 0) return SFK_OK;
+  if (a->dtype != SFK_F32) return attention_mma(a, true, as_stream(stream));
   attn::P p{a->batch, a->q_width, a->k_width, a->heads, a->dh, a->causal, a->k_len, 1.0f / sqrtf(float(a->dh))};
   const int64_t qwarps = int64_t(a->batch) * a->q_width * a->heads;
   const int64_t kwarps = int64_t(a->batch) * a->k_width * a->heads;

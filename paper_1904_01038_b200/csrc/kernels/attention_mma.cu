@@ -1,0 +1,549 @@
+// Tensor-core attention for fp16/bf16 (reference tape.cpp:229-258 forward,
+// 426-480 backward). Sentences are short (<= max_positions = 256) and ragged,
+// so each CTA owns one (sentence, head, 64-row block): the key/value (or
+// query/dO) rows of that sentence-head are staged whole in shared memory and
+// the products run on mma.sync m16n8k16 with fp32 accumulation:
+//   fwd      S = Q K^T -> online softmax -> O = P V          (per query block)
+//   bwd_dq   S, P (from saved {max, 1/sum}), dP = dO V^T,
+//            dS = P (dP - D), dQ = sc dS K;  D = rowsum(dO * O) (per query block)
+//   bwd_dkv  S^T = K Q^T, dP^T = V dO^T, dV = P^T dO, dK = sc dS^T Q (per key block)
+// Spans: query row t of sentence b sees keys j < (causal ? t+1 : len[b]).
+#include "common.cuh"
+
+namespace sfk {
+namespace fa {
+
+constexpr int kWarps = 4;
+constexpr int kRows = 16 * kWarps;  // rows per CTA block
+
+template <typename T>
+struct MmaT;
+template <>
+struct MmaT<__half> {
+  static __device__ __forceinline__ void mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+  static __device__ __forceinline__ uint32_t pack(float x, float y) {
+    __half2 h = __floats2half2_rn(x, y);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+template <>
+struct MmaT<__nv_bfloat16> {
+  static __device__ __forceinline__ void mma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+  static __device__ __forceinline__ uint32_t pack(float x, float y) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(su32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(su32(p)));
+}
+
+// A fragment (16x16) of a row-major smem tile at (r0, c0), row stride ld (elements)
+template <typename T>
+__device__ __forceinline__ void load_a(uint32_t (&a)[4], const T* s, int ld, int r0, int c0, int lane) {
+  const int r = r0 + (lane & 7) + ((lane >> 3) & 1) * 8, c = c0 + (lane >> 4) * 8;
+  ldsm_x4(a, s + r * ld + c);
+}
+// B fragments for two n8 tiles (n0, n0+8), k16 at k0, from smem stored [n][k] (k contiguous)
+template <typename T>
+__device__ __forceinline__ void load_b_nk(uint32_t (&b)[4], const T* s, int ld, int n0, int k0, int lane) {
+  const int r = n0 + (lane & 7) + (lane >> 4) * 8, c = k0 + ((lane >> 3) & 1) * 8;
+  ldsm_x4(b, s + r * ld + c);  // b[0],b[1]: tile n0 ; b[2],b[3]: tile n0+8
+}
+// B fragments for two n8 tiles from smem stored [k][n] (n contiguous): transposed load
+template <typename T>
+__device__ __forceinline__ void load_b_kn(uint32_t (&b)[4], const T* s, int ld, int k0, int n0, int lane) {
+  const int r = k0 + (lane & 7) + ((lane >> 3) & 1) * 8, c = n0 + (lane >> 4) * 8;
+  ldsm_x4_t(b, s + r * ld + c);
+}
+
+// copy rows [r0, r0+n) x dh of a strided global matrix into smem rows [0, rows_pad) x DH (zero padded)
+template <typename T, int DH>
+__device__ __forceinline__ void stage(T* s, int lds, const T* g, int64_t ldg, int r0, int n, int rows_pad, int dh) {
+  constexpr int V = 8;  // 16-byte vectors
+  const int vpr = DH / V;
+  for (int i = threadIdx.x; i < rows_pad * vpr; i += blockDim.x) {
+    const int r = i / vpr, c = (i % vpr) * V;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < n && c < dh) v = *reinterpret_cast<const uint4*>(g + int64_t(r0 + r) * ldg + c);
+    *reinterpret_cast<uint4*>(s + r * lds + c) = v;
+  }
+}
+
+struct Args {
+  int batch, qw, kw, heads, dh, causal;
+  const int32_t* klen;
+  float sc;
+  const void *q, *k, *v, *o, *dout;
+  int64_t ldq, ldk, ldv, ldo, lddo;
+  void *out, *dq, *dk, *dv;
+  int64_t ldout, lddq, lddk, lddv;
+  float2* stats;
+  float* dsum;
+};
+
+__device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.causal ? t + 1 : a.klen[b]; }
+
+// ------------------------------------------------------------------ forward
+template <typename T, int DH>
+__global__ void __launch_bounds__(kWarps * 32) fwd_k(Args a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int LD = DH + 8;
+  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kRows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
+  const int len = a.causal ? a.kw : a.klen[b];
+  // keys any row of this block can see
+  const int nk = a.causal ? min(a.kw, min(q0 + kRows, a.qw)) : len;
+  const int nk_pad = (nk + 63) & ~63;
+  T* Qs = reinterpret_cast<T*>(smem);
+  T* Ks = Qs + kRows * LD;
+  T* Vs = Ks + nk_pad * LD;
+  const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
+  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0) + q0, min(kRows, a.qw - q0), kRows,
+               a.dh);
+  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), nk, nk_pad, a.dh);
+  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), nk, nk_pad, a.dh);
+  __syncthreads();
+  const int r0 = warp * 16;
+  if (q0 + r0 >= a.qw) return;
+  uint32_t qa[DH / 16][4];
+#pragma unroll
+  for (int ks = 0; ks < DH / 16; ++ks) load_a<T>(qa[ks], Qs, LD, r0, ks * 16, lane);
+  const int row_a = q0 + r0 + g, row_b = row_a + 8;  // the two rows this thread holds
+  const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 1;
+  const int lim_b = row_b < a.qw ? (a.causal ? row_b + 1 : len) : 1;
+  const int warp_keys = a.causal ? min(a.qw, q0 + r0 + 16) : len;
+  const float l2e = 1.4426950408889634f;
+  float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+  float o[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  for (int kc = 0; kc < warp_keys; kc += 64) {
+    float s[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < 8; nt += 2) {
+        uint32_t bb[4];
+        load_b_nk<T>(bb, Ks, LD, kc + nt * 8, ks * 16, lane);
+        MmaT<T>::mma(s[nt], qa[ks], bb[0], bb[1]);
+        MmaT<T>::mma(s[nt + 1], qa[ks], bb[2], bb[3]);
+      }
+    float mx_a = m_a, mx_b = m_b;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = kc + nt * 8 + 2 * tq + e;
+        s[nt][e] = j < lim_a ? s[nt][e] * a.sc : -INFINITY;
+        s[nt][2 + e] = j < lim_b ? s[nt][2 + e] * a.sc : -INFINITY;
+        mx_a = fmaxf(mx_a, s[nt][e]);
+        mx_b = fmaxf(mx_b, s[nt][2 + e]);
+      }
+#pragma unroll
+    for (int off = 1; off < 4; off <<= 1) {
+      mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, off));
+      mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, off));
+    }
+    const float al_a = exp2f((m_a - mx_a) * l2e), al_b = exp2f((m_b - mx_b) * l2e);
+    m_a = mx_a;
+    m_b = mx_b;
+    float rs_a = 0.f, rs_b = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      s[nt][0] = exp2f((s[nt][0] - m_a) * l2e);
+      s[nt][1] = exp2f((s[nt][1] - m_a) * l2e);
+      s[nt][2] = exp2f((s[nt][2] - m_b) * l2e);
+      s[nt][3] = exp2f((s[nt][3] - m_b) * l2e);
+      rs_a += s[nt][0] + s[nt][1];
+      rs_b += s[nt][2] + s[nt][3];
+    }
+    l_a = l_a * al_a + rs_a;
+    l_b = l_b * al_b + rs_b;
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) {
+      o[i][0] *= al_a;
+      o[i][1] *= al_a;
+      o[i][2] *= al_b;
+      o[i][3] *= al_b;
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {  // 16 keys per k-step
+      uint32_t pa[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
+                        MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                        MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+      for (int nt = 0; nt < DH / 8; nt += 2) {
+        uint32_t bb[4];
+        load_b_kn<T>(bb, Vs, LD, kc + kk * 16, nt * 8, lane);
+        MmaT<T>::mma(o[nt], pa, bb[0], bb[1]);
+        MmaT<T>::mma(o[nt + 1], pa, bb[2], bb[3]);
+      }
+    }
+  }
+  l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+  l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+  l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+  l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+  const float ia = 1.0f / l_a, ib = 1.0f / l_b;
+  T* out = static_cast<T*>(a.out) + h * a.dh;
+#pragma unroll
+  for (int nt = 0; nt < DH / 8; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (c >= a.dh) continue;
+    if (row_a < a.qw)
+      *reinterpret_cast<uint32_t*>(out + (qrow0 + row_a) * a.ldout + c) = MmaT<T>::pack(o[nt][0] * ia, o[nt][1] * ia);
+    if (row_b < a.qw)
+      *reinterpret_cast<uint32_t*>(out + (qrow0 + row_b) * a.ldout + c) = MmaT<T>::pack(o[nt][2] * ib, o[nt][3] * ib);
+  }
+  if (tq == 0) {
+    if (row_a < a.qw) a.stats[(qrow0 + row_a) * a.heads + h] = make_float2(m_a, ia);
+    if (row_b < a.qw) a.stats[(qrow0 + row_b) * a.heads + h] = make_float2(m_b, ib);
+  }
+}
+
+// ------------------------------------------------------------------ backward: dQ (+ D)
+template <typename T, int DH>
+__global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int LD = DH + 8;
+  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kRows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
+  const int len = a.causal ? a.kw : a.klen[b];
+  const int nk = a.causal ? min(a.kw, min(q0 + kRows, a.qw)) : len;
+  const int nk_pad = (nk + 63) & ~63;
+  T* Qs = reinterpret_cast<T*>(smem);
+  T* Gs = Qs + kRows * LD;  // dO
+  T* Ks = Gs + kRows * LD;
+  T* Vs = Ks + nk_pad * LD;
+  const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
+  const int nq = min(kRows, a.qw - q0);
+  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0) + q0, nq, kRows, a.dh);
+  stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0) + q0, nq, kRows, a.dh);
+  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), nk, nk_pad, a.dh);
+  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), nk, nk_pad, a.dh);
+  __syncthreads();
+  const int r0 = warp * 16;
+  if (q0 + r0 >= a.qw) return;
+  const int row_a = q0 + r0 + g, row_b = row_a + 8;
+  // D = rowsum(dO * O) for the two rows (4 threads of a quad split the columns)
+  float D_a = 0.f, D_b = 0.f;
+  {
+    const T* O = static_cast<const T*>(a.o) + h * a.dh;
+    for (int c = tq; c < a.dh; c += 4) {
+      if (row_a < a.qw)
+        D_a += Num<T>::ld(Gs + (r0 + g) * LD + c) * Num<T>::ld(O + (qrow0 + row_a) * a.ldo + c);
+      if (row_b < a.qw)
+        D_b += Num<T>::ld(Gs + (r0 + g + 8) * LD + c) * Num<T>::ld(O + (qrow0 + row_b) * a.ldo + c);
+    }
+    D_a += __shfl_xor_sync(0xffffffffu, D_a, 1);
+    D_a += __shfl_xor_sync(0xffffffffu, D_a, 2);
+    D_b += __shfl_xor_sync(0xffffffffu, D_b, 1);
+    D_b += __shfl_xor_sync(0xffffffffu, D_b, 2);
+    if (tq == 0) {
+      if (row_a < a.qw) a.dsum[(qrow0 + row_a) * a.heads + h] = D_a;
+      if (row_b < a.qw) a.dsum[(qrow0 + row_b) * a.heads + h] = D_b;
+    }
+  }
+  uint32_t qa[DH / 16][4], ga[DH / 16][4];
+#pragma unroll
+  for (int ks = 0; ks < DH / 16; ++ks) {
+    load_a<T>(qa[ks], Qs, LD, r0, ks * 16, lane);
+    load_a<T>(ga[ks], Gs, LD, r0, ks * 16, lane);
+  }
+  const float2 st_a = row_a < a.qw ? a.stats[(qrow0 + row_a) * a.heads + h] : make_float2(0.f, 0.f);
+  const float2 st_b = row_b < a.qw ? a.stats[(qrow0 + row_b) * a.heads + h] : make_float2(0.f, 0.f);
+  const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 0;
+  const int lim_b = row_b < a.qw ? (a.causal ? row_b + 1 : len) : 0;
+  const int warp_keys = a.causal ? min(a.qw, q0 + r0 + 16) : len;
+  const float l2e = 1.4426950408889634f;
+  float dq[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+  for (int kc = 0; kc < warp_keys; kc += 64) {
+    float s[8][4], dp[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < 8; nt += 2) {
+        uint32_t bk[4], bv[4];
+        load_b_nk<T>(bk, Ks, LD, kc + nt * 8, ks * 16, lane);
+        load_b_nk<T>(bv, Vs, LD, kc + nt * 8, ks * 16, lane);
+        MmaT<T>::mma(s[nt], qa[ks], bk[0], bk[1]);
+        MmaT<T>::mma(s[nt + 1], qa[ks], bk[2], bk[3]);
+        MmaT<T>::mma(dp[nt], ga[ks], bv[0], bv[1]);
+        MmaT<T>::mma(dp[nt + 1], ga[ks], bv[2], bv[3]);
+      }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = kc + nt * 8 + 2 * tq + e;
+        const float pa = j < lim_a ? exp2f((s[nt][e] * a.sc - st_a.x) * l2e) * st_a.y : 0.f;
+        const float pb = j < lim_b ? exp2f((s[nt][2 + e] * a.sc - st_b.x) * l2e) * st_b.y : 0.f;
+        s[nt][e] = pa * (dp[nt][e] - D_a);
+        s[nt][2 + e] = pb * (dp[nt][2 + e] - D_b);
+      }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t da[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
+                        MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                        MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+      for (int nt = 0; nt < DH / 8; nt += 2) {
+        uint32_t bb[4];
+        load_b_kn<T>(bb, Ks, LD, kc + kk * 16, nt * 8, lane);
+        MmaT<T>::mma(dq[nt], da, bb[0], bb[1]);
+        MmaT<T>::mma(dq[nt + 1], da, bb[2], bb[3]);
+      }
+    }
+  }
+  T* out = static_cast<T*>(a.dq) + h * a.dh;
+#pragma unroll
+  for (int nt = 0; nt < DH / 8; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (c >= a.dh) continue;
+    if (row_a < a.qw)
+      *reinterpret_cast<uint32_t*>(out + (qrow0 + row_a) * a.lddq + c) =
+          MmaT<T>::pack(dq[nt][0] * a.sc, dq[nt][1] * a.sc);
+    if (row_b < a.qw)
+      *reinterpret_cast<uint32_t*>(out + (qrow0 + row_b) * a.lddq + c) =
+          MmaT<T>::pack(dq[nt][2] * a.sc, dq[nt][3] * a.sc);
+  }
+}
+
+// ------------------------------------------------------------------ backward: dK, dV
+template <typename T, int DH>
+__global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int LD = DH + 8;
+  constexpr int NC = DH >= 128 ? 32 : 64;  // query columns per chunk (register budget)
+  const int b = blockIdx.z, h = blockIdx.y, k0 = blockIdx.x * kRows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
+  const int len = a.causal ? a.kw : a.klen[b];
+  const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
+  // queries that can see a key of this block
+  const int qstart = a.causal ? k0 : 0;
+  const int nq = max(0, a.qw - qstart);
+  // +64: a warp's chunks start at its first key row (r0) and run NC past nq
+  const int nq_pad = ((nq + 63) & ~63) + 64;
+  T* Ks = reinterpret_cast<T*>(smem);
+  T* Vs = Ks + kRows * LD;
+  T* Qs = Vs + kRows * LD;
+  T* Gs = Qs + nq_pad * LD;
+  float2* St = reinterpret_cast<float2*>(Gs + nq_pad * LD);
+  float* Ds = reinterpret_cast<float*>(St + nq_pad);
+  const int nk = min(kRows, a.kw - k0);
+  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0) + k0, nk, kRows, a.dh);
+  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0) + k0, nk, kRows, a.dh);
+  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0) + qstart, nq, nq_pad, a.dh);
+  stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0) + qstart, nq, nq_pad, a.dh);
+  for (int i = threadIdx.x; i < nq_pad; i += blockDim.x) {
+    const bool ok = i < nq;
+    St[i] = ok ? a.stats[(qrow0 + qstart + i) * a.heads + h] : make_float2(0.f, 0.f);
+    Ds[i] = ok ? a.dsum[(qrow0 + qstart + i) * a.heads + h] : 0.f;
+  }
+  __syncthreads();
+  const int r0 = warp * 16;
+  if (k0 + r0 >= a.kw) return;
+  const int key_a = k0 + r0 + g, key_b = key_a + 8;
+  float dk[DH / 8][4], dv[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
+  // non-causal: keys at or beyond len are never attended
+  const bool any = a.causal ? true : (k0 + r0 < len);
+  if (any) {
+    uint32_t ka[DH / 16][4], va[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      load_a<T>(ka[ks], Ks, LD, r0, ks * 16, lane);
+      load_a<T>(va[ks], Vs, LD, r0, ks * 16, lane);
+    }
+    const float l2e = 1.4426950408889634f;
+    // causal: queries before this warp's first key never see it
+    const int qbeg = a.causal ? ((k0 + r0 - qstart) & ~15) : 0;
+    for (int qc = qbeg; qc < nq; qc += NC) {
+      float s[NC / 8][4], dp[NC / 8][4];
+#pragma unroll
+      for (int i = 0; i < NC / 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < NC / 8; nt += 2) {
+          uint32_t bq[4], bg[4];
+          load_b_nk<T>(bq, Qs, LD, qc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bg, Gs, LD, qc + nt * 8, ks * 16, lane);
+          MmaT<T>::mma(s[nt], ka[ks], bq[0], bq[1]);
+          MmaT<T>::mma(s[nt + 1], ka[ks], bq[2], bq[3]);
+          MmaT<T>::mma(dp[nt], va[ks], bg[0], bg[1]);
+          MmaT<T>::mma(dp[nt + 1], va[ks], bg[2], bg[3]);
+        }
+      // s: rows = keys (key_a / key_b), cols = queries qstart + qc + nt*8 + 2tq + e
+      float p[NC / 8][4];
+#pragma unroll
+      for (int nt = 0; nt < NC / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int qi = qc + nt * 8 + 2 * tq + e;  // index into staged queries
+          const int t = qstart + qi;               // query position
+          const float2 st = St[qi];
+          const float D = Ds[qi];
+          const bool qok = qi < nq;
+          const bool va_ok = qok && key_a < a.kw && (a.causal ? key_a <= t : key_a < len);
+          const bool vb_ok = qok && key_b < a.kw && (a.causal ? key_b <= t : key_b < len);
+          const float pa = va_ok ? exp2f((s[nt][e] * a.sc - st.x) * l2e) * st.y : 0.f;
+          const float pb = vb_ok ? exp2f((s[nt][2 + e] * a.sc - st.x) * l2e) * st.y : 0.f;
+          p[nt][e] = pa;
+          p[nt][2 + e] = pb;
+          s[nt][e] = pa * (dp[nt][e] - D);
+          s[nt][2 + e] = pb * (dp[nt][2 + e] - D);
+        }
+#pragma unroll
+      for (int kk = 0; kk < NC / 16; ++kk) {
+        uint32_t pa[4] = {MmaT<T>::pack(p[2 * kk][0], p[2 * kk][1]), MmaT<T>::pack(p[2 * kk][2], p[2 * kk][3]),
+                          MmaT<T>::pack(p[2 * kk + 1][0], p[2 * kk + 1][1]),
+                          MmaT<T>::pack(p[2 * kk + 1][2], p[2 * kk + 1][3])};
+        uint32_t da[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
+                          MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                          MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+        for (int nt = 0; nt < DH / 8; nt += 2) {
+          uint32_t bg[4], bq[4];
+          load_b_kn<T>(bg, Gs, LD, qc + kk * 16, nt * 8, lane);
+          load_b_kn<T>(bq, Qs, LD, qc + kk * 16, nt * 8, lane);
+          MmaT<T>::mma(dv[nt], pa, bg[0], bg[1]);
+          MmaT<T>::mma(dv[nt + 1], pa, bg[2], bg[3]);
+          MmaT<T>::mma(dk[nt], da, bq[0], bq[1]);
+          MmaT<T>::mma(dk[nt + 1], da, bq[2], bq[3]);
+        }
+      }
+    }
+  }
+  T* dko = static_cast<T*>(a.dk) + h * a.dh;
+  T* dvo = static_cast<T*>(a.dv) + h * a.dh;
+#pragma unroll
+  for (int nt = 0; nt < DH / 8; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (c >= a.dh) continue;
+    if (key_a < a.kw) {
+      *reinterpret_cast<uint32_t*>(dko + (krow0 + key_a) * a.lddk + c) =
+          MmaT<T>::pack(dk[nt][0] * a.sc, dk[nt][1] * a.sc);
+      *reinterpret_cast<uint32_t*>(dvo + (krow0 + key_a) * a.lddv + c) = MmaT<T>::pack(dv[nt][0], dv[nt][1]);
+    }
+    if (key_b < a.kw) {
+      *reinterpret_cast<uint32_t*>(dko + (krow0 + key_b) * a.lddk + c) =
+          MmaT<T>::pack(dk[nt][2] * a.sc, dk[nt][3] * a.sc);
+      *reinterpret_cast<uint32_t*>(dvo + (krow0 + key_b) * a.lddv + c) = MmaT<T>::pack(dv[nt][2], dv[nt][3]);
+    }
+  }
+}
+
+template <typename T, int DH>
+int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
+  Args a{};
+  a.batch = s->batch;
+  a.qw = s->q_width;
+  a.kw = s->k_width;
+  a.heads = s->heads;
+  a.dh = s->dh;
+  a.causal = s->causal;
+  a.klen = s->k_len;
+  a.sc = 1.0f / sqrtf(float(s->dh));
+  a.q = s->q;
+  a.k = s->k;
+  a.v = s->v;
+  a.o = s->o;
+  a.dout = s->dout;
+  a.ldq = s->ldq;
+  a.ldk = s->ldk;
+  a.ldv = s->ldv;
+  a.ldo = s->ldo;
+  a.lddo = s->lddo;
+  a.out = s->o;
+  a.ldout = s->ldo;
+  a.dq = s->dq;
+  a.lddq = s->lddq;
+  a.dk = s->dk;
+  a.lddk = s->lddk;
+  a.dv = s->dv;
+  a.lddv = s->lddv;
+  a.stats = reinterpret_cast<float2*>(s->stats);
+  a.dsum = s->scratch;
+  constexpr int LD = DH + 8;
+  const int kpad = (a.kw + 63) & ~63, qpad = ((a.qw + 63) & ~63) + 64;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(fwd_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_dq_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = true;
+  }
+  const dim3 gq((a.qw + kRows - 1) / kRows, a.heads, a.batch);
+  if (!bwd) {
+    const size_t smem = size_t(kRows + 2 * kpad) * LD * sizeof(T);
+    fwd_k<T, DH><<<gq, kWarps * 32, smem, st>>>(a);
+    return check_launch("sfk_attention_fwd(mma)");
+  }
+  const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
+  bwd_dq_k<T, DH><<<gq, kWarps * 32, smem_q, st>>>(a);
+  if (int e = check_launch("sfk_attention_bwd(dq)")) return e;
+  const dim3 gk((a.kw + kRows - 1) / kRows, a.heads, a.batch);
+  const size_t smem_k = size_t(2 * kRows + 2 * qpad) * LD * sizeof(T) + size_t(qpad) * 12;
+  bwd_dkv_k<T, DH><<<gk, kWarps * 32, smem_k, st>>>(a);
+  return check_launch("sfk_attention_bwd(dkv)");
+}
+
+template <typename T>
+int dispatch_dh(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
+  if (s->dh <= 16) return run<T, 16>(s, bwd, st);
+  if (s->dh <= 32) return run<T, 32>(s, bwd, st);
+  if (s->dh <= 64) return run<T, 64>(s, bwd, st);
+  return run<T, 128>(s, bwd, st);
+}
+
+}  // namespace fa
+
+// entry used by attention.cu for fp16/bf16
+int attention_mma(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
+  if (s->dh % 8 != 0 || s->dh > 128 || (s->ldq % 8) || (s->ldk % 8) || (s->ldv % 8) || (s->ldo % 8) ||
+      (bwd && ((s->lddo % 8) || (s->lddq % 2) || (s->lddk % 2) || (s->lddv % 2)))) {
+    set_error("sfk_attention(mma): dh must be a multiple of 8 (<= 128) and rows 16-byte aligned");
+    return SFK_EINVAL;
+  }
+  if (s->dtype == SFK_F16) return fa::dispatch_dh<__half>(s, bwd, st);
+  return fa::dispatch_dh<__nv_bfloat16>(s, bwd, st);
+}
+
+}  // namespace sfk

@@ -236,13 +236,141 @@ __device__ __forceinline__ void epilogue_row32(const Epi& e, int64_t row, int co
   for (int i = 0; i < 32 && col0 + i < N; ++i) Num<T>::st(out + i, epi_value<T>(e, row, col0 + i, v[i]));
 }
 
+// 8 consecutive accumulators of one row (coalesced layout) -> fused epilogue -> global
+template <typename T>
+__device__ __forceinline__ void epilogue8(const Epi& e, int64_t row, int col, int N, float (&v)[8], bool vec_ok) {
+  T* out = static_cast<T*>(e.c) + row * e.ldc + col;
+  if (!vec_ok || col + 8 > N) {
+    for (int i = 0; i < 8 && col + i < N; ++i) Num<T>::st(out + i, epi_value<T>(e, row, col + i, v[i]));
+    return;
+  }
+  auto ld8 = [](const T* p, float (&f)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 t = Pack<T>::unpack(w[j]);
+      f[2 * j] = t.x;
+      f[2 * j + 1] = t.y;
+    }
+  };
+  const int fl = e.flags;
+  if (fl & SFK_EPI_ACCUM) {
+    float o[8];
+    ld8(out, o);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = o[j] + v[j];
+  } else {
+    if (fl & SFK_EPI_PREROUND)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = Num<T>::rnd(v[j]);
+    if (fl & SFK_EPI_BIAS) {
+      float b[8];
+      ld8(static_cast<const T*>(e.bias) + col, b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = Num<T>::rnd(v[j] + b[j]);
+    }
+    if (fl & SFK_EPI_RELU)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = v[j] > 0.0f ? v[j] : 0.0f;
+    if (fl & SFK_EPI_MASK) {
+      float mk[8];
+      ld8(static_cast<const T*>(e.mask) + row * e.ldm + col, mk);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = mk[j] > 0.0f ? Num<T>::rnd(v[j]) : 0.0f;
+    }
+    if (fl & SFK_EPI_RESIDUAL) {
+      float rs[8];
+      ld8(static_cast<const T*>(e.res) + row * e.ldr + col, rs);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = Num<T>::rnd(rs[j] + v[j]);
+    }
+  }
+  *reinterpret_cast<uint4*>(out) = make_uint4(Pack<T>::two(v[0], v[1]), Pack<T>::two(v[2], v[3]),
+                                              Pack<T>::two(v[4], v[5]), Pack<T>::two(v[6], v[7]));
+}
+
+constexpr int kStg = 36;  // staging row stride (floats): conflict-free float4 writes and reads
+
+// Four row segments (rows row0 + 8i, i<4) x 8 columns, all loads of side
+// inputs issued before any math so their latencies overlap.
+template <typename T>
+__device__ __forceinline__ void epilogue_seg4(const Epi& e, int64_t row0, int col, int M, const float* stg) {
+  const int fl = e.flags;
+  float v[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float4 a = *reinterpret_cast<const float4*>(stg + 8 * i * kStg);
+    const float4 b = *reinterpret_cast<const float4*>(stg + 8 * i * kStg + 4);
+    v[i][0] = a.x, v[i][1] = a.y, v[i][2] = a.z, v[i][3] = a.w, v[i][4] = b.x, v[i][5] = b.y, v[i][6] = b.z,
+    v[i][7] = b.w;
+  }
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  uint4 side[4] = {z, z, z, z}, side2[4] = {z, z, z, z}, bias = z;
+  T* out = static_cast<T*>(e.c);
+  if (fl & SFK_EPI_BIAS) bias = *reinterpret_cast<const uint4*>(static_cast<const T*>(e.bias) + col);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = row0 + 8 * i;
+    if (row >= M) continue;
+    if (fl & SFK_EPI_ACCUM) side[i] = *reinterpret_cast<const uint4*>(out + row * e.ldc + col);
+    if (fl & SFK_EPI_RESIDUAL)
+      side[i] = *reinterpret_cast<const uint4*>(static_cast<const T*>(e.res) + row * e.ldr + col);
+    if (fl & SFK_EPI_MASK)
+      side2[i] = *reinterpret_cast<const uint4*>(static_cast<const T*>(e.mask) + row * e.ldm + col);
+  }
+  auto unpack = [](const uint4& u, float (&f)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 t = Pack<T>::unpack(w[j]);
+      f[2 * j] = t.x;
+      f[2 * j + 1] = t.y;
+    }
+  };
+  float bf[8];
+  unpack(bias, bf);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t row = row0 + 8 * i;
+    if (row >= M) continue;
+    float s1[8], s2[8];
+    unpack(side[i], s1);
+    unpack(side2[i], s2);
+    float* x = v[i];
+    if (fl & SFK_EPI_ACCUM) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = s1[j] + x[j];
+    } else {
+      if (fl & SFK_EPI_PREROUND)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = Num<T>::rnd(x[j]);
+      if (fl & SFK_EPI_BIAS)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = Num<T>::rnd(x[j] + bf[j]);
+      if (fl & SFK_EPI_RELU)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = x[j] > 0.0f ? x[j] : 0.0f;
+      if (fl & SFK_EPI_MASK)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = s2[j] > 0.0f ? Num<T>::rnd(x[j]) : 0.0f;
+      if (fl & SFK_EPI_RESIDUAL)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = Num<T>::rnd(s1[j] + x[j]);
+    }
+    *reinterpret_cast<uint4*>(out + row * e.ldc + col) =
+        make_uint4(Pack<T>::two(x[0], x[1]), Pack<T>::two(x[2], x[3]), Pack<T>::two(x[4], x[5]),
+                   Pack<T>::two(x[6], x[7]));
+  }
+}
+
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (192 * 1024) / STAGE;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/ + 4 * 32 * kStg * 4;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -345,20 +473,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
+    // Epilogue: TMEM gives each thread one row x 32 columns; bounce the 32x32
+    // fp32 block through shared memory so a warp then reads/writes 8 rows x
+    // 64 contiguous bytes per instruction (coalesced) instead of 32 rows.
     const int quarter = warp & 3;
-    const int row_in_tile = quarter * 32 + lane;
+    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * (32 * kStg);
     int t = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
-      const int64_t row = m0 + row_in_tile;
 #pragma unroll 1
       for (int ch = 0; ch < BN / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + buf * BN + ch * 32, r);
-        if (row < M && n0 + ch * 32 < N) epilogue_row32<T>(e, row, n0 + ch * 32, N, r, vec_ok != 0);
+        if (n0 + ch * 32 >= N) continue;  // warp-uniform
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(stg + lane * kStg + 4 * j) =
+              make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                          __uint_as_float(r[4 * j + 3]));
+        __syncwarp();
+        const int cc = (lane & 3) * 8, col = n0 + ch * 32 + cc;
+        const int64_t row0 = m0 + quarter * 32 + (lane >> 2);
+        if (vec_ok && col + 8 <= N) {
+          epilogue_seg4<T>(e, row0, col, M, stg + (lane >> 2) * kStg + cc);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = (lane >> 2) + 8 * i;
+            const int64_t row = row0 + 8 * i;
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = stg[rr * kStg + cc + j];
+            if (row < M && col < N) epilogue8<T>(e, row, col, N, v, false);
+          }
+        }
+        __syncwarp();
       }
       fence_before();
       __syncwarp();
@@ -463,7 +615,7 @@ int pick_bn(int m, int n) {
 
 template <typename T>
 int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
-  const int bn = pick_bn(g->m, g->n);
+  const int bn = g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
 #define SFK_TC(BNV)                                                    \
   switch (layout) {                                                    \

@@ -325,12 +325,53 @@ __global__ void xent_reduce_k(const float* __restrict__ row_out, int rows, doubl
 
 }  // namespace sfk
 
+namespace sfk {
+int embed_fwd_vec(int, const int32_t*, int, int, int, const void*, const float*, float, void*, cudaStream_t);
+int embed_bwd_vec(int, const int32_t*, const int32_t*, const int32_t*, int, int, const void*, float, void*,
+                  cudaStream_t);
+int ln_fwd_vec(int, const void*, int, int, const void*, const void*, void*, float*, cudaStream_t);
+int ln_bwd_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*, int*,
+               cudaStream_t);
+int colsum_partial_vec(int, const void*, int, int, int64_t, float*, int*, cudaStream_t);
+int ln_bwd_fused_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*,
+                     int32_t*, void*, void*, cudaStream_t);
+int colsum_fused_vec(int, const void*, int, int, int64_t, float*, int32_t*, void*, cudaStream_t);
+}  // namespace sfk
+
+extern "C" int sfk_layernorm_bwd_fused(int dtype, const void* x, const void* dy, int rows, int d, const void* gamma,
+                                       const float* stats, void* dx, int accumulate, float* part, int32_t* counter,
+                                       void* dgamma, void* dbeta, void* stream) {
+  if (rows == 0) return SFK_OK;
+  cudaStream_t s = sfk::as_stream(stream);
+  if (int e = sfk::ln_bwd_fused_vec(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, part, counter, dgamma, dbeta,
+                                    s);
+      e != SFK_EUNSUP)
+    return e;
+  int nparts = 0;
+  if (int e = sfk_layernorm_bwd(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, part, &nparts, stream)) return e;
+  if (int e = sfk_colsum_finish(dtype, part, nparts, d, dgamma, stream)) return e;
+  return sfk_colsum_finish(dtype, part + size_t(nparts) * d, nparts, d, dbeta, stream);
+}
+
+extern "C" int sfk_colsum(int dtype, const void* x, int rows, int n, int64_t ld, float* part, int32_t* counters,
+                          void* out, void* stream) {
+  if (rows == 0 || n == 0) return SFK_OK;
+  if (int e = sfk::colsum_fused_vec(dtype, x, rows, n, ld, part, counters, out, sfk::as_stream(stream));
+      e != SFK_EUNSUP)
+    return e;
+  int nparts = 0;
+  if (int e = sfk_colsum_partial(dtype, x, rows, n, ld, part, &nparts, stream)) return e;
+  return sfk_colsum_finish(dtype, part, nparts, n, out, stream);
+}
+
 using namespace sfk;
 
 extern "C" int sfk_embed_fwd(int dtype, const int32_t* ids, int rows, int width, int d, const void* table,
                              const float* pe, float scale, void* out, void* stream) {
   if (rows == 0) return SFK_OK;
   if (rows < 0 || width <= 0 || d <= 0) return SFK_EINVAL;
+  if (int e = embed_fwd_vec(dtype, ids, rows, width, d, table, pe, scale, out, as_stream(stream)); e != SFK_EUNSUP)
+    return e;
   SFK_DISPATCH(dtype, T,
                embed_fwd_k<T><<<rows, 128, 0, as_stream(stream)>>>(ids, rows, width, d, static_cast<const T*>(table),
                                                                     pe, scale, static_cast<T*>(out)));
@@ -340,6 +381,9 @@ extern "C" int sfk_embed_fwd(int dtype, const int32_t* ids, int rows, int width,
 extern "C" int sfk_embed_bwd(int dtype, const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_rows,
                              int nuniq, int d, const void* dx, float scale, void* grad, void* stream) {
   if (nuniq == 0) return SFK_OK;
+  if (int e = embed_bwd_vec(dtype, uniq, seg_off, seg_rows, nuniq, d, dx, scale, grad, as_stream(stream));
+      e != SFK_EUNSUP)
+    return e;
   SFK_DISPATCH(dtype, T,
                embed_bwd_k<T><<<nuniq, 128, 0, as_stream(stream)>>>(uniq, seg_off, seg_rows, d,
                                                                     static_cast<const T*>(dx), scale,
@@ -354,6 +398,7 @@ extern "C" int sfk_layernorm_fwd(int dtype, const void* x, int rows, int d, cons
     set_error("sfk_layernorm_fwd: d > 1024 unsupported");
     return SFK_EUNSUP;
   }
+  if (int e = ln_fwd_vec(dtype, x, rows, d, gamma, beta, y, stats, as_stream(stream)); e != SFK_EUNSUP) return e;
   const int blocks = (rows + 7) / 8;
   SFK_DISPATCH(dtype, T,
                ln_fwd_k<T><<<blocks, 256, 0, as_stream(stream)>>>(
@@ -369,6 +414,13 @@ extern "C" int sfk_layernorm_bwd(int dtype, const void* x, const void* dy, int r
     set_error("sfk_layernorm_bwd: d > 1024 unsupported");
     return SFK_EUNSUP;
   }
+  if (rows == 0) {
+    *nparts = 0;
+    return SFK_OK;
+  }
+  if (int e = ln_bwd_vec(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, part, nparts, as_stream(stream));
+      e != SFK_EUNSUP)
+    return e;
   int nblk = (rows + 31) / 32;
   if (nblk > 296) nblk = 296;
   if (nblk < 1) nblk = 1;
@@ -383,6 +435,7 @@ extern "C" int sfk_layernorm_bwd(int dtype, const void* x, const void* dy, int r
 
 extern "C" int sfk_colsum_partial(int dtype, const void* x, int rows, int n, int64_t ld, float* part, int* nparts,
                                   void* stream) {
+  if (int e = colsum_partial_vec(dtype, x, rows, n, ld, part, nparts, as_stream(stream)); e != SFK_EUNSUP) return e;
   int nblk = (rows + 63) / 64;
   if (nblk > 64) nblk = 64;
   if (nblk < 1) nblk = 1;

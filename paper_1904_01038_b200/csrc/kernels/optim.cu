@@ -41,6 +41,49 @@ __global__ void adam_k(float* __restrict__ master, S* __restrict__ shadow, const
   }
 }
 
+// 4 elements per thread per iteration: vector loads of the fp32 state and
+// the 16-bit gradient; the per-element arithmetic is adam_k's exactly.
+template <typename G, typename S>
+__global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __restrict__ shadow,
+                                               const G* __restrict__ grad, float* __restrict__ m,
+                                               float* __restrict__ v, int64_t n4, double lr, double b1, double b2,
+                                               double eps, double bc1, double bc2, float scale, int unscale,
+                                               float ntok, const int32_t* __restrict__ skip) {
+  if (skip && *skip) return;
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = 4 * q;
+    float4 p4 = *reinterpret_cast<const float4*>(master + i);
+    float4 m4 = *reinterpret_cast<const float4*>(m + i);
+    float4 v4 = *reinterpret_cast<const float4*>(v + i);
+    const uint2 g2 = *reinterpret_cast<const uint2*>(grad + i);
+    const G* gg = reinterpret_cast<const G*>(&g2);
+    float* pp = &p4.x;
+    float* mp = &m4.x;
+    float* vp = &v4.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float gf = Num<G>::ld(gg + j);
+      if (unscale) gf = __fdiv_rn(gf, scale);
+      gf = __fdiv_rn(gf, ntok);
+      const double g = gf;
+      const double mm = __dadd_rn(__dmul_rn(b1, double(mp[j])), __dmul_rn(1.0 - b1, g));
+      const double vv = __dadd_rn(__dmul_rn(b2, double(vp[j])), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
+      mp[j] = float(mm);
+      vp[j] = float(vv);
+      const double mhat = __ddiv_rn(double(mp[j]), bc1);
+      const double vhat = __ddiv_rn(double(vp[j]), bc2);
+      pp[j] = float(__dsub_rn(double(pp[j]), __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps))));
+    }
+    *reinterpret_cast<float4*>(master + i) = p4;
+    *reinterpret_cast<float4*>(m + i) = m4;
+    *reinterpret_cast<float4*>(v + i) = v4;
+    if (shadow) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) Num<S>::st(shadow + i + j, pp[j]);
+    }
+  }
+}
+
 template <typename G, typename S>
 __global__ void sgd_k(float* __restrict__ master, S* __restrict__ shadow, const G* __restrict__ grad, int64_t n,
                       double lr, float scale, int unscale, float ntok, const int32_t* __restrict__ skip) {
@@ -98,6 +141,18 @@ extern "C" int sfk_adam(int grad_dtype, float* master, void* shadow, int shadow_
                         float* v, int64_t n, double lr, double b1, double b2, double eps, double bc1, double bc2,
                         float scale, int unscale, float ntokens, const int32_t* skip, void* stream) {
   if (n == 0) return SFK_OK;
+  const bool vec = grad_dtype != SFK_F32 && n % 4 == 0 && ((reinterpret_cast<uintptr_t>(master) |
+                                                             reinterpret_cast<uintptr_t>(m) |
+                                                             reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(grad) & 7) == 0;
+  if (vec) {
+    const int64_t n4 = n / 4;
+    SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
+                  adam4_k<G, S><<<grid_for(n4), 256, 0, as_stream(stream)>>>(
+                      master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n4, lr, b1, b2, eps, bc1,
+                      bc2, scale, unscale, ntokens, skip));
+    return check_launch("sfk_adam(vec)");
+  }
   SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
                 adam_k<G, S><<<grid_for(n), 256, 0, as_stream(stream)>>>(
                     master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n, lr, b1, b2, eps, bc1, bc2,

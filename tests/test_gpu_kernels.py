@@ -260,3 +260,61 @@ def test_nonfinite_flag():
     lib.check(lib.sfk_nonfinite(1, ptr(g), g.numel(), ptr(flag), stream()), True)
     torch.cuda.synchronize()
     assert flag[0].item() == 1
+
+
+@pytest.mark.parametrize("dt", [0, 1, 2])
+@pytest.mark.parametrize("rows,n,ld", [(3584, 1024, 1024), (77, 3072, 3072), (5, 40, 48), (1000, 32768, 32768)])
+def test_colsum_single_launch(dt, rows, n, ld):
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn(rows, ld, device="cuda", generator=g).to(TDT[dt])
+    out = torch.randn(n, device="cuda", generator=g).to(TDT[dt])
+    want = (out.double() + x[:, :n].double().sum(0))
+    part = torch.zeros(64 * n, device="cuda")
+    ctr = torch.zeros(64, dtype=torch.int32, device="cuda")
+    for _ in range(2):  # counters must re-arm
+        o = out.clone()
+        lib.check(lib.sfk_colsum(dt, ptr(x), rows, n, ld, ptr(part), ptr(ctr), ptr(o), stream()), True)
+        torch.cuda.synchronize()
+        tol = 1e-5 if dt == 0 else (4e-3 if dt == 1 else 2e-2)
+        torch.testing.assert_close(o.double(), want.to(TDT[dt]).double(), rtol=tol, atol=tol * rows ** 0.5)
+        assert int(ctr.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("rows,d", [(300, 512), (3584, 1024), (7, 64)])
+def test_layernorm_bwd_fused_equals_two_phase(rows, d):
+    lib = L()
+    g = torch.Generator(device="cuda").manual_seed(d)
+    x = torch.randn(rows, d, device="cuda", generator=g).half()
+    dy = torch.randn(rows, d, device="cuda", generator=g).half()
+    gm = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).half()
+    bt = torch.zeros(d, device="cuda").half()
+    y = torch.zeros_like(x)
+    stats = torch.zeros(rows, 2, device="cuda")
+    lib.check(lib.sfk_layernorm_fwd(1, ptr(x), rows, d, ptr(gm), ptr(bt), ptr(y), ptr(stats), stream()), True)
+    part = torch.zeros(2 * 296 * d, device="cuda")
+    dx1, dx2 = torch.zeros_like(x), torch.zeros_like(x)
+    dg1, db1 = torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
+    dg2, db2 = dg1.clone(), db1.clone()
+    npart = C.c_int()
+    lib.check(lib.sfk_layernorm_bwd(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx1), 0, ptr(part),
+                                    C.byref(npart), stream()), True)
+    lib.check(lib.sfk_colsum_finish(1, ptr(part), npart.value, d, ptr(dg1), stream()), True)
+    lib.check(lib.sfk_colsum_finish(1, C.c_void_p(part.data_ptr() + 4 * npart.value * d), npart.value, d, ptr(db1),
+                                    stream()), True)
+    ctr = torch.zeros(4, dtype=torch.int32, device="cuda")
+    part2 = torch.zeros_like(part)
+    lib.check(lib.sfk_layernorm_bwd_fused(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx2), 0, ptr(part2),
+                                          ptr(ctr), ptr(dg2), ptr(db2), stream()), True)
+    torch.cuda.synchronize()
+    # dx identical; dgamma/dbeta fold the same partials in a different fixed
+    # association (8-way ILP), so they agree to fp32 rounding before the fp16 store
+    assert torch.equal(dx1, dx2)
+    torch.testing.assert_close(dg1.float(), dg2.float(), rtol=2e-3, atol=2e-3)
+    torch.testing.assert_close(db1.float(), db2.float(), rtol=2e-3, atol=2e-3)
+    # deterministic: a second run is bitwise identical
+    dx3, dg3, db3 = torch.zeros_like(x), torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
+    lib.check(lib.sfk_layernorm_bwd_fused(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx3), 0, ptr(part2),
+                                          ptr(ctr), ptr(dg3), ptr(db3), stream()), True)
+    torch.cuda.synchronize()
+    assert torch.equal(dx2, dx3) and torch.equal(dg2, dg3) and torch.equal(db2, db3)
