@@ -157,7 +157,7 @@ DeviceBatch PackedBatch::bind(const int32_t* d) const {
 
 // ------------------------------------------------------------------ tape
 DeviceTape::DeviceTape(Arena& arena, const DeviceParams& params, int dtype, cudaStream_t stream)
-    : arena_(arena), params_(params), dtype_(dtype), esize_(dtype == SFK_F32 ? 4 : 2), stream_(stream) {}
+    : arena_(arena), params_(params), dtype_(dtype), esize_(dtype == SFK_F32 ? 4 : 2), stream_(stream), cur_(stream) {}
 
 int DeviceTape::embedding(ParamRef table, const int32_t* ids, int rows, int width, float scale, const float* pe,
                           const DeviceBatch::Segs& segs) {
@@ -172,7 +172,7 @@ int DeviceTape::embedding(ParamRef table, const int32_t* ids, int rows, int widt
   n.segs = segs;
   n.out = alloc_elems(int64_t(rows) * n.cols);
   pbegin();
-  sfk_check(sfk_embed_fwd(dtype_, ids, rows, width, n.cols, pptr(table), pe, scale, n.out, stream_), "embed_fwd");
+  sfk_check(sfk_embed_fwd(dtype_, ids, rows, width, n.cols, pptr(table), pe, scale, n.out, cur_), "embed_fwd");
   pend(Profiler::Embed, 0, double(rows) * n.cols * (2.0 * esize_ + 4));
   ++launches_;
   nodes_.push_back(n);
@@ -192,7 +192,7 @@ int DeviceTape::layer_norm(int x, ParamRef gamma, ParamRef beta) {
   n.out = alloc_elems(int64_t(n.rows) * n.cols);
   n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * 8));
   pbegin();
-  sfk_check(sfk_layernorm_fwd(dtype_, in.out, n.rows, n.cols, pptr(gamma), pptr(beta), n.out, n.stats, stream_),
+  sfk_check(sfk_layernorm_fwd(dtype_, in.out, n.rows, n.cols, pptr(gamma), pptr(beta), n.out, n.stats, cur_),
             "layernorm_fwd");
   pend(Profiler::LayerNorm, 0, double(n.rows) * (2.0 * n.cols * esize_ + 8));
   ++launches_;
@@ -223,7 +223,7 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   g.ldm = ldm;
   g.flags = flags;
   pbegin();
-  sfk_check(sfk_gemm(&g, stream_), "gemm");
+  sfk_check(sfk_gemm(&g, cur_), "gemm");
   pend(cat, 2.0 * m * n * k, double(esize_) * (double(m) * k + double(n) * k + double(m) * n));
   ++launches_;
 }
@@ -305,7 +305,7 @@ int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d,
   a.ldo = d;
   a.stats = n.stats;
   pbegin();
-  sfk_check(sfk_attention_fwd(&a, stream_), "attention_fwd");
+  sfk_check(sfk_attention_fwd(&a, cur_), "attention_fwd");
   pend(Profiler::AttnFwd, attn_flops(batch, q_width, k_width, k_len, d, causal, false),
        double(esize_) * d * (2.0 * n.rows + 2.0 * kn.rows));
   ++launches_;
@@ -339,9 +339,9 @@ void DeviceTape::run_xent(Node& n, float seed, bool with_grad, double* stats_acc
   // the logits buffer becomes its own gradient (dlogits written in place)
   pbegin();
   sfk_check(sfk_xent_fwd_bwd(dtype_, lg.out, lg.rows, lg.cols, lg.cols, n.gold, kPad, n.eps, seed,
-                             with_grad ? lg.out : nullptr, n.row_out, stream_),
+                             with_grad ? lg.out : nullptr, n.row_out, cur_),
             "xent");
-  sfk_check(sfk_xent_reduce(n.row_out, n.rows, stats_acc, stream_), "xent_reduce");
+  sfk_check(sfk_xent_reduce(n.row_out, n.rows, stats_acc, cur_), "xent_reduce");
   pend(Profiler::Xent, 0, double(lg.rows) * lg.cols * esize_ * (with_grad ? 2.0 : 1.0));
   launches_ += 2;
   if (with_grad) lg.grad = lg.out;
@@ -359,13 +359,36 @@ void DeviceTape::backward(int loss_node, float seed, double* stats_acc) {
   if (n.kind != Kind::Xent) throw ShapeError("backward: loss node must be a softmax_xent node");
   run_xent(n, seed, true, stats_acc);
   for (int i = loss_node - 1; i >= 0; --i) backward_node(i);
+  join_side();
+}
+
+cudaEvent_t DeviceTape::event() {
+  if (!evpool_) throw DeviceError("device tape: no event pool");
+  if (ev_next_ == evpool_->size()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+    evpool_->push_back(e);
+  }
+  return (*evpool_)[ev_next_++];
+}
+
+void DeviceTape::wait_side_reader(const void* buf) {
+  for (auto it = side_readers_.rbegin(); it != side_readers_.rend(); ++it)
+    if (it->first == buf) {
+      cuda_check(cudaStreamWaitEvent(stream_, it->second, 0), "stream wait");
+      return;
+    }
+}
+
+void DeviceTape::join_side() {
+  if (side_last_) cuda_check(cudaStreamWaitEvent(stream_, side_last_, 0), "stream join");
 }
 
 void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out) {
   const int max_parts = 64;
   float* part = static_cast<float*>(arena_.alloc(size_t(max_parts) * cols * 4));
   pbegin();
-  sfk_check(sfk_colsum(dtype_, dy, rows, cols, ld, part, counters((cols + 1023) / 1024), out, stream_), "colsum");
+  sfk_check(sfk_colsum(dtype_, dy, rows, cols, ld, part, counters((cols + 1023) / 1024), out, cur_), "colsum");
   pend(Profiler::BiasGrad, 0, double(rows) * cols * esize_);
   launches_ += 1;
 }
@@ -377,9 +400,10 @@ void DeviceTape::backward_node(int id) {
     case Kind::Xent:
       return;
     case Kind::Embedding: {
+      join_side();  // a tied output projection's wgrad writes the same parameter rows
       pbegin();
       sfk_check(sfk_embed_bwd(dtype_, n.segs.uniq, n.segs.off, n.segs.rows, n.segs.n, n.cols, n.grad, n.scale,
-                              gptr(n.p0), stream_),
+                              gptr(n.p0), cur_),
                 "embed_bwd");
       pend(Profiler::Embed, 0, double(n.rows) * n.cols * esize_ + 2.0 * n.segs.n * n.cols * esize_);
       ++launches_;
@@ -390,9 +414,10 @@ void DeviceTape::backward_node(int id) {
       auto [dx, fresh] = grad_of(n.in0);
       const int max_parts = 296;
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
+      if (!fresh) wait_side_reader(dx);  // in-place accumulate into a buffer a wgrad may still read
       pbegin();
       sfk_check(sfk_layernorm_bwd_fused(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx,
-                                        fresh ? 0 : 1, part, counters(1), gptr(n.p0), gptr(n.p1), stream_),
+                                        fresh ? 0 : 1, part, counters(1), gptr(n.p0), gptr(n.p1), cur_),
                 "layernorm_bwd");
       pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
       launches_ += 1;
@@ -407,7 +432,24 @@ void DeviceTape::backward_node(int id) {
         if (r.grad) throw ShapeError("linear: residual input already has a gradient (unsupported fan-out)");
         r.grad = dy;
       }
+      // parameter gradients (bias column sums + wgrad dW += dy^T x) only feed
+      // the optimizer: they run on the side stream, ordered after dy is ready
+      if (side_) {
+        cudaEvent_t ready = event();
+        cuda_check(cudaEventRecord(ready, stream_), "event record");
+        cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
+        cur_ = side_;
+      }
       if (n.has_bias) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
+      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
+           n.p0.cols, SFK_EPI_ACCUM);
+      if (side_) {
+        cudaEvent_t done = event();
+        cuda_check(cudaEventRecord(done, side_), "event record");
+        side_readers_.emplace_back(dy, done);
+        side_last_ = done;
+        cur_ = stream_;
+      }
       // dgrad into the input; a relu input gets the masked (pre-activation) grad
       Node& inm = nodes_[n.in0];
       auto [dx, fresh] = grad_of(n.in0);
@@ -419,11 +461,9 @@ void DeviceTape::backward_node(int id) {
         mask = inm.out;
         inm.grad_masked = true;
       }
+      if (!fresh) wait_side_reader(dx);
       gemm(Profiler::GemmDgrad, n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols,
            flags, nullptr, nullptr, 0, mask, in.cols);
-      // wgrad: dW += dy^T x
-      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
-           n.p0.cols, SFK_EPI_ACCUM);
       return;
     }
     case Kind::Attention: {
@@ -460,7 +500,7 @@ void DeviceTape::backward_node(int id) {
       a.lddv = kn.cols;
       a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
       pbegin();
-      sfk_check(sfk_attention_bwd(&a, stream_), "attention_bwd");
+      sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
       pend(Profiler::AttnBwd, attn_flops(n.batch, n.q_width, n.k_width, n.k_len, n.cols, n.causal, true),
            double(esize_) * n.cols * (4.0 * n.rows + 4.0 * kn.rows));
       launches_ += 2;

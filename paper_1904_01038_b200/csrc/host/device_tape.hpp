@@ -137,6 +137,13 @@ class DeviceTape {
   // number of our kernels launched so far (bench evidence)
   int64_t launches() const { return launches_; }
   void set_profiler(Profiler* p) { prof_ = p; }
+  // second stream for parameter-gradient work (wgrad GEMM + bias grad) that is
+  // off the critical path of the backward sweep; events order it against the
+  // main stream (see backward_node). The tape joins it before returning.
+  void set_side_stream(cudaStream_t s, std::vector<cudaEvent_t>* event_pool) {
+    side_ = s;
+    evpool_ = event_pool;
+  }
   // pool of zeroed int32 counters for single-launch deterministic reductions
   // (each user re-arms its slots to 0); handed out round-robin
   void set_counters(int32_t* base, int64_t n, int64_t* cursor) {
@@ -188,11 +195,20 @@ class DeviceTape {
     *ctr_cursor_ += k;
     return p;
   }
+  cudaStream_t cur_ = nullptr;  // stream the next launches go to (main or side)
+  cudaStream_t side_ = nullptr;
+  std::vector<cudaEvent_t>* evpool_ = nullptr;
+  size_t ev_next_ = 0;
+  std::vector<std::pair<const void*, cudaEvent_t>> side_readers_;  // grad buffer -> last side reader
+  cudaEvent_t side_last_ = nullptr;
+  cudaEvent_t event();
+  void wait_side_reader(const void* buf);
+  void join_side();
   void pbegin() {
-    if (prof_) prof_->begin(stream_);
+    if (prof_) prof_->begin(cur_);
   }
   void pend(int cat, double flops, double bytes) {
-    if (prof_) prof_->end(stream_, cat, flops, bytes);
+    if (prof_) prof_->end(cur_, cat, flops, bytes);
   }
 
   void* alloc_elems(int64_t n) { return arena_.alloc(size_t(n) * esize_); }

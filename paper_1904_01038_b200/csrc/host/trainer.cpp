@@ -46,6 +46,8 @@ Trainer::~Trainer() {
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
+  if (side_) cudaStreamDestroy(side_);
+  for (cudaEvent_t e : evpool_) cudaEventDestroy(e);
 }
 
 void Trainer::init(const Registry& reg) {
@@ -95,6 +97,7 @@ void Trainer::init(const Registry& reg) {
   // device state
   n_ = model_->num_params();
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
   cuda_check(cudaEventCreate(&ev0_), "event");
   cuda_check(cudaEventCreate(&ev1_), "event");
   cuda_check(cudaMalloc(&master_, size_t(n_) * 4), "master");
@@ -296,6 +299,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     DeviceTape tape(arena_, DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
+    tape.set_side_stream(side_, &evpool_);
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
     tape.backward(out.loss_node, float(scale), stats_dev_);

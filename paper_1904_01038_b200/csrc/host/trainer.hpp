@@ -115,6 +115,8 @@ class Trainer {
   size_t blob_host_cap_ = 0;
   void* readback_host_ = nullptr;  // pinned: stats + flag
   cudaStream_t stream_ = nullptr;
+  cudaStream_t side_ = nullptr;        // parameter-gradient stream (wgrad, bias grad)
+  std::vector<cudaEvent_t> evpool_;    // ordering events handed to the tapes
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   ncclComm_t comm_ = nullptr;
   Arena arena_;
