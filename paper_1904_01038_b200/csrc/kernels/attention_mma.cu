@@ -109,6 +109,8 @@ __device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.cau
 // ------------------------------------------------------------------ forward
 template <typename T, int DH>
 __global__ void __launch_bounds__(kWarps * 32) fwd_k(Args a) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
   const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kRows;
@@ -229,6 +231,8 @@ __global__ void __launch_bounds__(kWarps * 32) fwd_k(Args a) {
 // ------------------------------------------------------------------ backward: dQ (+ D)
 template <typename T, int DH>
 __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
   const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kRows;
@@ -343,6 +347,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
 // ------------------------------------------------------------------ backward: dK, dV
 template <typename T, int DH>
 __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
   constexpr int NC = DH >= 128 ? 32 : 64;  // query columns per chunk (register budget)
@@ -513,15 +519,15 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   const dim3 gq((a.qw + kRows - 1) / kRows, a.heads, a.batch);
   if (!bwd) {
     const size_t smem = size_t(kRows + 2 * kpad) * LD * sizeof(T);
-    fwd_k<T, DH><<<gq, kWarps * 32, smem, st>>>(a);
+    launch_pdl(fwd_k<T, DH>, gq, kWarps * 32, smem, st, a);
     return check_launch("sfk_attention_fwd(mma)");
   }
   const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
-  bwd_dq_k<T, DH><<<gq, kWarps * 32, smem_q, st>>>(a);
+  launch_pdl(bwd_dq_k<T, DH>, gq, kWarps * 32, smem_q, st, a);
   if (int e = check_launch("sfk_attention_bwd(dq)")) return e;
   const dim3 gk((a.kw + kRows - 1) / kRows, a.heads, a.batch);
   const size_t smem_k = size_t(2 * kRows + 2 * qpad) * LD * sizeof(T) + size_t(qpad) * 12;
-  bwd_dkv_k<T, DH><<<gk, kWarps * 32, smem_k, st>>>(a);
+  launch_pdl(bwd_dkv_k<T, DH>, gk, kWarps * 32, smem_k, st, a);
   return check_launch("sfk_attention_bwd(dkv)");
 }
 

@@ -75,4 +75,27 @@ __device__ __forceinline__ float warp_max(float v) {
 
 inline int elem_size(int dtype) { return dtype == SFK_F32 ? 4 : 2; }
 
+// Programmatic dependent launch: every kernel is launched with the PDL
+// attribute, waits for its stream predecessor's completion (and memory flush)
+// before touching global memory, and immediately allows its own successor to
+// be scheduled, so launch latency and prologues overlap the predecessor's tail.
+#define SFK_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define SFK_PDL_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 }  // namespace sfk

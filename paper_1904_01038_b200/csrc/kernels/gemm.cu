@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // everything above overlapped the previous kernel's tail (PDL)
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
@@ -591,7 +594,8 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   }
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
   const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
-  gemm_tc<BN, A_MN, B_MN, T><<<grid, kThreads, C::SMEM, s>>>(ta, tb, e, g->m, g->n, g->k, vec_ok ? 1 : 0);
+  launch_pdl(gemm_tc<BN, A_MN, B_MN, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, e, g->m, g->n, g->k,
+             vec_ok ? 1 : 0);
   return check_launch("sfk_gemm(tcgen05)");
 }
 

@@ -14,6 +14,8 @@ namespace sfk {
 template <typename T>
 __global__ void embed_fwd_k(const int32_t* __restrict__ ids, int rows, int width, int d, const T* __restrict__ table,
                             const float* __restrict__ pe, float scale, T* __restrict__ out) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int r = blockIdx.x;
   if (r >= rows) return;
   const int64_t id = ids[r];
@@ -32,6 +34,8 @@ template <typename T>
 __global__ void embed_bwd_k(const int32_t* __restrict__ uniq, const int32_t* __restrict__ seg_off,
                             const int32_t* __restrict__ seg_rows, int d, const T* __restrict__ dx, float scale,
                             T* __restrict__ grad) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int u = blockIdx.x;
   const int64_t id = uniq[u];
   const int s0 = seg_off[u], s1 = seg_off[u + 1];
@@ -53,6 +57,8 @@ constexpr int kLnMaxPerLane = 32;  // d <= 1024
 template <typename T>
 __global__ void __launch_bounds__(256) ln_fwd_k(const T* __restrict__ x, int rows, int d, const T* __restrict__ g,
                                                 const T* __restrict__ b, T* __restrict__ y, float2* __restrict__ stats) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= rows) return;
   const T* xr = x + int64_t(warp) * d;
@@ -95,6 +101,8 @@ __global__ void __launch_bounds__(256) ln_bwd_k(const T* __restrict__ x, const T
                                                 const T* __restrict__ g, const float2* __restrict__ stats,
                                                 T* __restrict__ dx, int accumulate, int rows_per_block,
                                                 float* __restrict__ part, int nblk) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   __shared__ float red[2][8][kLnMaxPerLane * 32 / 8];  // reused per column slab
   const int wid = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int r0 = blockIdx.x * rows_per_block;
@@ -168,6 +176,8 @@ __global__ void __launch_bounds__(256) ln_bwd_k(const T* __restrict__ x, const T
 template <typename T>
 __global__ void colsum_partial_k(const T* __restrict__ x, int rows, int n, int64_t ld, int rows_per_block,
                                  float* __restrict__ part) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
@@ -178,6 +188,8 @@ __global__ void colsum_partial_k(const T* __restrict__ x, int rows, int n, int64
 
 template <typename T>
 __global__ void colsum_finish_k(const float* __restrict__ part, int nparts, int n, T* __restrict__ out) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   float s = 0.f;
@@ -193,6 +205,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024) xent_k(T* __restrict__ logits, int rows, int V, int64_t ld,
                                                const int32_t* __restrict__ gold, int pad, float eps, float seed,
                                                T* __restrict__ dlogits, float* __restrict__ row_out) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   extern __shared__ uint8_t xs_raw[];
   T* row = reinterpret_cast<T*>(xs_raw);
   __shared__ float rv[32];
@@ -303,6 +317,8 @@ __global__ void __launch_bounds__(1024) xent_k(T* __restrict__ logits, int rows,
 }
 
 __global__ void xent_reduce_k(const float* __restrict__ row_out, int rows, double* __restrict__ acc) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   __shared__ double red[4][256];
   const int tid = threadIdx.x;
   const int per = (rows + blockDim.x - 1) / blockDim.x;
@@ -373,7 +389,7 @@ extern "C" int sfk_embed_fwd(int dtype, const int32_t* ids, int rows, int width,
   if (int e = embed_fwd_vec(dtype, ids, rows, width, d, table, pe, scale, out, as_stream(stream)); e != SFK_EUNSUP)
     return e;
   SFK_DISPATCH(dtype, T,
-               embed_fwd_k<T><<<rows, 128, 0, as_stream(stream)>>>(ids, rows, width, d, static_cast<const T*>(table),
+               launch_pdl(embed_fwd_k<T>, rows, 128, 0, as_stream(stream), ids, rows, width, d, static_cast<const T*>(table),
                                                                     pe, scale, static_cast<T*>(out)));
   return check_launch("sfk_embed_fwd");
 }
@@ -385,7 +401,7 @@ extern "C" int sfk_embed_bwd(int dtype, const int32_t* uniq, const int32_t* seg_
       e != SFK_EUNSUP)
     return e;
   SFK_DISPATCH(dtype, T,
-               embed_bwd_k<T><<<nuniq, 128, 0, as_stream(stream)>>>(uniq, seg_off, seg_rows, d,
+               launch_pdl(embed_bwd_k<T>, nuniq, 128, 0, as_stream(stream), uniq, seg_off, seg_rows, d,
                                                                     static_cast<const T*>(dx), scale,
                                                                     static_cast<T*>(grad)));
   return check_launch("sfk_embed_bwd");
@@ -401,7 +417,7 @@ extern "C" int sfk_layernorm_fwd(int dtype, const void* x, int rows, int d, cons
   if (int e = ln_fwd_vec(dtype, x, rows, d, gamma, beta, y, stats, as_stream(stream)); e != SFK_EUNSUP) return e;
   const int blocks = (rows + 7) / 8;
   SFK_DISPATCH(dtype, T,
-               ln_fwd_k<T><<<blocks, 256, 0, as_stream(stream)>>>(
+               launch_pdl(ln_fwd_k<T>, blocks, 256, 0, as_stream(stream), 
                    static_cast<const T*>(x), rows, d, static_cast<const T*>(gamma), static_cast<const T*>(beta),
                    static_cast<T*>(y), reinterpret_cast<float2*>(stats)));
   return check_launch("sfk_layernorm_fwd");
@@ -427,7 +443,7 @@ extern "C" int sfk_layernorm_bwd(int dtype, const void* x, const void* dy, int r
   const int rpb = (rows + nblk - 1) / nblk;
   *nparts = nblk;
   SFK_DISPATCH(dtype, T,
-               ln_bwd_k<T><<<nblk, 256, 0, as_stream(stream)>>>(
+               launch_pdl(ln_bwd_k<T>, nblk, 256, 0, as_stream(stream), 
                    static_cast<const T*>(x), static_cast<const T*>(dy), rows, d, static_cast<const T*>(gamma),
                    reinterpret_cast<const float2*>(stats), static_cast<T*>(dx), accumulate, rpb, part, nblk));
   return check_launch("sfk_layernorm_bwd");
@@ -443,14 +459,14 @@ extern "C" int sfk_colsum_partial(int dtype, const void* x, int rows, int n, int
   *nparts = nblk;
   dim3 grid((n + 255) / 256, nblk);
   SFK_DISPATCH(dtype, T,
-               colsum_partial_k<T><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const T*>(x), rows, n, ld, rpb,
+               launch_pdl(colsum_partial_k<T>, grid, 256, 0, as_stream(stream), static_cast<const T*>(x), rows, n, ld, rpb,
                                                                         part));
   return check_launch("sfk_colsum_partial");
 }
 
 extern "C" int sfk_colsum_finish(int dtype, const float* part, int nparts, int n, void* out, void* stream) {
   SFK_DISPATCH(dtype, T,
-               colsum_finish_k<T><<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(part, nparts, n,
+               launch_pdl(colsum_finish_k<T>, (n + 255) / 256, 256, 0, as_stream(stream), part, nparts, n,
                                                                                   static_cast<T*>(out)));
   return check_launch("sfk_colsum_finish");
 }
@@ -469,13 +485,13 @@ extern "C" int sfk_xent_fwd_bwd(int dtype, void* logits, int rows, int vocab, in
       cudaFuncSetAttribute(xent_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       configured = 1;
     }
-    xent_k<T><<<rows, 1024, smem, as_stream(stream)>>>(static_cast<T*>(logits), rows, vocab, ld, gold, pad_id, eps,
+    launch_pdl(xent_k<T>, rows, 1024, smem, as_stream(stream), static_cast<T*>(logits), rows, vocab, ld, gold, pad_id, eps,
                                                        seed, static_cast<T*>(dlogits), row_out);
   });
   return check_launch("sfk_xent_fwd_bwd");
 }
 
 extern "C" int sfk_xent_reduce(const float* row_out, int rows, double* acc, void* stream) {
-  xent_reduce_k<<<1, 256, 0, as_stream(stream)>>>(row_out, rows, acc);
+  launch_pdl(xent_reduce_k, 1, 256, 0, as_stream(stream), row_out, rows, acc);
   return check_launch("sfk_xent_reduce");
 }

@@ -47,6 +47,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) embed_fwd_v(const int32_t* __restrict__ ids, int rows, int width, int d,
                                                   const T* __restrict__ table, const float* __restrict__ pe,
                                                   float scale, T* __restrict__ out) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (r >= rows) return;
   const T* e = table + int64_t(ids[r]) * d;
@@ -67,6 +69,8 @@ template <typename T>
 __global__ void __launch_bounds__(128) embed_bwd_v(const int32_t* __restrict__ uniq, const int32_t* __restrict__ off,
                                                   const int32_t* __restrict__ srows, int d, const T* __restrict__ dx,
                                                   float scale, T* __restrict__ grad) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int u = blockIdx.x;
   const int s0 = off[u], s1 = off[u + 1];
   T* g = grad + int64_t(uniq[u]) * d;
@@ -89,6 +93,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) ln_fwd_v(const T* __restrict__ x, int rows, int d, const T* __restrict__ g,
                                                const T* __restrict__ b, T* __restrict__ y,
                                                float2* __restrict__ stats) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (r >= rows) return;
   const T* xr = x + int64_t(r) * d;
@@ -148,6 +154,8 @@ __global__ void __launch_bounds__(256) ln_bwd_v(const T* __restrict__ x, const T
                                                const T* __restrict__ g, const float2* __restrict__ stats,
                                                T* __restrict__ dx, int accumulate, int rpb, float* __restrict__ part,
                                                int nblk) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   ln_bwd_body<T>(x, dy, rows, d, g, stats, dx, accumulate, rpb, part, nblk);
 }
 
@@ -257,6 +265,8 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_v(const T* __restrict__ x, c
                                                      T* __restrict__ dx, int accumulate, int rpb,
                                                      float* __restrict__ part, int nblk, int32_t* counter,
                                                      T* __restrict__ dgamma, T* __restrict__ dbeta) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   ln_bwd_body<T>(x, dy, rows, d, g, stats, dx, accumulate, rpb, part, nblk);
   // partials for gamma then beta are contiguous: fold them as one 2d-wide vector
   __shared__ int last;
@@ -281,6 +291,8 @@ __global__ void __launch_bounds__(256) ln_bwd_fused_v(const T* __restrict__ x, c
 template <typename T>
 __global__ void colsum_fused_v(const T* __restrict__ x, int rows, int n, int64_t ld, int rpb, float* __restrict__ part,
                                int nblk, int32_t* counter, T* __restrict__ out) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c < n) {
     const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
@@ -316,6 +328,8 @@ __global__ void colsum_fused_v(const T* __restrict__ x, int rows, int n, int64_t
 template <typename T>
 __global__ void colsum_partial_v(const T* __restrict__ x, int rows, int n, int64_t ld, int rpb,
                                  float* __restrict__ part) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c >= n) return;
   const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
@@ -343,10 +357,10 @@ int embed_fwd_vec(int dtype, const int32_t* ids, int rows, int width, int d, con
   if (dtype == SFK_F32 || d % 8 || !al16(table) || !al16(out) || !al16(pe)) return SFK_EUNSUP;
   const int blocks = (rows + 7) / 8;
   if (dtype == SFK_F16)
-    vec::embed_fwd_v<__half><<<blocks, 256, 0, s>>>(ids, rows, width, d, static_cast<const __half*>(table), pe, scale,
+    launch_pdl(vec::embed_fwd_v<__half>, blocks, 256, 0, s, ids, rows, width, d, static_cast<const __half*>(table), pe, scale,
                                                     static_cast<__half*>(out));
   else
-    vec::embed_fwd_v<__nv_bfloat16><<<blocks, 256, 0, s>>>(ids, rows, width, d,
+    launch_pdl(vec::embed_fwd_v<__nv_bfloat16>, blocks, 256, 0, s, ids, rows, width, d,
                                                            static_cast<const __nv_bfloat16*>(table), pe, scale,
                                                            static_cast<__nv_bfloat16*>(out));
   return check_launch("sfk_embed_fwd(vec)");
@@ -357,10 +371,10 @@ int embed_bwd_vec(int dtype, const int32_t* uniq, const int32_t* off, const int3
   if (dtype == SFK_F32 || d % 8 || !al16(dx) || !al16(grad)) return SFK_EUNSUP;
   const int threads = std::min(128, std::max(32, d / 8));
   if (dtype == SFK_F16)
-    vec::embed_bwd_v<__half><<<nuniq, threads, 0, s>>>(uniq, off, rows, d, static_cast<const __half*>(dx), scale,
+    launch_pdl(vec::embed_bwd_v<__half>, nuniq, threads, 0, s, uniq, off, rows, d, static_cast<const __half*>(dx), scale,
                                                        static_cast<__half*>(grad));
   else
-    vec::embed_bwd_v<__nv_bfloat16><<<nuniq, threads, 0, s>>>(uniq, off, rows, d,
+    launch_pdl(vec::embed_bwd_v<__nv_bfloat16>, nuniq, threads, 0, s, uniq, off, rows, d,
                                                               static_cast<const __nv_bfloat16*>(dx), scale,
                                                               static_cast<__nv_bfloat16*>(grad));
   return check_launch("sfk_embed_bwd(vec)");
@@ -371,11 +385,11 @@ int ln_fwd_vec(int dtype, const void* x, int rows, int d, const void* g, const v
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(y) || !al16(g) || !al16(b)) return SFK_EUNSUP;
   const int blocks = (rows + 7) / 8;
   if (dtype == SFK_F16)
-    vec::ln_fwd_v<__half><<<blocks, 256, 0, s>>>(static_cast<const __half*>(x), rows, d,
+    launch_pdl(vec::ln_fwd_v<__half>, blocks, 256, 0, s, static_cast<const __half*>(x), rows, d,
                                                  static_cast<const __half*>(g), static_cast<const __half*>(b),
                                                  static_cast<__half*>(y), reinterpret_cast<float2*>(stats));
   else
-    vec::ln_fwd_v<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+    launch_pdl(vec::ln_fwd_v<__nv_bfloat16>, blocks, 256, 0, s, 
         static_cast<const __nv_bfloat16*>(x), rows, d, static_cast<const __nv_bfloat16*>(g),
         static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(y), reinterpret_cast<float2*>(stats));
   return check_launch("sfk_layernorm_fwd(vec)");
@@ -396,12 +410,12 @@ int ln_bwd_vec(int dtype, const void* x, const void* dy, int rows, int d, const 
     cfg = true;
   }
   if (dtype == SFK_F16)
-    vec::ln_bwd_v<__half><<<nblk, 256, smem, s>>>(static_cast<const __half*>(x), static_cast<const __half*>(dy), rows,
+    launch_pdl(vec::ln_bwd_v<__half>, nblk, 256, smem, s, static_cast<const __half*>(x), static_cast<const __half*>(dy), rows,
                                                   d, static_cast<const __half*>(g),
                                                   reinterpret_cast<const float2*>(stats), static_cast<__half*>(dx),
                                                   accumulate, rpb, part, nblk);
   else
-    vec::ln_bwd_v<__nv_bfloat16><<<nblk, 256, smem, s>>>(
+    launch_pdl(vec::ln_bwd_v<__nv_bfloat16>, nblk, 256, smem, s, 
         static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), rows, d,
         static_cast<const __nv_bfloat16*>(g), reinterpret_cast<const float2*>(stats),
         static_cast<__nv_bfloat16*>(dx), accumulate, rpb, part, nblk);
@@ -417,6 +431,8 @@ int colsum_partial_vec(int dtype, const void* x, int rows, int n, int64_t ld, fl
 template <typename T>
 __global__ void fold_k(const float* __restrict__ pa, const float* __restrict__ pb, int nparts, int n,
                        T* __restrict__ oa, T* __restrict__ ob) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const bool second = blockIdx.y == 1;
   if (c >= n) return;
@@ -440,10 +456,10 @@ int ln_bwd_fused_vec(int dtype, const void* x, const void* dy, int rows, int d, 
   if (int e = ln_bwd_vec(dtype, x, dy, rows, d, g, stats, dx, accumulate, part, &nparts, s)) return e;
   dim3 grid((d + 127) / 128, 2);
   if (dtype == SFK_F16)
-    fold_k<__half><<<grid, 128, 0, s>>>(part, part + size_t(nparts) * d, nparts, d, static_cast<__half*>(dgamma),
+    launch_pdl(fold_k<__half>, grid, 128, 0, s, part, part + size_t(nparts) * d, nparts, d, static_cast<__half*>(dgamma),
                                         static_cast<__half*>(dbeta));
   else
-    fold_k<__nv_bfloat16><<<grid, 128, 0, s>>>(part, part + size_t(nparts) * d, nparts, d,
+    launch_pdl(fold_k<__nv_bfloat16>, grid, 128, 0, s, part, part + size_t(nparts) * d, nparts, d,
                                                static_cast<__nv_bfloat16*>(dgamma),
                                                static_cast<__nv_bfloat16*>(dbeta));
   return check_launch("sfk_layernorm_bwd_fused(fold)");
@@ -456,9 +472,9 @@ int colsum_fused_vec(int dtype, const void* x, int rows, int n, int64_t ld, floa
   if (int e = colsum_partial_vec(dtype, x, rows, n, ld, part, &nparts, s)) return e;
   dim3 grid((n + 127) / 128, 1);
   if (dtype == SFK_F16)
-    fold_k<__half><<<grid, 128, 0, s>>>(part, nullptr, nparts, n, static_cast<__half*>(out), nullptr);
+    launch_pdl(fold_k<__half>, grid, 128, 0, s, part, nullptr, nparts, n, static_cast<__half*>(out), nullptr);
   else
-    fold_k<__nv_bfloat16><<<grid, 128, 0, s>>>(part, nullptr, nparts, n, static_cast<__nv_bfloat16*>(out), nullptr);
+    launch_pdl(fold_k<__nv_bfloat16>, grid, 128, 0, s, part, nullptr, nparts, n, static_cast<__nv_bfloat16*>(out), nullptr);
   return check_launch("sfk_colsum(fold)");
 }
 
@@ -473,9 +489,9 @@ int colsum_partial_vec(int dtype, const void* x, int rows, int n, int64_t ld, fl
   *nparts = nblk;
   dim3 grid(col_blocks, nblk);
   if (dtype == SFK_F16)
-    vec::colsum_partial_v<__half><<<grid, 128, 0, s>>>(static_cast<const __half*>(x), rows, n, ld, rpb, part);
+    launch_pdl(vec::colsum_partial_v<__half>, grid, 128, 0, s, static_cast<const __half*>(x), rows, n, ld, rpb, part);
   else
-    vec::colsum_partial_v<__nv_bfloat16><<<grid, 128, 0, s>>>(static_cast<const __nv_bfloat16*>(x), rows, n, ld, rpb,
+    launch_pdl(vec::colsum_partial_v<__nv_bfloat16>, grid, 128, 0, s, static_cast<const __nv_bfloat16*>(x), rows, n, ld, rpb,
                                                               part);
   return check_launch("sfk_colsum_partial(vec)");
 }

@@ -9,6 +9,8 @@ namespace sfk {
 
 template <typename T>
 __global__ void nonfinite_k(const T* __restrict__ g, int64_t n, int32_t* flag) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   int bad = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     bad |= !isfinite(Num<T>::ld(g + i));
@@ -21,6 +23,8 @@ __global__ void adam_k(float* __restrict__ master, S* __restrict__ shadow, const
                        float* __restrict__ m, float* __restrict__ v, int64_t n, double lr, double b1, double b2,
                        double eps, double bc1, double bc2, float scale, int unscale, float ntok,
                        const int32_t* __restrict__ skip) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   if (skip && *skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     float gf = Num<G>::ld(grad + i);
@@ -49,6 +53,8 @@ __global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __
                                                float* __restrict__ v, int64_t n4, double lr, double b1, double b2,
                                                double eps, double bc1, double bc2, float scale, int unscale,
                                                float ntok, const int32_t* __restrict__ skip) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   if (skip && *skip) return;
   for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = 4 * q;
@@ -87,6 +93,8 @@ __global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __
 template <typename G, typename S>
 __global__ void sgd_k(float* __restrict__ master, S* __restrict__ shadow, const G* __restrict__ grad, int64_t n,
                       double lr, float scale, int unscale, float ntok, const int32_t* __restrict__ skip) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   if (skip && *skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     float gf = Num<G>::ld(grad + i);
@@ -100,12 +108,16 @@ __global__ void sgd_k(float* __restrict__ master, S* __restrict__ shadow, const 
 
 template <typename S, typename D>
 __global__ void convert_k(const S* __restrict__ src, D* __restrict__ dst, int64_t n) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     Num<D>::st(dst + i, Num<S>::ld(src + i));
 }
 
 template <typename T>
 __global__ void accumulate_k(T* __restrict__ dst, const T* __restrict__ src, int64_t n) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     Num<T>::st(dst + i, __fadd_rn(Num<T>::ld(dst + i), Num<T>::ld(src + i)));
 }
@@ -123,7 +135,7 @@ using namespace sfk;
 extern "C" int sfk_nonfinite(int dtype, const void* g, int64_t n, int32_t* flag, void* stream) {
   if (n == 0) return SFK_OK;
   SFK_DISPATCH(dtype, T,
-               nonfinite_k<T><<<grid_for(n), 256, 0, as_stream(stream)>>>(static_cast<const T*>(g), n, flag));
+               launch_pdl(nonfinite_k<T>, grid_for(n), 256, 0, as_stream(stream), static_cast<const T*>(g), n, flag));
   return check_launch("sfk_nonfinite");
 }
 
@@ -148,13 +160,13 @@ extern "C" int sfk_adam(int grad_dtype, float* master, void* shadow, int shadow_
   if (vec) {
     const int64_t n4 = n / 4;
     SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
-                  adam4_k<G, S><<<grid_for(n4), 256, 0, as_stream(stream)>>>(
+                  launch_pdl(adam4_k<G, S>, grid_for(n4), 256, 0, as_stream(stream), 
                       master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n4, lr, b1, b2, eps, bc1,
                       bc2, scale, unscale, ntokens, skip));
     return check_launch("sfk_adam(vec)");
   }
   SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
-                adam_k<G, S><<<grid_for(n), 256, 0, as_stream(stream)>>>(
+                launch_pdl(adam_k<G, S>, grid_for(n), 256, 0, as_stream(stream), 
                     master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n, lr, b1, b2, eps, bc1, bc2,
                     scale, unscale, ntokens, skip));
   return check_launch("sfk_adam");
@@ -164,7 +176,7 @@ extern "C" int sfk_sgd(int grad_dtype, float* master, void* shadow, int shadow_d
                        double lr, float scale, int unscale, float ntokens, const int32_t* skip, void* stream) {
   if (n == 0) return SFK_OK;
   SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
-                sgd_k<G, S><<<grid_for(n), 256, 0, as_stream(stream)>>>(master, static_cast<S*>(shadow),
+                launch_pdl(sgd_k<G, S>, grid_for(n), 256, 0, as_stream(stream), master, static_cast<S*>(shadow),
                                                                         static_cast<const G*>(grad), n, lr, scale,
                                                                         unscale, ntokens, skip));
   return check_launch("sfk_sgd");
@@ -177,7 +189,7 @@ extern "C" int sfk_cast(const float* src, void* dst, int dst_dtype, int64_t n, v
 extern "C" int sfk_convert(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n, void* stream) {
   if (n == 0) return SFK_OK;
   SFK_DISPATCH2(src_dtype, S, dst_dtype, D,
-                convert_k<S, D><<<grid_for(n), 256, 0, as_stream(stream)>>>(static_cast<const S*>(src),
+                launch_pdl(convert_k<S, D>, grid_for(n), 256, 0, as_stream(stream), static_cast<const S*>(src),
                                                                             static_cast<D*>(dst), n));
   return check_launch("sfk_convert");
 }
@@ -185,7 +197,7 @@ extern "C" int sfk_convert(int src_dtype, const void* src, int dst_dtype, void* 
 extern "C" int sfk_accumulate(int dtype, void* dst, const void* src, int64_t n, void* stream) {
   if (n == 0) return SFK_OK;
   SFK_DISPATCH(dtype, T,
-               accumulate_k<T><<<grid_for(n), 256, 0, as_stream(stream)>>>(static_cast<T*>(dst),
+               launch_pdl(accumulate_k<T>, grid_for(n), 256, 0, as_stream(stream), static_cast<T*>(dst),
                                                                           static_cast<const T*>(src), n));
   return check_launch("sfk_accumulate");
 }
