@@ -72,6 +72,7 @@ typedef struct sfk_gemm_args {
   int flags;
   int force_simt;                 /* testing: run the SIMT kernel for any dtype */
   int tile_n;                     /* tuning: force the tcgen05 tile width (64/128/256), 0 = auto */
+  int pair;                       /* tuning: 1 = CTA-pair (cta_group::2) 256-row tiles, -1 = single-CTA, 0 = auto */
 } sfk_gemm_args;
 
 int sfk_gemm(const sfk_gemm_args* g, void* stream);
@@ -103,7 +104,8 @@ int sfk_layernorm_fwd(int dtype, const void* x, int rows, int d, const void* gam
 /* tape.cpp:383-418: dx = q(dx + rstd*(dxh - mean(dxh) - xh*mean(dxh*xh)))
  * when accumulate, else dx = q(...) ; column partial sums of dy*xh and dy are
  * written to part[2][nblk][d] (fp32) and folded into dgamma/dbeta by
- * sfk_colsum_finish. Returns nblk through *nparts. */
+ * sfk_colsum_finish. Returns nblk (<= 592) through *nparts; part holds
+ * >= 2*592*d floats. */
 int sfk_layernorm_bwd(int dtype, const void* x, const void* dy, int rows, int d,
                       const void* gamma, const float* stats, void* dx, int accumulate,
                       float* part, int* nparts, void* stream);
@@ -111,10 +113,22 @@ int sfk_layernorm_bwd(int dtype, const void* x, const void* dy, int rows, int d,
 /* Complete LN backward: dx as above plus dgamma = q(dgamma + sum dy*xh),
  * dbeta = q(dbeta + sum dy), the column partials folded in a fixed order
  * (deterministic) by one fold kernel for both vectors.
- * part: >= 2*296*d floats scratch; counter: reserved (may be NULL). */
+ * part: >= 2*592*d floats scratch; counter: reserved (may be NULL). */
 int sfk_layernorm_bwd_fused(int dtype, const void* x, const void* dy, int rows, int d,
                             const void* gamma, const float* stats, void* dx, int accumulate,
                             float* part, int32_t* counter, void* dgamma, void* dbeta, void* stream);
+
+/* The same backward split for the B200 schedule (16-bit data, d % 8 == 0,
+ * SFK_EUNSUP otherwise): the activation gradient alone (one warp per row, on
+ * the critical path) and the gamma/beta gradients alone (column reduction
+ * over rows, parameter work; part >= 2*256*d floats). Same formulas and
+ * rounding points as sfk_layernorm_bwd_fused. */
+int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, int rows, int d,
+                         const void* gamma, const float* stats, void* dx, int accumulate,
+                         void* stream);
+int sfk_layernorm_bwd_params(int dtype, const void* x, const void* dy, int rows, int d,
+                             const float* stats, float* part, void* dgamma, void* dbeta,
+                             void* stream);
 
 /* ------------------------------------------- column sums (bias grad, a11)
  * tape.cpp:347-358: db = q(db + sum_rows dy). Two deterministic passes:
@@ -124,8 +138,8 @@ int sfk_colsum_partial(int dtype, const void* x, int rows, int n, int64_t ld,
                        float* part, int* nparts, void* stream);
 int sfk_colsum_finish(int dtype, const float* part, int nparts, int n, void* out,
                       void* stream);
-/* Both passes in one call: out = q(out + sum_rows x). part: >= 64*n floats
- * scratch; counters: reserved (may be NULL). */
+/* Both passes in one call: out = q(out + sum_rows x). part: >= min(512*n, 4M)
+ * floats scratch; counters: reserved (may be NULL). */
 int sfk_colsum(int dtype, const void* x, int rows, int n, int64_t ld, float* part,
                int32_t* counters, void* out, void* stream);
 

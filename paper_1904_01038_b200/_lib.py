@@ -33,7 +33,7 @@ class GemmArgs(C.Structure):
                 ("b", vp), ("ldb", i64), ("b_kmajor", C.c_int),
                 ("c", vp), ("ldc", i64),
                 ("bias", vp), ("res", vp), ("ldr", i64), ("mask", vp), ("ldm", i64),
-                ("flags", C.c_int), ("force_simt", C.c_int), ("tile_n", C.c_int)]
+                ("flags", C.c_int), ("force_simt", C.c_int), ("tile_n", C.c_int), ("pair", C.c_int)]
 
 
 class AttnArgs(C.Structure):
@@ -73,6 +73,10 @@ sfk_layernorm_bwd = _sig("sfk_layernorm_bwd", C.c_int, C.c_int, vp, vp, C.c_int,
 sfk_colsum_partial = _sig("sfk_colsum_partial", C.c_int, C.c_int, vp, C.c_int, C.c_int, i64, vp, P(C.c_int), vp)
 sfk_colsum_finish = _sig("sfk_colsum_finish", C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp)
 sfk_colsum = _sig("sfk_colsum", C.c_int, C.c_int, vp, C.c_int, C.c_int, i64, vp, vp, vp, vp)
+sfk_layernorm_bwd_dx = _sig("sfk_layernorm_bwd_dx", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int,
+                            vp)
+sfk_layernorm_bwd_params = _sig("sfk_layernorm_bwd_params", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp,
+                                vp, vp)
 sfk_layernorm_bwd_fused = _sig("sfk_layernorm_bwd_fused", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp,
                                C.c_int, vp, vp, vp, vp, vp)
 sfk_attention_fwd = _sig("sfk_attention_fwd", C.c_int, P(AttnArgs), vp)

@@ -385,8 +385,9 @@ void DeviceTape::join_side() {
 }
 
 void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out) {
-  const int max_parts = 64;
-  float* part = static_cast<float*>(arena_.alloc(size_t(max_parts) * cols * 4));
+  // sfk_colsum scratch: min(512 * cols, 4M) floats
+  const size_t part_floats = std::min<size_t>(size_t(512) * cols, size_t(4) << 20);
+  float* part = static_cast<float*>(arena_.alloc(part_floats * 4));
   pbegin();
   sfk_check(sfk_colsum(dtype_, dy, rows, cols, ld, part, counters((cols + 1023) / 1024), out, cur_), "colsum");
   pend(Profiler::BiasGrad, 0, double(rows) * cols * esize_);
@@ -412,9 +413,37 @@ void DeviceTape::backward_node(int id) {
     case Kind::LayerNorm: {
       const Node& in = nodes_[n.in0];
       auto [dx, fresh] = grad_of(n.in0);
-      const int max_parts = 296;
+      const int max_parts = 4 * 148;  // sfk_layernorm_bwd_fused: <= 592 row blocks
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
       if (!fresh) wait_side_reader(dx);  // in-place accumulate into a buffer a wgrad may still read
+      if (dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024) {
+        // gamma/beta gradients are parameter work: side stream, after dy is ready
+        if (side_) {
+          cudaEvent_t ready = event();
+          cuda_check(cudaEventRecord(ready, stream_), "event record");
+          cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
+          cur_ = side_;
+        }
+        pbegin();
+        sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part, gptr(n.p0),
+                                           gptr(n.p1), cur_),
+                  "layernorm_bwd_params");
+        pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
+        if (side_) {
+          cudaEvent_t done = event();
+          cuda_check(cudaEventRecord(done, side_), "event record");
+          side_readers_.emplace_back(n.grad, done);
+          side_last_ = done;
+          cur_ = stream_;
+        }
+        pbegin();
+        sfk_check(sfk_layernorm_bwd_dx(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx,
+                                       fresh ? 0 : 1, cur_),
+                  "layernorm_bwd_dx");
+        pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
+        launches_ += 3;
+        return;
+      }
       pbegin();
       sfk_check(sfk_layernorm_bwd_fused(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx,
                                         fresh ? 0 : 1, part, counters(1), gptr(n.p0), gptr(n.p1), cur_),

@@ -80,17 +80,24 @@ __device__ __forceinline__ void load_b_kn(uint32_t (&b)[4], const T* s, int ld, 
 }
 
 // copy rows [r0, r0+n) x dh of a strided global matrix into smem rows [0, rows_pad) x DH (zero padded)
+// cp.async (LDGSTS) staging: every 16-byte chunk of the tile is in flight at
+// once (no register round trip, no load->store serialisation); rows past `n`
+// and columns past `dh` are zero-filled via src-size 0. Caller waits with
+// stage_wait() + __syncthreads().
 template <typename T, int DH>
 __device__ __forceinline__ void stage(T* s, int lds, const T* g, int64_t ldg, int r0, int n, int rows_pad, int dh) {
   constexpr int V = 8;  // 16-byte vectors
   const int vpr = DH / V;
   for (int i = threadIdx.x; i < rows_pad * vpr; i += blockDim.x) {
     const int r = i / vpr, c = (i % vpr) * V;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < n && c < dh) v = *reinterpret_cast<const uint4*>(g + int64_t(r0 + r) * ldg + c);
-    *reinterpret_cast<uint4*>(s + r * lds + c) = v;
+    const bool ok = r < n && c < dh;
+    const T* src = ok ? g + int64_t(r0 + r) * ldg + c : g;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(s + r * lds + c)), "l"(src),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
   }
 }
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct Args {
   int batch, qw, kw, heads, dh, causal;
@@ -127,6 +134,7 @@ __global__ void __launch_bounds__(kWarps * 32) fwd_k(Args a) {
                a.dh);
   stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), nk, nk_pad, a.dh);
   stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), nk, nk_pad, a.dh);
+  stage_wait();
   __syncthreads();
   const int r0 = warp * 16;
   if (q0 + r0 >= a.qw) return;
@@ -250,6 +258,7 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
   stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0) + q0, nq, kRows, a.dh);
   stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), nk, nk_pad, a.dh);
   stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), nk, nk_pad, a.dh);
+  stage_wait();
   __syncthreads();
   const int r0 = warp * 16;
   if (q0 + r0 >= a.qw) return;
@@ -377,6 +386,7 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
     St[i] = ok ? a.stats[(qrow0 + qstart + i) * a.heads + h] : make_float2(0.f, 0.f);
     Ds[i] = ok ? a.dsum[(qrow0 + qstart + i) * a.heads + h] : 0.f;
   }
+  stage_wait();
   __syncthreads();
   const int r0 = warp * 16;
   if (k0 + r0 >= a.kw) return;

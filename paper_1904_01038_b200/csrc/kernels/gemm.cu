@@ -528,6 +528,220 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------- 2-CTA (cta_group::2)
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with one
+// tcgen05.mma.cta_group::2 stream issued by the leader CTA: each CTA stages
+// its 128-row half of A and its BN/2-row half of B, so per SM the smem
+// operand traffic and the L2 re-read traffic are half of a 128 x BN 1-CTA
+// tile. Each CTA's TMEM holds its 128 accumulator rows; both run the same
+// coalesced epilogue.
+template <int BN>
+struct Cfg2 {
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + 4 * 32 * kStg * 4;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load whose completion bytes land on the leader CTA's barrier
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t leader_bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+}
+// commit: arrive on the barrier at this smem offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          saddr(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(saddr(bar)),
+      "r"(cta)
+      : "memory");
+}
+
+template <int BN, bool A_MN, bool B_MN, typename T>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Epi e, int M,
+             int N, int K, int vec_ok) {
+  using C = Cfg2<BN>;
+  constexpr int PM = 256;      // rows per pair tile
+  constexpr int HB = BN / 2;   // B rows staged by each CTA
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+
+  const int num_m = (M + PM - 1) / PM, num_n = (N + BN - 1) / BN;
+  const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
+  const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = pair; tile < tiles; tile += npairs) {
+        const int m0 = (tile % num_m) * PM + 128 * int(rank);
+        const int n0 = (tile / num_m) * BN + HB * int(rank);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE);
+          const uint32_t lbar = saddr(&full[s]) & 0xFEFFFFFFu;  // the leader CTA's barrier
+          uint8_t* a_dst = smem + s * C::STAGE;
+          uint8_t* b_dst = a_dst + C::A_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_pair(&ta, lbar, a_dst, k0, m0);
+          } else {
+            tma_load_2d_pair(&ta, lbar, a_dst, m0, k0);
+            tma_load_2d_pair(&ta, lbar, a_dst + 8192, m0 + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(&tb, lbar, b_dst, k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < HB / 64; ++j) tma_load_2d_pair(&tb, lbar, b_dst + j * 8192, n0 + 64 * j, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+      const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(A_MN) << 15) |
+                             (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(PM >> 4) << 24);
+      int it = 0, t = 0;
+      for (int tile = pair; tile < tiles; tile += npairs, ++t) {
+        const int buf = t & 1;
+        mbar_wait(&tempty[buf], ((t >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          fence_after();
+          const uint32_t a_addr = saddr(smem + s * C::STAGE);
+          const uint32_t b_addr = a_addr + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? smem_desc(a_addr + k * 2048, 8192, 1024) : smem_desc(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc(b_addr + k * 2048, 8192, 1024) : smem_desc(b_addr + k * 32, 16, 1024);
+            umma_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit_pair(&empty[s]);
+        }
+        umma_commit_pair(&tfull[buf]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * (32 * kStg);
+    int t = 0;
+    for (int tile = pair; tile < tiles; tile += npairs, ++t) {
+      const int buf = t & 1;
+      const int m0 = (tile % num_m) * PM + 128 * int(rank), n0 = (tile / num_m) * BN;
+      mbar_wait(&tfull[buf], (t >> 1) & 1);
+      fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + buf * BN + ch * 32, r);
+        if (n0 + ch * 32 >= N) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(stg + lane * kStg + 4 * j) =
+              make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                          __uint_as_float(r[4 * j + 3]));
+        __syncwarp();
+        const int cc = (lane & 3) * 8, col = n0 + ch * 32 + cc;
+        const int64_t row0 = m0 + quarter * 32 + (lane >> 2);
+        if (vec_ok && col + 8 <= N) {
+          epilogue_seg4<T>(e, row0, col, M, stg + (lane >> 2) * kStg + cc);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int rr = (lane >> 2) + 8 * i;
+            const int64_t row = row0 + 8 * i;
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = stg[rr * kStg + cc + j];
+            if (row < M && col < N) epilogue8<T>(e, row, col, N, v, false);
+          }
+        }
+        __syncwarp();
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(&tempty[buf]);
+        else mbar_arrive_cta(&tempty[buf], 0);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -599,6 +813,45 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   return check_launch("sfk_gemm(tcgen05)");
 }
 
+template <int BN, bool A_MN, bool B_MN, typename T>
+int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
+  using C = Cfg2<BN>;
+  CUtensorMap ta, tb;
+  bool ok = A_MN ? make_map(&ta, g->dtype, g->a, g->m, g->k, g->lda, 64)
+                 : make_map(&ta, g->dtype, g->a, g->k, g->m, g->lda, 128);
+  ok = ok && (B_MN ? make_map(&tb, g->dtype, g->b, g->n, g->k, g->ldb, 64)
+                   : make_map(&tb, g->dtype, g->b, g->k, g->n, g->ldb, BN / 2));
+  if (!ok) {
+    set_error("sfk_gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
+    return SFK_EINVAL;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(gemm_tc2<BN, A_MN, B_MN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+        cudaSuccess)
+      return check_launch("sfk_gemm: smem attribute");
+    attr_set = true;
+  }
+  const int tiles = ((g->m + 255) / 256) * ((g->n + BN - 1) / BN);
+  const int pairs = tiles < num_sms_cached() / 2 ? tiles : num_sms_cached() / 2;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, gemm_tc2<BN, A_MN, B_MN, T>, ta, tb, e, g->m, g->n, g->k, vec_ok ? 1 : 0);
+  return check_launch("sfk_gemm(tcgen05 pair)");
+}
+
 // tile width by wave efficiency (tiles / (waves * SMs)); wider wins ties
 int pick_bn(int m, int n) {
   const int sms = num_sms_cached();
@@ -621,6 +874,18 @@ template <typename T>
 int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   const int bn = g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
+  if (g->pair > 0) {
+#define SFK_TC2(BNV)                                                    \
+  switch (layout) {                                                     \
+    case 0: return launch2<BNV, false, false, T>(g, e, vec_ok, s);      \
+    case 1: return launch2<BNV, false, true, T>(g, e, vec_ok, s);       \
+    case 3: return launch2<BNV, true, true, T>(g, e, vec_ok, s);        \
+    default: return launch2<BNV, true, false, T>(g, e, vec_ok, s);      \
+  }
+    if (bn == 256) { SFK_TC2(256) }
+    SFK_TC2(128)
+#undef SFK_TC2
+  }
 #define SFK_TC(BNV)                                                    \
   switch (layout) {                                                    \
     case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s);      \

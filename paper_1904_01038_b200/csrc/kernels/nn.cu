@@ -352,7 +352,26 @@ int colsum_partial_vec(int, const void*, int, int, int64_t, float*, int*, cudaSt
 int ln_bwd_fused_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*,
                      int32_t*, void*, void*, cudaStream_t);
 int colsum_fused_vec(int, const void*, int, int, int64_t, float*, int32_t*, void*, cudaStream_t);
+int xent_vec(int, void*, int, int, int64_t, const int32_t*, int, float, float, void*, float*, cudaStream_t);
+int ln_dx_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, cudaStream_t);
+int ln_params_vec(int, const void*, const void*, int, int, const float*, float*, void*, void*, cudaStream_t);
 }  // namespace sfk
+
+extern "C" int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, int rows, int d, const void* gamma,
+                                    const float* stats, void* dx, int accumulate, void* stream) {
+  if (rows == 0) return SFK_OK;
+  const int e = sfk::ln_dx_vec(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_dx: needs 16-bit data, d % 8 == 0, d <= 1024, aligned rows");
+  return e;
+}
+
+extern "C" int sfk_layernorm_bwd_params(int dtype, const void* x, const void* dy, int rows, int d, const float* stats,
+                                        float* part, void* dgamma, void* dbeta, void* stream) {
+  if (rows == 0) return SFK_OK;
+  const int e = sfk::ln_params_vec(dtype, x, dy, rows, d, stats, part, dgamma, dbeta, sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_params: needs 16-bit data, d % 8 == 0, aligned rows");
+  return e;
+}
 
 extern "C" int sfk_layernorm_bwd_fused(int dtype, const void* x, const void* dy, int rows, int d, const void* gamma,
                                        const float* stats, void* dx, int accumulate, float* part, int32_t* counter,
@@ -474,6 +493,9 @@ extern "C" int sfk_colsum_finish(int dtype, const float* part, int nparts, int n
 extern "C" int sfk_xent_fwd_bwd(int dtype, void* logits, int rows, int vocab, int64_t ld, const int32_t* gold,
                                 int pad_id, float eps, float seed, void* dlogits, float* row_out, void* stream) {
   if (rows == 0) return SFK_OK;
+  if (int e = xent_vec(dtype, logits, rows, vocab, ld, gold, pad_id, eps, seed, dlogits, row_out, as_stream(stream));
+      e != SFK_EUNSUP)
+    return e;
   const size_t smem = size_t(vocab) * elem_size(dtype);
   if (smem > 200 * 1024) {
     set_error("sfk_xent_fwd_bwd: vocab too large for the staged row");

@@ -10,8 +10,8 @@ namespace vec {
 
 template <typename T>
 struct V8 {
-  static __device__ __forceinline__ void load(const T* p, float (&f)[8]) {
-    const uint4 u = *reinterpret_cast<const uint4*>(p);
+  static __device__ __forceinline__ void load(const T* p, float (&f)[8]) { unpack(*reinterpret_cast<const uint4*>(p), f); }
+  static __device__ __forceinline__ void unpack(const uint4& u, float (&f)[8]) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -77,7 +77,18 @@ __global__ void __launch_bounds__(128) embed_bwd_v(const int32_t* __restrict__ u
   for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
     float acc[8];
     V8<T>::load(g + c, acc);
-    for (int s = s0; s < s1; ++s) {
+    int s = s0;
+    // rows are added strictly in recording order; only the loads run ahead
+    for (; s + 4 <= s1; s += 4) {
+      float f[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) V8<T>::load(dx + int64_t(srows[s + u]) * d + c, f[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], Num<T>::rnd(__fmul_rn(scale, f[u][i])));
+    }
+    for (; s < s1; ++s) {
       float f[8];
       V8<T>::load(dx + int64_t(srows[s]) * d + c, f);
 #pragma unroll
@@ -173,24 +184,35 @@ __device__ __forceinline__ void ln_bwd_body(const T* __restrict__ x, const T* __
 #pragma unroll
     for (int e = 0; e < 8; ++e) pg[i][e] = pb[i][e] = 0.f;
   const float inv_n = __fdiv_rn(1.0f, float(d));
+  // x and dy stay packed (16-bit) between the two passes over the row; only
+  // the per-column gamma/beta partials live in fp32 registers
   for (int r = r0 + wid; r < r1; r += 8) {
     const float2 st = stats[r];
-    float xh[kMaxCh][8], gy[kMaxCh][8];
+    uint4 xr[kMaxCh], gr[kMaxCh], dxo[kMaxCh];
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < d) {
+        xr[i] = *reinterpret_cast<const uint4*>(x + int64_t(r) * d + c);
+        gr[i] = *reinterpret_cast<const uint4*>(dy + int64_t(r) * d + c);
+        if (accumulate) dxo[i] = *reinterpret_cast<const uint4*>(dx + int64_t(r) * d + c);
+      }
+    }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < kMaxCh; ++i) {
       const int c = (lane + 32 * i) * 8;
       if (c < d) {
-        float gg[8];
-        V8<T>::load(x + int64_t(r) * d + c, xh[i]);
-        V8<T>::load(dy + int64_t(r) * d + c, gy[i]);
+        float gg[8], xh[8], gy[8];
         V8<T>::load(g + c, gg);
+        V8<T>::unpack(xr[i], xh);
+        V8<T>::unpack(gr[i], gy);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          xh[i][e] = __fmul_rn(__fsub_rn(xh[i][e], st.x), st.y);
-          const float dxh = __fmul_rn(gy[i][e], gg[e]);
+          const float xhat = __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+          const float dxh = __fmul_rn(gy[e], gg[e]);
           s1 += dxh;
-          s2 += dxh * xh[i][e];
+          s2 += dxh * xhat;
         }
       }
     }
@@ -201,16 +223,19 @@ __device__ __forceinline__ void ln_bwd_body(const T* __restrict__ x, const T* __
     for (int i = 0; i < kMaxCh; ++i) {
       const int c = (lane + 32 * i) * 8;
       if (c < d) {
-        float gg[8], o[8];
+        float gg[8], xh[8], gy[8], o[8];
         V8<T>::load(g + c, gg);
-        if (accumulate) V8<T>::load(dx + int64_t(r) * d + c, o);
+        V8<T>::unpack(xr[i], xh);
+        V8<T>::unpack(gr[i], gy);
+        if (accumulate) V8<T>::unpack(dxo[i], o);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float dxh = __fmul_rn(gy[i][e], gg[e]);
-          const float v = __fmul_rn(st.y, __fsub_rn(__fsub_rn(dxh, m1), __fmul_rn(xh[i][e], m2)));
+          const float xhat = __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+          const float dxh = __fmul_rn(gy[e], gg[e]);
+          const float v = __fmul_rn(st.y, __fsub_rn(__fsub_rn(dxh, m1), __fmul_rn(xhat, m2)));
           o[e] = accumulate ? __fadd_rn(o[e], v) : v;
-          pg[i][e] += gy[i][e] * xh[i][e];
-          pb[i][e] += gy[i][e];
+          pg[i][e] += gy[e] * xhat;
+          pb[i][e] += gy[e];
         }
         V8<T>::store(dx + int64_t(r) * d + c, o);
       }
@@ -334,7 +359,20 @@ __global__ void colsum_partial_v(const T* __restrict__ x, int rows, int n, int64
   if (c >= n) return;
   const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int r = r0; r < r1; ++r) {
+  int r = r0;
+  for (; r + 4 <= r1; r += 4) {  // 4 loads in flight, sums still in row order
+    uint4 u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u[j] = *reinterpret_cast<const uint4*>(x + int64_t(r + j) * ld + c);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float f[8];
+      V8<T>::unpack(u[j], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] += f[e];
+    }
+  }
+  for (; r < r1; ++r) {
     float f[8];
     V8<T>::load(x + int64_t(r) * ld + c, f);
 #pragma unroll
@@ -345,7 +383,250 @@ __global__ void colsum_partial_v(const T* __restrict__ x, int rows, int n, int64
   *reinterpret_cast<float4*>(o + 4) = make_float4(s[4], s[5], s[6], s[7]);
 }
 
+// LN backward split for the B200 schedule: the activation gradient (critical
+// path) is one warp per row with no column state; the gamma/beta gradients
+// (parameter work, run on the side stream) are a column reduction over rows.
+template <typename T>
+__global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T* __restrict__ dy, int rows, int d,
+                                              const T* __restrict__ g, const float2* __restrict__ stats,
+                                              T* __restrict__ dx, int accumulate) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  const float2 st = stats[r];
+  const float inv_n = __fdiv_rn(1.0f, float(d));
+  uint4 xr[kMaxCh], gr[kMaxCh], dxo[kMaxCh];
+#pragma unroll
+  for (int i = 0; i < kMaxCh; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < d) {
+      xr[i] = *reinterpret_cast<const uint4*>(x + int64_t(r) * d + c);
+      gr[i] = *reinterpret_cast<const uint4*>(dy + int64_t(r) * d + c);
+      if (accumulate) dxo[i] = *reinterpret_cast<const uint4*>(dx + int64_t(r) * d + c);
+    }
+  }
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxCh; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < d) {
+      float gg[8], xh[8], gy[8];
+      V8<T>::load(g + c, gg);
+      V8<T>::unpack(xr[i], xh);
+      V8<T>::unpack(gr[i], gy);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float dxh = __fmul_rn(gy[e], gg[e]);
+        s1 += dxh;
+        s2 += dxh * __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+      }
+    }
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  const float m1 = __fmul_rn(s1, inv_n), m2 = __fmul_rn(s2, inv_n);
+#pragma unroll
+  for (int i = 0; i < kMaxCh; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < d) {
+      float gg[8], xh[8], gy[8], o[8];
+      V8<T>::load(g + c, gg);
+      V8<T>::unpack(xr[i], xh);
+      V8<T>::unpack(gr[i], gy);
+      if (accumulate) V8<T>::unpack(dxo[i], o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xhat = __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+        const float v = __fmul_rn(st.y, __fsub_rn(__fsub_rn(__fmul_rn(gy[e], gg[e]), m1), __fmul_rn(xhat, m2)));
+        o[e] = accumulate ? __fadd_rn(o[e], v) : v;
+      }
+      V8<T>::store(dx + int64_t(r) * d + c, o);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) ln_dgb_partial_v(const T* __restrict__ x, const T* __restrict__ dy, int rows,
+                                                       int d, const float2* __restrict__ stats, int rpb,
+                                                       float* __restrict__ part, int nblk) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= d) return;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  float pg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int r = r0;
+  for (; r + 2 <= r1; r += 2) {
+    uint4 xu[2], gu[2];
+    float2 st[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      xu[j] = *reinterpret_cast<const uint4*>(x + int64_t(r + j) * d + c);
+      gu[j] = *reinterpret_cast<const uint4*>(dy + int64_t(r + j) * d + c);
+      st[j] = stats[r + j];
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      float xh[8], gy[8];
+      V8<T>::unpack(xu[j], xh);
+      V8<T>::unpack(gu[j], gy);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        pg[e] += gy[e] * __fmul_rn(__fsub_rn(xh[e], st[j].x), st[j].y);
+        pb[e] += gy[e];
+      }
+    }
+  }
+  for (; r < r1; ++r) {
+    float xh[8], gy[8];
+    V8<T>::load(x + int64_t(r) * d + c, xh);
+    V8<T>::load(dy + int64_t(r) * d + c, gy);
+    const float2 st = stats[r];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      pg[e] += gy[e] * __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+      pb[e] += gy[e];
+    }
+  }
+  float* og = part + int64_t(blockIdx.y) * d + c;
+  float* ob = part + int64_t(nblk + blockIdx.y) * d + c;
+  *reinterpret_cast<float4*>(og) = make_float4(pg[0], pg[1], pg[2], pg[3]);
+  *reinterpret_cast<float4*>(og + 4) = make_float4(pg[4], pg[5], pg[6], pg[7]);
+  *reinterpret_cast<float4*>(ob) = make_float4(pb[0], pb[1], pb[2], pb[3]);
+  *reinterpret_cast<float4*>(ob + 4) = make_float4(pb[4], pb[5], pb[6], pb[7]);
+}
+
+// Fused label-smoothed cross entropy fwd+bwd for one vocabulary row per
+// block (tape.cpp:259-290, 481-502): the row is staged in shared memory with
+// 16-byte loads; pass 1 computes max / first argmax / sum-exp online,
+// pass 2 writes dlogits = q(seed*(softmax - target)) with 16-byte stores and
+// accumulates the smoothing sum of (lse - l).
+template <typename T>
+__global__ void __launch_bounds__(512) xent_v(const T* __restrict__ logits, int V, int64_t ld,
+                                             const int32_t* __restrict__ gold, int pad, float eps, float seed,
+                                             T* __restrict__ dlogits, float* __restrict__ row_out) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  extern __shared__ uint4 xrow[];
+  __shared__ float rm[16], rs[16];
+  __shared__ int ri[16];
+  const int r = blockIdx.x, tid = threadIdx.x, lane = tid % 32, wid = tid / 32, nw = blockDim.x / 32;
+  const int gid = gold[r];
+  const int nch = V / 8;
+  const T* src = logits + int64_t(r) * ld;
+  T* dst = dlogits ? dlogits + int64_t(r) * ld : nullptr;
+  if (gid == pad) {
+    if (dst)
+      for (int ch = tid; ch < nch; ch += blockDim.x) reinterpret_cast<uint4*>(dst)[ch] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) reinterpret_cast<float4*>(row_out)[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const float L2E = 1.4426950408889634f;
+  float m = -INFINITY, s = 0.f;
+  int mi = 0x7fffffff;
+  for (int ch = tid; ch < nch; ch += blockDim.x) {
+    const uint4 u = reinterpret_cast<const uint4*>(src)[ch];
+    xrow[ch] = u;
+    float f[8];
+    V8<T>::unpack(u, f);
+    float cm = f[0];
+    int ci = 0;
+#pragma unroll
+    for (int e = 1; e < 8; ++e)
+      if (f[e] > cm) cm = f[e], ci = e;
+    if (cm > m) {
+      s *= exp2f((m - cm) * L2E);
+      m = cm;
+      mi = ch * 8 + ci;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += exp2f((f[e] - m) * L2E);
+  }
+  // (max, sum, first argmax) combine
+  auto comb = [&](float om, float os, int oi) {
+    const float M = fmaxf(m, om);
+    const float a = m == -INFINITY ? 0.f : s * exp2f((m - M) * L2E);
+    const float b = om == -INFINITY ? 0.f : os * exp2f((om - M) * L2E);
+    const int idx = (om > m || (om == m && oi < mi)) ? oi : mi;
+    m = M;
+    s = a + b;
+    mi = idx;
+  };
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+    comb(om, os, oi);
+  }
+  if (lane == 0) rm[wid] = m, rs[wid] = s, ri[wid] = mi;
+  __syncthreads();
+  if (wid == 0) {
+    m = lane < nw ? rm[lane] : -INFINITY;
+    s = lane < nw ? rs[lane] : 0.f;
+    mi = lane < nw ? ri[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o), os = __shfl_xor_sync(0xffffffffu, s, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, mi, o);
+      comb(om, os, oi);
+    }
+    if (lane == 0) rm[0] = m, rs[0] = s, ri[0] = mi;
+  }
+  __syncthreads();
+  const float lse = __fadd_rn(rm[0], logf(rs[0]));
+  const int amax = ri[0];
+  __syncthreads();
+  const float uni = __fdiv_rn(eps, float(V)), on = __fadd_rn(1.0f - eps, uni);
+  float sm = 0.f;
+  for (int ch = tid; ch < nch; ch += blockDim.x) {
+    float f[8], o[8];
+    V8<T>::unpack(xrow[ch], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float p = exp2f((f[e] - lse) * L2E);
+      o[e] = __fmul_rn(seed, __fsub_rn(p, ch * 8 + e == gid ? on : uni));
+      sm += __fsub_rn(lse, f[e]);
+    }
+    if (dst) V8<T>::store(dst + ch * 8, o);
+  }
+  sm = warp_sum(sm);
+  if (lane == 0) rs[wid] = sm;
+  __syncthreads();
+  if (tid == 0) {
+    float tot = 0.f;
+    for (int w = 0; w < nw; ++w) tot += rs[w];
+    float gl[8];
+    V8<T>::unpack(xrow[gid / 8], gl);
+    const float nll = __fsub_rn(lse, gl[gid % 8]);
+    float loss = nll;
+    if (eps != 0.0f) loss = __fadd_rn(__fmul_rn(1.0f - eps, nll), __fmul_rn(__fdiv_rn(eps, float(V)), tot));
+    reinterpret_cast<float4*>(row_out)[r] = make_float4(Num<T>::rnd(loss), nll, amax == gid ? 1.f : 0.f, 1.f);
+  }
+}
+
 }  // namespace vec
+
+int xent_vec(int dtype, void* logits, int rows, int V, int64_t ld, const int32_t* gold, int pad, float eps, float seed,
+             void* dlogits, float* row_out, cudaStream_t s) {
+  const uintptr_t al = reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits) |
+                       reinterpret_cast<uintptr_t>(row_out);
+  if (dtype == SFK_F32 || V % 8 || ld % 8 || (al & 15) || size_t(V) * 2 > 200 * 1024) return SFK_EUNSUP;
+  const size_t smem = size_t(V) * 2;
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(vec::xent_v<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(vec::xent_v<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  if (dtype == SFK_F16)
+    launch_pdl(vec::xent_v<__half>, dim3(rows), dim3(512), smem, s, static_cast<const __half*>(logits), V, ld, gold,
+               pad, eps, seed, static_cast<__half*>(dlogits), row_out);
+  else
+    launch_pdl(vec::xent_v<__nv_bfloat16>, dim3(rows), dim3(512), smem, s, static_cast<const __nv_bfloat16*>(logits), V,
+               ld, gold, pad, eps, seed, static_cast<__nv_bfloat16*>(dlogits), row_out);
+  return check_launch("sfk_xent_fwd_bwd(vec)");
+}
 
 namespace {
 inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -398,8 +679,8 @@ int ln_fwd_vec(int dtype, const void* x, int rows, int d, const void* g, const v
 int ln_bwd_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats, void* dx,
                int accumulate, float* part, int* nparts, cudaStream_t s) {
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g)) return SFK_EUNSUP;
-  int nblk = (rows + 31) / 32;
-  nblk = std::max(1, std::min(nblk, 296));
+  int nblk = (rows + 15) / 16;
+  nblk = std::max(1, std::min(nblk, 4 * 148));
   const int rpb = (rows + nblk - 1) / nblk;
   *nparts = nblk;
   const size_t smem = size_t(2) * 8 * d * sizeof(float);
@@ -428,24 +709,35 @@ int colsum_partial_vec(int dtype, const void* x, int rows, int n, int64_t ld, fl
 // Fold of `nparts` column partials with 8 independent accumulators per thread
 // (the loads of a column no longer serialise behind one add chain); up to two
 // vectors (gamma and beta) per launch. Fixed association order: deterministic.
+// block = 8 partial-groups x 32 columns: thread (g, c) folds partials
+// g, g+8, ... with 4 independent chains, then group sums combine in order.
 template <typename T>
-__global__ void fold_k(const float* __restrict__ pa, const float* __restrict__ pb, int nparts, int n,
-                       T* __restrict__ oa, T* __restrict__ ob) {
+__global__ void __launch_bounds__(256) fold_k(const float* __restrict__ pa, const float* __restrict__ pb, int nparts,
+                                             int n, T* __restrict__ oa, T* __restrict__ ob) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float red[8][33];
+  const int g = threadIdx.x / 32, cl = threadIdx.x % 32;
+  const int c = blockIdx.x * 32 + cl;
   const bool second = blockIdx.y == 1;
-  if (c >= n) return;
   const float* p = second ? pb : pa;
   T* o = second ? ob : oa;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int q = 0;
-  for (; q + 8 <= nparts; q += 8)
+  float acc[4] = {0, 0, 0, 0};
+  if (c < n) {
+    int q = g, u = 0;
+    for (; q + 24 < nparts; q += 32)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += p[int64_t(q + u) * n + c];
-  for (; q < nparts; ++q) acc[q & 7] += p[int64_t(q) * n + c];
-  const float s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-  Num<T>::st(o + c, Num<T>::ld(o + c) + s);
+      for (int j = 0; j < 4; ++j) acc[j] += p[int64_t(q + 8 * j) * n + c];
+    for (; q < nparts; q += 8, ++u) acc[u & 3] += p[int64_t(q) * n + c];
+  }
+  red[g][cl] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  __syncthreads();
+  if (g == 0 && c < n) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][cl];
+    Num<T>::st(o + c, Num<T>::ld(o + c) + s);
+  }
 }
 
 int ln_bwd_fused_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats,
@@ -454,15 +746,54 @@ int ln_bwd_fused_vec(int dtype, const void* x, const void* dy, int rows, int d, 
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g)) return SFK_EUNSUP;
   int nparts = 0;
   if (int e = ln_bwd_vec(dtype, x, dy, rows, d, g, stats, dx, accumulate, part, &nparts, s)) return e;
-  dim3 grid((d + 127) / 128, 2);
+  dim3 grid((d + 31) / 32, 2);
   if (dtype == SFK_F16)
-    launch_pdl(fold_k<__half>, grid, 128, 0, s, part, part + size_t(nparts) * d, nparts, d, static_cast<__half*>(dgamma),
+    launch_pdl(fold_k<__half>, grid, 256, 0, s, part, part + size_t(nparts) * d, nparts, d, static_cast<__half*>(dgamma),
                                         static_cast<__half*>(dbeta));
   else
-    launch_pdl(fold_k<__nv_bfloat16>, grid, 128, 0, s, part, part + size_t(nparts) * d, nparts, d,
+    launch_pdl(fold_k<__nv_bfloat16>, grid, 256, 0, s, part, part + size_t(nparts) * d, nparts, d,
                                                static_cast<__nv_bfloat16*>(dgamma),
                                                static_cast<__nv_bfloat16*>(dbeta));
   return check_launch("sfk_layernorm_bwd_fused(fold)");
+}
+
+int ln_dx_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats, void* dx,
+              int accumulate, cudaStream_t s) {
+  if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g)) return SFK_EUNSUP;
+  const int blocks = (rows + 7) / 8;
+  if (dtype == SFK_F16)
+    launch_pdl(vec::ln_dx_v<__half>, dim3(blocks), dim3(256), 0, s, static_cast<const __half*>(x),
+               static_cast<const __half*>(dy), rows, d, static_cast<const __half*>(g),
+               reinterpret_cast<const float2*>(stats), static_cast<__half*>(dx), accumulate);
+  else
+    launch_pdl(vec::ln_dx_v<__nv_bfloat16>, dim3(blocks), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(x),
+               static_cast<const __nv_bfloat16*>(dy), rows, d, static_cast<const __nv_bfloat16*>(g),
+               reinterpret_cast<const float2*>(stats), static_cast<__nv_bfloat16*>(dx), accumulate);
+  return check_launch("sfk_layernorm_bwd_dx(vec)");
+}
+
+int ln_params_vec(int dtype, const void* x, const void* dy, int rows, int d, const float* stats, float* part,
+                  void* dgamma, void* dbeta, cudaStream_t s) {
+  if (dtype == SFK_F32 || d % 8 || !al16(x) || !al16(dy)) return SFK_EUNSUP;
+  const int col_blocks = (d / 8 + 127) / 128;
+  int nblk = std::max(1, std::min(256, (148 * 4) / col_blocks));
+  nblk = std::min(nblk, std::max(1, rows / 8));
+  const int rpb = (rows + nblk - 1) / nblk;
+  if (dtype == SFK_F16)
+    launch_pdl(vec::ln_dgb_partial_v<__half>, dim3(col_blocks, nblk), dim3(128), 0, s, static_cast<const __half*>(x),
+               static_cast<const __half*>(dy), rows, d, reinterpret_cast<const float2*>(stats), rpb, part, nblk);
+  else
+    launch_pdl(vec::ln_dgb_partial_v<__nv_bfloat16>, dim3(col_blocks, nblk), dim3(128), 0, s,
+               static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), rows, d,
+               reinterpret_cast<const float2*>(stats), rpb, part, nblk);
+  dim3 grid((d + 31) / 32, 2);
+  if (dtype == SFK_F16)
+    launch_pdl(fold_k<__half>, grid, 256, 0, s, part, part + size_t(nblk) * d, nblk, d, static_cast<__half*>(dgamma),
+               static_cast<__half*>(dbeta));
+  else
+    launch_pdl(fold_k<__nv_bfloat16>, grid, 256, 0, s, part, part + size_t(nblk) * d, nblk, d,
+               static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
+  return check_launch("sfk_layernorm_bwd_params(vec)");
 }
 
 int colsum_fused_vec(int dtype, const void* x, int rows, int n, int64_t ld, float* part, int32_t* /*counters*/,
@@ -470,11 +801,11 @@ int colsum_fused_vec(int dtype, const void* x, int rows, int n, int64_t ld, floa
   if (dtype == SFK_F32 || n % 8 || ld % 8 || !al16(x)) return SFK_EUNSUP;
   int nparts = 0;
   if (int e = colsum_partial_vec(dtype, x, rows, n, ld, part, &nparts, s)) return e;
-  dim3 grid((n + 127) / 128, 1);
+  dim3 grid((n + 31) / 32, 1);
   if (dtype == SFK_F16)
-    launch_pdl(fold_k<__half>, grid, 128, 0, s, part, nullptr, nparts, n, static_cast<__half*>(out), nullptr);
+    launch_pdl(fold_k<__half>, grid, 256, 0, s, part, nullptr, nparts, n, static_cast<__half*>(out), nullptr);
   else
-    launch_pdl(fold_k<__nv_bfloat16>, grid, 128, 0, s, part, nullptr, nparts, n, static_cast<__nv_bfloat16*>(out), nullptr);
+    launch_pdl(fold_k<__nv_bfloat16>, grid, 256, 0, s, part, nullptr, nparts, n, static_cast<__nv_bfloat16*>(out), nullptr);
   return check_launch("sfk_colsum(fold)");
 }
 
@@ -482,9 +813,11 @@ int colsum_partial_vec(int dtype, const void* x, int rows, int n, int64_t ld, fl
                        cudaStream_t s) {
   if (dtype == SFK_F32 || n % 8 || ld % 8 || !al16(x)) return SFK_EUNSUP;
   // enough row chunks to fill the machine: ~4 blocks of 128 threads per SM
+  // enough row chunks for ~4 blocks per SM; partial scratch capped at 4M floats
   const int col_blocks = (n / 8 + 127) / 128;
-  int nblk = std::max(1, std::min(64, (148 * 4) / std::max(1, col_blocks)));
-  nblk = std::min(nblk, std::max(1, rows / 16));
+  int nblk = std::max(1, std::min(512, (148 * 4) / std::max(1, col_blocks)));
+  nblk = std::min(nblk, std::max(1, (4 << 20) / std::max(1, n)));
+  nblk = std::min(nblk, std::max(1, rows / 8));
   const int rpb = (rows + nblk - 1) / nblk;
   *nparts = nblk;
   dim3 grid(col_blocks, nblk);

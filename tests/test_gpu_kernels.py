@@ -30,7 +30,7 @@ def ptr(t):
 TDT = {0: torch.float32, 1: torch.float16, 2: torch.bfloat16}
 
 
-def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=False, with_c=None):
+def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=False, with_c=None, pair=0, tile_n=0):
     lib = L()
     g = torch.Generator(device="cuda").manual_seed(seed)
     td = TDT[dtype]
@@ -46,7 +46,7 @@ def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=Fal
     args = lib.GemmArgs(m=m, n=n, k=k, dtype=dtype, a=ptr(a_store), lda=a_store.shape[1], a_kmajor=int(a_kmajor),
                         b=ptr(b_store), ldb=b_store.shape[1], b_kmajor=int(b_kmajor), c=ptr(c), ldc=n,
                         bias=ptr(bias), res=ptr(res), ldr=n, mask=ptr(mask), ldm=n, flags=flags,
-                        force_simt=int(force_simt))
+                        force_simt=int(force_simt), pair=pair, tile_n=tile_n)
     lib.check(lib.sfk_gemm(C.byref(args), stream()), kernel=True)
     torch.cuda.synchronize()
     acc = (A.double() @ B.double().t()).float()
@@ -84,6 +84,22 @@ def test_gemm_tc_layouts(dtype, layout, shape):
     got, want = run_gemm(m, n, k, dtype, *layout)
     tol = 4e-3 if dtype == 1 else 2e-2
     torch.testing.assert_close(got, want, rtol=tol, atol=tol * max(1.0, k ** 0.5 * 0.25))
+
+
+@pytest.mark.parametrize("tile_n", [128, 256])
+@pytest.mark.parametrize("layout", [(True, True), (True, False), (False, False), (False, True)])
+@pytest.mark.parametrize("shape", [(256, 256, 64), (300, 200, 96), (1000, 136, 520), (3584, 1024, 1024),
+                                   (4096, 3072, 1024), (64, 40, 32)])
+def test_gemm_tc_cta_pair(tile_n, layout, shape):
+    # cta_group::2 tiles (256 x tile_n per CTA pair), fp16 and a fused epilogue
+    m, n, k = shape
+    lda = k if layout[0] else m
+    ldb = k if layout[1] else n
+    if lda % 8 or ldb % 8:
+        pytest.skip("TMA pitch")
+    flags = (1 | 2 | 16) if layout == (True, True) else (32 if layout == (False, False) else 0)
+    got, want = run_gemm(m, n, k, 1, *layout, flags=flags, pair=1, tile_n=tile_n)
+    torch.testing.assert_close(got, want, rtol=4e-3, atol=4e-3 * max(1.0, k ** 0.5 * 0.25))
 
 
 @pytest.mark.parametrize("flags", [1 | 2, 1 | 2 | 4, 1 | 2 | 16, 8, 32, 1 | 2 | 4 | 16])
@@ -161,7 +177,7 @@ def test_layernorm_matches_reference(fp16, rows, d):
     stats = torch.zeros(rows, 2, device="cuda")
     lib.check(lib.sfk_layernorm_fwd(dt, ptr(tx), rows, d, ptr(tg), ptr(tb), ptr(ty), ptr(stats), stream()), True)
     tdx = torch.zeros_like(tx)
-    part = torch.zeros(2 * 296 * d, device="cuda")
+    part = torch.zeros(2 * 592 * d, device="cuda")
     npart = C.c_int()
     lib.check(lib.sfk_layernorm_bwd(dt, ptr(tx), ptr(tdy), rows, d, ptr(tg), ptr(stats), ptr(tdx), 0, ptr(part),
                                     C.byref(npart), stream()), True)
@@ -270,7 +286,7 @@ def test_colsum_single_launch(dt, rows, n, ld):
     x = torch.randn(rows, ld, device="cuda", generator=g).to(TDT[dt])
     out = torch.randn(n, device="cuda", generator=g).to(TDT[dt])
     want = (out.double() + x[:, :n].double().sum(0))
-    part = torch.zeros(64 * n, device="cuda")
+    part = torch.zeros(min(512 * n, 4 << 20), device="cuda")
     ctr = torch.zeros(64, dtype=torch.int32, device="cuda")
     for _ in range(2):  # counters must re-arm
         o = out.clone()
@@ -292,7 +308,7 @@ def test_layernorm_bwd_fused_equals_two_phase(rows, d):
     y = torch.zeros_like(x)
     stats = torch.zeros(rows, 2, device="cuda")
     lib.check(lib.sfk_layernorm_fwd(1, ptr(x), rows, d, ptr(gm), ptr(bt), ptr(y), ptr(stats), stream()), True)
-    part = torch.zeros(2 * 296 * d, device="cuda")
+    part = torch.zeros(2 * 592 * d, device="cuda")
     dx1, dx2 = torch.zeros_like(x), torch.zeros_like(x)
     dg1, db1 = torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
     dg2, db2 = dg1.clone(), db1.clone()
@@ -312,6 +328,15 @@ def test_layernorm_bwd_fused_equals_two_phase(rows, d):
     assert torch.equal(dx1, dx2)
     torch.testing.assert_close(dg1.float(), dg2.float(), rtol=2e-3, atol=2e-3)
     torch.testing.assert_close(db1.float(), db2.float(), rtol=2e-3, atol=2e-3)
+    # split form (dx on the critical path, gamma/beta as a column reduction)
+    dx4, dg4, db4 = torch.zeros_like(x), torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
+    lib.check(lib.sfk_layernorm_bwd_dx(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx4), 0, stream()), True)
+    lib.check(lib.sfk_layernorm_bwd_params(1, ptr(x), ptr(dy), rows, d, ptr(stats), ptr(part2), ptr(dg4), ptr(db4),
+                                           stream()), True)
+    torch.cuda.synchronize()
+    assert torch.equal(dx1, dx4)
+    torch.testing.assert_close(dg1.float(), dg4.float(), rtol=2e-3, atol=2e-3)
+    torch.testing.assert_close(db1.float(), db4.float(), rtol=2e-3, atol=2e-3)
     # deterministic: a second run is bitwise identical
     dx3, dg3, db3 = torch.zeros_like(x), torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
     lib.check(lib.sfk_layernorm_bwd_fused(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx3), 0, ptr(part2),

@@ -23,7 +23,7 @@ SHAPES = [  # (name, m, n, k, a_kmajor, b_kmajor, flags)
 ]
 
 
-def run(name, m, n, k, ak, bk, flags, tile_n, iters=20):
+def run(name, m, n, k, ak, bk, flags, tile_n, iters=20, pair=0):
     dt = torch.float16
     a = torch.randn(m * k, device="cuda").to(dt)
     b = torch.randn(n * k, device="cuda").to(dt)
@@ -32,11 +32,22 @@ def run(name, m, n, k, ak, bk, flags, tile_n, iters=20):
     res = torch.randn(m * n, device="cuda").to(dt)
     args = L.GemmArgs(m=m, n=n, k=k, dtype=1, a=a.data_ptr(), lda=k if ak else m, a_kmajor=ak, b=b.data_ptr(),
                       ldb=k if bk else n, b_kmajor=bk, c=c.data_ptr(), ldc=n, bias=bias.data_ptr(),
-                      res=res.data_ptr(), ldr=n, mask=res.data_ptr(), ldm=n, flags=flags, tile_n=tile_n)
+                      res=res.data_ptr(), ldr=n, mask=res.data_ptr(), ldm=n, flags=flags, tile_n=tile_n, pair=pair)
     st = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(3):
         L.check(L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream)), True)
+    if os.environ.get("GB_BACK2BACK"):
+        # back-to-back launches between two events: GPU time per GEMM with the
+        # host ahead of the device (L2 warm: steady-state in-step conditions)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(iters):
+            L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream))
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        return 2.0 * m * n * k / (ms * 1e-3) / 1e12, ms
     ts = []
     for _ in range(iters):
         flush.zero_()
@@ -55,9 +66,12 @@ def main():
     out = {}
     for sh in SHAPES:
         row = {}
-        for tn in (0, 64, 128, 256):
+        for tn in (0, 128, 256):
             tf, ms = run(*sh, tile_n=tn)
             row[str(tn)] = (round(tf, 1), round(ms * 1e3, 1))
+        for tn in (128, 256):
+            tf, ms = run(*sh, tile_n=tn, pair=1)
+            row["p" + str(tn)] = (round(tf, 1), round(ms * 1e3, 1))
         out[sh[0]] = row
         print(sh[0], json.dumps(row), flush=True)
 
