@@ -253,6 +253,7 @@ def run_ours(args, cfg):
             tokens += s["ntokens"]
             skipped += int(s["skipped"])
             dev_ms += tr.last_step_ms
+            h2d += tr.last_io_bytes[0]
             launches += tr.kernel_launches
         e1.record(ext)
         torch.cuda.synchronize()
@@ -260,8 +261,8 @@ def run_ours(args, cfg):
     e2e_ms = e0.elapsed_time(e1)
     dev_ms_max = allmax(dev_ms, world)
     e2e_ms_max = allmax(e2e_ms, world)
-    # ids blob per sub-batch: ~ (2*S*B + 2*T*B + ...) int32; measure from one packed step
-    h2d = int(allsum(0, world))
+    # packed id matrices + embedding-backward segments uploaded per step (this rank)
+    h2d = int(h2d / max(1, args.steps))
 
     # profiling pass (not timed): CUDA events around every launch on the trainer stream
     tr.set_profile(True)

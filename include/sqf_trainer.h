@@ -77,6 +77,8 @@ int sqf_trainer_restore(void* t, int64_t step, int32_t epoch, int32_t cursor, do
 /* our kernel launches during the last train_step, and its device time (ms) */
 int64_t sqf_trainer_kernel_launches(void* t);
 float sqf_trainer_last_step_ms(void* t);
+/* host->device bytes of the last step (returned) and device->host (*d2h) */
+int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h);
 /* CUDA stream the trainer launches on (cudaStream_t) */
 void* sqf_trainer_stream(void* t);
 /* per-launch CUDA-event profiling of the following steps (on = 1) and its

@@ -297,6 +297,13 @@ class Trainer:
         return float(L.sqf_trainer_last_step_ms(self._h))
 
     @property
+    def last_io_bytes(self):
+        """(host->device, device->host) bytes moved by the last step."""
+        d2h = C.c_int64()
+        h2d = L.sqf_trainer_last_io_bytes(self._h, C.byref(d2h))
+        return int(h2d), int(d2h.value)
+
+    @property
     def stream(self) -> int:
         return int(L.sqf_trainer_stream(self._h) or 0)
 

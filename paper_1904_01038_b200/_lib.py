@@ -115,6 +115,7 @@ sqf_trainer_set_injector = _sig("sqf_trainer_set_injector", C.c_int, vp, vp, C.c
 sqf_trainer_restore = _sig("sqf_trainer_restore", C.c_int, vp, i64, i32, i32, f64, i64)
 sqf_trainer_kernel_launches = _sig("sqf_trainer_kernel_launches", i64, vp)
 sqf_trainer_last_step_ms = _sig("sqf_trainer_last_step_ms", f32, vp)
+sqf_trainer_last_io_bytes = _sig("sqf_trainer_last_io_bytes", i64, vp, P(i64))
 sqf_trainer_stream = _sig("sqf_trainer_stream", vp, vp)
 sqf_trainer_set_profile = _sig("sqf_trainer_set_profile", C.c_int, vp, C.c_int)
 sqf_trainer_profile = _sig("sqf_trainer_profile", cp, vp, C.c_int, P(f64), P(f64), P(f64), P(i64))

@@ -258,6 +258,10 @@ int sqf_trainer_restore(void* t, int64_t step, int32_t epoch, int32_t cursor, do
 
 int64_t sqf_trainer_kernel_launches(void* t) { return T(t)->kernel_launches(); }
 float sqf_trainer_last_step_ms(void* t) { return T(t)->last_step_ms(); }
+int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h) {
+  *d2h = T(t)->last_d2h_bytes();
+  return T(t)->last_h2d_bytes();
+}
 void* sqf_trainer_stream(void* t) { return static_cast<void*>(T(t)->stream()); }
 
 int sqf_trainer_set_profile(void* t, int on) { SQF_GUARD(T(t)->set_profile(on != 0)) }

@@ -222,6 +222,7 @@ std::optional<StepStats> Trainer::train_one() {
 void Trainer::upload(const std::vector<PackedBatch>& packs, std::vector<DeviceBatch>& out) {
   size_t total = 0;
   for (const auto& p : packs) total += p.blob.size();
+  h2d_bytes_ = int64_t(total) * 4;
   if (total == 0) return;
   if (total > blob_host_cap_) {
     cudaFreeHost(blob_host_);

@@ -76,6 +76,9 @@ class Trainer {
   int world() const { return world_; }
   // timing hook: events recorded on the compute stream around the last step
   float last_step_ms() const { return last_ms_; }
+  // host<->device bytes of the last step (packed batch ids up; stats + flag down)
+  int64_t last_h2d_bytes() const { return h2d_bytes_; }
+  int64_t last_d2h_bytes() const { return 36; }
   // per-launch event profiling of subsequent steps (bench roofline evidence)
   void set_profile(bool on) {
     if (on && !prof_) prof_ = std::make_unique<Profiler>();
@@ -129,6 +132,7 @@ class Trainer {
   std::function<bool(int64_t)> injector_;
   int64_t launches_ = 0;
   float last_ms_ = 0.f;
+  int64_t h2d_bytes_ = 0;
   std::unique_ptr<Profiler> prof_;
 
   void init(const Registry& reg);
