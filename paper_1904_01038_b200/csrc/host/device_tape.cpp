@@ -394,6 +394,25 @@ void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void*
   launches_ += 1;
 }
 
+std::vector<std::pair<int64_t, int64_t>> DeviceTape::planned_grad_writes() const {
+  // mirrors backward_node: reverse recording order, same per-kind write order
+  std::vector<std::pair<int64_t, int64_t>> w;
+  auto put = [&](const ParamRef& p) { w.emplace_back(p.offset, int64_t(p.rows) * p.cols); };
+  for (int i = int(nodes_.size()) - 1; i >= 0; --i) {
+    const Node& n = nodes_[size_t(i)];
+    switch (n.kind) {
+      case Kind::Embedding: put(n.p0); break;
+      case Kind::LayerNorm: put(n.p0); put(n.p1); break;
+      case Kind::Linear:
+        if (n.has_bias) put(n.p1);
+        put(n.p0);
+        break;
+      default: break;
+    }
+  }
+  return w;
+}
+
 void DeviceTape::backward_node(int id) {
   Node& n = nodes_[id];
   if (!n.grad) return;  // no consumer contributed (e.g. unused branch)
@@ -408,6 +427,7 @@ void DeviceTape::backward_node(int id) {
                 "embed_bwd");
       pend(Profiler::Embed, 0, double(n.rows) * n.cols * esize_ + 2.0 * n.segs.n * n.cols * esize_);
       ++launches_;
+      grad_done(n.p0);
       return;
     }
     case Kind::LayerNorm: {
@@ -429,6 +449,8 @@ void DeviceTape::backward_node(int id) {
                                            gptr(n.p1), cur_),
                   "layernorm_bwd_params");
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
+        grad_done(n.p0);
+        grad_done(n.p1);
         if (side_) {
           cudaEvent_t done = event();
           cuda_check(cudaEventRecord(done, side_), "event record");
@@ -450,6 +472,8 @@ void DeviceTape::backward_node(int id) {
                 "layernorm_bwd");
       pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
       launches_ += 1;
+      grad_done(n.p0);
+      grad_done(n.p1);
       return;
     }
     case Kind::Linear: {
@@ -469,9 +493,13 @@ void DeviceTape::backward_node(int id) {
         cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
         cur_ = side_;
       }
-      if (n.has_bias) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
+      if (n.has_bias) {
+        bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
+        grad_done(n.p1);
+      }
       gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
            n.p0.cols, SFK_EPI_ACCUM);
+      grad_done(n.p0);
       if (side_) {
         cudaEvent_t done = event();
         cuda_check(cudaEventRecord(done, side_), "event record");

@@ -6,6 +6,8 @@
 // `accum`/update_freq delayed updates).
 #pragma once
 
+#include <functional>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -146,6 +148,15 @@ class DeviceTape {
   }
   // pool of zeroed int32 counters for single-launch deterministic reductions
   // (each user re-arms its slots to 0); handed out round-robin
+  // parameter-gradient completion hook, called right after the launch that
+  // writes a parameter range's gradient contribution is enqueued (on `stream`);
+  // the trainer uses it to start bucket all-reduces while backward continues
+  using GradHook = std::function<void(int64_t offset, int64_t numel, cudaStream_t stream)>;
+  void set_grad_hook(GradHook h) { hook_ = std::move(h); }
+  // every parameter-gradient write backward() makes, as (offset, numel), in the
+  // order the hook will report them
+  std::vector<std::pair<int64_t, int64_t>> planned_grad_writes() const;
+  cudaStream_t side_stream() const { return side_; }
   void set_counters(int32_t* base, int64_t n, int64_t* cursor) {
     ctr_base_ = base;
     ctr_n_ = n;
@@ -194,6 +205,10 @@ class DeviceTape {
     int32_t* p = ctr_base_ + *ctr_cursor_;
     *ctr_cursor_ += k;
     return p;
+  }
+  GradHook hook_;
+  void grad_done(const ParamRef& p) {
+    if (hook_) hook_(p.offset, int64_t(p.rows) * p.cols, cur_);
   }
   cudaStream_t cur_ = nullptr;  // stream the next launches go to (main or side)
   cudaStream_t side_ = nullptr;

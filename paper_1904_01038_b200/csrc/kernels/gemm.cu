@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(256) gemm_simt(const T* __restrict__ a, int64_
 
 // ------------------------------------------------------------------ tcgen05
 namespace tc {
-constexpr int BM = 128, BK = 64, kThreads = 192;
+constexpr int BM = 128, BK = 64;
+constexpr int kEpiWarps = 8, kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 8 epilogue warps
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -159,7 +160,10 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// tcgen05.ld issue and wait are separate so the next chunk's TMEM read
+// overlaps this chunk's global epilogue; the wait names the destination
+// registers as read-write so the compiler cannot consume them before it.
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -170,7 +174,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
         "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
 }
 
 template <typename T>
@@ -290,18 +303,23 @@ __device__ __forceinline__ void epilogue8(const Epi& e, int64_t row, int col, in
                                               Pack<T>::two(v[4], v[5]), Pack<T>::two(v[6], v[7]));
 }
 
-constexpr int kStg = 36;  // staging row stride (floats): conflict-free float4 writes and reads
+// Per-warp staging of a 32 x 32 fp32 block: row stride 32 floats, the eight
+// 16-byte chunks of row r stored at chunk index (j ^ (r & 7)) -- conflict-free
+// float4 writes (one row per lane) and reads (8 rows x 64 B per instruction).
+constexpr int kStgFloats = 32 * 32;
+__device__ __forceinline__ int stg_off(int row, int j) { return row * 32 + ((j ^ (row & 7)) << 2); }
 
 // Four row segments (rows row0 + 8i, i<4) x 8 columns, all loads of side
 // inputs issued before any math so their latencies overlap.
 template <typename T>
-__device__ __forceinline__ void epilogue_seg4(const Epi& e, int64_t row0, int col, int M, const float* stg) {
+__device__ __forceinline__ void epilogue_seg4(const Epi& e, int64_t row0, int col, int M, const float* stg, int rr0,
+                                              int j0) {
   const int fl = e.flags;
   float v[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float4 a = *reinterpret_cast<const float4*>(stg + 8 * i * kStg);
-    const float4 b = *reinterpret_cast<const float4*>(stg + 8 * i * kStg + 4);
+    const float4 a = *reinterpret_cast<const float4*>(stg + stg_off(rr0 + 8 * i, j0));
+    const float4 b = *reinterpret_cast<const float4*>(stg + stg_off(rr0 + 8 * i, j0 + 1));
     v[i][0] = a.x, v[i][1] = a.y, v[i][2] = a.z, v[i][3] = a.w, v[i][4] = b.x, v[i][5] = b.y, v[i][6] = b.z,
     v[i][7] = b.w;
   }
@@ -364,13 +382,57 @@ __device__ __forceinline__ void epilogue_seg4(const Epi& e, int64_t row0, int co
   }
 }
 
+// Drain one BM x BN accumulator tile from TMEM through the fused epilogue.
+// Eight epilogue warps: warp w may only touch TMEM lanes 32*(w%4)..+31, so two
+// warps share each lane quarter and take alternate 32-column chunks. The TMEM
+// read of a warp's next chunk is in flight while it runs the current chunk's
+// global loads/stores.
+template <int BN, typename T>
+__device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, int warp, int lane, float* stg, int64_t m0,
+                                              int n0, int M, int N, int vec_ok) {
+  const int quarter = warp & 3, half = (warp - 2) >> 2;
+  const uint32_t lane_base = tacc + (uint32_t(quarter * 32) << 16);
+  int nch = (N - n0 + 31) / 32;
+  if (nch > BN / 32) nch = BN / 32;
+  uint32_t r[32];
+  if (half < nch) tmem_ld32_issue(lane_base + half * 32, r);
+#pragma unroll 1
+  for (int ch = half; ch < nch; ch += 2) {
+    tmem_ld_wait(r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(stg + stg_off(lane, j)) =
+          make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                      __uint_as_float(r[4 * j + 3]));
+    if (ch + 2 < nch) tmem_ld32_issue(lane_base + (ch + 2) * 32, r);
+    __syncwarp();
+    const int cc = (lane & 3) * 8, col = n0 + ch * 32 + cc;
+    const int rr0 = lane >> 2;
+    const int64_t row0 = m0 + quarter * 32 + rr0;
+    if (vec_ok && col + 8 <= N) {
+      epilogue_seg4<T>(e, row0, col, M, stg, rr0, cc >> 2);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rr = rr0 + 8 * i;
+        const int64_t row = row0 + 8 * i;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = stg[stg_off(rr, (cc + j) >> 2) + ((cc + j) & 3)];
+        if (row < M && col < N) epilogue8<T>(e, row, col, N, v, false);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (192 * 1024) / STAGE;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/ + 4 * 32 * kStg * 4;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/ + kEpiWarps * kStgFloats * 4;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -395,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -476,45 +538,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // Epilogue: TMEM gives each thread one row x 32 columns; bounce the 32x32
-    // fp32 block through shared memory so a warp then reads/writes 8 rows x
+    // Epilogue: TMEM gives each thread one row x 32 columns; the 32x32 fp32
+    // block bounces through shared memory so a warp then reads/writes 8 rows x
     // 64 contiguous bytes per instruction (coalesced) instead of 32 rows.
-    const int quarter = warp & 3;
-    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * (32 * kStg);
+    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
     int t = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
-#pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + buf * BN + ch * 32, r);
-        if (n0 + ch * 32 >= N) continue;  // warp-uniform
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<float4*>(stg + lane * kStg + 4 * j) =
-              make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                          __uint_as_float(r[4 * j + 3]));
-        __syncwarp();
-        const int cc = (lane & 3) * 8, col = n0 + ch * 32 + cc;
-        const int64_t row0 = m0 + quarter * 32 + (lane >> 2);
-        if (vec_ok && col + 8 <= N) {
-          epilogue_seg4<T>(e, row0, col, M, stg + (lane >> 2) * kStg + cc);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rr = (lane >> 2) + 8 * i;
-            const int64_t row = row0 + 8 * i;
-            float v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = stg[rr * kStg + cc + j];
-            if (row < M && col < N) epilogue8<T>(e, row, col, N, v, false);
-          }
-        }
-        __syncwarp();
-      }
+      epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -541,7 +575,7 @@ struct Cfg2 {
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (192 * 1024) / STAGE > 8 ? 8 : (192 * 1024) / STAGE;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + 4 * 32 * kStg * 4;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256 + kEpiWarps * kStgFloats * 4;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -609,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[b], 2 * kEpiWarps);  // epilogue warps of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -689,42 +723,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
-    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * (32 * kStg);
+    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
     int t = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++t) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * PM + 128 * int(rank), n0 = (tile / num_m) * BN;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
-#pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (uint32_t(quarter * 32) << 16) + buf * BN + ch * 32, r);
-        if (n0 + ch * 32 >= N) continue;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<float4*>(stg + lane * kStg + 4 * j) =
-              make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
-                          __uint_as_float(r[4 * j + 3]));
-        __syncwarp();
-        const int cc = (lane & 3) * 8, col = n0 + ch * 32 + cc;
-        const int64_t row0 = m0 + quarter * 32 + (lane >> 2);
-        if (vec_ok && col + 8 <= N) {
-          epilogue_seg4<T>(e, row0, col, M, stg + (lane >> 2) * kStg + cc);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int rr = (lane >> 2) + 8 * i;
-            const int64_t row = row0 + 8 * i;
-            float v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = stg[rr * kStg + cc + j];
-            if (row < M && col < N) epilogue8<T>(e, row, col, N, v, false);
-          }
-        }
-        __syncwarp();
-      }
+      epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
       fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -852,16 +858,19 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   return check_launch("sfk_gemm(tcgen05 pair)");
 }
 
-// tile width by wave efficiency (tiles / (waves * SMs)); wider wins ties
+// tile width by wave efficiency (tiles / (waves * SMs)); wider wins ties.
+// 64-wide tiles are never picked: at 128 x 64 the operand traffic per MMA
+// (24 KB per 64-deep k-block for 128 MMA cycles) starves the tensor pipe on
+// L2 bandwidth, which costs more than any wave-quantisation loss.
 int pick_bn(int m, int n) {
   const int sms = num_sms_cached();
   int best = 256;
   double best_eff = -1;
-  for (int bn : {256, 128, 64}) {
+  for (int bn : {256, 128}) {
     const long tiles = long((m + BM - 1) / BM) * ((n + bn - 1) / bn);
     const long waves = (tiles + sms - 1) / sms;
     double eff = double(tiles) / double(waves * sms);
-    eff *= (bn == 256 ? 1.0 : bn == 128 ? 0.97 : 0.80);  // smem-bandwidth penalty of narrow tiles
+    eff *= (bn == 256 ? 1.0 : 0.85);  // operand-bandwidth penalty of 128-wide tiles
     if (eff > best_eff + 1e-9) {
       best_eff = eff;
       best = bn;

@@ -706,38 +706,45 @@ int ln_bwd_vec(int dtype, const void* x, const void* dy, int rows, int d, const 
 int colsum_partial_vec(int dtype, const void* x, int rows, int n, int64_t ld, float* part, int* nparts,
                        cudaStream_t s);
 
-// Fold of `nparts` column partials with 8 independent accumulators per thread
-// (the loads of a column no longer serialise behind one add chain); up to two
-// vectors (gamma and beta) per launch. Fixed association order: deterministic.
-// block = 8 partial-groups x 32 columns: thread (g, c) folds partials
-// g, g+8, ... with 4 independent chains, then group sums combine in order.
+// Fold of `nparts` column partials, up to two vectors (gamma and beta) per
+// launch. One block per 8-column slice (so n/8 blocks cover the machine):
+// thread (g, c) sums partials g, g+32, ... in two fixed chains, then the 32
+// group sums are added in group order. Fixed association order: deterministic.
 template <typename T>
 __global__ void __launch_bounds__(256) fold_k(const float* __restrict__ pa, const float* __restrict__ pb, int nparts,
                                              int n, T* __restrict__ oa, T* __restrict__ ob) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
-  __shared__ float red[8][33];
-  const int g = threadIdx.x / 32, cl = threadIdx.x % 32;
-  const int c = blockIdx.x * 32 + cl;
+  __shared__ float red[32][9];
+  const int g = threadIdx.x >> 3, cl = threadIdx.x & 7;
+  const int c = blockIdx.x * 8 + cl;
   const bool second = blockIdx.y == 1;
   const float* p = second ? pb : pa;
   T* o = second ? ob : oa;
-  float acc[4] = {0, 0, 0, 0};
+  float a0 = 0.f, a1 = 0.f;
   if (c < n) {
-    int q = g, u = 0;
-    for (; q + 24 < nparts; q += 32)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] += p[int64_t(q + 8 * j) * n + c];
-    for (; q < nparts; q += 8, ++u) acc[u & 3] += p[int64_t(q) * n + c];
+    int q = g;
+    for (; q + 32 < nparts; q += 64) {
+      a0 += __ldcg(p + int64_t(q) * n + c);
+      a1 += __ldcg(p + int64_t(q + 32) * n + c);
+    }
+    if (q < nparts) a0 += __ldcg(p + int64_t(q) * n + c);
   }
-  red[g][cl] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  red[g][cl] = a0 + a1;
   __syncthreads();
   if (g == 0 && c < n) {
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += red[k][cl];
+    for (int k = 0; k < 32; ++k) s += red[k][cl];
     Num<T>::st(o + c, Num<T>::ld(o + c) + s);
   }
+}
+
+// row chunks for a column reduction: about two blocks per SM in total
+static int fold_parts(int rows, int col_blocks) {
+  int nblk = std::max(1, (148 * 2) / std::max(1, col_blocks));
+  nblk = std::min(nblk, std::max(1, rows / 8));
+  return nblk;
 }
 
 int ln_bwd_fused_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats,
@@ -746,7 +753,7 @@ int ln_bwd_fused_vec(int dtype, const void* x, const void* dy, int rows, int d, 
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g)) return SFK_EUNSUP;
   int nparts = 0;
   if (int e = ln_bwd_vec(dtype, x, dy, rows, d, g, stats, dx, accumulate, part, &nparts, s)) return e;
-  dim3 grid((d + 31) / 32, 2);
+  dim3 grid((d + 7) / 8, 2);
   if (dtype == SFK_F16)
     launch_pdl(fold_k<__half>, grid, 256, 0, s, part, part + size_t(nparts) * d, nparts, d, static_cast<__half*>(dgamma),
                                         static_cast<__half*>(dbeta));
@@ -776,8 +783,7 @@ int ln_params_vec(int dtype, const void* x, const void* dy, int rows, int d, con
                   void* dgamma, void* dbeta, cudaStream_t s) {
   if (dtype == SFK_F32 || d % 8 || !al16(x) || !al16(dy)) return SFK_EUNSUP;
   const int col_blocks = (d / 8 + 127) / 128;
-  int nblk = std::max(1, std::min(256, (148 * 4) / col_blocks));
-  nblk = std::min(nblk, std::max(1, rows / 8));
+  const int nblk = fold_parts(rows, col_blocks);
   const int rpb = (rows + nblk - 1) / nblk;
   if (dtype == SFK_F16)
     launch_pdl(vec::ln_dgb_partial_v<__half>, dim3(col_blocks, nblk), dim3(128), 0, s, static_cast<const __half*>(x),
@@ -786,7 +792,7 @@ int ln_params_vec(int dtype, const void* x, const void* dy, int rows, int d, con
     launch_pdl(vec::ln_dgb_partial_v<__nv_bfloat16>, dim3(col_blocks, nblk), dim3(128), 0, s,
                static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), rows, d,
                reinterpret_cast<const float2*>(stats), rpb, part, nblk);
-  dim3 grid((d + 31) / 32, 2);
+  dim3 grid((d + 7) / 8, 2);
   if (dtype == SFK_F16)
     launch_pdl(fold_k<__half>, grid, 256, 0, s, part, part + size_t(nblk) * d, nblk, d, static_cast<__half*>(dgamma),
                static_cast<__half*>(dbeta));
@@ -801,7 +807,7 @@ int colsum_fused_vec(int dtype, const void* x, int rows, int n, int64_t ld, floa
   if (dtype == SFK_F32 || n % 8 || ld % 8 || !al16(x)) return SFK_EUNSUP;
   int nparts = 0;
   if (int e = colsum_partial_vec(dtype, x, rows, n, ld, part, &nparts, s)) return e;
-  dim3 grid((n + 31) / 32, 1);
+  dim3 grid((n + 7) / 8, 1);
   if (dtype == SFK_F16)
     launch_pdl(fold_k<__half>, grid, 256, 0, s, part, nullptr, nparts, n, static_cast<__half*>(out), nullptr);
   else
@@ -815,9 +821,8 @@ int colsum_partial_vec(int dtype, const void* x, int rows, int n, int64_t ld, fl
   // enough row chunks to fill the machine: ~4 blocks of 128 threads per SM
   // enough row chunks for ~4 blocks per SM; partial scratch capped at 4M floats
   const int col_blocks = (n / 8 + 127) / 128;
-  int nblk = std::max(1, std::min(512, (148 * 4) / std::max(1, col_blocks)));
+  int nblk = fold_parts(rows, col_blocks);
   nblk = std::min(nblk, std::max(1, (4 << 20) / std::max(1, n)));
-  nblk = std::min(nblk, std::max(1, rows / 8));
   const int rpb = (rows + nblk - 1) / nblk;
   *nparts = nblk;
   dim3 grid(col_blocks, nblk);
