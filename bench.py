@@ -226,7 +226,7 @@ def run_ours(args, cfg):
     corpus = sqf.synthetic_corpus(npairs, V, V, 1.1, 1)
     ov = {"max_tokens": cfg["max_tokens"], "accum": cfg["accum"], "workers": world, "dispatch": "deal",
           "fp16": cfg["prec"] == "fp16", "bf16": cfg["prec"] == "bf16", "seed": 1, "max_epochs": 1000,
-          "warmup": 4000, "lr": 5e-4, "bucket_threshold": 1 << 23,
+          "warmup": 4000, "lr": 5e-4, "bucket_threshold": 1 << 23, "overlap_allreduce": not args.no_overlap,
           # gradients are un-normalised token sums in fp16 until after the all-reduce
           # (trainer.cpp:264-265); at ~57k tokens per update the scale settles near 1
           "fp16_init_scale": 1.0, "fp16_min_scale": 2.0 ** -14}
@@ -289,7 +289,9 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["desc"], "arch": cfg["arch"], "max_tokens_per_gpu": cfg["max_tokens"],
                    "update_freq": cfg["accum"], "dispatch": "deal", "global_batch_tokens": tokens // args.steps,
                    "parallelism": f"dp{world}", "l2": "inputs > L2 (weights+grads+Adam state+activations, GBs)",
-                   "skipped_steps": skipped},
+                   "skipped_steps": skipped,
+                   "allreduce": ("bucketed NCCL, overlapped with the last backward" if not args.no_overlap
+                                 else "bucketed NCCL after backward") if world > 1 else "none (1 GPU)"},
         "e2e": {"value": e2e, "unit": "tgt_tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 36},
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (fwd/dgrad/wgrad, fused epilogues)",
@@ -324,6 +326,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-max-tokens", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="all-reduce after backward (C5 'overlap off')")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -127,8 +127,10 @@ int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, int rows, int
                          const void* gamma, const float* stats, void* dx, int accumulate,
                          void* stream);
 int sfk_layernorm_bwd_params(int dtype, const void* x, const void* dy, int rows, int d,
-                             const float* stats, float* part, void* dgamma, void* dbeta,
-                             void* stream);
+                             const float* stats, float* part, int32_t* counters, void* dgamma,
+                             void* dbeta, void* stream);
+/* (counters: >= ceil(d/256) zeroed int32 slots, re-armed to 0 by the kernel,
+ * selects the single-launch form; NULL falls back to partial + fold launches) */
 
 /* ------------------------------------------- column sums (bias grad, a11)
  * tape.cpp:347-358: db = q(db + sum_rows dy). Two deterministic passes:
@@ -139,7 +141,8 @@ int sfk_colsum_partial(int dtype, const void* x, int rows, int n, int64_t ld,
 int sfk_colsum_finish(int dtype, const float* part, int nparts, int n, void* out,
                       void* stream);
 /* Both passes in one call: out = q(out + sum_rows x). part: >= min(512*n, 4M)
- * floats scratch; counters: reserved (may be NULL). */
+ * floats scratch; counters: >= ceil(n/256) zeroed int32 slots (re-armed to 0 by
+ * the kernel) for the single-launch form, or NULL for partial + fold launches. */
 int sfk_colsum(int dtype, const void* x, int rows, int n, int64_t ld, float* part,
                int32_t* counters, void* out, void* stream);
 

@@ -81,6 +81,12 @@ float sqf_trainer_last_step_ms(void* t);
 int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h);
 /* CUDA stream the trainer launches on (cudaStream_t) */
 void* sqf_trainer_stream(void* t);
+/* all-reduce/backward overlap of the last step (config overlap_allreduce; with
+ * world 1 only under overlap_simulate): bucket indices in issue order (up to
+ * cap written), *early = how many were issued while backward was running.
+ * Returns the number of buckets issued. Replaces the single post-backward
+ * all_reduce of trainer.cpp:246 (all_reduce, trainer.cpp:75-87). */
+int sqf_trainer_overlap_log(void* t, int32_t* order, int cap, int32_t* early);
 /* per-launch CUDA-event profiling of the following steps (on = 1) and its
  * accumulated per-class totals: class 0..9 = gemm_fwd, gemm_dgrad,
  * gemm_wgrad, attn_fwd, attn_bwd, layernorm, xent, embed, bias_grad, optim.

@@ -303,6 +303,14 @@ class Trainer:
         h2d = L.sqf_trainer_last_io_bytes(self._h, C.byref(d2h))
         return int(h2d), int(d2h.value)
 
+    def overlap_log(self):
+        """(bucket issue order, number issued while backward was running) of the last step."""
+        cap = 1 << 16
+        buf = (C.c_int32 * cap)()
+        early = C.c_int32()
+        n = L.sqf_trainer_overlap_log(self._h, buf, cap, C.byref(early))
+        return list(buf[:n]), int(early.value)
+
     @property
     def stream(self) -> int:
         return int(L.sqf_trainer_stream(self._h) or 0)

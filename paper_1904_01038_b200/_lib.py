@@ -76,7 +76,7 @@ sfk_colsum = _sig("sfk_colsum", C.c_int, C.c_int, vp, C.c_int, C.c_int, i64, vp,
 sfk_layernorm_bwd_dx = _sig("sfk_layernorm_bwd_dx", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int,
                             vp)
 sfk_layernorm_bwd_params = _sig("sfk_layernorm_bwd_params", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp,
-                                vp, vp)
+                                vp, vp, vp)
 sfk_layernorm_bwd_fused = _sig("sfk_layernorm_bwd_fused", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp,
                                C.c_int, vp, vp, vp, vp, vp)
 sfk_attention_fwd = _sig("sfk_attention_fwd", C.c_int, P(AttnArgs), vp)
@@ -115,6 +115,7 @@ sqf_trainer_set_injector = _sig("sqf_trainer_set_injector", C.c_int, vp, vp, C.c
 sqf_trainer_restore = _sig("sqf_trainer_restore", C.c_int, vp, i64, i32, i32, f64, i64)
 sqf_trainer_kernel_launches = _sig("sqf_trainer_kernel_launches", i64, vp)
 sqf_trainer_last_step_ms = _sig("sqf_trainer_last_step_ms", f32, vp)
+sqf_trainer_overlap_log = _sig("sqf_trainer_overlap_log", C.c_int, vp, P(i32), C.c_int, P(i32))
 sqf_trainer_last_io_bytes = _sig("sqf_trainer_last_io_bytes", i64, vp, P(i64))
 sqf_trainer_stream = _sig("sqf_trainer_stream", vp, vp)
 sqf_trainer_set_profile = _sig("sqf_trainer_set_profile", C.c_int, vp, C.c_int)

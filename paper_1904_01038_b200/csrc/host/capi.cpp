@@ -264,6 +264,14 @@ int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h) {
 }
 void* sqf_trainer_stream(void* t) { return static_cast<void*>(T(t)->stream()); }
 
+int sqf_trainer_overlap_log(void* t, int32_t* order, int cap, int32_t* early) {
+  const std::vector<int>& log = T(t)->overlap_log();
+  const int n = int(log.size());
+  for (int i = 0; i < n && i < cap; ++i) order[i] = log[size_t(i)];
+  *early = T(t)->overlap_early();
+  return n;
+}
+
 int sqf_trainer_set_profile(void* t, int on) { SQF_GUARD(T(t)->set_profile(on != 0)) }
 
 const char* sqf_trainer_profile(void* t, int cls, double* ms, double* flops, double* bytes, int64_t* launches) {

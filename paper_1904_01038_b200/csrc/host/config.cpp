@@ -264,6 +264,8 @@ Config engine_default_config() {
       {"synthetic_pairs", int64_t{0}},         // task "synthetic": corpus size
       {"zipf_s", 1.1},                         // task "synthetic": token-id skew
       {"rank", int64_t{0}},                    // data-parallel rank of this process
+      {"overlap_allreduce", true},             // start bucket all-reduces during the last backward
+      {"overlap_simulate", false},             // testing: run the overlap schedule without NCCL (world 1)
   };
   for (const auto& kv : keys) c.declare(kv.first, kv.second);
   return c;

@@ -389,7 +389,7 @@ void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void*
   const size_t part_floats = std::min<size_t>(size_t(512) * cols, size_t(4) << 20);
   float* part = static_cast<float*>(arena_.alloc(part_floats * 4));
   pbegin();
-  sfk_check(sfk_colsum(dtype_, dy, rows, cols, ld, part, counters((cols + 1023) / 1024), out, cur_), "colsum");
+  sfk_check(sfk_colsum(dtype_, dy, rows, cols, ld, part, counters((cols + 255) / 256), out, cur_), "colsum");
   pend(Profiler::BiasGrad, 0, double(rows) * cols * esize_);
   launches_ += 1;
 }
@@ -445,8 +445,8 @@ void DeviceTape::backward_node(int id) {
           cur_ = side_;
         }
         pbegin();
-        sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part, gptr(n.p0),
-                                           gptr(n.p1), cur_),
+        sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
+                                           counters((n.cols + 255) / 256), gptr(n.p0), gptr(n.p1), cur_),
                   "layernorm_bwd_params");
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
         grad_done(n.p0);

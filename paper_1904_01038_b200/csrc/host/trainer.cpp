@@ -47,6 +47,8 @@ Trainer::~Trainer() {
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
   if (side_) cudaStreamDestroy(side_);
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  for (cudaEvent_t e : ovl_events_) cudaEventDestroy(e);
   for (cudaEvent_t e : evpool_) cudaEventDestroy(e);
 }
 
@@ -85,6 +87,10 @@ void Trainer::init(const Registry& reg) {
   std::vector<int64_t> sizes;
   for (auto& p : dev) sizes.push_back(p.second);
   buckets_ = bucket_gradients(sizes, cfg_.get_int("bucket_threshold"));
+  for (size_t b = 0; b < buckets_.size(); ++b) bucket_index_.emplace_back(buckets_[b].start, int(b));
+  std::sort(bucket_index_.begin(), bucket_index_.end());
+  overlap_ = cfg_.get_bool("overlap_allreduce");
+  overlap_sim_ = cfg_.get_bool("overlap_simulate");
 
   const int64_t ms = cfg_.get_int("max_sentences");
   // deal dispatch packs at the per-replica budget; split packs one global batch
@@ -98,6 +104,7 @@ void Trainer::init(const Registry& reg) {
   n_ = model_->num_params();
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+  cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
   cuda_check(cudaEventCreate(&ev0_), "event");
   cuda_check(cudaEventCreate(&ev1_), "event");
   cuda_check(cudaMalloc(&master_, size_t(n_) * 4), "master");
@@ -260,6 +267,79 @@ void Trainer::allreduce_grads() {
   nccl_check(NcclApi::get().GroupEnd(), "group");
 }
 
+// ---------------------------------------------------------------- overlap
+// The reference all-reduces after every replica finished backward
+// (trainer.cpp:75-87, 246). Here the buckets (reverse device order, the order
+// backward completes them) are all-reduced on a comm stream while the last
+// sub-batch's backward is still running: the tape reports every parameter-
+// gradient write, a bucket is issued once all of its planned writes are
+// enqueued, always in bucket order so every rank issues the identical NCCL
+// sequence. The comm stream waits on events of both compute streams taken at
+// issue time, which covers every earlier write to that bucket.
+cudaEvent_t Trainer::ovl_event() {
+  if (ovl_next_event_ == ovl_events_.size()) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+    ovl_events_.push_back(e);
+  }
+  return ovl_events_[ovl_next_event_++];
+}
+
+int Trainer::bucket_of(int64_t offset) const {
+  auto it = std::upper_bound(bucket_index_.begin(), bucket_index_.end(), std::make_pair(offset, INT32_MAX));
+  if (it == bucket_index_.begin()) throw BoundsError("overlap: offset below the first bucket");
+  --it;
+  return it->second;
+}
+
+void Trainer::ovl_begin(const DeviceTape& tape) {
+  ovl_remaining_.assign(buckets_.size(), 0);
+  for (const auto& w : tape.planned_grad_writes()) ++ovl_remaining_[size_t(bucket_of(w.first))];
+  ovl_next_ = 0;
+  ovl_next_event_ = 0;
+  overlap_log_.clear();
+  overlap_early_ = 0;
+  while (ovl_next_ < int(buckets_.size()) && ovl_remaining_[size_t(ovl_next_)] == 0) ovl_issue(ovl_next_++);
+}
+
+void Trainer::ovl_on_write(int64_t offset) {
+  const int b = bucket_of(offset);
+  if (--ovl_remaining_[size_t(b)] < 0) throw DeviceError("overlap: more gradient writes than planned");
+  while (ovl_next_ < int(buckets_.size()) && ovl_remaining_[size_t(ovl_next_)] == 0) {
+    ovl_issue(ovl_next_++);
+    ++overlap_early_;
+  }
+}
+
+void Trainer::ovl_issue(int b) {
+  cudaEvent_t em = ovl_event(), es = ovl_event();
+  cuda_check(cudaEventRecord(em, stream_), "event record");
+  cuda_check(cudaEventRecord(es, side_), "event record");
+  cuda_check(cudaStreamWaitEvent(comm_stream_, em, 0), "stream wait");
+  cuda_check(cudaStreamWaitEvent(comm_stream_, es, 0), "stream wait");
+  const GradientBucket& bk = buckets_[size_t(b)];
+  if (world_ > 1)
+    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grads_[0]) + bk.start * esize(),
+                                        static_cast<char*>(grads_[0]) + bk.start * esize(), size_t(bk.end - bk.start),
+                                        nccl_type(dtype_), ncclSum, comm_, comm_stream_),
+               "allreduce bucket");
+  overlap_log_.push_back(b);
+}
+
+void Trainer::ovl_finish() {
+  // anything the plan did not see completed (a node without a gradient)
+  while (ovl_next_ < int(buckets_.size())) ovl_issue(ovl_next_++);
+  cudaEvent_t em = ovl_event();
+  cuda_check(cudaEventRecord(em, stream_), "event record");
+  cuda_check(cudaStreamWaitEvent(comm_stream_, em, 0), "stream wait");
+  if (world_ > 1)
+    nccl_check(NcclApi::get().AllReduce(stats_dev_, stats_dev_, 4, ncclFloat64, ncclSum, comm_, comm_stream_),
+               "allreduce stats");
+  cudaEvent_t done = ovl_event();
+  cuda_check(cudaEventRecord(done, comm_stream_), "event record");
+  cuda_check(cudaStreamWaitEvent(stream_, done, 0), "stream wait");
+}
+
 StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
   if (int(sub.size()) != workers_) throw ShapeError("train_step: need one sub-batch list per replica");
   for (const auto& l : sub)
@@ -292,6 +372,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
   for (int lw = 0; lw < local_; ++lw)
     cuda_check(cudaMemsetAsync(grads_[size_t(lw)], 0, size_t(n_) * esize(), stream_), "grad zero");
   launches_ = 0;
+  const bool overlap = overlap_ && local_ == 1 && (world_ > 1 || overlap_sim_) && !dev.empty();
   for (size_t i = 0; i < dev.size(); ++i) {
     const int lw = which[i].first, a = which[i].second;
     const int w = rank_ * local_ + lw;
@@ -302,6 +383,10 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     tape.set_side_stream(side_, &evpool_);
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
+    if (overlap && i + 1 == dev.size()) {
+      ovl_begin(tape);
+      tape.set_grad_hook([this](int64_t off, int64_t, cudaStream_t) { ovl_on_write(off); });
+    }
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
     tape.backward(out.loss_node, float(scale), stats_dev_);
     launches_ += tape.launches();
@@ -311,7 +396,10 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     sfk_check(sfk_accumulate(dtype_, grads_[0], grads_[size_t(lw)], n_, stream_), "replica fold");
     ++launches_;
   }
-  allreduce_grads();
+  if (overlap)
+    ovl_finish();
+  else
+    allreduce_grads();
   if (prof_) prof_->begin(stream_);
   sfk_check(sfk_nonfinite(dtype_, grads_[0], n_, flag_dev_, stream_), "overflow check");
   ++launches_;

@@ -85,6 +85,10 @@ class Trainer {
     if (!on) prof_.reset();
   }
   Profiler* profiler() { return prof_.get(); }
+  // all-reduce/backward overlap of the last step: bucket indices in issue
+  // order, and how many were issued while backward was still running
+  const std::vector<int>& overlap_log() const { return overlap_log_; }
+  int overlap_early() const { return overlap_early_; }
 
  private:
   Config cfg_;
@@ -140,6 +144,23 @@ class Trainer {
   size_t esize() const { return dtype_ == SFK_F32 ? 4 : 2; }
   void upload(const std::vector<PackedBatch>& packs, std::vector<DeviceBatch>& out);
   void allreduce_grads();
+
+  // ---- bucketed all-reduce overlapped with the last sub-batch's backward
+  bool overlap_ = true, overlap_sim_ = false;
+  cudaStream_t comm_stream_ = nullptr;
+  std::vector<cudaEvent_t> ovl_events_;
+  size_t ovl_next_event_ = 0;
+  std::vector<int> ovl_remaining_;   // outstanding gradient writes per bucket
+  int ovl_next_ = 0;                 // next bucket to issue (issue order = bucket order)
+  std::vector<int> overlap_log_;
+  int overlap_early_ = 0;
+  std::vector<std::pair<int64_t, int>> bucket_index_;  // (start, bucket) sorted by start
+  cudaEvent_t ovl_event();
+  int bucket_of(int64_t offset) const;
+  void ovl_begin(const DeviceTape& tape);
+  void ovl_on_write(int64_t offset);
+  void ovl_issue(int b);
+  void ovl_finish();
 };
 
 }  // namespace sqf

@@ -486,6 +486,224 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
   }
 }
 
+// ------------------------------------------------------------------ backward, one CTA
+// Short sentences (query and key widths <= 64, the common case for the
+// length-bucketed batches): one CTA per (sentence, head) stages Q, dO, K, V
+// once and runs both halves of the backward -- dQ per query warp, then dK/dV
+// per key warp -- with D = rowsum(dO * O) and the saved softmax stats kept in
+// shared memory. Same arithmetic, in the same order, as bwd_dq_k + bwd_dkv_k.
+template <typename T, int DH>
+__global__ void __launch_bounds__(kWarps * 32) bwd_small_k(Args a) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int LD = DH + 8;
+  constexpr int QP = 2 * kRows;  // staged query rows (zero-padded: dK/dV chunks run past qw)
+  constexpr int NC = DH >= 128 ? 32 : 64;
+  const int b = blockIdx.z, h = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
+  const int len = a.causal ? a.kw : a.klen[b];
+  const int nk = a.causal ? min(a.kw, a.qw) : len;
+  T* Qs = reinterpret_cast<T*>(smem);
+  T* Gs = Qs + QP * LD;
+  T* Ks = Gs + QP * LD;
+  T* Vs = Ks + kRows * LD;
+  float2* St = reinterpret_cast<float2*>(Vs + kRows * LD);
+  float* Ds = reinterpret_cast<float*>(St + QP);
+  const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
+  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0), a.qw, QP, a.dh);
+  stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0), a.qw, QP, a.dh);
+  // dQ reads keys < nk; dK/dV rows are all kw key rows (rows >= nk get zero grads)
+  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), a.kw, kRows, a.dh);
+  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), a.kw, kRows, a.dh);
+  for (int i = threadIdx.x; i < QP; i += blockDim.x) {
+    St[i] = i < a.qw ? a.stats[(qrow0 + i) * a.heads + h] : make_float2(0.f, 0.f);
+    Ds[i] = 0.f;
+  }
+  stage_wait();
+  __syncthreads();
+  const int r0 = warp * 16;
+  const float l2e = 1.4426950408889634f;
+  // ---- phase 1: D and dQ for query rows r0..r0+15
+  if (r0 < a.qw) {
+    const int row_a = r0 + g, row_b = row_a + 8;
+    float D_a = 0.f, D_b = 0.f;
+    const T* O = static_cast<const T*>(a.o) + h * a.dh;
+    for (int c = tq; c < a.dh; c += 4) {
+      if (row_a < a.qw) D_a += Num<T>::ld(Gs + row_a * LD + c) * Num<T>::ld(O + (qrow0 + row_a) * a.ldo + c);
+      if (row_b < a.qw) D_b += Num<T>::ld(Gs + row_b * LD + c) * Num<T>::ld(O + (qrow0 + row_b) * a.ldo + c);
+    }
+    D_a += __shfl_xor_sync(0xffffffffu, D_a, 1);
+    D_a += __shfl_xor_sync(0xffffffffu, D_a, 2);
+    D_b += __shfl_xor_sync(0xffffffffu, D_b, 1);
+    D_b += __shfl_xor_sync(0xffffffffu, D_b, 2);
+    if (tq == 0) {
+      if (row_a < a.qw) Ds[row_a] = D_a;
+      if (row_b < a.qw) Ds[row_b] = D_b;
+    }
+    uint32_t qa[DH / 16][4], ga[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      load_a<T>(qa[ks], Qs, LD, r0, ks * 16, lane);
+      load_a<T>(ga[ks], Gs, LD, r0, ks * 16, lane);
+    }
+    const float2 st_a = St[row_a], st_b = St[row_b];
+    const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 0;
+    const int lim_b = row_b < a.qw ? (a.causal ? row_b + 1 : len) : 0;
+    float dq[DH / 8][4];
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+    {
+      constexpr int kc = 0;  // all keys fit one 64-key chunk
+      float s[8][4], dp[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 8; nt += 2) {
+          uint32_t bk[4], bv[4];
+          load_b_nk<T>(bk, Ks, LD, kc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bv, Vs, LD, kc + nt * 8, ks * 16, lane);
+          MmaT<T>::mma(s[nt], qa[ks], bk[0], bk[1]);
+          MmaT<T>::mma(s[nt + 1], qa[ks], bk[2], bk[3]);
+          MmaT<T>::mma(dp[nt], ga[ks], bv[0], bv[1]);
+          MmaT<T>::mma(dp[nt + 1], ga[ks], bv[2], bv[3]);
+        }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = kc + nt * 8 + 2 * tq + e;
+          const float pa = j < lim_a ? exp2f((s[nt][e] * a.sc - st_a.x) * l2e) * st_a.y : 0.f;
+          const float pb = j < lim_b ? exp2f((s[nt][2 + e] * a.sc - st_b.x) * l2e) * st_b.y : 0.f;
+          s[nt][e] = pa * (dp[nt][e] - D_a);
+          s[nt][2 + e] = pb * (dp[nt][2 + e] - D_b);
+        }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint32_t da[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
+                          MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                          MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+        for (int nt = 0; nt < DH / 8; nt += 2) {
+          uint32_t bb[4];
+          load_b_kn<T>(bb, Ks, LD, kc + kk * 16, nt * 8, lane);
+          MmaT<T>::mma(dq[nt], da, bb[0], bb[1]);
+          MmaT<T>::mma(dq[nt + 1], da, bb[2], bb[3]);
+        }
+      }
+    }
+    T* out = static_cast<T*>(a.dq) + h * a.dh;
+#pragma unroll
+    for (int nt = 0; nt < DH / 8; ++nt) {
+      const int c = nt * 8 + 2 * tq;
+      if (c >= a.dh) continue;
+      if (row_a < a.qw)
+        *reinterpret_cast<uint32_t*>(out + (qrow0 + row_a) * a.lddq + c) =
+            MmaT<T>::pack(dq[nt][0] * a.sc, dq[nt][1] * a.sc);
+      if (row_b < a.qw)
+        *reinterpret_cast<uint32_t*>(out + (qrow0 + row_b) * a.lddq + c) =
+            MmaT<T>::pack(dq[nt][2] * a.sc, dq[nt][3] * a.sc);
+    }
+  }
+  __syncthreads();  // Ds complete
+  // ---- phase 2: dK, dV for key rows r0..r0+15
+  if (r0 >= a.kw) return;
+  const int nq = a.qw;
+  const int key_a = r0 + g, key_b = key_a + 8;
+  float dk[DH / 8][4], dv[DH / 8][4];
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.f;
+  const bool any = a.causal ? true : (r0 < len);
+  if (any) {
+    uint32_t ka[DH / 16][4], va[DH / 16][4];
+#pragma unroll
+    for (int ks = 0; ks < DH / 16; ++ks) {
+      load_a<T>(ka[ks], Ks, LD, r0, ks * 16, lane);
+      load_a<T>(va[ks], Vs, LD, r0, ks * 16, lane);
+    }
+    const int qbeg = a.causal ? (r0 & ~15) : 0;
+    for (int qc = qbeg; qc < nq; qc += NC) {
+      float s[NC / 8][4], dp[NC / 8][4];
+#pragma unroll
+      for (int i = 0; i < NC / 8; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < NC / 8; nt += 2) {
+          uint32_t bq[4], bg[4];
+          load_b_nk<T>(bq, Qs, LD, qc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bg, Gs, LD, qc + nt * 8, ks * 16, lane);
+          MmaT<T>::mma(s[nt], ka[ks], bq[0], bq[1]);
+          MmaT<T>::mma(s[nt + 1], ka[ks], bq[2], bq[3]);
+          MmaT<T>::mma(dp[nt], va[ks], bg[0], bg[1]);
+          MmaT<T>::mma(dp[nt + 1], va[ks], bg[2], bg[3]);
+        }
+      float p[NC / 8][4];
+#pragma unroll
+      for (int nt = 0; nt < NC / 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int t = qc + nt * 8 + 2 * tq + e;
+          const float2 st = St[t];
+          const float D = Ds[t];
+          const bool qok = t < nq;
+          const bool va_ok = qok && key_a < a.kw && (a.causal ? key_a <= t : key_a < len);
+          const bool vb_ok = qok && key_b < a.kw && (a.causal ? key_b <= t : key_b < len);
+          const float pa = va_ok ? exp2f((s[nt][e] * a.sc - st.x) * l2e) * st.y : 0.f;
+          const float pb = vb_ok ? exp2f((s[nt][2 + e] * a.sc - st.x) * l2e) * st.y : 0.f;
+          p[nt][e] = pa;
+          p[nt][2 + e] = pb;
+          s[nt][e] = pa * (dp[nt][e] - D);
+          s[nt][2 + e] = pb * (dp[nt][2 + e] - D);
+        }
+#pragma unroll
+      for (int kk = 0; kk < NC / 16; ++kk) {
+        uint32_t pa[4] = {MmaT<T>::pack(p[2 * kk][0], p[2 * kk][1]), MmaT<T>::pack(p[2 * kk][2], p[2 * kk][3]),
+                          MmaT<T>::pack(p[2 * kk + 1][0], p[2 * kk + 1][1]),
+                          MmaT<T>::pack(p[2 * kk + 1][2], p[2 * kk + 1][3])};
+        uint32_t da[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
+                          MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                          MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+#pragma unroll
+        for (int nt = 0; nt < DH / 8; nt += 2) {
+          uint32_t bg[4], bq[4];
+          load_b_kn<T>(bg, Gs, LD, qc + kk * 16, nt * 8, lane);
+          load_b_kn<T>(bq, Qs, LD, qc + kk * 16, nt * 8, lane);
+          MmaT<T>::mma(dv[nt], pa, bg[0], bg[1]);
+          MmaT<T>::mma(dv[nt + 1], pa, bg[2], bg[3]);
+          MmaT<T>::mma(dk[nt], da, bq[0], bq[1]);
+          MmaT<T>::mma(dk[nt + 1], da, bq[2], bq[3]);
+        }
+      }
+    }
+  }
+  T* dko = static_cast<T*>(a.dk) + h * a.dh;
+  T* dvo = static_cast<T*>(a.dv) + h * a.dh;
+#pragma unroll
+  for (int nt = 0; nt < DH / 8; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (c >= a.dh) continue;
+    if (key_a < a.kw) {
+      *reinterpret_cast<uint32_t*>(dko + (krow0 + key_a) * a.lddk + c) =
+          MmaT<T>::pack(dk[nt][0] * a.sc, dk[nt][1] * a.sc);
+      *reinterpret_cast<uint32_t*>(dvo + (krow0 + key_a) * a.lddv + c) = MmaT<T>::pack(dv[nt][0], dv[nt][1]);
+    }
+    if (key_b < a.kw) {
+      *reinterpret_cast<uint32_t*>(dko + (krow0 + key_b) * a.lddk + c) =
+          MmaT<T>::pack(dk[nt][2] * a.sc, dk[nt][3] * a.sc);
+      *reinterpret_cast<uint32_t*>(dvo + (krow0 + key_b) * a.lddv + c) = MmaT<T>::pack(dv[nt][2], dv[nt][3]);
+    }
+  }
+}
+
 template <typename T, int DH>
 int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   Args a{};
@@ -524,6 +742,7 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     cudaFuncSetAttribute(fwd_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dq_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   const dim3 gq((a.qw + kRows - 1) / kRows, a.heads, a.batch);
@@ -531,6 +750,11 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     const size_t smem = size_t(kRows + 2 * kpad) * LD * sizeof(T);
     launch_pdl(fwd_k<T, DH>, gq, kWarps * 32, smem, st, a);
     return check_launch("sfk_attention_fwd(mma)");
+  }
+  if (a.qw <= kRows && a.kw <= kRows) {
+    const size_t smem_s = size_t(4 * kRows + 2 * kRows) * LD * sizeof(T) + size_t(2 * kRows) * 12;
+    launch_pdl(bwd_small_k<T, DH>, dim3(1, a.heads, a.batch), kWarps * 32, smem_s, st, a);
+    return check_launch("sfk_attention_bwd(small)");
   }
   const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
   launch_pdl(bwd_dq_k<T, DH>, gq, kWarps * 32, smem_q, st, a);

@@ -352,6 +352,8 @@ int colsum_partial_vec(int, const void*, int, int, int64_t, float*, int*, cudaSt
 int ln_bwd_fused_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*,
                      int32_t*, void*, void*, cudaStream_t);
 int colsum_fused_vec(int, const void*, int, int, int64_t, float*, int32_t*, void*, cudaStream_t);
+int colred_launch(int, bool, const void*, const void*, const float*, int, int, int64_t, float*, int32_t*, void*, void*,
+                  cudaStream_t);
 int xent_vec(int, void*, int, int, int64_t, const int32_t*, int, float, float, void*, float*, cudaStream_t);
 int ln_dx_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, cudaStream_t);
 int ln_params_vec(int, const void*, const void*, int, int, const float*, float*, void*, void*, cudaStream_t);
@@ -366,8 +368,12 @@ extern "C" int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, in
 }
 
 extern "C" int sfk_layernorm_bwd_params(int dtype, const void* x, const void* dy, int rows, int d, const float* stats,
-                                        float* part, void* dgamma, void* dbeta, void* stream) {
+                                        float* part, int32_t* counters, void* dgamma, void* dbeta, void* stream) {
   if (rows == 0) return SFK_OK;
+  if (int e = sfk::colred_launch(dtype, true, dy, x, stats, rows, d, d, part, counters, dgamma, dbeta,
+                                 sfk::as_stream(stream));
+      e != SFK_EUNSUP)
+    return e;
   const int e = sfk::ln_params_vec(dtype, x, dy, rows, d, stats, part, dgamma, dbeta, sfk::as_stream(stream));
   if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_params: needs 16-bit data, d % 8 == 0, aligned rows");
   return e;
@@ -391,6 +397,10 @@ extern "C" int sfk_layernorm_bwd_fused(int dtype, const void* x, const void* dy,
 extern "C" int sfk_colsum(int dtype, const void* x, int rows, int n, int64_t ld, float* part, int32_t* counters,
                           void* out, void* stream) {
   if (rows == 0 || n == 0) return SFK_OK;
+  if (int e = sfk::colred_launch(dtype, false, x, nullptr, nullptr, rows, n, ld, part, counters, out, nullptr,
+                                 sfk::as_stream(stream));
+      e != SFK_EUNSUP)
+    return e;
   if (int e = sfk::colsum_fused_vec(dtype, x, rows, n, ld, part, counters, out, sfk::as_stream(stream));
       e != SFK_EUNSUP)
     return e;

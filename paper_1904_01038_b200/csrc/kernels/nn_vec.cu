@@ -469,8 +469,8 @@ __global__ void __launch_bounds__(128) ln_dgb_partial_v(const T* __restrict__ x,
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       float xh[8], gy[8];
-      V8<T>::unpack(xu[j], xh);
-      V8<T>::unpack(gu[j], gy);
+      vec::V8<T>::unpack(xu[j], xh);
+      vec::V8<T>::unpack(gu[j], gy);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         pg[e] += gy[e] * __fmul_rn(__fsub_rn(xh[e], st[j].x), st[j].y);
@@ -738,6 +738,158 @@ __global__ void __launch_bounds__(256) fold_k(const float* __restrict__ pa, cons
     for (int k = 0; k < 32; ++k) s += red[k][cl];
     Num<T>::st(o + c, Num<T>::ld(o + c) + s);
   }
+}
+
+// Single-launch column reductions (bias gradient, LayerNorm gamma/beta).
+// One block = 8 warps over a 256-column slice and a chunk of rows: warp w sums
+// rows w, w+8, ... (four 512-byte warp loads in flight), the 8 warp sums are
+// combined in warp order through shared memory into one fp32 partial per
+// block, and the last block of each column slice (arrival counter) folds the
+// partials in block order into out = q(out + sum) and re-arms the counter.
+// Every association is fixed, so the result is deterministic.
+// LN: vector 0 = sum dy * xhat (dgamma), vector 1 = sum dy (dbeta).
+template <typename T, bool LN>
+__global__ void __launch_bounds__(256) colred_k(const T* __restrict__ dy, const T* __restrict__ x,
+                                               const float2* __restrict__ stats, int rows, int n, int64_t ld, int rpb,
+                                               float* __restrict__ part, int nblk, int32_t* __restrict__ counters,
+                                               T* __restrict__ out0, T* __restrict__ out1) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  constexpr int NV = LN ? 2 : 1;
+  constexpr int U = LN ? 4 : 8;  // rows in flight per warp
+  __shared__ __align__(16) float red[NV][8][256];
+  __shared__ int last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cb0 = blockIdx.x * 256, c = cb0 + lane * 8;
+  const bool cok = c < n;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  float sb[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sg[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (cok) {
+    for (int r = r0 + warp; r < r1; r += 8 * U) {
+      uint4 gu[U], xu[U];
+      float2 st[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int rr = r + 8 * j;
+        if (rr < r1) {
+          gu[j] = *reinterpret_cast<const uint4*>(dy + int64_t(rr) * ld + c);
+          if (LN) {
+            xu[j] = *reinterpret_cast<const uint4*>(x + int64_t(rr) * ld + c);
+            st[j] = stats[rr];
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        if (r + 8 * j >= r1) break;
+        float gy[8];
+        vec::V8<T>::unpack(gu[j], gy);
+        if (LN) {
+          float xh[8];
+          vec::V8<T>::unpack(xu[j], xh);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sg[e] += gy[e] * __fmul_rn(__fsub_rn(xh[e], st[j].x), st[j].y);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sb[e] += gy[e];
+      }
+    }
+  }
+  {
+    float* d0 = &red[0][warp][lane * 8];
+    *reinterpret_cast<float4*>(d0) = LN ? make_float4(sg[0], sg[1], sg[2], sg[3]) : make_float4(sb[0], sb[1], sb[2], sb[3]);
+    *reinterpret_cast<float4*>(d0 + 4) =
+        LN ? make_float4(sg[4], sg[5], sg[6], sg[7]) : make_float4(sb[4], sb[5], sb[6], sb[7]);
+    if (LN) {
+      float* d1 = &red[NV - 1][warp][lane * 8];
+      *reinterpret_cast<float4*>(d1) = make_float4(sb[0], sb[1], sb[2], sb[3]);
+      *reinterpret_cast<float4*>(d1 + 4) = make_float4(sb[4], sb[5], sb[6], sb[7]);
+    }
+  }
+  __syncthreads();
+  const int col = cb0 + threadIdx.x;
+  if (col < n) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[v][w][threadIdx.x];
+      part[(int64_t(v) * nblk + blockIdx.y) * n + col] = t;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counters + blockIdx.x, 1) == nblk - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // fold: warp w sums partials p = w, w+8, ... for 8 columns per lane (all
+  // loads of a thread in flight together), then the 8 warp sums combine in
+  // warp order -- a fixed association
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cok) {
+      const float* pv = part + int64_t(v) * nblk * n + c;
+      for (int p = warp; p < nblk; p += 64) {
+        float4 q[8][2];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (p + 8 * j < nblk) {
+            q[j][0] = __ldcg(reinterpret_cast<const float4*>(pv + int64_t(p + 8 * j) * n));
+            q[j][1] = __ldcg(reinterpret_cast<const float4*>(pv + int64_t(p + 8 * j) * n + 4));
+          }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (p + 8 * j < nblk) {
+            f[0] += q[j][0].x, f[1] += q[j][0].y, f[2] += q[j][0].z, f[3] += q[j][0].w;
+            f[4] += q[j][1].x, f[5] += q[j][1].y, f[6] += q[j][1].z, f[7] += q[j][1].w;
+          }
+      }
+    }
+    __syncthreads();
+    float* d = &red[0][warp][lane * 8];
+    *reinterpret_cast<float4*>(d) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(d + 4) = make_float4(f[4], f[5], f[6], f[7]);
+    __syncthreads();
+    if (col < n) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[0][w][threadIdx.x];
+      T* o = v == 0 ? out0 : out1;
+      Num<T>::st(o + col, Num<T>::ld(o + col) + t);
+    }
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0;
+}
+
+// rows per block of colred_k: about two blocks per SM in total
+static void colred_grid(int rows, int n, int& col_blocks, int& nblk, int& rpb) {
+  col_blocks = (n + 255) / 256;
+  nblk = std::max(1, (2 * 148) / col_blocks);
+  nblk = std::min(nblk, std::max(1, rows / 16));
+  rpb = (rows + nblk - 1) / nblk;
+  nblk = (rows + rpb - 1) / rpb;
+}
+
+int colred_launch(int dtype, bool ln, const void* dy, const void* x, const float* stats, int rows, int n, int64_t ld,
+                  float* part, int32_t* counters, void* out0, void* out1, cudaStream_t s) {
+  if (dtype == SFK_F32 || n % 8 || ld % 8 || !al16(dy) || (ln && !al16(x)) || !counters) return SFK_EUNSUP;
+  int cbk, nblk, rpb;
+  colred_grid(rows, n, cbk, nblk, rpb);
+  const dim3 grid(cbk, nblk);
+  auto st = reinterpret_cast<const float2*>(stats);
+  if (dtype == SFK_F16) {
+    auto k = ln ? colred_k<__half, true> : colred_k<__half, false>;
+    launch_pdl(k, grid, dim3(256), 0, s, static_cast<const __half*>(dy), static_cast<const __half*>(x), st, rows, n, ld,
+               rpb, part, nblk, counters, static_cast<__half*>(out0), static_cast<__half*>(out1));
+  } else {
+    auto k = ln ? colred_k<__nv_bfloat16, true> : colred_k<__nv_bfloat16, false>;
+    launch_pdl(k, grid, dim3(256), 0, s, static_cast<const __nv_bfloat16*>(dy), static_cast<const __nv_bfloat16*>(x),
+               st, rows, n, ld, rpb, part, nblk, counters, static_cast<__nv_bfloat16*>(out0),
+               static_cast<__nv_bfloat16*>(out1));
+  }
+  return check_launch(ln ? "sfk_layernorm_bwd_params(colred)" : "sfk_colsum(colred)");
 }
 
 // row chunks for a column reduction: about two blocks per SM in total

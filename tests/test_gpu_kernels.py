@@ -206,7 +206,10 @@ def _spans(batch, qw, kw, lens, causal):
 @pytest.mark.parametrize("fp16", [False, True])
 @pytest.mark.parametrize("batch,qw,kw,heads,dh,causal", [(3, 7, 7, 2, 8, False), (2, 9, 9, 4, 16, True),
                                                         (4, 6, 11, 8, 64, False), (2, 40, 40, 4, 128, True),
-                                                        (3, 25, 31, 16, 64, False)])
+                                                        (3, 25, 31, 16, 64, False),
+                                                        # widths > 64: the two-kernel (dQ | dK,dV) backward
+                                                        (2, 100, 100, 4, 64, True), (2, 70, 90, 4, 64, False),
+                                                        (1, 200, 200, 2, 32, True), (2, 64, 65, 2, 64, False)])
 def test_attention_matches_reference(fp16, batch, qw, kw, heads, dh, causal):
     lib = L()
     rng = np.random.default_rng(qw * kw)
@@ -287,7 +290,7 @@ def test_colsum_single_launch(dt, rows, n, ld):
     out = torch.randn(n, device="cuda", generator=g).to(TDT[dt])
     want = (out.double() + x[:, :n].double().sum(0))
     part = torch.zeros(min(512 * n, 4 << 20), device="cuda")
-    ctr = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ctr = torch.zeros((n + 255) // 256, dtype=torch.int32, device="cuda")
     for _ in range(2):  # counters must re-arm
         o = out.clone()
         lib.check(lib.sfk_colsum(dt, ptr(x), rows, n, ld, ptr(part), ptr(ctr), ptr(o), stream()), True)
@@ -331,8 +334,19 @@ def test_layernorm_bwd_fused_equals_two_phase(rows, d):
     # split form (dx on the critical path, gamma/beta as a column reduction)
     dx4, dg4, db4 = torch.zeros_like(x), torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
     lib.check(lib.sfk_layernorm_bwd_dx(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx4), 0, stream()), True)
-    lib.check(lib.sfk_layernorm_bwd_params(1, ptr(x), ptr(dy), rows, d, ptr(stats), ptr(part2), ptr(dg4), ptr(db4),
-                                           stream()), True)
+    lib.check(lib.sfk_layernorm_bwd_params(1, ptr(x), ptr(dy), rows, d, ptr(stats), ptr(part2), None, ptr(dg4),
+                                           ptr(db4), stream()), True)
+    # single-launch form (arrival counter, fused fold): same sums, fixed order
+    ctr5 = torch.zeros((d + 255) // 256, dtype=torch.int32, device="cuda")
+    dg5, db5 = torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
+    for _ in range(2):
+        dg5.zero_(), db5.zero_()
+        lib.check(lib.sfk_layernorm_bwd_params(1, ptr(x), ptr(dy), rows, d, ptr(stats), ptr(part2), ptr(ctr5),
+                                               ptr(dg5), ptr(db5), stream()), True)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(dg1.float(), dg5.float(), rtol=2e-3, atol=2e-3)
+        torch.testing.assert_close(db1.float(), db5.float(), rtol=2e-3, atol=2e-3)
+        assert int(ctr5.abs().sum()) == 0
     torch.cuda.synchronize()
     assert torch.equal(dx1, dx4)
     torch.testing.assert_close(dg1.float(), dg4.float(), rtol=2e-3, atol=2e-3)

@@ -130,3 +130,28 @@ def test_larger_config_fp16_runs_and_matches_first_steps():
         a, b = mine.train_one(), theirs.train_one()
         assert a["ntokens"] == b["ntokens"] and a["skipped"] == b["skipped"]
         assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"])
+
+
+def test_allreduce_overlap_schedule():
+    """Bucket all-reduces overlapped with the last backward (§8(e)): run the
+    schedule on one GPU (overlap_simulate: the same events/streams, no NCCL).
+    Every bucket is issued exactly once, in bucket order (the identical NCCL
+    sequence on every rank), almost all of them while backward still runs, and
+    the step's numbers are bitwise those of the post-backward schedule."""
+    import paper_1904_01038_b200 as sqf
+    V = 1000
+    c = sqf.synthetic_corpus(200, V, V, 1.1, 1)
+    base = dict(BASE, max_tokens=1024, accum=2, fp16=True, bucket_threshold=20000)
+    on = sqf.Trainer("transformer_base_defaults", dict(base, overlap_simulate=True), corpus=c, src_vocab=V, tgt_vocab=V)
+    off = sqf.Trainer("transformer_base_defaults", dict(base, overlap_allreduce=False), corpus=c, src_vocab=V,
+                      tgt_vocab=V)
+    sizes = [e[2] for e in sorted(on.manifest(), key=lambda e: e[3])]
+    nb = len(sqf.bucket_gradients(sizes, 20000))
+    for _ in range(3):
+        a, b = on.train_one(), off.train_one()
+        order, early = on.overlap_log()
+        assert order == list(range(nb))
+        assert early >= nb - 1
+        assert off.overlap_log()[0] == []
+        assert a == b
+    assert np.array_equal(on.params(), off.params())
