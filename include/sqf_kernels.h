@@ -94,6 +94,16 @@ int sfk_embed_fwd(int dtype, const int32_t* ids, int rows, int width, int d,
 int sfk_embed_bwd(int dtype, const int32_t* uniq, const int32_t* seg_off,
                   const int32_t* seg_rows, int nuniq, int d, const void* dx,
                   float scale, void* grad_table, void* stream);
+/* The same sums with the segments cut into chunks of <= 16 rows so a
+ * frequent id (eos, pad, a Zipf head) no longer serialises one block:
+ * chunks[4*c..] = {id, s0, s1, slot} over seg_rows[s0..s1); slot < 0: the id's
+ * only chunk, grad[id] = q(grad[id] + sum) directly; slot >= 0: the chunk sum
+ * goes to scratch[slot*d..], and multi[4*m..] = {id, first_slot, nslots, 0}
+ * folds grad[id] = q(grad[id] + sum over its slots in order). Deterministic
+ * (fixed association). 16-bit dtypes, d % 8 == 0; scratch >= nslots*d floats. */
+int sfk_embed_bwd_chunked(int dtype, const int32_t* chunks, int nchunks, const int32_t* multi,
+                          int nmulti, const int32_t* seg_rows, int d, const void* dx, float scale,
+                          float* scratch, void* grad_table, void* stream);
 
 /* ------------------------------------------------------ layer norm (a14)
  * kernels.cpp:30-45 / tape.cpp:211-222: two-pass mean/biased var,

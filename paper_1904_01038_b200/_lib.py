@@ -66,6 +66,8 @@ sfk_last_error = _sig("sfk_last_error", cp)
 sfk_num_sms = _sig("sfk_num_sms", C.c_int)
 sfk_gemm = _sig("sfk_gemm", C.c_int, P(GemmArgs), vp)
 sfk_embed_fwd = _sig("sfk_embed_fwd", C.c_int, C.c_int, vp, C.c_int, C.c_int, C.c_int, vp, vp, f32, vp, vp)
+sfk_embed_bwd_chunked = _sig("sfk_embed_bwd_chunked", C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, f32,
+                             vp, vp, vp)
 sfk_embed_bwd = _sig("sfk_embed_bwd", C.c_int, C.c_int, vp, vp, vp, C.c_int, C.c_int, vp, f32, vp, vp)
 sfk_layernorm_fwd = _sig("sfk_layernorm_fwd", C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp, vp, vp)
 sfk_layernorm_bwd = _sig("sfk_layernorm_bwd", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int,

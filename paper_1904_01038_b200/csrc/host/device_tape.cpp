@@ -108,6 +108,25 @@ void build_segments(const std::vector<int>& ids, std::vector<int32_t>& uniq, std
   }
   off.push_back(int32_t(order.size()));
 }
+
+// chunk tables of sfk_embed_bwd_chunked: segments cut into <= 16-row chunks
+void build_chunks(const std::vector<int32_t>& uniq, const std::vector<int32_t>& off, std::vector<int32_t>& chunks,
+                  std::vector<int32_t>& multi, int& nslots) {
+  constexpr int kChunk = 16;
+  chunks.clear();
+  multi.clear();
+  nslots = 0;
+  for (size_t u = 0; u < uniq.size(); ++u) {
+    const int s0 = off[u], s1 = off[u + 1];
+    const int n = (s1 - s0 + kChunk - 1) / kChunk;
+    if (n == 1) {
+      chunks.insert(chunks.end(), {uniq[u], s0, s1, -1});
+      continue;
+    }
+    multi.insert(multi.end(), {uniq[u], nslots, n, 0});
+    for (int c = 0; c < n; ++c) chunks.insert(chunks.end(), {uniq[u], s0 + c * kChunk, std::min(s1, s0 + (c + 1) * kChunk), nslots++});
+  }
+}
 }  // namespace
 
 PackedBatch PackedBatch::pack(const MiniBatch& b) {
@@ -119,6 +138,9 @@ PackedBatch PackedBatch::pack(const MiniBatch& b) {
   std::vector<int32_t> su, so, sr, tu, to, tr;
   build_segments(b.source, su, so, sr);
   build_segments(b.target_in, tu, to, tr);
+  std::vector<int32_t> sc, sm, tc, tm;
+  build_chunks(su, so, sc, sm, p.n_ss);
+  build_chunks(tu, to, tc, tm, p.n_ts);
   auto put = [&](const auto& v) {
     const size_t at = p.blob.size();
     p.blob.insert(p.blob.end(), v.begin(), v.end());
@@ -135,8 +157,16 @@ PackedBatch PackedBatch::pack(const MiniBatch& b) {
   p.off_tu = put(tu);
   p.off_to = put(to);
   p.off_tr = put(tr);
+  p.off_sc = put(sc);
+  p.off_sm = put(sm);
+  p.off_tc = put(tc);
+  p.off_tm = put(tm);
   p.n_su = int(su.size());
   p.n_tu = int(tu.size());
+  p.n_sc = int(sc.size() / 4);
+  p.n_sm = int(sm.size() / 4);
+  p.n_tc = int(tc.size() / 4);
+  p.n_tm = int(tm.size() / 4);
   return p;
 }
 
@@ -150,8 +180,8 @@ DeviceBatch PackedBatch::bind(const int32_t* d) const {
   b.target_in = d + off_tin;
   b.target_out = d + off_tout;
   b.src_lens = d + off_slens;
-  b.src_segs = {d + off_su, d + off_so, d + off_sr, n_su};
-  b.tgt_segs = {d + off_tu, d + off_to, d + off_tr, n_tu};
+  b.src_segs = {d + off_su, d + off_so, d + off_sr, n_su, d + off_sc, d + off_sm, n_sc, n_sm, n_ss};
+  b.tgt_segs = {d + off_tu, d + off_to, d + off_tr, n_tu, d + off_tc, d + off_tm, n_tc, n_tm, n_ts};
   return b;
 }
 
@@ -422,9 +452,17 @@ void DeviceTape::backward_node(int id) {
     case Kind::Embedding: {
       join_side();  // a tied output projection's wgrad writes the same parameter rows
       pbegin();
-      sfk_check(sfk_embed_bwd(dtype_, n.segs.uniq, n.segs.off, n.segs.rows, n.segs.n, n.cols, n.grad, n.scale,
-                              gptr(n.p0), cur_),
-                "embed_bwd");
+      if (dtype_ != SFK_F32 && n.segs.chunks) {
+        float* scratch = n.segs.nslots ? static_cast<float*>(arena_.alloc(size_t(n.segs.nslots) * n.cols * 4)) : nullptr;
+        sfk_check(sfk_embed_bwd_chunked(dtype_, n.segs.chunks, n.segs.nchunks, n.segs.multi, n.segs.nmulti,
+                                        n.segs.rows, n.cols, n.grad, n.scale, scratch, gptr(n.p0), cur_),
+                  "embed_bwd");
+        launches_ += n.segs.nmulti ? 1 : 0;
+      } else {
+        sfk_check(sfk_embed_bwd(dtype_, n.segs.uniq, n.segs.off, n.segs.rows, n.segs.n, n.cols, n.grad, n.scale,
+                                gptr(n.p0), cur_),
+                  "embed_bwd");
+      }
       pend(Profiler::Embed, 0, double(n.rows) * n.cols * esize_ + 2.0 * n.segs.n * n.cols * esize_);
       ++launches_;
       grad_done(n.p0);

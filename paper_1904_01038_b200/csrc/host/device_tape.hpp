@@ -53,6 +53,10 @@ struct DeviceBatch {
     const int32_t* off = nullptr;
     const int32_t* rows = nullptr;
     int n = 0;
+    // <= 16-row chunks {id, s0, s1, slot} and multi-chunk folds {id, first_slot, nslots, 0}
+    const int32_t* chunks = nullptr;
+    const int32_t* multi = nullptr;
+    int nchunks = 0, nmulti = 0, nslots = 0;
   } src_segs, tgt_segs;
 };
 
@@ -65,7 +69,9 @@ struct PackedBatch {
   int64_t ntokens = 0;
   size_t off_source = 0, off_tin = 0, off_tout = 0, off_slens = 0;
   size_t off_su = 0, off_so = 0, off_sr = 0, off_tu = 0, off_to = 0, off_tr = 0;
+  size_t off_sc = 0, off_sm = 0, off_tc = 0, off_tm = 0;
   int n_su = 0, n_tu = 0;
+  int n_sc = 0, n_sm = 0, n_ss = 0, n_tc = 0, n_tm = 0, n_ts = 0;
   static PackedBatch pack(const MiniBatch& b);
   DeviceBatch bind(const int32_t* dev_blob) const;
 };

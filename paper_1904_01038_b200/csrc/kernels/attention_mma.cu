@@ -508,7 +508,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_small_k(Args a) {
   T* Gs = Qs + QP * LD;
   T* Ks = Gs + QP * LD;
   T* Vs = Ks + kRows * LD;
-  float2* St = reinterpret_cast<float2*>(Vs + kRows * LD);
+  T* Os = Vs + kRows * LD;  // forward output, for D = rowsum(dO * O)
+  float2* St = reinterpret_cast<float2*>(Os + kRows * LD);
   float* Ds = reinterpret_cast<float*>(St + QP);
   const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
   stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0), a.qw, QP, a.dh);
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_small_k(Args a) {
   // dQ reads keys < nk; dK/dV rows are all kw key rows (rows >= nk get zero grads)
   stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), a.kw, kRows, a.dh);
   stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), a.kw, kRows, a.dh);
+  stage<T, DH>(Os, LD, static_cast<const T*>(a.o) + h * a.dh, a.ldo, int(qrow0), a.qw, kRows, a.dh);
   for (int i = threadIdx.x; i < QP; i += blockDim.x) {
     St[i] = i < a.qw ? a.stats[(qrow0 + i) * a.heads + h] : make_float2(0.f, 0.f);
     Ds[i] = 0.f;
@@ -528,10 +530,11 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_small_k(Args a) {
   if (r0 < a.qw) {
     const int row_a = r0 + g, row_b = row_a + 8;
     float D_a = 0.f, D_b = 0.f;
-    const T* O = static_cast<const T*>(a.o) + h * a.dh;
-    for (int c = tq; c < a.dh; c += 4) {
-      if (row_a < a.qw) D_a += Num<T>::ld(Gs + row_a * LD + c) * Num<T>::ld(O + (qrow0 + row_a) * a.ldo + c);
-      if (row_b < a.qw) D_b += Num<T>::ld(Gs + row_b * LD + c) * Num<T>::ld(O + (qrow0 + row_b) * a.ldo + c);
+    // rows past qw are zero-filled in Gs/Os, so their D is 0
+#pragma unroll
+    for (int c = tq; c < DH; c += 4) {
+      D_a += Num<T>::ld(Gs + row_a * LD + c) * Num<T>::ld(Os + row_a * LD + c);
+      D_b += Num<T>::ld(Gs + row_b * LD + c) * Num<T>::ld(Os + row_b * LD + c);
     }
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 1);
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 2);
@@ -752,7 +755,7 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     return check_launch("sfk_attention_fwd(mma)");
   }
   if (a.qw <= kRows && a.kw <= kRows) {
-    const size_t smem_s = size_t(4 * kRows + 2 * kRows) * LD * sizeof(T) + size_t(2 * kRows) * 12;
+    const size_t smem_s = size_t(4 * kRows + 3 * kRows) * LD * sizeof(T) + size_t(2 * kRows) * 12;
     launch_pdl(bwd_small_k<T, DH>, dim3(1, a.heads, a.batch), kWarps * 32, smem_s, st, a);
     return check_launch("sfk_attention_bwd(small)");
   }

@@ -343,6 +343,8 @@ __global__ void xent_reduce_k(const float* __restrict__ row_out, int rows, doubl
 
 namespace sfk {
 int embed_fwd_vec(int, const int32_t*, int, int, int, const void*, const float*, float, void*, cudaStream_t);
+int embed_bwd_chunked_vec(int, const int32_t*, int, const int32_t*, int, const int32_t*, int, const void*, float, float*,
+                          void*, cudaStream_t);
 int embed_bwd_vec(int, const int32_t*, const int32_t*, const int32_t*, int, int, const void*, float, void*,
                   cudaStream_t);
 int ln_fwd_vec(int, const void*, int, int, const void*, const void*, void*, float*, cudaStream_t);
@@ -421,6 +423,16 @@ extern "C" int sfk_embed_fwd(int dtype, const int32_t* ids, int rows, int width,
                launch_pdl(embed_fwd_k<T>, rows, 128, 0, as_stream(stream), ids, rows, width, d, static_cast<const T*>(table),
                                                                     pe, scale, static_cast<T*>(out)));
   return check_launch("sfk_embed_fwd");
+}
+
+extern "C" int sfk_embed_bwd_chunked(int dtype, const int32_t* chunks, int nchunks, const int32_t* multi, int nmulti,
+                                     const int32_t* seg_rows, int d, const void* dx, float scale, float* scratch,
+                                     void* grad, void* stream) {
+  if (nchunks == 0) return SFK_OK;
+  const int e = embed_bwd_chunked_vec(dtype, chunks, nchunks, multi, nmulti, seg_rows, d, dx, scale, scratch, grad,
+                                      as_stream(stream));
+  if (e == SFK_EUNSUP) set_error("sfk_embed_bwd_chunked: needs 16-bit data, d % 8 == 0, aligned rows, scratch");
+  return e;
 }
 
 extern "C" int sfk_embed_bwd(int dtype, const int32_t* uniq, const int32_t* seg_off, const int32_t* seg_rows,

@@ -98,6 +98,78 @@ __global__ void __launch_bounds__(128) embed_bwd_v(const int32_t* __restrict__ u
   }
 }
 
+// Chunked embedding backward: one block per <= 16-row chunk of an id's
+// recording-order segment (all loads in flight), then one block per id with
+// several chunks folding the chunk sums in chunk order.
+constexpr int kEmbChunk = 16;
+template <typename T>
+__global__ void __launch_bounds__(128) embed_bwd_chunk_v(const int4* __restrict__ chunks,
+                                                        const int32_t* __restrict__ srows, int d,
+                                                        const T* __restrict__ dx, float scale,
+                                                        float* __restrict__ scratch, T* __restrict__ grad) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  const int4 ch = chunks[blockIdx.x];  // {id, s0, s1, slot}
+  const int n = ch.z - ch.y;
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    uint4 u[kEmbChunk];
+#pragma unroll
+    for (int j = 0; j < kEmbChunk; ++j)
+      if (j < n) u[j] = *reinterpret_cast<const uint4*>(dx + int64_t(srows[ch.y + j]) * d + c);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (ch.w < 0) V8<T>::load(grad + int64_t(ch.x) * d + c, acc);
+#pragma unroll
+    for (int j = 0; j < kEmbChunk; ++j) {
+      if (j >= n) break;
+      float f[8];
+      V8<T>::unpack(u[j], f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = __fadd_rn(acc[i], Num<T>::rnd(__fmul_rn(scale, f[i])));
+    }
+    if (ch.w < 0) {
+      V8<T>::store(grad + int64_t(ch.x) * d + c, acc);
+    } else {
+      float* o = scratch + int64_t(ch.w) * d + c;
+      *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) embed_bwd_fold_v(const int4* __restrict__ multi, int d,
+                                                       const float* __restrict__ scratch, T* __restrict__ grad) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  const int4 m = multi[blockIdx.x];  // {id, first_slot, nslots, 0}
+  for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+    float acc[8];
+    V8<T>::load(grad + int64_t(m.x) * d + c, acc);
+    int k = 0;
+    for (; k + 4 <= m.z; k += 4) {
+      float4 q[4][2];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float* p = scratch + int64_t(m.y + k + j) * d + c;
+        q[j][0] = __ldcg(reinterpret_cast<const float4*>(p));
+        q[j][1] = __ldcg(reinterpret_cast<const float4*>(p + 4));
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[0] += q[j][0].x, acc[1] += q[j][0].y, acc[2] += q[j][0].z, acc[3] += q[j][0].w;
+        acc[4] += q[j][1].x, acc[5] += q[j][1].y, acc[6] += q[j][1].z, acc[7] += q[j][1].w;
+      }
+    }
+    for (; k < m.z; ++k) {
+      const float* p = scratch + int64_t(m.y + k) * d + c;
+      const float4 a = __ldcg(reinterpret_cast<const float4*>(p)), b = __ldcg(reinterpret_cast<const float4*>(p + 4));
+      acc[0] += a.x, acc[1] += a.y, acc[2] += a.z, acc[3] += a.w;
+      acc[4] += b.x, acc[5] += b.y, acc[6] += b.z, acc[7] += b.w;
+    }
+    V8<T>::store(grad + int64_t(m.x) * d + c, acc);
+  }
+}
+
 constexpr int kMaxCh = 4;  // d <= 32 lanes * 4 chunks * 8 = 1024
 
 template <typename T>
@@ -659,6 +731,29 @@ int embed_bwd_vec(int dtype, const int32_t* uniq, const int32_t* off, const int3
                                                               static_cast<const __nv_bfloat16*>(dx), scale,
                                                               static_cast<__nv_bfloat16*>(grad));
   return check_launch("sfk_embed_bwd(vec)");
+}
+
+int embed_bwd_chunked_vec(int dtype, const int32_t* chunks, int nchunks, const int32_t* multi, int nmulti,
+                          const int32_t* rows, int d, const void* dx, float scale, float* scratch, void* grad,
+                          cudaStream_t s) {
+  if (dtype == SFK_F32 || d % 8 || !al16(dx) || !al16(grad) || (nmulti && !scratch)) return SFK_EUNSUP;
+  const int threads = std::min(128, std::max(32, d / 8));
+  auto c4 = reinterpret_cast<const int4*>(chunks);
+  auto m4 = reinterpret_cast<const int4*>(multi);
+  if (dtype == SFK_F16) {
+    launch_pdl(vec::embed_bwd_chunk_v<__half>, nchunks, threads, 0, s, c4, rows, d, static_cast<const __half*>(dx),
+               scale, scratch, static_cast<__half*>(grad));
+    if (nmulti)
+      launch_pdl(vec::embed_bwd_fold_v<__half>, nmulti, threads, 0, s, m4, d, static_cast<const float*>(scratch),
+                 static_cast<__half*>(grad));
+  } else {
+    launch_pdl(vec::embed_bwd_chunk_v<__nv_bfloat16>, nchunks, threads, 0, s, c4, rows, d,
+               static_cast<const __nv_bfloat16*>(dx), scale, scratch, static_cast<__nv_bfloat16*>(grad));
+    if (nmulti)
+      launch_pdl(vec::embed_bwd_fold_v<__nv_bfloat16>, nmulti, threads, 0, s, m4, d,
+                 static_cast<const float*>(scratch), static_cast<__nv_bfloat16*>(grad));
+  }
+  return check_launch("sfk_embed_bwd_chunked");
 }
 
 int ln_fwd_vec(int dtype, const void* x, int rows, int d, const void* g, const void* b, void* y, float* stats,

@@ -357,3 +357,64 @@ def test_layernorm_bwd_fused_equals_two_phase(rows, d):
                                           ptr(ctr), ptr(dg3), ptr(db3), stream()), True)
     torch.cuda.synchronize()
     assert torch.equal(dx2, dx3) and torch.equal(dg2, dg3) and torch.equal(db2, db3)
+
+
+def _segments(ids, chunk=16):
+    """Host segment + chunk tables exactly as PackedBatch::pack builds them."""
+    order = np.argsort(ids, kind="stable").astype(np.int32)
+    uniq, off = [], []
+    for i, r in enumerate(order):
+        if i == 0 or ids[r] != ids[order[i - 1]]:
+            uniq.append(int(ids[r]))
+            off.append(i)
+    off.append(len(order))
+    chunks, multi, nslots = [], [], 0
+    for u in range(len(uniq)):
+        s0, s1 = off[u], off[u + 1]
+        n = (s1 - s0 + chunk - 1) // chunk
+        if n == 1:
+            chunks += [uniq[u], s0, s1, -1]
+            continue
+        multi += [uniq[u], nslots, n, 0]
+        for c in range(n):
+            chunks += [uniq[u], s0 + c * chunk, min(s1, s0 + (c + 1) * chunk), nslots]
+            nslots += 1
+    return order, np.array(uniq, np.int32), np.array(off, np.int32), chunks, multi, nslots
+
+
+@pytest.mark.parametrize("dt", [1, 2])
+@pytest.mark.parametrize("rows,d,vocab", [(3584, 1024, 32768), (300, 64, 50), (33, 512, 5)])
+def test_embedding_backward_chunked(dt, rows, d, vocab):
+    """Embedding backward (tape.cpp:311-323): the chunked form (frequent ids
+    split into <= 16-row chunks, chunk sums folded in order) equals the
+    per-id sequential form to fp32 rounding and an fp64 reference within the
+    storage tolerance; ids follow a Zipf head (eos/pad-like repeats)."""
+    lib = L()
+    rng = np.random.default_rng(rows)
+    ids = np.minimum(rng.zipf(1.1, rows) - 1, vocab - 1).astype(np.int32)
+    ids[::7] = 1  # a pad-like id repeated rows/7 times
+    order, uniq, off, chunks, multi, nslots = _segments(ids)
+    g = torch.Generator(device="cuda").manual_seed(d)
+    dx = torch.randn(rows, d, device="cuda", generator=g).to(TDT[dt])
+    table0 = (torch.randn(vocab, d, device="cuda", generator=g) * 0.1).to(TDT[dt])
+    scale = float(np.sqrt(d))
+    T = lambda a: torch.tensor(a, dtype=torch.int32, device="cuda")  # noqa: E731
+    t_order, t_uniq, t_off = T(order), T(uniq), T(off)
+    t_chunks, t_multi = T(chunks), T(multi if multi else [0, 0, 0, 0])
+    scratch = torch.zeros(max(1, nslots) * d, device="cuda")
+    a, b = table0.clone(), table0.clone()
+    lib.check(lib.sfk_embed_bwd(dt, ptr(t_uniq), ptr(t_off), ptr(t_order), len(uniq), d, ptr(dx), scale, ptr(a),
+                                stream()), True)
+    lib.check(lib.sfk_embed_bwd_chunked(dt, ptr(t_chunks), len(chunks) // 4, ptr(t_multi), len(multi) // 4,
+                                        ptr(t_order), d, ptr(dx), scale, ptr(scratch), ptr(b), stream()), True)
+    torch.cuda.synchronize()
+    q = lambda x: x.to(TDT[dt]).double()  # noqa: E731
+    want = table0.double().index_add(0, torch.tensor(ids, device="cuda").long(), q(dx.double() * scale))
+    tol = 4e-3 if dt == 1 else 2e-2
+    torch.testing.assert_close(b.double(), q(want), rtol=tol, atol=tol)
+    torch.testing.assert_close(a.double(), b.double(), rtol=tol, atol=tol)
+    c = table0.clone()
+    lib.check(lib.sfk_embed_bwd_chunked(dt, ptr(t_chunks), len(chunks) // 4, ptr(t_multi), len(multi) // 4,
+                                        ptr(t_order), d, ptr(dx), scale, ptr(scratch), ptr(c), stream()), True)
+    torch.cuda.synchronize()
+    assert torch.equal(b, c)  # deterministic
