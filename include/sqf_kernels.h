@@ -73,6 +73,14 @@ typedef struct sfk_gemm_args {
   int force_simt;                 /* testing: run the SIMT kernel for any dtype */
   int tile_n;                     /* tuning: force the tcgen05 tile width (64/128/256), 0 = auto */
   int pair;                       /* tuning: 1 = CTA-pair (cta_group::2) 256-row tiles, -1 = single-CTA, 0 = auto */
+  /* stream-K (optional): with a workspace of >= 2*SMs*128*256 floats and
+   * zeroed counters (>= tiles; re-armed to 0 by the kernel) the 128x256
+   * kernel may split the k-loop of the last wave's tiles across all SMs;
+   * the parts are summed in k order by the last arriving CTA (deterministic).
+   * Concurrent launches need distinct workspaces and counters. */
+  float* workspace; int64_t workspace_floats;
+  int32_t* counters; int n_counters;
+  int stream_k;                   /* 0 = auto, -1 = off, 1 = force when possible */
 } sfk_gemm_args;
 
 int sfk_gemm(const sfk_gemm_args* g, void* stream);

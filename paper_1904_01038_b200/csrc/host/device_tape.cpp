@@ -252,6 +252,13 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   g.mask = mask;
   g.ldm = ldm;
   g.flags = flags;
+  float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
+  if (ws && ctr_base_) {
+    g.workspace = ws;
+    g.workspace_floats = ws_floats_;
+    g.n_counters = 2 * 148;
+    g.counters = counters(g.n_counters);
+  }
   pbegin();
   sfk_check(sfk_gemm(&g, cur_), "gemm");
   pend(cat, 2.0 * m * n * k, double(esize_) * (double(m) * k + double(n) * k + double(m) * n));

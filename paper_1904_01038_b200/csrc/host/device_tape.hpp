@@ -163,6 +163,12 @@ class DeviceTape {
   // order the hook will report them
   std::vector<std::pair<int64_t, int64_t>> planned_grad_writes() const;
   cudaStream_t side_stream() const { return side_; }
+  // stream-K GEMM workspaces, one per stream (concurrent GEMMs must not share)
+  void set_gemm_workspace(float* main_ws, float* side_ws, int64_t floats) {
+    ws_main_ = main_ws;
+    ws_side_ = side_ws;
+    ws_floats_ = floats;
+  }
   void set_counters(int32_t* base, int64_t n, int64_t* cursor) {
     ctr_base_ = base;
     ctr_n_ = n;
@@ -213,6 +219,9 @@ class DeviceTape {
     return p;
   }
   GradHook hook_;
+  float* ws_main_ = nullptr;
+  float* ws_side_ = nullptr;
+  int64_t ws_floats_ = 0;
   void grad_done(const ParamRef& p) {
     if (hook_) hook_(p.offset, int64_t(p.rows) * p.cols, cur_);
   }

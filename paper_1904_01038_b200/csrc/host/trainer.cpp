@@ -37,6 +37,7 @@ Trainer::~Trainer() {
   if (compute_ != master_) cudaFree(compute_);
   for (void* g : grads_) cudaFree(g);
   cudaFree(pe_);
+  cudaFree(gemm_ws_);
   cudaFree(stats_dev_);
   cudaFree(flag_dev_);
   cudaFree(counters_);
@@ -127,6 +128,12 @@ void Trainer::init(const Registry& reg) {
   cuda_check(cudaMalloc(&stats_dev_, 4 * sizeof(double)), "stats");
   cuda_check(cudaMalloc(&flag_dev_, 16), "flag");
   cuda_check(cudaMalloc(&counters_, size_t(kCounters) * 4), "counters");
+  {
+    int sms = sfk_num_sms();
+    if (sms <= 0) sms = 148;
+    gemm_ws_floats_ = int64_t(sms) * 2 * 128 * 256;
+    cuda_check(cudaMalloc(&gemm_ws_, size_t(gemm_ws_floats_) * 2 * 4), "gemm workspace");
+  }
   cuda_check(cudaMemset(counters_, 0, size_t(kCounters) * 4), "counters");
   cuda_check(cudaMallocHost(&readback_host_, 64), "readback");
   push_params();
@@ -382,6 +389,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     tape.set_side_stream(side_, &evpool_);
+    tape.set_gemm_workspace(gemm_ws_, gemm_ws_ + gemm_ws_floats_, gemm_ws_floats_);
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     if (overlap && i + 1 == dev.size()) {
       ovl_begin(tape);

@@ -148,6 +148,8 @@ class Trainer {
   // ---- bucketed all-reduce overlapped with the last sub-batch's backward
   bool overlap_ = true, overlap_sim_ = false;
   cudaStream_t comm_stream_ = nullptr;
+  float* gemm_ws_ = nullptr;          // stream-K partial tiles: [main | side]
+  int64_t gemm_ws_floats_ = 0;        // per stream
   std::vector<cudaEvent_t> ovl_events_;
   size_t ovl_next_event_ = 0;
   std::vector<int> ovl_remaining_;   // outstanding gradient writes per bucket

@@ -13,6 +13,7 @@
 // fp32: a SIMT kernel (true fp32 FMA, no TF32) for the reference's fp32 mode.
 #include <cuda.h>
 
+#include <cmath>
 #include <mutex>
 
 #include "common.cuh"
@@ -426,6 +427,128 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, int w
   }
 }
 
+// ---------------------------------------------------------- stream-K schedule
+// Work of a persistent CTA b (of G): first its share of the stream-K region
+// -- tiles [0, sk_tiles) flattened to sk_tiles*kblocks k-block iterations and
+// cut into G equal contiguous ranges, so a range may start/end inside a tile --
+// then whole data-parallel tiles sk_tiles + b + i*G. Producer, MMA and
+// epilogue warps walk the identical unit sequence.
+struct Sk {
+  float* ws;          // [G][2][BM*BN] fp32 partial tiles (slot 0: a CTA's first unit, 1: its last)
+  int32_t* flags;     // [sk_tiles] arrival counters, zero on entry, re-armed by the reducer
+  int sk_tiles;
+};
+
+struct Sched {
+  int tiles, kblocks, G, b, sk_tiles;
+  int64_t tsk, it0, it1, it;
+  int dp;
+  __device__ __forceinline__ Sched(int tiles_, int kblocks_, int sk_tiles_)
+      : tiles(tiles_), kblocks(kblocks_), G(int(gridDim.x)), b(int(blockIdx.x)), sk_tiles(sk_tiles_) {
+    tsk = int64_t(sk_tiles) * kblocks;
+    it0 = int64_t(b) * tsk / G;
+    it1 = int64_t(b + 1) * tsk / G;
+    it = it0;
+    dp = sk_tiles + b;
+  }
+  __device__ __forceinline__ int64_t start_of(int c) const { return int64_t(c) * tsk / G; }
+  __device__ __forceinline__ bool next(int& tile, int& kb0, int& kb1) {
+    if (it < it1) {
+      tile = int(it / kblocks);
+      kb0 = int(it % kblocks);
+      kb1 = int(min(int64_t(kblocks), kb0 + (it1 - it)));
+      it += kb1 - kb0;
+      return true;
+    }
+    if (dp < tiles) {
+      tile = dp;
+      kb0 = 0;
+      kb1 = kblocks;
+      dp += G;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
+
+// Partial (stream-K) unit: this warp's chunks of the fp32 accumulator tile go
+// to the CTA's workspace slot, one 128-byte row segment per thread.
+template <int BN>
+__device__ __forceinline__ void store_partial(uint32_t tacc, int warp, int lane, float* slot) {
+  const int quarter = warp & 3, half = (warp - 2) >> 2;
+  const uint32_t lane_base = tacc + (uint32_t(quarter * 32) << 16);
+  float* row = slot + size_t(quarter * 32 + lane) * BN;
+  uint32_t r[32];
+  tmem_ld32_issue(lane_base + half * 32, r);
+#pragma unroll 1
+  for (int ch = half; ch < BN / 32; ch += 2) {
+    tmem_ld_wait(r);
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      v[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                         __uint_as_float(r[4 * j + 3]));
+    if (ch + 2 < BN / 32) tmem_ld32_issue(lane_base + (ch + 2) * 32, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) __stcg(reinterpret_cast<float4*>(row + ch * 32) + j, v[j]);
+  }
+}
+
+// Reducer of a stream-K tile: sum the partial slots of its CTAs in k order
+// (fixed association: deterministic) and run the fused epilogue on the sum.
+template <int BN, typename T>
+__device__ __forceinline__ void reduce_partials(const Epi& e, const Sched& sc, const Sk& sk, int tile, int warp,
+                                                int lane, float* stg, int64_t m0, int n0, int M, int N, int vec_ok) {
+  const int quarter = warp & 3, half = (warp - 2) >> 2;
+  const int64_t i_beg = int64_t(tile) * sc.kblocks, i_end = i_beg + sc.kblocks;
+  const int c0 = int(((i_beg + 1) * sc.G + sc.tsk - 1) / sc.tsk) - 1;
+  const size_t row_off = size_t(quarter * 32 + lane) * BN;
+  int nch = (N - n0 + 31) / 32;
+  if (nch > BN / 32) nch = BN / 32;
+#pragma unroll 1
+  for (int ch = half; ch < nch; ch += 2) {
+    float4 acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = c0; c < sc.G && sc.start_of(c) < i_end; ++c) {
+      const int slot = i_beg <= sc.start_of(c) ? 0 : 1;
+      const float4* src = reinterpret_cast<const float4*>(sk.ws + (size_t(c) * 2 + slot) * (BM * BN) + row_off + ch * 32);
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(src + j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        acc[j].x += v[j].x;
+        acc[j].y += v[j].y;
+        acc[j].z += v[j].z;
+        acc[j].w += v[j].w;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) *reinterpret_cast<float4*>(stg + stg_off(lane, j)) = acc[j];
+    __syncwarp();
+    const int cc = (lane & 3) * 8, col = n0 + ch * 32 + cc;
+    const int rr0 = lane >> 2;
+    const int64_t row0 = m0 + quarter * 32 + rr0;
+    if (vec_ok && col + 8 <= N) {
+      epilogue_seg4<T>(e, row0, col, M, stg, rr0, cc >> 2);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rr = rr0 + 8 * i;
+        const int64_t row = row0 + 8 * i;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = stg[stg_off(rr, (cc + j) >> 2) + ((cc + j) & 3)];
+        if (row < M && col < N) epilogue8<T>(e, row, col, N, v, false);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -439,7 +562,7 @@ struct Cfg {
 template <int BN, bool A_MN, bool B_MN, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Epi e, int M,
-            int N, int K, int vec_ok) {
+            int N, int K, int vec_ok, const Sk sk) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -477,13 +600,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
+  (void)num_n;
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      Sched sc(tiles, kblocks, sk.sk_tiles);
+      int it = 0, tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
         const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -512,13 +637,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(A_MN) << 15) |
                              (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-      int it = 0, t = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+      Sched sc(tiles, kblocks, sk.sk_tiles);
+      int it = 0, t = 0, tile, kb0, kb1;
+      while (sc.next(tile, kb0, kb1)) {
         const int buf = t & 1;
         mbar_wait(&tempty[buf], ((t >> 1) & 1) ^ 1);
         fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           mbar_wait(&full[s], (it / C::STAGES) & 1);
           fence_after();
@@ -530,11 +656,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // advance 16 K-rows (2 KB) to the next pair of 8-row groups
             const uint64_t ad = A_MN ? smem_desc(a_addr + k * 2048, 8192, 1024) : smem_desc(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc(b_addr + k * 2048, 8192, 1024) : smem_desc(b_addr + k * 32, 16, 1024);
-            umma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            umma(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
         }
         umma_commit(&tfull[buf]);
+        ++t;
       }
     }
   } else {
@@ -542,16 +669,45 @@ __global__ void __launch_bounds__(kThreads, 1)
     // block bounces through shared memory so a warp then reads/writes 8 rows x
     // 64 contiguous bytes per instruction (coalesced) instead of 32 rows.
     float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
-    int t = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++t) {
+    volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    Sched sc(tiles, kblocks, sk.sk_tiles);
+    int t = 0, tile, kb0, kb1;
+    while (sc.next(tile, kb0, kb1)) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
-      epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (kb0 == 0 && kb1 == kblocks) {
+        epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      } else {
+        // stream-K partial: park the fp32 accumulators, count the arrival;
+        // the last of the tile's CTAs sums the parts and runs the epilogue
+        const int slot = int64_t(tile) * kblocks <= sc.it0 ? 0 : 1;
+        store_partial<BN>(tmem_base + buf * BN, warp, lane, sk.ws + (size_t(sc.b) * 2 + slot) * (BM * BN));
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 64) {
+          const int64_t i_beg = int64_t(tile) * kblocks, i_end = i_beg + kblocks;
+          const int c0 = int(((i_beg + 1) * sc.G + sc.tsk - 1) / sc.tsk) - 1;
+          const int c1 = int((i_end * sc.G + sc.tsk - 1) / sc.tsk) - 1;
+          const int old = atomicAdd(sk.flags + tile, 1);
+          const bool last = old == c1 - c0;
+          if (last) sk.flags[tile] = 0;  // every part has arrived: re-arm
+          *last_flag = last ? 1 : 0;
+        }
+        epi_bar();
+        if (*last_flag) {
+          __threadfence();
+          reduce_partials<BN, T>(e, sc, sk, tile, warp, lane, stg, m0, n0, M, N, vec_ok);
+        }
+      }
+      ++t;
     }
   }
   fence_before();
@@ -793,7 +949,7 @@ int num_sms_cached() {
 }
 
 template <int BN, bool A_MN, bool B_MN, typename T>
-int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
+int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, int sk_tiles) {
   using C = Cfg<BN>;
   CUtensorMap ta, tb;
   // A: K-major [m][k] -> map cols=k rows=m, box rows 128; MN-major [k][m] -> cols=m rows=k, box 64x64
@@ -813,9 +969,10 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
     attr_set = true;
   }
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
-  const int grid = tiles < num_sms_cached() ? tiles : num_sms_cached();
+  const int grid = sk_tiles > 0 ? num_sms_cached() : (tiles < num_sms_cached() ? tiles : num_sms_cached());
+  Sk sk{sk_tiles > 0 ? g->workspace : nullptr, sk_tiles > 0 ? g->counters : nullptr, sk_tiles};
   launch_pdl(gemm_tc<BN, A_MN, B_MN, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, e, g->m, g->n, g->k,
-             vec_ok ? 1 : 0);
+             vec_ok ? 1 : 0, sk);
   return check_launch("sfk_gemm(tcgen05)");
 }
 
@@ -879,9 +1036,32 @@ int pick_bn(int m, int n) {
   return best;
 }
 
+// Stream-K region size (in tiles) for a 128 x 256 1-CTA GEMM, 0 = plain
+// data-parallel. Cost model in k-block units: a tile costs kblocks + 4 (fill,
+// epilogue); a stream-K range costs its k-blocks + 4 per unit, plus storing
+// a partial (2) and the reducer reading ~2 per contributing CTA.
+int pick_stream_k(const sfk_gemm_args* g) {
+  if (g->stream_k < 0 || !g->workspace || !g->counters) return 0;
+  const int G = num_sms_cached();
+  if (g->workspace_floats < int64_t(G) * 2 * BM * 256) return 0;
+  const int tiles = ((g->m + BM - 1) / BM) * ((g->n + 255) / 256);
+  const int kb = (g->k + BK - 1) / BK;
+  if (kb < 4 || tiles % G == 0) return 0;
+  const int waves = (tiles + G - 1) / G;
+  const double dp = double(waves) * (kb + 4);
+  const int sk_tiles = tiles < G ? tiles : tiles % G + G;
+  if (sk_tiles > g->n_counters) return 0;
+  const double per = double(sk_tiles) * kb / G;
+  const double segs = std::ceil(double(G) / sk_tiles) + 1;
+  const double sk = double((tiles - sk_tiles) / G) * (kb + 4) + per + 8 + 2 + 2 * segs;
+  if (g->stream_k > 0) return sk_tiles;
+  return sk < 0.92 * dp ? sk_tiles : 0;
+}
+
 template <typename T>
 int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
-  const int bn = g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
+  const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 ? pick_stream_k(g) : 0;
+  const int bn = skt > 0 ? 256 : g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
   if (g->pair > 0) {
 #define SFK_TC2(BNV)                                                    \
@@ -895,12 +1075,12 @@ int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) 
     SFK_TC2(128)
 #undef SFK_TC2
   }
-#define SFK_TC(BNV)                                                    \
-  switch (layout) {                                                    \
-    case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s);      \
-    case 1: return launch<BNV, false, true, T>(g, e, vec_ok, s);       \
-    case 3: return launch<BNV, true, true, T>(g, e, vec_ok, s);        \
-    default: return launch<BNV, true, false, T>(g, e, vec_ok, s);      \
+#define SFK_TC(BNV)                                                         \
+  switch (layout) {                                                         \
+    case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s, skt);      \
+    case 1: return launch<BNV, false, true, T>(g, e, vec_ok, s, skt);       \
+    case 3: return launch<BNV, true, true, T>(g, e, vec_ok, s, skt);        \
+    default: return launch<BNV, true, false, T>(g, e, vec_ok, s, skt);      \
   }
   if (bn == 256) { SFK_TC(256) }
   if (bn == 128) { SFK_TC(128) }

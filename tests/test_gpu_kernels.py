@@ -30,7 +30,8 @@ def ptr(t):
 TDT = {0: torch.float32, 1: torch.float16, 2: torch.bfloat16}
 
 
-def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=False, with_c=None, pair=0, tile_n=0):
+def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=False, with_c=None, pair=0, tile_n=0,
+             stream_k=-1, ws=None):
     lib = L()
     g = torch.Generator(device="cuda").manual_seed(seed)
     td = TDT[dtype]
@@ -46,7 +47,10 @@ def run_gemm(m, n, k, dtype, a_kmajor, b_kmajor, flags=0, seed=0, force_simt=Fal
     args = lib.GemmArgs(m=m, n=n, k=k, dtype=dtype, a=ptr(a_store), lda=a_store.shape[1], a_kmajor=int(a_kmajor),
                         b=ptr(b_store), ldb=b_store.shape[1], b_kmajor=int(b_kmajor), c=ptr(c), ldc=n,
                         bias=ptr(bias), res=ptr(res), ldr=n, mask=ptr(mask), ldm=n, flags=flags,
-                        force_simt=int(force_simt), pair=pair, tile_n=tile_n)
+                        force_simt=int(force_simt), pair=pair, tile_n=tile_n, stream_k=stream_k)
+    if ws is not None:
+        args.workspace, args.workspace_floats = ptr(ws[0]), ws[0].numel()
+        args.counters, args.n_counters = ptr(ws[1]), ws[1].numel()
     lib.check(lib.sfk_gemm(C.byref(args), stream()), kernel=True)
     torch.cuda.synchronize()
     acc = (A.double() @ B.double().t()).float()
@@ -418,3 +422,26 @@ def test_embedding_backward_chunked(dt, rows, d, vocab):
                                         ptr(t_order), d, ptr(dx), scale, ptr(scratch), ptr(c), stream()), True)
     torch.cuda.synchronize()
     assert torch.equal(b, c)  # deterministic
+
+
+def sk_workspace():
+    sms = L().sfk_num_sms()
+    return (torch.zeros(sms * 2 * 128 * 256, device="cuda"), torch.zeros(2 * sms, dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("layout", [(True, True), (True, False), (False, False)])
+@pytest.mark.parametrize("shape", [(1024, 1024, 3584), (3584, 1024, 1024), (3000, 4096, 1024), (200, 300, 640),
+                                   (3584, 3072, 1024), (130, 250, 4096)])
+@pytest.mark.parametrize("flags", [0, 7, 32])
+def test_gemm_stream_k(layout, shape, flags):
+    """Stream-K (k-loop of the last wave split across all SMs, parts summed
+    in k order by the last arriving CTA) against fp64; deterministic, and the
+    arrival counters are re-armed for the next launch."""
+    ws = sk_workspace()
+    m, n, k = shape
+    got, want = run_gemm(m, n, k, 1, *layout, flags=flags, seed=3, stream_k=1, ws=ws)
+    tol = 2e-3 * (k ** 0.5)
+    torch.testing.assert_close(got, want, rtol=4e-3, atol=tol)
+    assert int(ws[1].abs().sum()) == 0
+    again, _ = run_gemm(m, n, k, 1, *layout, flags=flags, seed=3, stream_k=1, ws=ws)
+    assert torch.equal(got, again)
