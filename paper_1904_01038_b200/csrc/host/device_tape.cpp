@@ -1,6 +1,7 @@
 #include "device_tape.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 namespace sqf {
@@ -253,7 +254,12 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   g.ldm = ldm;
   g.flags = flags;
   float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
-  if (ws && ctr_base_) {
+  static const int sk_mode = [] {
+    const char* v = std::getenv("SQF_GEMM_STREAM_K");  // 0 off (default), 1 auto, 2 force
+    return v ? std::atoi(v) : 0;
+  }();
+  if (ws && ctr_base_ && sk_mode > 0) {
+    g.stream_k = sk_mode > 1 ? 1 : 0;
     g.workspace = ws;
     g.workspace_floats = ws_floats_;
     g.n_counters = 2 * 148;

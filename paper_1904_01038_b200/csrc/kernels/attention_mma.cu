@@ -493,13 +493,13 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
 // per key warp -- with D = rowsum(dO * O) and the saved softmax stats kept in
 // shared memory. Same arithmetic, in the same order, as bwd_dq_k + bwd_dkv_k.
 template <typename T, int DH>
-__global__ void __launch_bounds__(kWarps * 32) bwd_small_k(Args a) {
+__global__ void __launch_bounds__(kWarps * 32, DH <= 64 ? 3 : 1) bwd_small_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
   constexpr int QP = 2 * kRows;  // staged query rows (zero-padded: dK/dV chunks run past qw)
-  constexpr int NC = DH >= 128 ? 32 : 64;
+  constexpr int NC = 32;  // query columns per dK/dV chunk (register budget: 3 CTAs per SM)
   const int b = blockIdx.z, h = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];

@@ -949,7 +949,7 @@ int num_sms_cached() {
 }
 
 template <int BN, bool A_MN, bool B_MN, typename T>
-int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, int sk_tiles) {
+int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, int sk_tiles, int sk_grid) {
   using C = Cfg<BN>;
   CUtensorMap ta, tb;
   // A: K-major [m][k] -> map cols=k rows=m, box rows 128; MN-major [k][m] -> cols=m rows=k, box 64x64
@@ -969,7 +969,7 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
     attr_set = true;
   }
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
-  const int grid = sk_tiles > 0 ? num_sms_cached() : (tiles < num_sms_cached() ? tiles : num_sms_cached());
+  const int grid = sk_tiles > 0 ? sk_grid : (tiles < num_sms_cached() ? tiles : num_sms_cached());
   Sk sk{sk_tiles > 0 ? g->workspace : nullptr, sk_tiles > 0 ? g->counters : nullptr, sk_tiles};
   launch_pdl(gemm_tc<BN, A_MN, B_MN, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, e, g->m, g->n, g->k,
              vec_ok ? 1 : 0, sk);
@@ -1036,31 +1036,36 @@ int pick_bn(int m, int n) {
   return best;
 }
 
-// Stream-K region size (in tiles) for a 128 x 256 1-CTA GEMM, 0 = plain
-// data-parallel. Cost model in k-block units: a tile costs kblocks + 4 (fill,
-// epilogue); a stream-K range costs its k-blocks + 4 per unit, plus storing
-// a partial (2) and the reducer reading ~2 per contributing CTA.
-int pick_stream_k(const sfk_gemm_args* g) {
+// Stream-K plan for a 128 x 256 1-CTA GEMM: returns the stream-K region size
+// in tiles (0 = plain data-parallel) and the grid through *grid. Measured on
+// B200, the fp32 partial tiles (128 KB each) make the fix-up expensive, so
+// auto mode only splits few-tile GEMMs (the long-k weight gradients whose
+// output is a handful of tiles), each tile over at most 3 CTAs; stream_k > 0
+// forces the general form (last wave + remainder split over all SMs).
+int pick_stream_k(const sfk_gemm_args* g, int* grid) {
   if (g->stream_k < 0 || !g->workspace || !g->counters) return 0;
   const int G = num_sms_cached();
   if (g->workspace_floats < int64_t(G) * 2 * BM * 256) return 0;
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + 255) / 256);
   const int kb = (g->k + BK - 1) / BK;
   if (kb < 4 || tiles % G == 0) return 0;
-  const int waves = (tiles + G - 1) / G;
-  const double dp = double(waves) * (kb + 4);
   const int sk_tiles = tiles < G ? tiles : tiles % G + G;
   if (sk_tiles > g->n_counters) return 0;
-  const double per = double(sk_tiles) * kb / G;
-  const double segs = std::ceil(double(G) / sk_tiles) + 1;
-  const double sk = double((tiles - sk_tiles) / G) * (kb + 4) + per + 8 + 2 + 2 * segs;
-  if (g->stream_k > 0) return sk_tiles;
-  return sk < 0.92 * dp ? sk_tiles : 0;
+  if (g->stream_k > 0) {
+    // every CTA gets at least one k-block
+    *grid = int(std::min<int64_t>(G, int64_t(sk_tiles) * kb));
+    if (tiles >= G) *grid = G;
+    return sk_tiles;
+  }
+  if (3 * tiles > G || kb < 16) return 0;
+  *grid = std::min(G, 3 * tiles);
+  return tiles;
 }
 
 template <typename T>
 int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
-  const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 ? pick_stream_k(g) : 0;
+  int sk_grid = 0;
+  const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 ? pick_stream_k(g, &sk_grid) : 0;
   const int bn = skt > 0 ? 256 : g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
   if (g->pair > 0) {
@@ -1077,10 +1082,10 @@ int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) 
   }
 #define SFK_TC(BNV)                                                         \
   switch (layout) {                                                         \
-    case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s, skt);      \
-    case 1: return launch<BNV, false, true, T>(g, e, vec_ok, s, skt);       \
-    case 3: return launch<BNV, true, true, T>(g, e, vec_ok, s, skt);        \
-    default: return launch<BNV, true, false, T>(g, e, vec_ok, s, skt);      \
+    case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s, skt, sk_grid);      \
+    case 1: return launch<BNV, false, true, T>(g, e, vec_ok, s, skt, sk_grid);       \
+    case 3: return launch<BNV, true, true, T>(g, e, vec_ok, s, skt, sk_grid);        \
+    default: return launch<BNV, true, false, T>(g, e, vec_ok, s, skt, sk_grid);      \
   }
   if (bn == 256) { SFK_TC(256) }
   if (bn == 128) { SFK_TC(128) }

@@ -430,8 +430,8 @@ def sk_workspace():
 
 
 @pytest.mark.parametrize("layout", [(True, True), (True, False), (False, False)])
-@pytest.mark.parametrize("shape", [(1024, 1024, 3584), (3584, 1024, 1024), (3000, 4096, 1024), (200, 300, 640),
-                                   (3584, 3072, 1024), (130, 250, 4096)])
+@pytest.mark.parametrize("shape", [(1024, 1024, 3584), (3584, 1024, 1024), (3000, 4096, 1024), (200, 296, 640),
+                                   (3584, 3072, 1024), (136, 248, 4096)])
 @pytest.mark.parametrize("flags", [0, 7, 32])
 def test_gemm_stream_k(layout, shape, flags):
     """Stream-K (k-loop of the last wave split across all SMs, parts summed
