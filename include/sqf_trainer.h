@@ -81,6 +81,21 @@ float sqf_trainer_last_step_ms(void* t);
 int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h);
 /* CUDA stream the trainer launches on (cudaStream_t) */
 void* sqf_trainer_stream(void* t);
+/* Checkpoints in the reference's SQFG v2 container (docs/checkpoint_format.md;
+ * save_checkpoint / load_checkpoint, checkpoint.cpp:187-389). save: atomic,
+ * canonical-order FP32 params and Adam moments, config with provenance,
+ * scaler and epoch cursor. load: restores all of it into a trainer built with
+ * the same architecture (manifest must match; IntegrityError otherwise);
+ * *version = the file's format version (v1 files are upgraded). */
+int sqf_trainer_save(void* t, const char* path);
+int sqf_trainer_load(void* t, const char* path, int32_t* version);
+/* Raw parse (read_checkpoint, checkpoint.cpp:226-320): header, table and
+ * FNV-1a checksums verified. info gives the sizes; read fills params[nparams],
+ * opt[nopt] and meta (sorted "key = value\n" lines, NUL-terminated). */
+int sqf_checkpoint_info(const char* path, int32_t* version, int64_t* nparams, int64_t* nopt,
+                        int64_t* meta_bytes);
+int sqf_checkpoint_read(const char* path, float* params, float* opt, char* meta, int64_t meta_cap);
+
 /* all-reduce/backward overlap of the last step (config overlap_allreduce; with
  * world 1 only under overlap_simulate): bucket indices in issue order (up to
  * cap written), *early = how many were issued while backward was running.

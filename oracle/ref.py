@@ -107,6 +107,9 @@ def _declare(L):
     s("sqfref_trainer_buckets", C.c_int, vp, P(i32), vp, vp)
     s("sqfref_trainer_subbatch_grad", C.c_int, vp, vp, vp, C.c_int, f32, vp, P(StatsC))
     s("sqfref_trainer_evaluate", C.c_int, vp, vp, P(f64), P(f64), P(i64), P(i64))
+    s("sqfref_trainer_save", C.c_int, vp, cp)
+    s("sqfref_checkpoint_read", C.c_int, cp, P(i32), P(i64), vp, P(i64), vp)
+    s("sqfref_checkpoint_meta", C.c_int, cp, cp, vp, C.c_int)
 
 
 class RefError(RuntimeError):
@@ -313,6 +316,24 @@ def _kv(overrides):
     return ka, va, len(keys)
 
 
+def checkpoint_read(path):
+    """The reference's read_checkpoint (checkpoint.cpp:226-320): (version, params, opt)."""
+    L = lib()
+    v, npar, nopt = C.c_int32(), C.c_int64(), C.c_int64()
+    p = str(path).encode()
+    _ck(L.sqfref_checkpoint_read(p, C.byref(v), C.byref(npar), None, C.byref(nopt), None))
+    params = np.zeros(npar.value, np.float32)
+    opt = np.zeros(max(1, nopt.value), np.float32)
+    _ck(L.sqfref_checkpoint_read(p, C.byref(v), C.byref(npar), _ptr(params), C.byref(nopt), _ptr(opt)))
+    return int(v.value), params, opt[:nopt.value]
+
+
+def checkpoint_meta(path, key):
+    buf = C.create_string_buffer(4096)
+    _ck(lib().sqfref_checkpoint_meta(str(path).encode(), key.encode(), buf, 4096))
+    return buf.value.decode()
+
+
 class RefTrainer:
     """The reference's own Trainer over an in-memory corpus (trainer.hpp:84-85)."""
 
@@ -391,6 +412,10 @@ class RefTrainer:
         st = StatsC()
         _ck(lib().sqfref_trainer_subbatch_grad(self.h, self.corpus.h, _ptr(m), len(m), seed, _ptr(g), C.byref(st)))
         return g, st.as_dict()
+
+    def save(self, path):
+        """The reference's save_checkpoint (checkpoint.cpp:187-224)."""
+        _ck(lib().sqfref_trainer_save(self.h, str(path).encode()))
 
     def evaluate(self, corpus):
         rc = RefCorpus(corpus)

@@ -14,6 +14,7 @@
 #include <string>
 #include <vector>
 
+#include "seqforge/checkpoint.hpp"
 #include "seqforge/common.hpp"
 #include "seqforge/criterions.hpp"
 #include "seqforge/data.hpp"
@@ -568,6 +569,32 @@ int sqfref_trainer_evaluate(void* h, void* corpus, double* loss, double* nll, in
     *nll = e.nll;
     *ntokens = e.ntokens;
     *ncorrect = e.ncorrect;
+  })
+}
+
+// ---------------------------------------------------------------- checkpoints
+// the reference's own writer (checkpoint.cpp:187-224) and raw reader (226-320)
+int sqfref_trainer_save(void* h, const char* path) {
+  GUARD(save_checkpoint(*static_cast<TrainerBox*>(h)->tr, path))
+}
+int sqfref_checkpoint_read(const char* path, int32_t* version, int64_t* nparams, float* params, int64_t* nopt,
+                           float* opt) {
+  GUARD({
+    RawCheckpoint raw = read_checkpoint(path);
+    *version = raw.version;
+    *nparams = int64_t(raw.params.size());
+    *nopt = int64_t(raw.opt.size());
+    if (params) std::memcpy(params, raw.params.data(), raw.params.size() * 4);
+    if (opt) std::memcpy(opt, raw.opt.data(), raw.opt.size() * 4);
+  })
+}
+int sqfref_checkpoint_meta(const char* path, const char* key, char* out, int cap) {
+  GUARD({
+    RawCheckpoint raw = read_checkpoint(path);
+    auto it = raw.meta.find(key);
+    if (it == raw.meta.end()) throw IntegrityError(std::string("no key ") + key);
+    if (int(it->second.size()) + 1 > cap) throw BoundsError("buffer");
+    std::memcpy(out, it->second.c_str(), it->second.size() + 1);
   })
 }
 

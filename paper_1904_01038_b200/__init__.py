@@ -9,6 +9,7 @@ sm_100a kernels; nothing here computes.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -164,6 +165,19 @@ def quantize_fp16(x: float) -> float:
     return float(L.sqf_quantize_fp16(x))
 
 
+def read_checkpoint(path):
+    """Raw parse of an SQFG checkpoint: (version, meta dict, params, opt)."""
+    v, npar, nopt, mb = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+    p = os.fspath(path).encode()
+    L.check(L.sqf_checkpoint_info(p, C.byref(v), C.byref(npar), C.byref(nopt), C.byref(mb)))
+    params = np.zeros(npar.value, np.float32)
+    opt = np.zeros(max(1, nopt.value), np.float32)
+    meta = C.create_string_buffer(mb.value)
+    L.check(L.sqf_checkpoint_read(p, _ptr(params), _ptr(opt), meta, mb.value))
+    kv = dict(line.split(" = ", 1) for line in meta.value.decode().splitlines() if line)
+    return int(v.value), kv, params, opt[:nopt.value]
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_char * 128)()
     L.check(L.sqf_nccl_unique_id(buf))
@@ -302,6 +316,16 @@ class Trainer:
         d2h = C.c_int64()
         h2d = L.sqf_trainer_last_io_bytes(self._h, C.byref(d2h))
         return int(h2d), int(d2h.value)
+
+    def save(self, path: str):
+        """Checkpoint (SQFG v2, the reference's container) of the full training state."""
+        L.check(L.sqf_trainer_save(self._h, os.fspath(path).encode()))
+
+    def load(self, path: str) -> int:
+        """Restore a checkpoint (ours or the reference's) into this trainer; returns the file version."""
+        v = C.c_int32()
+        L.check(L.sqf_trainer_load(self._h, os.fspath(path).encode(), C.byref(v)))
+        return int(v.value)
 
     def overlap_log(self):
         """(bucket issue order, number issued while backward was running) of the last step."""

@@ -6,6 +6,7 @@
 
 #include "../../../include/sqf_trainer.h"
 #include "nccl_dyn.hpp"
+#include "checkpoint.hpp"
 #include "trainer.hpp"
 
 namespace sqf {
@@ -263,6 +264,41 @@ int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h) {
   return T(t)->last_h2d_bytes();
 }
 void* sqf_trainer_stream(void* t) { return static_cast<void*>(T(t)->stream()); }
+
+int sqf_trainer_save(void* t, const char* path) { SQF_GUARD(save_checkpoint(*T(t), path)) }
+
+int sqf_trainer_load(void* t, const char* path, int32_t* version) {
+  SQF_GUARD({
+    const int v = load_checkpoint_into(*T(t), path);
+    if (version) *version = v;
+  })
+}
+
+int sqf_checkpoint_info(const char* path, int32_t* version, int64_t* nparams, int64_t* nopt, int64_t* meta_bytes) {
+  SQF_GUARD({
+    const RawCheckpoint raw = read_checkpoint(path);
+    int64_t mb = 0;
+    for (const auto& [k, v] : raw.meta) mb += int64_t(k.size() + v.size() + 4);
+    *version = raw.version;
+    *nparams = int64_t(raw.params.size());
+    *nopt = int64_t(raw.opt.size());
+    *meta_bytes = mb + 1;
+  })
+}
+
+int sqf_checkpoint_read(const char* path, float* params, float* opt, char* meta, int64_t meta_cap) {
+  SQF_GUARD({
+    const RawCheckpoint raw = read_checkpoint(path);
+    if (params) std::memcpy(params, raw.params.data(), raw.params.size() * 4);
+    if (opt) std::memcpy(opt, raw.opt.data(), raw.opt.size() * 4);
+    if (meta) {
+      std::string text;
+      for (const auto& [k, v] : raw.meta) text += k + " = " + v + "\n";
+      if (int64_t(text.size()) + 1 > meta_cap) throw BoundsError("sqf_checkpoint_read: meta buffer too small");
+      std::memcpy(meta, text.c_str(), text.size() + 1);
+    }
+  })
+}
 
 int sqf_trainer_overlap_log(void* t, int32_t* order, int cap, int32_t* early) {
   const std::vector<int>& log = T(t)->overlap_log();
