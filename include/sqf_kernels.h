@@ -113,6 +113,18 @@ int sfk_embed_bwd_chunked(int dtype, const int32_t* chunks, int nchunks, const i
                           int nmulti, const int32_t* seg_rows, int d, const void* dx, float scale,
                           float* scratch, void* grad_table, void* stream);
 
+/* ------------------------------------------------------ dropout (a15)
+ * Tape::dropout (tape.cpp:109-121, 223-228, 419-425) with the mask stream of
+ * model.cpp:156-163: element i keeps factor float(1/(1-p)) unless
+ * RngStream(seed, stream_id) draw number i is < p; the mask is recomputed
+ * from the counter-based RNG (rng.cpp:10-31), never stored.
+ * fwd: out = q(res + q(x*m)), or q(x*m) when res == NULL;
+ * bwd: dx = q(g*m), or q(dx + g*m) when accumulate. */
+int sfk_dropout_fwd(int dtype, const void* x, const void* res, void* out, int64_t n, float p,
+                    uint64_t seed, uint64_t stream_id, void* stream);
+int sfk_dropout_bwd(int dtype, const void* g, void* dx, int64_t n, float p, uint64_t seed,
+                    uint64_t stream_id, int accumulate, void* stream);
+
 /* ------------------------------------------------------ layer norm (a14)
  * kernels.cpp:30-45 / tape.cpp:211-222: two-pass mean/biased var,
  * rstd = 1/sqrt(var + 1e-5); y = q((x-mean)*rstd*g + b); stats[r] = {mean, rstd}.

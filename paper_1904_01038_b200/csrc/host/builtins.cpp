@@ -47,7 +47,6 @@ class TransformerModel : public ModelBase {
     if (ffn_ <= 0) throw ConfigError("transformer: d_ffn must be positive");
     if (dropout_ < 0.0f || dropout_ >= 1.0f) throw ConfigError("transformer: dropout must be in [0, 1)");
     if (max_pos_ < 2) throw ConfigError("transformer: max_positions must be at least 2");
-    if (dropout_ > 0.0f) throw ConfigError("transformer: dropout > 0 is not implemented on the B200 path yet");
     build_layout();
     init_params();
   }
@@ -76,8 +75,9 @@ class TransformerModel : public ModelBase {
       throw CapacityError("transformer: target length " + std::to_string(b.tgt_width) + " exceeds max_positions " +
                           std::to_string(max_pos_));
     if (!pe_dev_) throw ConfigError("transformer: position table not uploaded");
-    const int enc = encode(tape, b);
-    return decode(tape, b, enc);
+    int site = 0;  // model.cpp:277-281: one site counter across encoder and decoder
+    const int enc = encode(tape, b, site);
+    return decode(tape, b, enc, site);
   }
 
  private:
@@ -250,41 +250,57 @@ class TransformerModel : public ModelBase {
   }
 
   // model.cpp:199-227
-  int encode(DeviceTape& t, const DeviceBatch& b) const {
+  // model.cpp:156-163: dropout site n of the step draws from stream
+  // kStreamDropoutBase | (train_step << 8) | n; sites count in recording order
+  int maybe_dropout(DeviceTape& t, int x, int& site, int residual = -1) const {
+    if (dropout_ <= 0.0f) return x;
+    const uint64_t stream = (uint64_t(1) << 32) | (uint64_t(train_step_) << 8) | uint64_t(site++);
+    return t.dropout(x, dropout_, seed_, stream, residual);
+  }
+  // x + dropout(linear(in)): the residual add rides in the GEMM epilogue when
+  // there is no dropout, else in the dropout kernel (model.cpp:218-224)
+  int residual(DeviceTape& t, int in, const ParamRef& w, const ParamRef* b, bool relu, int x, int& site) const {
+    if (dropout_ <= 0.0f) return t.linear(in, w, b, relu, x);
+    return maybe_dropout(t, t.linear(in, w, b, relu), site, x);
+  }
+
+  int encode(DeviceTape& t, const DeviceBatch& b, int& site) const {
     const int B = b.rows, S = b.src_width;
     int x = t.embedding(src_embed_, b.source, B * S, S, std::sqrt(float(d_)), pe_dev_, b.src_segs);
+    x = maybe_dropout(t, x, site);
     for (const Layer& l : enc_) {
       const int z = t.layer_norm(x, l.ln1g, l.ln1b);
       const ParamRef bqkv = l.self.bqkv();
       const int qkv = t.linear(z, l.self.wqkv(), &bqkv, false);
       const int a = t.attention(qkv, 0, qkv, d_, 2 * d_, d_, heads_, B, S, S, false, b.src_lens);
-      x = t.linear(a, l.self.wo, &l.self.bo, false, x);
+      x = residual(t, a, l.self.wo, &l.self.bo, false, x, site);
       const int z2 = t.layer_norm(x, l.ln2g, l.ln2b);
       const int h = t.linear(z2, l.w1, &l.b1, true);
-      x = t.linear(h, l.w2, &l.b2, false, x);
+      x = residual(t, h, l.w2, &l.b2, false, x, site);
     }
     return t.layer_norm(x, enc_lng_, enc_lnb_);
   }
 
   // model.cpp:229-275
-  int decode(DeviceTape& t, const DeviceBatch& b, int enc) const {
+  int decode(DeviceTape& t, const DeviceBatch& b, int enc, int& site) const {
     const int B = b.rows, T = b.tgt_width, S = b.src_width;
     int x = t.embedding(tgt_embed_, b.target_in, B * T, T, std::sqrt(float(d_)), pe_dev_, b.tgt_segs);
+    x = maybe_dropout(t, x, site);
     for (const Layer& l : dec_) {
       const int z = t.layer_norm(x, l.ln1g, l.ln1b);
       const ParamRef bqkv = l.self.bqkv();
       const int qkv = t.linear(z, l.self.wqkv(), &bqkv, false);
       const int a = t.attention(qkv, 0, qkv, d_, 2 * d_, d_, heads_, B, T, T, true, nullptr);
-      x = t.linear(a, l.self.wo, &l.self.bo, false, x);
+      x = residual(t, a, l.self.wo, &l.self.bo, false, x, site);
       const int z2 = t.layer_norm(x, l.ln2g, l.ln2b);
       const int cq = t.linear(z2, l.cross.wq, &l.cross.bq, false);
       const ParamRef bkv = l.cross.bkv();
       const int ckv = t.linear(enc, l.cross.wkv(), &bkv, false);
       const int ca = t.attention(cq, 0, ckv, 0, d_, d_, heads_, B, T, S, false, b.src_lens);
-      x = t.linear(ca, l.cross.wo, &l.cross.bo, false, x);
+      x = residual(t, ca, l.cross.wo, &l.cross.bo, false, x, site);
       const int z3 = t.layer_norm(x, l.ln3g, l.ln3b);
       const int h = t.linear(z3, l.w1, &l.b1, true);
-      x = t.linear(h, l.w2, &l.b2, false, x);
+      x = residual(t, h, l.w2, &l.b2, false, x, site);
     }
     x = t.layer_norm(x, dec_lng_, dec_lnb_);
     return t.linear(x, out_proj_, nullptr, false);

@@ -6,6 +6,17 @@
 
 namespace sqf {
 
+// Timing experiments only (results are wrong when set): SQF_DEBUG_SKIP is a
+// bit mask of launch classes the tape does not enqueue -- 1 bias grads,
+// 2 LN gamma/beta, 4 wgrad GEMMs, 8 attention backward.
+static int debug_skip() {
+  static const int m = [] {
+    const char* v = std::getenv("SQF_DEBUG_SKIP");
+    return v ? std::atoi(v) : 0;
+  }();
+  return m;
+}
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -370,6 +381,31 @@ int DeviceTape::softmax_xent(int logits, const int32_t* gold, float epsilon) {
   return int(nodes_.size()) - 1;
 }
 
+int DeviceTape::dropout(int x, float p, uint64_t seed, uint64_t stream, int residual) {
+  const Node& in = nodes_[x];
+  if (residual >= 0 && (nodes_[residual].rows != in.rows || nodes_[residual].cols != in.cols))
+    throw ShapeError("add: shape mismatch");
+  Node n;
+  n.kind = Kind::Dropout;
+  n.in0 = x;
+  n.in1 = residual;
+  n.p = p;
+  n.seed = seed;
+  n.rng_stream = stream;
+  n.rows = in.rows;
+  n.cols = in.cols;
+  n.out = alloc_elems(int64_t(n.rows) * n.cols);
+  const int64_t cnt = int64_t(n.rows) * n.cols;
+  pbegin();
+  sfk_check(sfk_dropout_fwd(dtype_, in.out, residual >= 0 ? nodes_[residual].out : nullptr, n.out, cnt, p, seed, stream,
+                            cur_),
+            "dropout_fwd");
+  pend(Profiler::LayerNorm, 0, double(cnt) * esize_ * (residual >= 0 ? 3.0 : 2.0));
+  ++launches_;
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
 std::pair<void*, bool> DeviceTape::grad_of(int id) {
   Node& n = nodes_[id];
   if (n.grad) return {n.grad, false};
@@ -428,6 +464,7 @@ void DeviceTape::join_side() {
 }
 
 void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out) {
+  if (debug_skip() & 1) return;
   // sfk_colsum scratch: min(512 * cols, 4M) floats
   const size_t part_floats = std::min<size_t>(size_t(512) * cols, size_t(4) << 20);
   float* part = static_cast<float*>(arena_.alloc(part_floats * 4));
@@ -496,7 +533,7 @@ void DeviceTape::backward_node(int id) {
           cur_ = side_;
         }
         pbegin();
-        sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
+        if (!(debug_skip() & 2)) sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
                                            counters((n.cols + 255) / 256), gptr(n.p0), gptr(n.p1), cur_),
                   "layernorm_bwd_params");
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
@@ -548,8 +585,9 @@ void DeviceTape::backward_node(int id) {
         bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
         grad_done(n.p1);
       }
-      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
-           n.p0.cols, SFK_EPI_ACCUM);
+      if (!(debug_skip() & 4))
+        gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
+             n.p0.cols, SFK_EPI_ACCUM);
       grad_done(n.p0);
       if (side_) {
         cudaEvent_t done = event();
@@ -572,6 +610,22 @@ void DeviceTape::backward_node(int id) {
       if (!fresh) wait_side_reader(dx);
       gemm(Profiler::GemmDgrad, n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols,
            flags, nullptr, nullptr, 0, mask, in.cols);
+      return;
+    }
+    case Kind::Dropout: {
+      void* dy = n.grad;
+      if (n.in1 >= 0) {  // the fused residual add passes dy through unchanged
+        Node& r = nodes_[n.in1];
+        if (r.grad) throw ShapeError("dropout: residual input already has a gradient (unsupported fan-out)");
+        r.grad = dy;
+      }
+      auto [dx, fresh] = grad_of(n.in0);
+      if (!fresh) wait_side_reader(dx);
+      const int64_t cnt = int64_t(n.rows) * n.cols;
+      pbegin();
+      sfk_check(sfk_dropout_bwd(dtype_, dy, dx, cnt, n.p, n.seed, n.rng_stream, fresh ? 0 : 1, cur_), "dropout_bwd");
+      pend(Profiler::LayerNorm, 0, double(cnt) * esize_ * (fresh ? 2.0 : 3.0));
+      ++launches_;
       return;
     }
     case Kind::Attention: {
@@ -608,7 +662,7 @@ void DeviceTape::backward_node(int id) {
       a.lddv = kn.cols;
       a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
       pbegin();
-      sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
+      if (!(debug_skip() & 8)) sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
       pend(Profiler::AttnBwd, attn_flops(n.batch, n.q_width, n.k_width, n.k_len, n.cols, n.causal, true),
            double(esize_) * n.cols * (4.0 * n.rows + 4.0 * kn.rows));
       launches_ += 2;

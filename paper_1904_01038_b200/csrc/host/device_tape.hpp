@@ -114,7 +114,7 @@ struct DeviceParams {
 
 class DeviceTape {
  public:
-  enum class Kind { Embedding, LayerNorm, Linear, Attention, Xent };
+  enum class Kind { Embedding, LayerNorm, Linear, Attention, Xent, Dropout };
 
   DeviceTape(Arena& arena, const DeviceParams& params, int dtype, cudaStream_t stream);
 
@@ -130,6 +130,9 @@ class DeviceTape {
                 int k_width, bool causal, const int32_t* k_len);
   // a18: records the loss node; stats are produced when backward()/finish() runs
   int softmax_xent(int logits, const int32_t* gold, float epsilon);
+  // Tape::dropout (tape.cpp:109-121) with the mask drawn from RngStream(seed,
+  // stream); residual >= 0 fuses the following Tape::add: out = q(res + q(x*m))
+  int dropout(int x, float p, uint64_t seed, uint64_t stream, int residual = -1);
 
   // Seeds d(loss_row) = seed on active rows (tape.cpp:506-516), runs the fused
   // xent fwd+bwd and sweeps nodes in exact reverse order.
@@ -197,6 +200,9 @@ class DeviceTape {
     // xent
     const int32_t* gold = nullptr;
     float eps = 0.f;
+    // dropout
+    float p = 0.f;
+    uint64_t seed = 0, rng_stream = 0;
     float* row_out = nullptr;
   };
 
