@@ -81,6 +81,11 @@ typedef struct sfk_gemm_args {
   float* workspace; int64_t workspace_floats;
   int32_t* counters; int n_counters;
   int stream_k;                   /* 0 = auto, -1 = off, 1 = force when possible */
+  /* weight-gradient layout only (a_kmajor = 0, 16-bit): also accumulate the
+   * bias gradient of the layer, bias_grad[i] = q(bias_grad[i] + sum_k A(i,k))
+   * (add_bias backward, tape.cpp:347-358), summed from the A tiles already in
+   * shared memory by the epilogue warps -- no second pass over dY. */
+  void* bias_grad;
 } sfk_gemm_args;
 
 int sfk_gemm(const sfk_gemm_args* g, void* stream);

@@ -244,7 +244,7 @@ int DeviceTape::layer_norm(int x, ParamRef gamma, ParamRef beta) {
 
 void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b,
                       int64_t ldb, bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias, const void* res,
-                      int64_t ldr, const void* mask, int64_t ldm) {
+                      int64_t ldr, const void* mask, int64_t ldm, void* bias_grad) {
   sfk_gemm_args g{};
   g.m = m;
   g.n = n;
@@ -264,6 +264,7 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   g.mask = mask;
   g.ldm = ldm;
   g.flags = flags;
+  g.bias_grad = bias_grad;
   float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
   static const int sk_mode = [] {
     const char* v = std::getenv("SQF_GEMM_STREAM_K");  // 0 off (default), 1 auto, 2 force
@@ -581,13 +582,14 @@ void DeviceTape::backward_node(int id) {
         cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
         cur_ = side_;
       }
-      if (n.has_bias) {
-        bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
-        grad_done(n.p1);
-      }
+      // 16-bit: the bias gradient rides in the weight-gradient GEMM (its
+      // epilogue warps sum dY out of the A tiles in shared memory)
+      const bool fused_db = n.has_bias && dtype_ != SFK_F32 && !(debug_skip() & 16);
+      if (n.has_bias && !fused_db) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
       if (!(debug_skip() & 4))
         gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
-             n.p0.cols, SFK_EPI_ACCUM);
+             n.p0.cols, SFK_EPI_ACCUM, nullptr, nullptr, 0, nullptr, 0, fused_db ? gptr(n.p1) : nullptr);
+      if (n.has_bias) grad_done(n.p1);
       grad_done(n.p0);
       if (side_) {
         cudaEvent_t done = event();

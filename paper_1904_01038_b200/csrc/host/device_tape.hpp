@@ -256,7 +256,7 @@ class DeviceTape {
   void run_xent(Node& n, float seed, bool with_grad, double* stats_acc);
   void gemm(int cat, int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
             bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias = nullptr, const void* res = nullptr,
-            int64_t ldr = 0, const void* mask = nullptr, int64_t ldm = 0);
+            int64_t ldr = 0, const void* mask = nullptr, int64_t ldm = 0, void* bias_grad = nullptr);
   void bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out);
 };
 

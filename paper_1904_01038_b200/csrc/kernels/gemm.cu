@@ -437,6 +437,7 @@ struct Sk {
   float* ws;          // [G][2][BM*BN] fp32 partial tiles (slot 0: a CTA's first unit, 1: its last)
   int32_t* flags;     // [sk_tiles] arrival counters, zero on entry, re-armed by the reducer
   int sk_tiles;
+  void* bias_grad;    // weight-gradient GEMMs (A = dY, MN-major): db[m] = q(db[m] + sum_k A(m,k)), or null
 };
 
 struct Sched {
@@ -549,6 +550,49 @@ __device__ __forceinline__ void reduce_partials(const Epi& e, const Sched& sc, c
   }
 }
 
+// Bias gradient fused into the weight-gradient GEMM (add_bias backward,
+// tape.cpp:347-358): while the tensor pipe consumes a k-block of A = dY
+// (MN-major, two 64 m x 64 k SW128 boxes per stage), the otherwise idle
+// epilogue warps sum its columns out of shared memory: thread t owns the
+// m pair 2*(t%64), 2*(t%64)+1 (one 32-bit word per swizzled row) and k rows
+// 16*(t/64) .. +15. The four k-quarter sums meet in shared memory in a fixed
+// order; db[m] = q(db[m] + sum). Only the tiles with n0 == 0 do this, so every
+// db element has exactly one writer.
+template <typename T, int STAGES, int STAGE>
+__device__ __forceinline__ void bias_grad_tile(uint8_t* smem, uint64_t* full, uint64_t* bsum, int it0, int nkb,
+                                               int warp, int lane, float* stg, T* db, int m0, int M) {
+  const int t = (warp - 2) * 32 + lane;
+  const int mp = t & 63, kq = t >> 6;
+  const int ml = 2 * mp, box = ml >> 6, ch = (ml & 63) >> 3, el = ml & 7;
+  float s0 = 0.f, s1 = 0.f;
+  for (int i = 0; i < nkb; ++i) {
+    const int it = it0 + i, s = it % STAGES;
+    mbar_wait(&full[s], (it / STAGES) & 1);
+    const uint8_t* a = smem + s * STAGE + box * 8192;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int k = kq * 16 + j;
+      const uint32_t w = *reinterpret_cast<const uint32_t*>(a + k * 128 + ((ch ^ (k & 7)) << 4) + el * 2);
+      const float2 f = Pack<T>::unpack(w);
+      s0 += f.x;
+      s1 += f.y;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bsum[s]);
+  }
+  // combine the k quarters in order through the (idle) staging area
+  float* red = stg - (warp - 2) * kStgFloats;  // base of all epilogue staging
+  epi_bar();
+  red[kq * 128 + ml] = s0;
+  red[kq * 128 + ml + 1] = s1;
+  epi_bar();
+  if (t < 128 && m0 + t < M) {
+    const float sum = ((red[t] + red[128 + t]) + red[256 + t]) + red[384 + t];
+    Num<T>::st(db + m0 + t, Num<T>::ld(db + m0 + t) + sum);
+  }
+  epi_bar();
+}
+
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
@@ -570,13 +614,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bsum = tempty + 2;  // per stage: the epilogue warps finished their bias-gradient read
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bsum + C::STAGES);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&bsum[s], kEpiWarps);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -606,12 +652,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       Sched sc(tiles, kblocks, sk.sk_tiles);
       int it = 0, tile, kb0, kb1;
+      uint32_t bias_pend = 0, bias_ph = 0;  // per stage: a bias-tile read outstanding / its bsum phase
       while (sc.next(tile, kb0, kb1)) {
         const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+        const bool btile = A_MN && sk.bias_grad && n0 == 0;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
+          if (bias_pend >> s & 1) {
+            mbar_wait(&bsum[s], bias_ph >> s & 1);
+            bias_ph ^= 1u << s;
+            bias_pend &= ~(1u << s);
+          }
+          if (btile) bias_pend |= 1u << s;
           mbar_expect_tx(&full[s], C::STAGE);
           uint8_t* a_dst = smem + s * C::STAGE;
           uint8_t* b_dst = a_dst + C::A_BYTES;
@@ -671,10 +725,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
     volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
     Sched sc(tiles, kblocks, sk.sk_tiles);
-    int t = 0, tile, kb0, kb1;
+    int t = 0, it = 0, tile, kb0, kb1;
     while (sc.next(tile, kb0, kb1)) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+      if (A_MN && sk.bias_grad && n0 == 0) {
+        bias_grad_tile<T, C::STAGES, C::STAGE>(smem, full, bsum, it, kb1 - kb0, warp, lane, stg,
+                                               static_cast<T*>(sk.bias_grad), m0, M);
+      }
+      it += kb1 - kb0;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
       if (kb0 == 0 && kb1 == kblocks) {
@@ -970,7 +1029,7 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
   }
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
   const int grid = sk_tiles > 0 ? sk_grid : (tiles < num_sms_cached() ? tiles : num_sms_cached());
-  Sk sk{sk_tiles > 0 ? g->workspace : nullptr, sk_tiles > 0 ? g->counters : nullptr, sk_tiles};
+  Sk sk{sk_tiles > 0 ? g->workspace : nullptr, sk_tiles > 0 ? g->counters : nullptr, sk_tiles, g->bias_grad};
   launch_pdl(gemm_tc<BN, A_MN, B_MN, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, e, g->m, g->n, g->k,
              vec_ok ? 1 : 0, sk);
   return check_launch("sfk_gemm(tcgen05)");
@@ -1065,10 +1124,10 @@ int pick_stream_k(const sfk_gemm_args* g, int* grid) {
 template <typename T>
 int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   int sk_grid = 0;
-  const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 ? pick_stream_k(g, &sk_grid) : 0;
+  const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 && !g->bias_grad ? pick_stream_k(g, &sk_grid) : 0;
   const int bn = skt > 0 ? 256 : g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
-  if (g->pair > 0) {
+  if (g->pair > 0 && !g->bias_grad) {
 #define SFK_TC2(BNV)                                                    \
   switch (layout) {                                                     \
     case 0: return launch2<BNV, false, false, T>(g, e, vec_ok, s);      \
@@ -1112,6 +1171,14 @@ extern "C" int sfk_gemm(const sfk_gemm_args* g, void* stream) {
   cudaStream_t s = as_stream(stream);
   if (g->k == 0) {
     set_error("sfk_gemm: k == 0");
+    return SFK_EINVAL;
+  }
+  if (g->bias_grad && (g->a_kmajor || g->dtype == SFK_F32 || g->force_simt)) {
+    set_error("sfk_gemm: bias_grad needs the tensor-core path with an MN-major A (weight-gradient layout)");
+    return SFK_EINVAL;
+  }
+  if (g->bias_grad && (reinterpret_cast<uintptr_t>(g->bias_grad) & 3)) {
+    set_error("sfk_gemm: bias_grad must be 4-byte aligned");
     return SFK_EINVAL;
   }
   if (g->dtype == SFK_F32 || g->force_simt) {

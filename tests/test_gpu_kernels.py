@@ -445,3 +445,35 @@ def test_gemm_stream_k(layout, shape, flags):
     assert int(ws[1].abs().sum()) == 0
     again, _ = run_gemm(m, n, k, 1, *layout, flags=flags, seed=3, stream_k=1, ws=ws)
     assert torch.equal(got, again)
+
+
+@pytest.mark.parametrize("dtype", [1, 2])
+@pytest.mark.parametrize("shape", [(1024, 1024, 3584), (3072, 1024, 3000), (200, 296, 640), (4096, 1024, 37),
+                                   (1024, 4096, 2048)])
+def test_gemm_fused_bias_grad(dtype, shape):
+    """Weight-gradient GEMM with the bias gradient fused (add_bias backward,
+    tape.cpp:347-358): dW = q(dW + dY^T X) as before and db = q(db + sum_rows dY)
+    from the same A tiles; fp64 reference, deterministic."""
+    lib = L()
+    m, n, k = shape  # m = out features, n = in features, k = rows
+    g = torch.Generator(device="cuda").manual_seed(m + k)
+    td = TDT[dtype]
+    dy = (torch.randn(k, m, device="cuda", generator=g) * 0.5).to(td)   # A(i,kk) = dy[kk, i]: MN-major
+    x = (torch.randn(k, n, device="cuda", generator=g) * 0.5).to(td)    # B(j,kk) = x[kk, j]: MN-major
+    dw0 = torch.randn(m, n, device="cuda", generator=g).to(td)
+    db0 = torch.randn(m, device="cuda", generator=g).to(td)
+    outs = []
+    for _ in range(2):
+        dw, db = dw0.clone(), db0.clone()
+        args = lib.GemmArgs(m=m, n=n, k=k, dtype=dtype, a=ptr(dy), lda=m, a_kmajor=0, b=ptr(x), ldb=n, b_kmajor=0,
+                            c=ptr(dw), ldc=n, flags=lib.EPI_ACCUM, stream_k=-1, bias_grad=ptr(db))
+        lib.check(lib.sfk_gemm(C.byref(args), stream()), kernel=True)
+        torch.cuda.synchronize()
+        outs.append((dw, db))
+    q = lambda v: v.to(td).double()  # noqa: E731
+    want_w = q(dw0.double() + dy.double().t() @ x.double())
+    want_b = q(db0.double() + dy.double().sum(0))
+    tol = (4e-3 if dtype == 1 else 2e-2)
+    torch.testing.assert_close(outs[0][0].double(), want_w, rtol=tol, atol=tol * k ** 0.5)
+    torch.testing.assert_close(outs[0][1].double(), want_b, rtol=tol, atol=tol * k ** 0.5)
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])

@@ -155,3 +155,22 @@ def test_allreduce_overlap_schedule():
         assert off.overlap_log()[0] == []
         assert a == b
     assert np.array_equal(on.params(), off.params())
+
+
+@pytest.mark.parametrize("fp16", [False, True])
+def test_dropout_matches_reference(fp16):
+    """Dropout p = 0.1 (Tape::dropout tape.cpp:109-121, sites model.cpp:156-163):
+    the B200 masks come from the same counter-based RNG streams as the
+    reference's, so fp32 training stays within 1e-4 and fp16 within 1e-2."""
+    ov = {"max_tokens": 1024, "dropout": 0.1, "fp16": fp16}
+    mine, theirs, _ = pair("transformer_base_defaults", ov)
+    tol = 1e-2 if fp16 else 1e-4
+    for _ in range(4):
+        a, b = mine.train_one(), theirs.train_one()
+        assert a["ntokens"] == b["ntokens"] and a["skipped"] == b["skipped"]
+        assert abs(a["loss"] - b["loss"]) <= tol * abs(b["loss"])
+    if not fp16:
+        assert rel(mine.params(), theirs.params()) < 1e-4
+    # dropout is really on: the same model without it gives a different loss
+    nodrop, _, _ = pair("transformer_base_defaults", dict(ov, dropout=0.0))
+    assert abs(nodrop.train_one()["loss"] - pair("transformer_base_defaults", ov)[0].train_one()["loss"]) > 1e-6
