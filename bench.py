@@ -276,12 +276,18 @@ def run_ours(args, cfg):
     g_ms = sum(x[0] for x in gemm)
     g_fl = sum(x[1] for x in gemm)
     g_n = sum(x[3] for x in gemm)
+    g_by = sum(x[2] for x in gemm)
     tot_ms = sum(x[0] for x in prof.values())
     achieved = g_fl / (g_ms * 1e-3) / 1e12 if g_ms > 0 else 0.0
     peak = pk["bf16_tflops_sustained"]
     value = tokens / (dev_ms_max * 1e-3)
     e2e = tokens / (e2e_ms_max * 1e-3)
     mfu = value / world * cfg["flops_per_tok"] / 1e12 / pk["bf16_tflops"]
+    traffic = None
+    try:  # DRAM bytes per GEMM launch from the committed ncu --set full capture
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))["dram_bytes_per_launch"]
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": "tgt_tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
@@ -297,7 +303,8 @@ def run_ours(args, cfg):
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (fwd/dgrad/wgrad, fused epilogues)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                      "peak_source": f"{pk['source']} bf16_tflops_sustained (kernel timed inside the step)",
-                     "traffic": None, "gemm_share_of_step": g_ms / tot_ms if tot_ms else None,
+                     "traffic": traffic, "traffic_unit": "DRAM bytes per GEMM launch (ncu --set full capture)",
+                     "algorithmic_bytes_per_launch": g_by / g_n if g_n else None, "gemm_share_of_step": g_ms / tot_ms if tot_ms else None,
                      "gemm_launches_per_step": g_n},
         "model_flops_util": mfu,
         "profile_ms_per_step": {k: round(v[0], 3) for k, v in prof.items()},

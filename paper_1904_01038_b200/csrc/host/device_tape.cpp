@@ -9,6 +9,15 @@ namespace sqf {
 // Timing experiments only (results are wrong when set): SQF_DEBUG_SKIP is a
 // bit mask of launch classes the tape does not enqueue -- 1 bias grads,
 // 2 LN gamma/beta, 4 wgrad GEMMs, 8 attention backward.
+// SQF_WGRAD_TILE=0 restores the wave-efficiency tile choice for the side-stream GEMMs
+static int tile_env() {
+  static const int v = [] {
+    const char* e = std::getenv("SQF_WGRAD_TILE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 static int debug_skip() {
   static const int m = [] {
     const char* v = std::getenv("SQF_DEBUG_SKIP");
@@ -265,6 +274,10 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   g.ldm = ldm;
   g.flags = flags;
   g.bias_grad = bias_grad;
+  // parameter-gradient GEMMs run on the side stream, concurrently with the
+  // activation-gradient chain: what counts there is work per SM-cycle, not
+  // latency, so they always take the widest (most operand-efficient) tile
+  if (cat == Profiler::GemmWgrad && cur_ == side_ && side_ && tile_env() != 0) g.tile_n = 256;
   float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
   static const int sk_mode = [] {
     const char* v = std::getenv("SQF_GEMM_STREAM_K");  // 0 off (default), 1 auto, 2 force

@@ -211,6 +211,60 @@ std::optional<MiniBatch> Trainer::next_batch() {
   return make_minibatch(task_->train_pairs(), members);
 }
 
+Trainer::Prefetch Trainer::plan_deal(int epoch, int pos, std::vector<int> order) const {
+  // next_batch() (trainer.cpp:173-184) on a private copy of the cursor
+  Prefetch p;
+  p.epoch0 = epoch;
+  p.pos0 = pos;
+  const auto& pairs = task_->train_pairs();
+  auto next = [&]() -> std::optional<MiniBatch> {
+    if (plan_.batches.empty()) return std::nullopt;
+    if (pos >= int(order.size())) {
+      if (epoch >= max_epochs_) return std::nullopt;
+      ++epoch;
+      order = shuffle_epoch(plan_, epoch);
+      pos = 0;
+    }
+    const std::vector<int>& members = plan_.batches[size_t(order[size_t(pos)])];
+    ++pos;
+    return make_minibatch(pairs, members);
+  };
+  p.sub.resize(size_t(workers_));
+  for (int w = 0; w < workers_; ++w)
+    for (int a = 0; a < accum_; ++a) {
+      std::optional<MiniBatch> b = next();
+      if (!b) {
+        if (w == 0 && a == 0) {
+          p.exhausted = true;
+          return p;
+        }
+        p.sub[size_t(w)].push_back(MiniBatch{});
+      } else {
+        p.sub[size_t(w)].push_back(std::move(*b));
+      }
+    }
+  p.epoch1 = epoch;
+  p.pos1 = pos;
+  p.order1 = std::move(order);
+  pack_local(p.sub, p.packs, p.which);
+  return p;
+}
+
+void Trainer::pack_local(const std::vector<std::vector<MiniBatch>>& sub, std::vector<PackedBatch>& packs,
+                         std::vector<std::pair<int, int>>& which) const {
+  packs.clear();
+  which.clear();
+  for (int lw = 0; lw < local_; ++lw) {
+    const int w = rank_ * local_ + lw;
+    for (int a = 0; a < accum_; ++a) {
+      const MiniBatch& b = sub[size_t(w)][size_t(a)];
+      if (b.rows == 0) continue;
+      packs.push_back(PackedBatch::pack(b));
+      which.emplace_back(lw, a);
+    }
+  }
+}
+
 std::optional<StepStats> Trainer::train_one() {
   if (!deal_) {
     std::optional<MiniBatch> b = next_batch();
@@ -219,18 +273,18 @@ std::optional<StepStats> Trainer::train_one() {
   }
   // deal: W*A consecutive per-replica batches of the shuffled plan (fairseq
   // semantics); replayable on the reference through its train_step
-  std::vector<std::vector<MiniBatch>> sub(static_cast<size_t>(workers_));
-  for (int w = 0; w < workers_; ++w)
-    for (int a = 0; a < accum_; ++a) {
-      std::optional<MiniBatch> b = next_batch();
-      if (!b) {
-        if (w == 0 && a == 0) return std::nullopt;
-        sub[size_t(w)].push_back(MiniBatch{});
-      } else {
-        sub[size_t(w)].push_back(std::move(*b));
-      }
-    }
-  return train_step(sub);
+  Prefetch p;
+  bool have = false;
+  if (prefetch_.valid()) {
+    p = prefetch_.get();
+    have = p.epoch0 == epoch_ && p.pos0 == pos_;
+  }
+  if (!have) p = plan_deal(epoch_, pos_, order_);
+  if (p.exhausted) return std::nullopt;
+  epoch_ = p.epoch1;
+  pos_ = p.pos1;
+  order_ = std::move(p.order1);
+  return run_step(p.sub, p.packs, p.which);
 }
 
 void Trainer::upload(const std::vector<PackedBatch>& packs, std::vector<DeviceBatch>& out) {
@@ -351,6 +405,14 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
   if (int(sub.size()) != workers_) throw ShapeError("train_step: need one sub-batch list per replica");
   for (const auto& l : sub)
     if (int(l.size()) != accum_) throw ShapeError("train_step: every replica takes exactly accum sub-batches");
+  std::vector<PackedBatch> packs;
+  std::vector<std::pair<int, int>> which;
+  pack_local(sub, packs, which);
+  return run_step(sub, packs, which);
+}
+
+StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std::vector<PackedBatch>& packs,
+                            const std::vector<std::pair<int, int>>& which) {
   const double scale = fp16_ ? scaler_->scale() : 1.0;
   StepStats stats;
   stats.step = step_ + 1;
@@ -359,18 +421,7 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
     for (const auto& b : l) stats.ntokens += b.ntokens;  // == sum of active target rows
   if (stats.ntokens == 0) throw ShapeError("train_step: zero target tokens in the minibatch");
 
-  // pack + upload this rank's sub-batches in one copy
-  std::vector<PackedBatch> packs;
-  std::vector<std::pair<int, int>> which;
-  for (int lw = 0; lw < local_; ++lw) {
-    const int w = rank_ * local_ + lw;
-    for (int a = 0; a < accum_; ++a) {
-      const MiniBatch& b = sub[size_t(w)][size_t(a)];
-      if (b.rows == 0) continue;
-      packs.push_back(PackedBatch::pack(b));
-      which.emplace_back(lw, a);
-    }
-  }
+  // upload this rank's packed sub-batches in one copy
   std::vector<DeviceBatch> dev;
   cuda_check(cudaEventRecord(ev0_, stream_), "event");
   upload(packs, dev);
@@ -427,6 +478,9 @@ StepStats Trainer::train_step(const std::vector<std::vector<MiniBatch>>& sub) {
   }
   // overflow check + update: 2 B grad read (check) + 28 B/param update
   if (prof_) prof_->end(stream_, Profiler::Optim, 0, double(n_) * (esize() + (injected ? 0 : 16 + 2 * esize() + 8)));
+  // the next deal-mode step's batches are prepared while this one runs
+  if (deal_ && prefetch_on_ && !prefetch_.valid())
+    prefetch_ = std::async(std::launch::async, [this, e = epoch_, p = pos_, o = order_] { return plan_deal(e, p, o); });
   char* rb = static_cast<char*>(readback_host_);
   cuda_check(cudaMemcpyAsync(rb, stats_dev_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_), "stats D2H");
   cuda_check(cudaMemcpyAsync(rb + 32, flag_dev_, 4, cudaMemcpyDeviceToHost, stream_), "flag D2H");

@@ -13,6 +13,7 @@
 #include <nccl.h>
 
 #include <functional>
+#include <future>
 #include <memory>
 #include <optional>
 
@@ -138,6 +139,27 @@ class Trainer {
   float last_ms_ = 0.f;
   int64_t h2d_bytes_ = 0;
   std::unique_ptr<Profiler> prof_;
+
+  // Host-side batch preparation of the next deal-mode step (make_minibatch +
+  // packing, trainer.cpp:173-184 / data.cpp:172-219) runs on a worker thread
+  // while the GPU executes the current step; it works on a copy of the epoch
+  // cursor and is used only if the cursor is still where it started.
+  struct Prefetch {
+    int epoch0 = 0, pos0 = 0;
+    int epoch1 = 0, pos1 = 0;
+    std::vector<int> order1;
+    bool exhausted = false;
+    std::vector<std::vector<MiniBatch>> sub;
+    std::vector<PackedBatch> packs;
+    std::vector<std::pair<int, int>> which;
+  };
+  Prefetch plan_deal(int epoch, int pos, std::vector<int> order) const;
+  void pack_local(const std::vector<std::vector<MiniBatch>>& sub, std::vector<PackedBatch>& packs,
+                  std::vector<std::pair<int, int>>& which) const;
+  StepStats run_step(const std::vector<std::vector<MiniBatch>>& sub, std::vector<PackedBatch>& packs,
+                     const std::vector<std::pair<int, int>>& which);
+  std::future<Prefetch> prefetch_;
+  bool prefetch_on_ = true;
 
   void init(const Registry& reg);
   std::optional<MiniBatch> next_batch();

@@ -174,3 +174,46 @@ def test_dropout_matches_reference(fp16):
     # dropout is really on: the same model without it gives a different loss
     nodrop, _, _ = pair("transformer_base_defaults", dict(ov, dropout=0.0))
     assert abs(nodrop.train_one()["loss"] - pair("transformer_base_defaults", ov)[0].train_one()["loss"]) > 1e-6
+
+
+def test_deal_dispatch_with_prefetch_matches_reference_replay():
+    """Deal dispatch (W*A consecutive batches of the shuffled plan per step),
+    with the next step's batches prepared on a host thread while the GPU runs:
+    the step sequence -- across epoch rollovers -- equals the reference
+    replaying the same schedule through its own train_step."""
+    import paper_1904_01038_b200 as sqf
+    V = 1000
+    c = sqf.synthetic_corpus(60, V, V, 1.1, 1)
+    ov = dict(BASE, max_tokens=512, workers=2, accum=2, dispatch="deal", max_epochs=5)
+    mine = sqf.Trainer("transformer_base_defaults", ov, corpus=c, src_vocab=V, tgt_vocab=V)
+    ro = {k: v for k, v in ov.items() if k != "dispatch"}
+    theirs = ref.RefTrainer("transformer_base_defaults", ro, c, V, V)
+    plan = sqf.make_batches(c, 512, 0, 1)
+    nb = len(plan)
+    epoch, pos, order = 1, 0, sqf.shuffle_epoch(nb, 1, 1)
+    steps = 0
+    while True:
+        sub = []
+        for w in range(2):
+            row = []
+            for a in range(2):
+                if pos >= nb and epoch < 5:
+                    epoch, pos, order = epoch + 1, 0, sqf.shuffle_epoch(nb, 1, epoch + 1)
+                if pos < nb:
+                    row.append(plan[order[pos]])
+                    pos += 1
+                else:
+                    row.append([])
+            sub.append(row)
+        a = mine.train_one()
+        if not sub[0][0]:
+            assert a is None
+            break
+        b = theirs.train_step(sub)
+        assert a["ntokens"] == b["ntokens"] and abs(a["loss"] - b["loss"]) <= 1e-4 * abs(b["loss"])
+        assert mine.progress()["epoch"] == epoch and mine.progress()["cursor"] == pos
+        steps += 1
+        if steps == 12:
+            break
+    assert steps >= 6
+    assert rel(mine.params(), theirs.params()) < 1e-4
