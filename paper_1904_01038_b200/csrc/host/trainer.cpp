@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace sqf {
@@ -103,9 +104,18 @@ void Trainer::init(const Registry& reg) {
 
   // device state
   n_ = model_->num_params();
-  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
-  cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
-  cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
+  // the activation-gradient chain (main stream) is the critical path; the
+  // parameter-gradient side stream only has to finish by the end of the
+  // sub-batch, so its blocks yield to the main stream's (SQF_STREAM_PRIO=0
+  // disables); the comm stream gets the top priority
+  int lo = 0, hi = 0;
+  cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+  const char* prio_env = std::getenv("SQF_STREAM_PRIO");
+  const bool prio = !(prio_env && std::atoi(prio_env) == 0);
+  const int p_main = prio ? std::max(hi, lo - 1) : 0, p_side = prio ? lo : 0, p_comm = prio ? hi : 0;
+  cuda_check(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, p_main), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, p_side), "side stream");
+  cuda_check(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, p_comm), "comm stream");
   cuda_check(cudaEventCreate(&ev0_), "event");
   cuda_check(cudaEventCreate(&ev1_), "event");
   cuda_check(cudaMalloc(&master_, size_t(n_) * 4), "master");
