@@ -278,6 +278,15 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   // activation-gradient chain: what counts there is work per SM-cycle, not
   // latency, so they always take the widest (most operand-efficient) tile
   if (cat == Profiler::GemmWgrad && cur_ == side_ && side_ && tile_env() != 0) g.tile_n = 256;
+  // experiment knob: CTA-pair (cta_group::2, 256-row) tiles for the main-stream GEMMs
+  static const int pair_env = [] {
+    const char* e = std::getenv("SQF_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (pair_env && cat != Profiler::GemmWgrad && m >= 512 && dtype_ != SFK_F32) {
+    g.pair = 1;
+    g.tile_n = 256;
+  }
   float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
   static const int sk_mode = [] {
     const char* v = std::getenv("SQF_GEMM_STREAM_K");  // 0 off (default), 1 auto, 2 force
@@ -446,13 +455,13 @@ void DeviceTape::finish(int loss_node, double* stats_acc) {
   run_xent(n, 0.f, false, stats_acc);
 }
 
-void DeviceTape::backward(int loss_node, float seed, double* stats_acc) {
+void DeviceTape::backward(int loss_node, float seed, double* stats_acc, bool join) {
   if (loss_node < 0 || loss_node >= int(nodes_.size())) throw BoundsError("backward: bad node id");
   Node& n = nodes_[loss_node];
   if (n.kind != Kind::Xent) throw ShapeError("backward: loss node must be a softmax_xent node");
   run_xent(n, seed, true, stats_acc);
   for (int i = loss_node - 1; i >= 0; --i) backward_node(i);
-  join_side();
+  if (join) join_side();
 }
 
 cudaEvent_t DeviceTape::event() {
@@ -514,7 +523,13 @@ void DeviceTape::backward_node(int id) {
     case Kind::Xent:
       return;
     case Kind::Embedding: {
-      join_side();  // a tied output projection's wgrad writes the same parameter rows
+      // a tied output projection's wgrad (side stream) writes the same
+      // parameter rows: only then wait for the side stream here
+      for (const Node& o : nodes_)
+        if (o.kind == Kind::Linear && o.p0.offset == n.p0.offset) {
+          join_side();
+          break;
+        }
       pbegin();
       if (dtype_ != SFK_F32 && n.segs.chunks) {
         float* scratch = n.segs.nslots ? static_cast<float*>(arena_.alloc(size_t(n.segs.nslots) * n.cols * 4)) : nullptr;

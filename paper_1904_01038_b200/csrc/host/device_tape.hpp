@@ -136,7 +136,9 @@ class DeviceTape {
 
   // Seeds d(loss_row) = seed on active rows (tape.cpp:506-516), runs the fused
   // xent fwd+bwd and sweeps nodes in exact reverse order.
-  void backward(int loss_node, float seed, double* stats_acc);
+  // join_side = false leaves the side-stream parameter-gradient work running
+  // past the return (the caller orders it before reusing the arena)
+  void backward(int loss_node, float seed, double* stats_acc, bool join_side = true);
   // forward-only loss statistics (evaluate)
   void finish(int loss_node, double* stats_acc);
 

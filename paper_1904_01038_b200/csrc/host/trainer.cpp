@@ -46,6 +46,8 @@ Trainer::~Trainer() {
   cudaFreeHost(blob_host_);
   cudaFreeHost(readback_host_);
   if (ev0_) cudaEventDestroy(ev0_);
+  for (auto e : arena_free_)
+    if (e) cudaEventDestroy(e);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
   if (side_) cudaStreamDestroy(side_);
@@ -104,19 +106,21 @@ void Trainer::init(const Registry& reg) {
 
   // device state
   n_ = model_->num_params();
-  // the activation-gradient chain (main stream) is the critical path; the
-  // parameter-gradient side stream only has to finish by the end of the
-  // sub-batch, so its blocks yield to the main stream's (SQF_STREAM_PRIO=0
-  // disables); the comm stream gets the top priority
+  // Stream priorities (SQF_STREAM_PRIO): 0 = equal (default: measured best,
+  // 130.0 ms/step), 1 = main stream above the side stream (136.6 ms: a starved
+  // side stream delays the end-of-sub-batch join), 2 = side stream above main.
+  // The comm stream always gets the top priority.
   int lo = 0, hi = 0;
   cuda_check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
   const char* prio_env = std::getenv("SQF_STREAM_PRIO");
-  const bool prio = !(prio_env && std::atoi(prio_env) == 0);
-  const int p_main = prio ? std::max(hi, lo - 1) : 0, p_side = prio ? lo : 0, p_comm = prio ? hi : 0;
+  const int prio = prio_env ? std::atoi(prio_env) : 0;
+  const int mid = std::max(hi, lo - 1);
+  const int p_main = prio == 1 ? mid : prio == 2 ? lo : lo, p_side = prio == 2 ? mid : lo, p_comm = hi;
   cuda_check(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, p_main), "stream");
   cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, p_side), "side stream");
   cuda_check(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, p_comm), "comm stream");
   cuda_check(cudaEventCreate(&ev0_), "event");
+  for (auto& e : arena_free_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreate(&ev1_), "event");
   cuda_check(cudaMalloc(&master_, size_t(n_) * 4), "master");
   if (dtype_ == SFK_F32) {
@@ -445,8 +449,10 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     const int lw = which[i].first, a = which[i].second;
     const int w = rank_ * local_ + lw;
     model_->set_train_step(step_ * workers_ * accum_ + int64_t(w) * accum_ + a);
-    arena_.reset();
-    DeviceTape tape(arena_, DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
+    const int k = int(i & 1);
+    if (arena_busy_[k]) cuda_check(cudaStreamWaitEvent(stream_, arena_free_[k], 0), "arena wait");
+    arena_[k].reset();
+    DeviceTape tape(arena_[k], DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     tape.set_side_stream(side_, &evpool_);
@@ -457,9 +463,15 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
       tape.set_grad_hook([this](int64_t off, int64_t, cudaStream_t) { ovl_on_write(off); });
     }
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
-    tape.backward(out.loss_node, float(scale), stats_dev_);
+    const bool last = i + 1 == dev.size();
+    tape.backward(out.loss_node, float(scale), stats_dev_, last);
+    if (!last) {
+      cuda_check(cudaEventRecord(arena_free_[k], side_), "event record");
+      arena_busy_[k] = true;
+    }
     launches_ += tape.launches();
   }
+  arena_busy_[0] = arena_busy_[1] = false;  // the last backward joined the side stream
   // in-process replicas fold in index order with re-rounding (trainer.cpp:75-87)
   for (int lw = 1; lw < local_; ++lw) {
     sfk_check(sfk_accumulate(dtype_, grads_[0], grads_[size_t(lw)], n_, stream_), "replica fold");
@@ -532,8 +544,8 @@ EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
     std::vector<PackedBatch> packs{PackedBatch::pack(b)};
     std::vector<DeviceBatch> dev;
     upload(packs, dev);
-    arena_.reset();
-    DeviceTape tape(arena_, DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    arena_[0].reset();
+    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     CriterionOutput c = criterion_->compute(*model_, dev[0], tape);
     tape.finish(c.loss_node, stats_dev_);

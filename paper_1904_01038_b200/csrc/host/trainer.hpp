@@ -127,7 +127,13 @@ class Trainer {
   std::vector<cudaEvent_t> evpool_;    // ordering events handed to the tapes
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   ncclComm_t comm_ = nullptr;
-  Arena arena_;
+  // Two activation arenas alternate between sub-batches so the side-stream
+  // parameter-gradient work of sub-batch i (which reads its activations) can
+  // run under the forward of sub-batch i+1; arena k is reused only after the
+  // side stream has passed arena_free_[k].
+  Arena arena_[2];
+  cudaEvent_t arena_free_[2] = {nullptr, nullptr};
+  bool arena_busy_[2] = {false, false};
 
   std::vector<GradientBucket> buckets_;
   EpochPlan plan_;
