@@ -278,10 +278,12 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   // activation-gradient chain: what counts there is work per SM-cycle, not
   // latency, so they always take the widest (most operand-efficient) tile
   if (cat == Profiler::GemmWgrad && cur_ == side_ && side_ && tile_env() != 0) g.tile_n = 256;
-  // experiment knob: CTA-pair (cta_group::2, 256-row) tiles for the main-stream GEMMs
+  // CTA-pair (cta_group::2, 256 x 256) tiles for the main-stream GEMMs: half
+  // the per-SM operand traffic of 128 x 256 (measured 128.1 vs 131.1 ms/step
+  // on C4); SQF_PAIR=0 switches back to single-CTA tiles
   static const int pair_env = [] {
     const char* e = std::getenv("SQF_PAIR");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   if (pair_env && cat != Profiler::GemmWgrad && m >= 512 && dtype_ != SFK_F32) {
     g.pair = 1;

@@ -597,23 +597,35 @@ __global__ void __launch_bounds__(512) xent_v(const T* __restrict__ logits, int 
   const float L2E = 1.4426950408889634f;
   float m = -INFINITY, s = 0.f;
   int mi = 0x7fffffff;
-  for (int ch = tid; ch < nch; ch += blockDim.x) {
-    const uint4 u = reinterpret_cast<const uint4*>(src)[ch];
-    xrow[ch] = u;
-    float f[8];
-    V8<T>::unpack(u, f);
-    float cm = f[0];
-    int ci = 0;
+  // four 16-byte loads in flight per thread before any of them is consumed
+  for (int ch0 = tid; ch0 < nch; ch0 += 4 * blockDim.x) {
+    uint4 uu[4];
 #pragma unroll
-    for (int e = 1; e < 8; ++e)
-      if (f[e] > cm) cm = f[e], ci = e;
-    if (cm > m) {
-      s *= exp2f((m - cm) * L2E);
-      m = cm;
-      mi = ch * 8 + ci;
+    for (int j = 0; j < 4; ++j) {
+      const int ch = ch0 + j * blockDim.x;
+      if (ch < nch) uu[j] = reinterpret_cast<const uint4*>(src)[ch];
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) s += exp2f((f[e] - m) * L2E);
+    for (int j = 0; j < 4; ++j) {
+      const int ch = ch0 + j * blockDim.x;
+      if (ch >= nch) break;
+      const uint4 u = uu[j];
+      xrow[ch] = u;
+      float f[8];
+      V8<T>::unpack(u, f);
+      float cm = f[0];
+      int ci = 0;
+#pragma unroll
+      for (int e = 1; e < 8; ++e)
+        if (f[e] > cm) cm = f[e], ci = e;
+      if (cm > m) {
+        s *= exp2f((m - cm) * L2E);
+        m = cm;
+        mi = ch * 8 + ci;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += exp2f((f[e] - m) * L2E);
+    }
   }
   // (max, sum, first argmax) combine
   auto comb = [&](float om, float os, int oi) {
