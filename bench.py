@@ -13,8 +13,8 @@ Prints ONE JSON line (rank 0). `value` = whole-job target tokens / max-over-rank
 time of the K steps (CUDA events recorded inside the native trainer on its own stream);
 `e2e` = the same tokens over CUDA events on the trainer stream bracketing the K public
 `Trainer.train_one()` calls (host batch packing, pinned H2D of ids, D2H of StepStats
-included). `roofline` comes from a profiling pass after the timed region (CUDA events
-around every launch on the trainer stream) for the dominant kernel class (tcgen05 GEMM).
+included). `roofline` comes from a profiling pass after the timed region (all launches serialised on the
+trainer stream, CUDA events around every launch) for the dominant kernel class (tcgen05 GEMM).
 `cpu_baseline` times the reference itself (oracle/_ref, the seqforge C++ library built
 from its own sources) on a bounded sample of the same workload on the host cores.
 """

@@ -278,6 +278,16 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   // activation-gradient chain: what counts there is work per SM-cycle, not
   // latency, so they always take the widest (most operand-efficient) tile
   if (cat == Profiler::GemmWgrad && cur_ == side_ && side_ && tile_env() != 0) g.tile_n = 256;
+  // weight gradients may take CTA-pair tiles too (SQF_WGRAD_PAIR=1); the
+  // fused bias gradient works in both kernels
+  static const int wpair_env = [] {
+    const char* e = std::getenv("SQF_WGRAD_PAIR");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (wpair_env && cat == Profiler::GemmWgrad && m >= 512 && dtype_ != SFK_F32) {
+    g.pair = 1;
+    g.tile_n = 256;
+  }
   // CTA-pair (cta_group::2, 256 x 256) tiles for the main-stream GEMMs: half
   // the per-SM operand traffic of 128 x 256 (measured 128.1 vs 131.1 ms/step
   // on C4); SQF_PAIR=0 switches back to single-CTA tiles
@@ -556,8 +566,13 @@ void DeviceTape::backward_node(int id) {
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
       if (!fresh) wait_side_reader(dx);  // in-place accumulate into a buffer a wgrad may still read
       if (dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024) {
-        // gamma/beta gradients are parameter work: side stream, after dy is ready
-        if (side_) {
+        // gamma/beta gradients are parameter work: side stream, after dy is
+        // ready (SQF_LN_PARAMS_MAIN=1 keeps them on the main stream)
+        static const bool ln_main = [] {
+          const char* e = std::getenv("SQF_LN_PARAMS_MAIN");
+          return e && std::atoi(e) != 0;
+        }();
+        if (side_ && !ln_main) {
           cudaEvent_t ready = event();
           cuda_check(cudaEventRecord(ready, stream_), "event record");
           cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
@@ -570,7 +585,7 @@ void DeviceTape::backward_node(int id) {
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
         grad_done(n.p0);
         grad_done(n.p1);
-        if (side_) {
+        if (side_ && !ln_main) {
           cudaEvent_t done = event();
           cuda_check(cudaEventRecord(done, side_), "event record");
           side_readers_.emplace_back(n.grad, done);

@@ -456,7 +456,9 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     DeviceTape tape(arena_[k], DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
-    tape.set_side_stream(side_, &evpool_);
+    // a profiling pass serialises everything on the main stream so the
+    // per-launch event windows measure each kernel alone (no concurrency)
+    if (!prof_) tape.set_side_stream(side_, &evpool_);
     tape.set_gemm_workspace(gemm_ws_, gemm_ws_ + gemm_ws_floats_, gemm_ws_floats_);
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     if (overlap && i + 1 == dev.size()) {

@@ -559,7 +559,7 @@ __device__ __forceinline__ void reduce_partials(const Epi& e, const Sched& sc, c
 // order; db[m] = q(db[m] + sum). Only the tiles with n0 == 0 do this, so every
 // db element has exactly one writer.
 template <typename T, int STAGES, int STAGE>
-__device__ __forceinline__ void bias_grad_tile(uint8_t* smem, uint64_t* full, uint64_t* bsum, int it0, int nkb,
+__device__ __forceinline__ void bias_grad_tile(uint8_t* smem, uint64_t* ready, uint64_t* bsum, int it0, int nkb,
                                                int warp, int lane, float* stg, T* db, int m0, int M) {
   const int t = (warp - 2) * 32 + lane;
   const int mp = t & 63, kq = t >> 6;
@@ -567,7 +567,7 @@ __device__ __forceinline__ void bias_grad_tile(uint8_t* smem, uint64_t* full, ui
   float s0 = 0.f, s1 = 0.f;
   for (int i = 0; i < nkb; ++i) {
     const int it = it0 + i, s = it % STAGES;
-    mbar_wait(&full[s], (it / STAGES) & 1);
+    mbar_wait(&ready[s], (it / STAGES) & 1);  // the stage's A tile is in smem (and not yet refilled)
     const uint8_t* a = smem + s * STAGE + box * 8192;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -837,7 +837,7 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
 template <int BN, bool A_MN, bool B_MN, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Epi e, int M,
-             int N, int K, int vec_ok) {
+             int N, int K, int vec_ok, void* bias_grad) {
   using C = Cfg2<BN>;
   constexpr int PM = 256;      // rows per pair tile
   constexpr int HB = BN / 2;   // B rows staged by each CTA
@@ -847,7 +847,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bsum = tempty + 2;  // per stage: the epilogue warps finished their bias-gradient read
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bsum + C::STAGES);
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -855,6 +856,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&bsum[s], kEpiWarps);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -882,13 +884,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;
+      uint32_t bias_pend = 0, bias_ph = 0;  // per stage: a bias-tile read outstanding / its bsum phase
       for (int tile = pair; tile < tiles; tile += npairs) {
         const int m0 = (tile % num_m) * PM + 128 * int(rank);
         const int n0 = (tile / num_m) * BN + HB * int(rank);
+        const bool btile = A_MN && bias_grad && tile / num_m == 0;
         for (int kb = 0; kb < kblocks; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
+          if (bias_pend >> s & 1) {
+            mbar_wait(&bsum[s], bias_ph >> s & 1);
+            bias_ph ^= 1u << s;
+            bias_pend &= ~(1u << s);
+          }
+          if (btile) bias_pend |= 1u << s;
           if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE);
           const uint32_t lbar = saddr(&full[s]) & 0xFEFFFFFFu;  // the leader CTA's barrier
           uint8_t* a_dst = smem + s * C::STAGE;
@@ -939,10 +949,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
-    int t = 0;
+    int t = 0, it = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++t) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * PM + 128 * int(rank), n0 = (tile / num_m) * BN;
+      // fused bias gradient: each CTA sums its own 128-row half of A; the
+      // pair's MMA commit on empty[s] (multicast to both CTAs) says the stage
+      // is complete and still unrecycled
+      if (A_MN && bias_grad && n0 == 0)
+        bias_grad_tile<T, C::STAGES, C::STAGE>(smem, empty, bsum, it, kblocks, warp, lane, stg,
+                                               static_cast<T*>(bias_grad), m0, M);
+      it += kblocks;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
       epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
@@ -1070,7 +1087,7 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, gemm_tc2<BN, A_MN, B_MN, T>, ta, tb, e, g->m, g->n, g->k, vec_ok ? 1 : 0);
+  cudaLaunchKernelEx(&cfg, gemm_tc2<BN, A_MN, B_MN, T>, ta, tb, e, g->m, g->n, g->k, vec_ok ? 1 : 0, g->bias_grad);
   return check_launch("sfk_gemm(tcgen05 pair)");
 }
 
@@ -1127,7 +1144,7 @@ int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) 
   const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 && !g->bias_grad ? pick_stream_k(g, &sk_grid) : 0;
   const int bn = skt > 0 ? 256 : g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
-  if (g->pair > 0 && !g->bias_grad) {
+  if (g->pair > 0) {
 #define SFK_TC2(BNV)                                                    \
   switch (layout) {                                                     \
     case 0: return launch2<BNV, false, false, T>(g, e, vec_ok, s);      \

@@ -449,8 +449,9 @@ def test_gemm_stream_k(layout, shape, flags):
 
 @pytest.mark.parametrize("dtype", [1, 2])
 @pytest.mark.parametrize("shape", [(1024, 1024, 3584), (3072, 1024, 3000), (200, 296, 640), (4096, 1024, 37),
-                                   (1024, 4096, 2048)])
-def test_gemm_fused_bias_grad(dtype, shape):
+                                   (1024, 4096, 2048), (600, 512, 700)])
+@pytest.mark.parametrize("pair", [0, 1])
+def test_gemm_fused_bias_grad(dtype, shape, pair):
     """Weight-gradient GEMM with the bias gradient fused (add_bias backward,
     tape.cpp:347-358): dW = q(dW + dY^T X) as before and db = q(db + sum_rows dY)
     from the same A tiles; fp64 reference, deterministic."""
@@ -466,7 +467,8 @@ def test_gemm_fused_bias_grad(dtype, shape):
     for _ in range(2):
         dw, db = dw0.clone(), db0.clone()
         args = lib.GemmArgs(m=m, n=n, k=k, dtype=dtype, a=ptr(dy), lda=m, a_kmajor=0, b=ptr(x), ldb=n, b_kmajor=0,
-                            c=ptr(dw), ldc=n, flags=lib.EPI_ACCUM, stream_k=-1, bias_grad=ptr(db))
+                            c=ptr(dw), ldc=n, flags=lib.EPI_ACCUM, stream_k=-1, bias_grad=ptr(db), pair=pair,
+                            tile_n=256 if pair else 0)
         lib.check(lib.sfk_gemm(C.byref(args), stream()), kernel=True)
         torch.cuda.synchronize()
         outs.append((dw, db))
