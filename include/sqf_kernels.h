@@ -164,6 +164,15 @@ int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, int rows, int
 int sfk_layernorm_bwd_params(int dtype, const void* x, const void* dy, int rows, int d,
                              const float* stats, float* part, int32_t* counters, void* dgamma,
                              void* dbeta, void* stream);
+/* The activation gradient plus per-block gamma/beta column partials in one
+ * pass over x and dy (16 rows per block, warp-order combine): part[2][nblk][d]
+ * (*nparts = nblk = ceil(rows/16)); sfk_layernorm_bwd_fold then folds them in
+ * block order into dgamma = q(dgamma + sum), dbeta = q(dbeta + sum). */
+int sfk_layernorm_bwd_dx_part(int dtype, const void* x, const void* dy, int rows, int d,
+                              const void* gamma, const float* stats, void* dx, int accumulate,
+                              float* part, int* nparts, void* stream);
+int sfk_layernorm_bwd_fold(int dtype, const float* part, int nparts, int d, void* dgamma,
+                           void* dbeta, void* stream);
 /* (counters: >= ceil(d/256) zeroed int32 slots, re-armed to 0 by the kernel,
  * selects the single-launch form; NULL falls back to partial + fold launches) */
 

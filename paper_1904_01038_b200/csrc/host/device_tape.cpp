@@ -278,11 +278,11 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   // activation-gradient chain: what counts there is work per SM-cycle, not
   // latency, so they always take the widest (most operand-efficient) tile
   if (cat == Profiler::GemmWgrad && cur_ == side_ && side_ && tile_env() != 0) g.tile_n = 256;
-  // weight gradients may take CTA-pair tiles too (SQF_WGRAD_PAIR=1); the
-  // fused bias gradient works in both kernels
+  // weight gradients take CTA-pair tiles too (the fused bias gradient works in
+  // both kernels; measured 119.6 vs 121.6 ms/step on C4; SQF_WGRAD_PAIR=0 off)
   static const int wpair_env = [] {
     const char* e = std::getenv("SQF_WGRAD_PAIR");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 1;
   }();
   if (wpair_env && cat == Profiler::GemmWgrad && m >= 512 && dtype_ != SFK_F32) {
     g.pair = 1;
@@ -565,6 +565,41 @@ void DeviceTape::backward_node(int id) {
       const int max_parts = 4 * 148;  // sfk_layernorm_bwd_fused: <= 592 row blocks
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
       if (!fresh) wait_side_reader(dx);  // in-place accumulate into a buffer a wgrad may still read
+      static const bool ln_fused = [] {
+        const char* e = std::getenv("SQF_LN_FUSED");  // 0: separate gamma/beta pass on the side stream
+        return !(e && std::atoi(e) == 0);
+      }();
+      if (ln_fused && dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024 && !(debug_skip() & 2)) {
+        // dx and the gamma/beta column partials in one pass over x and dy on
+        // the main stream; only the small fold of the partials is side work
+        float* lpart = static_cast<float*>(arena_.alloc(size_t(2) * ((n.rows + 15) / 16) * n.cols * 4));
+        int nparts = 0;
+        pbegin();
+        sfk_check(sfk_layernorm_bwd_dx_part(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx,
+                                            fresh ? 0 : 1, lpart, &nparts, cur_),
+                  "layernorm_bwd_dx_part");
+        pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
+        if (side_) {
+          cudaEvent_t ready = event();
+          cuda_check(cudaEventRecord(ready, stream_), "event record");
+          cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
+          cur_ = side_;
+        }
+        pbegin();
+        sfk_check(sfk_layernorm_bwd_fold(dtype_, lpart, nparts, n.cols, gptr(n.p0), gptr(n.p1), cur_),
+                  "layernorm_bwd_fold");
+        pend(Profiler::LayerNorm, 0, double(nparts) * n.cols * 8.0);
+        grad_done(n.p0);
+        grad_done(n.p1);
+        if (side_) {
+          cudaEvent_t done = event();
+          cuda_check(cudaEventRecord(done, side_), "event record");
+          side_last_ = done;
+          cur_ = stream_;
+        }
+        launches_ += 2;
+        return;
+      }
       if (dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024) {
         // gamma/beta gradients are parameter work: side stream, after dy is
         // ready (SQF_LN_PARAMS_MAIN=1 keeps them on the main stream)

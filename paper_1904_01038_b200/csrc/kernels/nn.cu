@@ -354,6 +354,9 @@ int colsum_partial_vec(int, const void*, int, int, int64_t, float*, int*, cudaSt
 int ln_bwd_fused_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*,
                      int32_t*, void*, void*, cudaStream_t);
 int colsum_fused_vec(int, const void*, int, int, int64_t, float*, int32_t*, void*, cudaStream_t);
+int ln_dx_part_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*, int*,
+                   cudaStream_t);
+int fold2_vec(int, const float*, int, int, void*, void*, cudaStream_t);
 int colred_launch(int, bool, const void*, const void*, const float*, int, int, int64_t, float*, int32_t*, void*, void*,
                   cudaStream_t);
 int xent_vec(int, void*, int, int, int64_t, const int32_t*, int, float, float, void*, float*, cudaStream_t);
@@ -366,6 +369,25 @@ extern "C" int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, in
   if (rows == 0) return SFK_OK;
   const int e = sfk::ln_dx_vec(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, sfk::as_stream(stream));
   if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_dx: needs 16-bit data, d % 8 == 0, d <= 1024, aligned rows");
+  return e;
+}
+
+extern "C" int sfk_layernorm_bwd_dx_part(int dtype, const void* x, const void* dy, int rows, int d, const void* gamma,
+                                         const float* stats, void* dx, int accumulate, float* part, int* nparts,
+                                         void* stream) {
+  *nparts = 0;
+  if (rows == 0) return SFK_OK;
+  const int e = sfk::ln_dx_part_vec(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, part, nparts,
+                                    sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_dx_part: needs 16-bit data, d % 8 == 0, d <= 1024, aligned rows");
+  return e;
+}
+
+extern "C" int sfk_layernorm_bwd_fold(int dtype, const float* part, int nparts, int d, void* dgamma, void* dbeta,
+                                      void* stream) {
+  if (nparts == 0) return SFK_OK;
+  const int e = sfk::fold2_vec(dtype, part, nparts, d, dgamma, dbeta, sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_fold: needs 16-bit data");
   return e;
 }
 

@@ -518,6 +518,109 @@ __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T*
   }
 }
 
+// LN backward, activation gradient + gamma/beta column partials in one pass:
+// warp w of block b handles rows b*16 + 2w, +1 (same arithmetic as ln_dx_v),
+// and keeps per-lane column sums of dy*xhat and dy over its rows; the 8 warp
+// sums are combined in warp order in shared memory and block b writes
+// part[0][b][:] (dgamma) and part[1][b][:] (dbeta). A fold over the nblk
+// partials (fold_k, fixed order) finishes dgamma/dbeta off the critical path.
+constexpr int kLnRowsPerWarp = 2;
+template <typename T>
+__global__ void __launch_bounds__(256) ln_dx_part_v(const T* __restrict__ x, const T* __restrict__ dy, int rows, int d,
+                                                   const T* __restrict__ g, const float2* __restrict__ stats,
+                                                   T* __restrict__ dx, int accumulate, float* __restrict__ part,
+                                                   int nblk) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  extern __shared__ float red[];  // [8][d]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const float inv_n = __fdiv_rn(1.0f, float(d));
+  float pg[kMaxCh][8], pb[kMaxCh][8];
+#pragma unroll
+  for (int i = 0; i < kMaxCh; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) pg[i][e] = pb[i][e] = 0.f;
+#pragma unroll 1
+  for (int j = 0; j < kLnRowsPerWarp; ++j) {
+    const int r = blockIdx.x * (8 * kLnRowsPerWarp) + warp * kLnRowsPerWarp + j;
+    if (r >= rows) break;
+    const float2 st = stats[r];
+    uint4 xr[kMaxCh], gr[kMaxCh], dxo[kMaxCh];
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < d) {
+        xr[i] = *reinterpret_cast<const uint4*>(x + int64_t(r) * d + c);
+        gr[i] = *reinterpret_cast<const uint4*>(dy + int64_t(r) * d + c);
+        if (accumulate) dxo[i] = *reinterpret_cast<const uint4*>(dx + int64_t(r) * d + c);
+      }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < d) {
+        float gg[8], xh[8], gy[8];
+        V8<T>::load(g + c, gg);
+        V8<T>::unpack(xr[i], xh);
+        V8<T>::unpack(gr[i], gy);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float dxh = __fmul_rn(gy[e], gg[e]);
+          const float xhat = __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+          s1 += dxh;
+          s2 += dxh * xhat;
+          pg[i][e] += gy[e] * xhat;
+          pb[i][e] += gy[e];
+        }
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const float m1 = __fmul_rn(s1, inv_n), m2 = __fmul_rn(s2, inv_n);
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < d) {
+        float gg[8], xh[8], gy[8], o[8];
+        V8<T>::load(g + c, gg);
+        V8<T>::unpack(xr[i], xh);
+        V8<T>::unpack(gr[i], gy);
+        if (accumulate) V8<T>::unpack(dxo[i], o);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xhat = __fmul_rn(__fsub_rn(xh[e], st.x), st.y);
+          const float v = __fmul_rn(st.y, __fsub_rn(__fsub_rn(__fmul_rn(gy[e], gg[e]), m1), __fmul_rn(xhat, m2)));
+          o[e] = accumulate ? __fadd_rn(o[e], v) : v;
+        }
+        V8<T>::store(dx + int64_t(r) * d + c, o);
+      }
+    }
+  }
+  // block partials, one vector at a time through the [8][d] buffer
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < d) {
+        float* o = red + warp * d + c;
+        const float(&src)[8] = v == 0 ? pg[i] : pb[i];
+        *reinterpret_cast<float4*>(o) = make_float4(src[0], src[1], src[2], src[3]);
+        *reinterpret_cast<float4*>(o + 4) = make_float4(src[4], src[5], src[6], src[7]);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w * d + c];
+      part[(int64_t(v) * nblk + blockIdx.x) * d + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128) ln_dgb_partial_v(const T* __restrict__ x, const T* __restrict__ dy, int rows,
                                                        int d, const float2* __restrict__ stats, int rpb,
@@ -1021,6 +1124,42 @@ int ln_bwd_fused_vec(int dtype, const void* x, const void* dy, int rows, int d, 
                                                static_cast<__nv_bfloat16*>(dgamma),
                                                static_cast<__nv_bfloat16*>(dbeta));
   return check_launch("sfk_layernorm_bwd_fused(fold)");
+}
+
+int ln_dx_part_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats,
+                   void* dx, int accumulate, float* part, int* nparts, cudaStream_t s) {
+  if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g)) return SFK_EUNSUP;
+  const int per = 8 * vec::kLnRowsPerWarp;
+  const int nblk = (rows + per - 1) / per;
+  *nparts = nblk;
+  const size_t smem = size_t(8) * d * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(vec::ln_dx_part_v<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(vec::ln_dx_part_v<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cfg = true;
+  }
+  if (dtype == SFK_F16)
+    launch_pdl(vec::ln_dx_part_v<__half>, dim3(nblk), dim3(256), smem, s, static_cast<const __half*>(x),
+               static_cast<const __half*>(dy), rows, d, static_cast<const __half*>(g),
+               reinterpret_cast<const float2*>(stats), static_cast<__half*>(dx), accumulate, part, nblk);
+  else
+    launch_pdl(vec::ln_dx_part_v<__nv_bfloat16>, dim3(nblk), dim3(256), smem, s, static_cast<const __nv_bfloat16*>(x),
+               static_cast<const __nv_bfloat16*>(dy), rows, d, static_cast<const __nv_bfloat16*>(g),
+               reinterpret_cast<const float2*>(stats), static_cast<__nv_bfloat16*>(dx), accumulate, part, nblk);
+  return check_launch("sfk_layernorm_bwd_dx_part(vec)");
+}
+
+int fold2_vec(int dtype, const float* part, int nparts, int d, void* dgamma, void* dbeta, cudaStream_t s) {
+  if (dtype == SFK_F32) return SFK_EUNSUP;
+  dim3 grid((d + 7) / 8, dbeta ? 2 : 1);
+  if (dtype == SFK_F16)
+    launch_pdl(fold_k<__half>, grid, 256, 0, s, part, part + size_t(nparts) * d, nparts, d, static_cast<__half*>(dgamma),
+               static_cast<__half*>(dbeta));
+  else
+    launch_pdl(fold_k<__nv_bfloat16>, grid, 256, 0, s, part, part + size_t(nparts) * d, nparts, d,
+               static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
+  return check_launch("sfk_layernorm_bwd_fold");
 }
 
 int ln_dx_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats, void* dx,

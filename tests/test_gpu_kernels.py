@@ -355,6 +355,17 @@ def test_layernorm_bwd_fused_equals_two_phase(rows, d):
     assert torch.equal(dx1, dx4)
     torch.testing.assert_close(dg1.float(), dg4.float(), rtol=2e-3, atol=2e-3)
     torch.testing.assert_close(db1.float(), db4.float(), rtol=2e-3, atol=2e-3)
+    # one-pass form: dx plus per-block gamma/beta partials, folded in block order
+    dx6, dg6, db6 = torch.zeros_like(x), torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
+    part6 = torch.zeros(2 * ((rows + 15) // 16) * d, device="cuda")
+    np6 = C.c_int()
+    lib.check(lib.sfk_layernorm_bwd_dx_part(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx6), 0, ptr(part6),
+                                            C.byref(np6), stream()), True)
+    lib.check(lib.sfk_layernorm_bwd_fold(1, ptr(part6), np6.value, d, ptr(dg6), ptr(db6), stream()), True)
+    torch.cuda.synchronize()
+    assert torch.equal(dx1, dx6)
+    torch.testing.assert_close(dg1.float(), dg6.float(), rtol=2e-3, atol=2e-3)
+    torch.testing.assert_close(db1.float(), db6.float(), rtol=2e-3, atol=2e-3)
     # deterministic: a second run is bitwise identical
     dx3, dg3, db3 = torch.zeros_like(x), torch.zeros(d, device="cuda").half(), torch.zeros(d, device="cuda").half()
     lib.check(lib.sfk_layernorm_bwd_fused(1, ptr(x), ptr(dy), rows, d, ptr(gm), ptr(stats), ptr(dx3), 0, ptr(part2),
