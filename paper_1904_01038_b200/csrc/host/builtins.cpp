@@ -101,6 +101,7 @@ class TransformerModel : public ModelBase {
   std::vector<float> params_;
   std::vector<ParamManifestEntry> manifest_;
   ParamRef src_embed_, tgt_embed_, out_proj_, enc_lng_, enc_lnb_, dec_lng_, dec_lnb_;
+  ParamRef cross_kv_w_{}, cross_kv_b_{};  // all decoder layers' cross K/V projections, stacked
   std::vector<Layer> enc_, dec_;
   const float* pe_dev_ = nullptr;
 
@@ -157,8 +158,13 @@ class TransformerModel : public ModelBase {
     if (!share_) res("out_proj", tgt_vocab_, d);
     params_.assign(size_t(off), 0.0f);
 
-    // device order: canonical, except each attention block is laid out
-    // wq wk wv wo bq bk bv bo (weights contiguous, biases contiguous)
+    // device order: canonical, except (1) each attention block is laid out
+    // wq wk wv wo bq bk bv bo (weights contiguous, biases contiguous) and (2)
+    // the cross-attention K/V projections of all decoder layers form one
+    // region right after the encoder -- [wk wv] of layer 0..L-1, then [bk bv]
+    // of layer 0..L-1 -- so they are one GEMM over the encoder output in each
+    // direction (their gradients complete after the decoder's, before the
+    // encoder's, which is where the region sits in reverse device order)
     auto rank = [](const std::string& name) {
       static const char* order[] = {".wq", ".wk", ".wv", ".wo", ".bq", ".bk", ".bv", ".bo"};
       for (int i = 0; i < 8; ++i) {
@@ -167,20 +173,43 @@ class TransformerModel : public ModelBase {
       }
       return -1;
     };
+    auto is_cross_kv = [&](const std::string& name) {
+      const int r = rank(name);
+      return name.rfind("dec.", 0) == 0 && name.find(".cross.") != std::string::npos && (r == 1 || r == 2 || r == 5 || r == 6);
+    };
+    std::vector<size_t> kv_w, kv_b;  // manifest indices of the stacked region, in region order
+    for (int l = 0; l < dec_n_; ++l)
+      for (const char* s : {".wk", ".wv"}) kv_w.push_back(0), kv_w.back() = [&] {
+          const std::string nm = "dec." + std::to_string(l) + ".cross" + s;
+          for (size_t j = 0; j < manifest_.size(); ++j)
+            if (manifest_[j].name == nm) return j;
+          throw ConfigError("transformer: missing parameter " + nm);
+        }();
+    for (int l = 0; l < dec_n_; ++l)
+      for (const char* s : {".bk", ".bv"}) kv_b.push_back(0), kv_b.back() = [&] {
+          const std::string nm = "dec." + std::to_string(l) + ".cross" + s;
+          for (size_t j = 0; j < manifest_.size(); ++j)
+            if (manifest_[j].name == nm) return j;
+          throw ConfigError("transformer: missing parameter " + nm);
+        }();
     int64_t doff = 0;
+    auto place = [&](size_t j) {
+      manifest_[j].device_offset = doff;
+      doff += manifest_[j].numel;
+    };
     for (size_t i = 0; i < manifest_.size();) {
       if (rank(manifest_[i].name) < 0) {
-        manifest_[i].device_offset = doff;
-        doff += manifest_[i].numel;
+        place(i);
+        if (manifest_[i].name == "enc.ln.b") {
+          for (size_t j : kv_w) place(j);
+          for (size_t j : kv_b) place(j);
+        }
         ++i;
         continue;
       }
       for (int r = 0; r < 8; ++r)
         for (size_t j = i; j < i + 8; ++j)
-          if (rank(manifest_[j].name) == r) {
-            manifest_[j].device_offset = doff;
-            doff += manifest_[j].numel;
-          }
+          if (rank(manifest_[j].name) == r && !is_cross_kv(manifest_[j].name)) place(j);
       i += 8;
     }
     auto ref = [&](const std::string& name) {
@@ -200,6 +229,10 @@ class TransformerModel : public ModelBase {
     enc_lnb_ = ref("enc.ln.b");
     dec_lng_ = ref("dec.ln.g");
     dec_lnb_ = ref("dec.ln.b");
+    if (dec_n_ > 0) {
+      cross_kv_w_ = ParamRef{ref("dec.0.cross.wk").offset, dec_n_ * 2 * d, d};
+      cross_kv_b_ = ParamRef{ref("dec.0.cross.bk").offset, 1, dec_n_ * 2 * d};
+    }
     for (int i = 0; i < enc_n_; ++i) {
       const std::string p = "enc." + std::to_string(i);
       Layer l;
@@ -286,6 +319,10 @@ class TransformerModel : public ModelBase {
     const int B = b.rows, T = b.tgt_width, S = b.src_width;
     int x = t.embedding(tgt_embed_, b.target_in, B * T, T, std::sqrt(float(d_)), pe_dev_, b.tgt_segs);
     x = maybe_dropout(t, x, site);
+    // cross K/V of every decoder layer from the encoder output in one GEMM
+    // (model.cpp:262-263 per layer; same dot products, batched)
+    const int ckv_all = dec_.empty() ? -1 : t.linear(enc, cross_kv_w_, &cross_kv_b_, false);
+    int li = 0;
     for (const Layer& l : dec_) {
       const int z = t.layer_norm(x, l.ln1g, l.ln1b);
       const ParamRef bqkv = l.self.bqkv();
@@ -294,9 +331,8 @@ class TransformerModel : public ModelBase {
       x = residual(t, a, l.self.wo, &l.self.bo, false, x, site);
       const int z2 = t.layer_norm(x, l.ln2g, l.ln2b);
       const int cq = t.linear(z2, l.cross.wq, &l.cross.bq, false);
-      const ParamRef bkv = l.cross.bkv();
-      const int ckv = t.linear(enc, l.cross.wkv(), &bkv, false);
-      const int ca = t.attention(cq, 0, ckv, 0, d_, d_, heads_, B, T, S, false, b.src_lens);
+      const int kc = 2 * d_ * li++;
+      const int ca = t.attention(cq, 0, ckv_all, kc, kc + d_, d_, heads_, B, T, S, false, b.src_lens);
       x = residual(t, ca, l.cross.wo, &l.cross.bo, false, x, site);
       const int z3 = t.layer_norm(x, l.ln3g, l.ln3b);
       const int h = t.linear(z3, l.w1, &l.b1, true);

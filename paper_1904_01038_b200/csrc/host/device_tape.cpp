@@ -718,7 +718,11 @@ void DeviceTape::backward_node(int id) {
       const Node& kn = nodes_[n.in1];
       auto [dq, fq] = grad_of(n.in0);
       auto [dkv, fkv] = grad_of(n.in1);
-      if (!fq || (!fkv && n.in0 != n.in1)) throw ShapeError("attention: q/k/v inputs must not have other consumers");
+      // q is private to this node; a K/V node may feed several attention nodes
+      // through disjoint column slices (the stacked cross K/V of all decoder
+      // layers): each backward writes only its own slice
+      if (!fq) throw ShapeError("attention: the query input must not have other consumers");
+      (void)fkv;
       sfk_attn_args a{};
       a.dtype = dtype_;
       a.batch = n.batch;

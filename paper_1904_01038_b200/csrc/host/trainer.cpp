@@ -368,9 +368,19 @@ int Trainer::bucket_of(int64_t offset) const {
   return it->second;
 }
 
+// every bucket a gradient write [offset, offset + numel) touches (a stacked
+// parameter group may span several buckets)
+template <typename F>
+static void for_buckets(const std::vector<GradientBucket>& bk, int first, int64_t offset, int64_t numel, F f) {
+  (void)first;
+  for (size_t b = 0; b < bk.size(); ++b)
+    if (bk[b].start < offset + numel && offset < bk[b].end) f(int(b));
+}
+
 void Trainer::ovl_begin(const DeviceTape& tape) {
   ovl_remaining_.assign(buckets_.size(), 0);
-  for (const auto& w : tape.planned_grad_writes()) ++ovl_remaining_[size_t(bucket_of(w.first))];
+  for (const auto& w : tape.planned_grad_writes())
+    for_buckets(buckets_, 0, w.first, w.second, [&](int b) { ++ovl_remaining_[size_t(b)]; });
   ovl_next_ = 0;
   ovl_next_event_ = 0;
   overlap_log_.clear();
@@ -378,9 +388,10 @@ void Trainer::ovl_begin(const DeviceTape& tape) {
   while (ovl_next_ < int(buckets_.size()) && ovl_remaining_[size_t(ovl_next_)] == 0) ovl_issue(ovl_next_++);
 }
 
-void Trainer::ovl_on_write(int64_t offset) {
-  const int b = bucket_of(offset);
-  if (--ovl_remaining_[size_t(b)] < 0) throw DeviceError("overlap: more gradient writes than planned");
+void Trainer::ovl_on_write(int64_t offset, int64_t numel) {
+  for_buckets(buckets_, 0, offset, numel, [&](int b) {
+    if (--ovl_remaining_[size_t(b)] < 0) throw DeviceError("overlap: more gradient writes than planned");
+  });
   while (ovl_next_ < int(buckets_.size()) && ovl_remaining_[size_t(ovl_next_)] == 0) {
     ovl_issue(ovl_next_++);
     ++overlap_early_;
@@ -463,7 +474,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     if (overlap && i + 1 == dev.size()) {
       ovl_begin(tape);
-      tape.set_grad_hook([this](int64_t off, int64_t, cudaStream_t) { ovl_on_write(off); });
+      tape.set_grad_hook([this](int64_t off, int64_t n, cudaStream_t) { ovl_on_write(off, n); });
     }
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
     const bool last = i + 1 == dev.size();

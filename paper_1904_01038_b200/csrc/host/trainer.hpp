@@ -188,7 +188,7 @@ class Trainer {
   cudaEvent_t ovl_event();
   int bucket_of(int64_t offset) const;
   void ovl_begin(const DeviceTape& tape);
-  void ovl_on_write(int64_t offset);
+  void ovl_on_write(int64_t offset, int64_t numel);
   void ovl_issue(int b);
   void ovl_finish();
 };
