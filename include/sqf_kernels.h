@@ -161,6 +161,13 @@ int sfk_layernorm_bwd_fused(int dtype, const void* x, const void* dy, int rows, 
 int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, int rows, int d,
                          const void* gamma, const float* stats, void* dx, int accumulate,
                          void* stream);
+/* The activation gradient with an explicit accumulation source:
+ * dx = q(acc + contribution) (acc == NULL: dx = q(contribution); acc may be dx
+ * itself or another buffer, so an accumulation need not wait for a reader of
+ * the old gradient on another stream). */
+int sfk_layernorm_bwd_dx_acc(int dtype, const void* x, const void* dy, int rows, int d,
+                             const void* gamma, const float* stats, const void* acc, void* dx,
+                             void* stream);
 int sfk_layernorm_bwd_params(int dtype, const void* x, const void* dy, int rows, int d,
                              const float* stats, float* part, int32_t* counters, void* dgamma,
                              void* dbeta, void* stream);

@@ -79,6 +79,8 @@ sfk_colsum_finish = _sig("sfk_colsum_finish", C.c_int, C.c_int, vp, C.c_int, C.c
 sfk_colsum = _sig("sfk_colsum", C.c_int, C.c_int, vp, C.c_int, C.c_int, i64, vp, vp, vp, vp)
 sfk_layernorm_bwd_dx = _sig("sfk_layernorm_bwd_dx", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int,
                             vp)
+sfk_layernorm_bwd_dx_acc = _sig("sfk_layernorm_bwd_dx_acc", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp,
+                                vp, vp)
 sfk_layernorm_bwd_dx_part = _sig("sfk_layernorm_bwd_dx_part", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp,
                                  vp, C.c_int, vp, P(C.c_int), vp)
 sfk_layernorm_bwd_fold = _sig("sfk_layernorm_bwd_fold", C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)

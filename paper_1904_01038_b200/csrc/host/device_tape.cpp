@@ -1,6 +1,7 @@
 #include "device_tape.hpp"
 
 #include <algorithm>
+#include <tuple>
 #include <cstdlib>
 #include <cstring>
 
@@ -14,6 +15,14 @@ static int tile_env() {
   static const int v = [] {
     const char* e = std::getenv("SQF_WGRAD_TILE");
     return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+static bool ln_fused_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("SQF_LN_FUSED");
+    return e && std::atoi(e) != 0;
   }();
   return v;
 }
@@ -448,6 +457,21 @@ std::pair<void*, bool> DeviceTape::grad_of(int id) {
   return {n.grad, true};
 }
 
+std::pair<void*, const void*> DeviceTape::acc_target(int id) {
+  Node& n = nodes_[id];
+  if (!n.grad) {
+    n.grad = alloc_elems(int64_t(n.rows) * n.cols);
+    return {n.grad, nullptr};
+  }
+  for (const auto& r : side_readers_)
+    if (r.first == n.grad) {
+      const void* old = n.grad;
+      n.grad = alloc_elems(int64_t(n.rows) * n.cols);
+      return {n.grad, old};
+    }
+  return {n.grad, n.grad};
+}
+
 void DeviceTape::run_xent(Node& n, float seed, bool with_grad, double* stats_acc) {
   Node& lg = nodes_[n.in0];
   // the logits buffer becomes its own gradient (dlogits written in place)
@@ -561,18 +585,22 @@ void DeviceTape::backward_node(int id) {
     }
     case Kind::LayerNorm: {
       const Node& in = nodes_[n.in0];
-      auto [dx, fresh] = grad_of(n.in0);
       const int max_parts = 4 * 148;  // sfk_layernorm_bwd_fused: <= 592 row blocks
       float* part = static_cast<float*>(arena_.alloc(size_t(2) * max_parts * n.cols * 4));
-      if (!fresh) wait_side_reader(dx);  // in-place accumulate into a buffer a wgrad may still read
+      const bool split = dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024;
+      // 16-bit split path: accumulate out of place when a wgrad may still read
+      // the old gradient; other paths accumulate in place after waiting for it
+      void* dxw = nullptr;
+      const void* acc = nullptr;
+      if (split && !ln_fused_env()) {
+        std::tie(dxw, acc) = acc_target(n.in0);
+      }
+      auto [dx, fresh] = grad_of(n.in0);
+      if (!dxw && !fresh) wait_side_reader(dx);
       // SQF_LN_FUSED=1: one-pass dx + gamma/beta partials on the main stream
       // (measured slower on C4, 121.1 vs 119.3 ms/step: the longer
       // critical-path kernel costs more than the side-stream pass it saves)
-      static const bool ln_fused = [] {
-        const char* e = std::getenv("SQF_LN_FUSED");
-        return e && std::atoi(e) != 0;
-      }();
-      if (ln_fused && dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024 && !(debug_skip() & 2)) {
+      if (ln_fused_env() && dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024 && !(debug_skip() & 2)) {
         // dx and the gamma/beta column partials in one pass over x and dy on
         // the main stream; only the small fold of the partials is side work
         float* lpart = static_cast<float*>(arena_.alloc(size_t(2) * ((n.rows + 15) / 16) * n.cols * 4));
@@ -631,10 +659,10 @@ void DeviceTape::backward_node(int id) {
           cur_ = stream_;
         }
         pbegin();
-        sfk_check(sfk_layernorm_bwd_dx(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, dx,
-                                       fresh ? 0 : 1, cur_),
+        sfk_check(sfk_layernorm_bwd_dx_acc(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, acc, dxw,
+                                           cur_),
                   "layernorm_bwd_dx");
-        pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (fresh ? 3.0 : 4.0));
+        pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (acc ? 4.0 : 3.0));
         launches_ += 3;
         return;
       }
@@ -683,18 +711,28 @@ void DeviceTape::backward_node(int id) {
       }
       // dgrad into the input; a relu input gets the masked (pre-activation) grad
       Node& inm = nodes_[n.in0];
-      auto [dx, fresh] = grad_of(n.in0);
-      int flags = fresh ? 0 : SFK_EPI_ACCUM;
+      const bool relu_in = inm.kind == Kind::Linear && inm.relu;
+      if (relu_in && inm.grad) throw ShapeError("linear: relu output with several consumers is unsupported");
+      // an accumulation whose old buffer a side-stream wgrad may still read
+      // goes out of place: new = q(old + dY W) via the residual epilogue
+      auto [dx, acc] = dtype_ != SFK_F32 ? acc_target(n.in0) : std::pair<void*, const void*>{nullptr, nullptr};
+      bool fresh = true;
+      if (!dx) {
+        auto g = grad_of(n.in0);
+        dx = g.first;
+        fresh = g.second;
+        acc = fresh ? nullptr : dx;
+        if (!fresh) wait_side_reader(dx);
+      }
+      int flags = acc == nullptr ? 0 : acc == dx ? SFK_EPI_ACCUM : SFK_EPI_RESIDUAL;
       const void* mask = nullptr;
-      if (inm.kind == Kind::Linear && inm.relu) {
-        if (!fresh) throw ShapeError("linear: relu output with several consumers is unsupported");
+      if (relu_in) {
         flags = SFK_EPI_MASK;
         mask = inm.out;
         inm.grad_masked = true;
       }
-      if (!fresh) wait_side_reader(dx);
       gemm(Profiler::GemmDgrad, n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols,
-           flags, nullptr, nullptr, 0, mask, in.cols);
+           flags, nullptr, flags == SFK_EPI_RESIDUAL ? acc : nullptr, in.cols, mask, in.cols);
       return;
     }
     case Kind::Dropout: {

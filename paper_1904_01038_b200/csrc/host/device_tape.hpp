@@ -254,6 +254,11 @@ class DeviceTape {
   void* gptr(const ParamRef& p) const { return static_cast<char*>(params_.grad) + p.offset * esize_; }
   // gradient buffer of node `id`: returns {ptr, fresh}; allocates on first use
   std::pair<void*, bool> grad_of(int id);
+  // accumulation target for node id's gradient: (buffer to write, buffer to
+  // accumulate from or nullptr when fresh). If a side-stream reader may still
+  // be reading the current buffer, the sum goes to a new buffer instead of
+  // making the main stream wait for it.
+  std::pair<void*, const void*> acc_target(int id);
   void backward_node(int id);
   void run_xent(Node& n, float seed, bool with_grad, double* stats_acc);
   void gemm(int cat, int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,

@@ -354,6 +354,7 @@ int colsum_partial_vec(int, const void*, int, int, int64_t, float*, int*, cudaSt
 int ln_bwd_fused_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*,
                      int32_t*, void*, void*, cudaStream_t);
 int colsum_fused_vec(int, const void*, int, int, int64_t, float*, int32_t*, void*, cudaStream_t);
+int ln_dx_acc_vec(int, const void*, const void*, int, int, const void*, const float*, const void*, void*, cudaStream_t);
 int ln_dx_part_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*, int*,
                    cudaStream_t);
 int fold2_vec(int, const float*, int, int, void*, void*, cudaStream_t);
@@ -369,6 +370,14 @@ extern "C" int sfk_layernorm_bwd_dx(int dtype, const void* x, const void* dy, in
   if (rows == 0) return SFK_OK;
   const int e = sfk::ln_dx_vec(dtype, x, dy, rows, d, gamma, stats, dx, accumulate, sfk::as_stream(stream));
   if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_dx: needs 16-bit data, d % 8 == 0, d <= 1024, aligned rows");
+  return e;
+}
+
+extern "C" int sfk_layernorm_bwd_dx_acc(int dtype, const void* x, const void* dy, int rows, int d, const void* gamma,
+                                        const float* stats, const void* acc, void* dx, void* stream) {
+  if (rows == 0) return SFK_OK;
+  const int e = sfk::ln_dx_acc_vec(dtype, x, dy, rows, d, gamma, stats, acc, dx, sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_dx_acc: needs 16-bit data, d % 8 == 0, d <= 1024, aligned rows");
   return e;
 }
 

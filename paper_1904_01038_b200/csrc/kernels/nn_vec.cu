@@ -461,7 +461,9 @@ __global__ void colsum_partial_v(const T* __restrict__ x, int rows, int n, int64
 template <typename T>
 __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T* __restrict__ dy, int rows, int d,
                                               const T* __restrict__ g, const float2* __restrict__ stats,
-                                              T* __restrict__ dx, int accumulate) {
+                                              T* dx, const T* acc) {
+  // acc: nullptr (dx = contribution), dx (in place) or another buffer (out of place)
+  const int accumulate = acc != nullptr;
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T*
     if (c < d) {
       xr[i] = *reinterpret_cast<const uint4*>(x + int64_t(r) * d + c);
       gr[i] = *reinterpret_cast<const uint4*>(dy + int64_t(r) * d + c);
-      if (accumulate) dxo[i] = *reinterpret_cast<const uint4*>(dx + int64_t(r) * d + c);
+      if (accumulate) dxo[i] = *reinterpret_cast<const uint4*>(acc + int64_t(r) * d + c);
     }
   }
   float s1 = 0.f, s2 = 0.f;
@@ -1162,19 +1164,26 @@ int fold2_vec(int dtype, const float* part, int nparts, int d, void* dgamma, voi
   return check_launch("sfk_layernorm_bwd_fold");
 }
 
-int ln_dx_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats, void* dx,
-              int accumulate, cudaStream_t s) {
-  if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g)) return SFK_EUNSUP;
+int ln_dx_acc_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats,
+                  const void* acc, void* dx, cudaStream_t s) {
+  if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g) || (acc && !al16(acc)))
+    return SFK_EUNSUP;
   const int blocks = (rows + 7) / 8;
   if (dtype == SFK_F16)
     launch_pdl(vec::ln_dx_v<__half>, dim3(blocks), dim3(256), 0, s, static_cast<const __half*>(x),
                static_cast<const __half*>(dy), rows, d, static_cast<const __half*>(g),
-               reinterpret_cast<const float2*>(stats), static_cast<__half*>(dx), accumulate);
+               reinterpret_cast<const float2*>(stats), static_cast<__half*>(dx), static_cast<const __half*>(acc));
   else
     launch_pdl(vec::ln_dx_v<__nv_bfloat16>, dim3(blocks), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(x),
                static_cast<const __nv_bfloat16*>(dy), rows, d, static_cast<const __nv_bfloat16*>(g),
-               reinterpret_cast<const float2*>(stats), static_cast<__nv_bfloat16*>(dx), accumulate);
+               reinterpret_cast<const float2*>(stats), static_cast<__nv_bfloat16*>(dx),
+               static_cast<const __nv_bfloat16*>(acc));
   return check_launch("sfk_layernorm_bwd_dx(vec)");
+}
+
+int ln_dx_vec(int dtype, const void* x, const void* dy, int rows, int d, const void* g, const float* stats, void* dx,
+              int accumulate, cudaStream_t s) {
+  return ln_dx_acc_vec(dtype, x, dy, rows, d, g, stats, accumulate ? dx : nullptr, dx, s);
 }
 
 int ln_params_vec(int dtype, const void* x, const void* dy, int rows, int d, const float* stats, float* part,
