@@ -463,6 +463,14 @@ std::pair<void*, const void*> DeviceTape::acc_target(int id) {
     n.grad = alloc_elems(int64_t(n.rows) * n.cols);
     return {n.grad, nullptr};
   }
+  static const bool inplace = [] {  // SQF_ACC_INPLACE=1: wait for the reader, accumulate in place
+    const char* e = std::getenv("SQF_ACC_INPLACE");
+    return e && std::atoi(e) != 0;
+  }();
+  if (inplace) {
+    wait_side_reader(n.grad);
+    return {n.grad, n.grad};
+  }
   for (const auto& r : side_readers_)
     if (r.first == n.grad) {
       const void* old = n.grad;
