@@ -463,9 +463,12 @@ std::pair<void*, const void*> DeviceTape::acc_target(int id) {
     n.grad = alloc_elems(int64_t(n.rows) * n.cols);
     return {n.grad, nullptr};
   }
-  static const bool inplace = [] {  // SQF_ACC_INPLACE=1: wait for the reader, accumulate in place
+  // default: wait for the reader and accumulate in place (measured 118.6 vs
+  // 120.5 ms/step on C4 for out of place: the extra buffers and the unthrottled
+  // main stream cost more than the waits); SQF_ACC_INPLACE=0 goes out of place
+  static const bool inplace = [] {
     const char* e = std::getenv("SQF_ACC_INPLACE");
-    return e && std::atoi(e) != 0;
+    return !(e && std::atoi(e) == 0);
   }();
   if (inplace) {
     wait_side_reader(n.grad);
