@@ -114,23 +114,24 @@ struct Args {
 __device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.causal ? t + 1 : a.klen[b]; }
 
 // ------------------------------------------------------------------ forward
-template <typename T, int DH>
-__global__ void __launch_bounds__(kWarps * 32) fwd_k(Args a) {
+// R = query rows per CTA (64: 4 warps; 32: 2 warps for short sentences)
+template <typename T, int DH, int R>
+__global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
-  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kRows;
+  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * R;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];
   // keys any row of this block can see
-  const int nk = a.causal ? min(a.kw, min(q0 + kRows, a.qw)) : len;
+  const int nk = a.causal ? min(a.kw, min(q0 + R, a.qw)) : len;
   const int nk_pad = (nk + 63) & ~63;
   T* Qs = reinterpret_cast<T*>(smem);
-  T* Ks = Qs + kRows * LD;
+  T* Ks = Qs + R * LD;
   T* Vs = Ks + nk_pad * LD;
   const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
-  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0) + q0, min(kRows, a.qw - q0), kRows,
+  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0) + q0, min(R, a.qw - q0), R,
                a.dh);
   stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), nk, nk_pad, a.dh);
   stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), nk, nk_pad, a.dh);
@@ -492,13 +493,14 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
 // once and runs both halves of the backward -- dQ per query warp, then dK/dV
 // per key warp -- with D = rowsum(dO * O) and the saved softmax stats kept in
 // shared memory. Same arithmetic, in the same order, as bwd_dq_k + bwd_dkv_k.
-template <typename T, int DH>
-__global__ void __launch_bounds__(kWarps * 32, DH <= 64 ? 3 : 1) bwd_small_k(Args a) {
+// R = rows per CTA: 64 (4 warps) for widths <= 64, 32 (2 warps) for widths <= 32
+template <typename T, int DH, int R>
+__global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_small_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
-  constexpr int QP = 2 * kRows;  // staged query rows (zero-padded: dK/dV chunks run past qw)
+  constexpr int QP = R + 32;  // staged query rows (zero-padded: dK/dV chunks run up to 31 past qw)
   constexpr int NC = 32;  // query columns per dK/dV chunk (register budget: 3 CTAs per SM)
   const int b = blockIdx.z, h = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
@@ -507,17 +509,17 @@ __global__ void __launch_bounds__(kWarps * 32, DH <= 64 ? 3 : 1) bwd_small_k(Arg
   T* Qs = reinterpret_cast<T*>(smem);
   T* Gs = Qs + QP * LD;
   T* Ks = Gs + QP * LD;
-  T* Vs = Ks + kRows * LD;
-  T* Os = Vs + kRows * LD;  // forward output, for D = rowsum(dO * O)
-  float2* St = reinterpret_cast<float2*>(Os + kRows * LD);
+  T* Vs = Ks + R * LD;
+  T* Os = Vs + R * LD;  // forward output, for D = rowsum(dO * O)
+  float2* St = reinterpret_cast<float2*>(Os + R * LD);
   float* Ds = reinterpret_cast<float*>(St + QP);
   const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
   stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0), a.qw, QP, a.dh);
   stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0), a.qw, QP, a.dh);
   // dQ reads keys < nk; dK/dV rows are all kw key rows (rows >= nk get zero grads)
-  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), a.kw, kRows, a.dh);
-  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), a.kw, kRows, a.dh);
-  stage<T, DH>(Os, LD, static_cast<const T*>(a.o) + h * a.dh, a.ldo, int(qrow0), a.qw, kRows, a.dh);
+  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), a.kw, R, a.dh);
+  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), a.kw, R, a.dh);
+  stage<T, DH>(Os, LD, static_cast<const T*>(a.o) + h * a.dh, a.ldo, int(qrow0), a.qw, R, a.dh);
   for (int i = threadIdx.x; i < QP; i += blockDim.x) {
     St[i] = i < a.qw ? a.stats[(qrow0 + i) * a.heads + h] : make_float2(0.f, 0.f);
     Ds[i] = 0.f;
@@ -557,16 +559,17 @@ __global__ void __launch_bounds__(kWarps * 32, DH <= 64 ? 3 : 1) bwd_small_k(Arg
 #pragma unroll
     for (int i = 0; i < DH / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
     {
-      constexpr int kc = 0;  // all keys fit one 64-key chunk
-      float s[8][4], dp[8][4];
+      constexpr int kc = 0;  // all keys fit one R-key chunk
+      constexpr int NT = R / 8;
+      float s[NT][4], dp[NT][4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < NT; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e) s[i][e] = dp[i][e] = 0.f;
 #pragma unroll
       for (int ks = 0; ks < DH / 16; ++ks)
 #pragma unroll
-        for (int nt = 0; nt < 8; nt += 2) {
+        for (int nt = 0; nt < NT; nt += 2) {
           uint32_t bk[4], bv[4];
           load_b_nk<T>(bk, Ks, LD, kc + nt * 8, ks * 16, lane);
           load_b_nk<T>(bv, Vs, LD, kc + nt * 8, ks * 16, lane);
@@ -576,7 +579,7 @@ __global__ void __launch_bounds__(kWarps * 32, DH <= 64 ? 3 : 1) bwd_small_k(Arg
           MmaT<T>::mma(dp[nt + 1], ga[ks], bv[2], bv[3]);
         }
 #pragma unroll
-      for (int nt = 0; nt < 8; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int j = kc + nt * 8 + 2 * tq + e;
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(kWarps * 32, DH <= 64 ? 3 : 1) bwd_small_k(Arg
           s[nt][2 + e] = pb * (dp[nt][2 + e] - D_b);
         }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < NT / 2; ++kk) {
         uint32_t da[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
                           MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
                           MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
@@ -742,21 +745,37 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   const int kpad = (a.kw + 63) & ~63, qpad = ((a.qw + 63) & ~63) + 64;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(fwd_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dq_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   const dim3 gq((a.qw + kRows - 1) / kRows, a.heads, a.batch);
+  // sentences of <= 32 positions: 32-row CTAs of 2 warps, so no warp idles
+  const bool short32 = a.qw <= 32 && (bwd ? a.kw <= 32 : true);
   if (!bwd) {
-    const size_t smem = size_t(kRows + 2 * kpad) * LD * sizeof(T);
-    launch_pdl(fwd_k<T, DH>, gq, kWarps * 32, smem, st, a);
+    if (short32) {
+      const size_t smem = size_t(32 + 2 * kpad) * LD * sizeof(T);
+      launch_pdl(fwd_k<T, DH, 32>, dim3(1, a.heads, a.batch), 64, smem, st, a);
+    } else {
+      const size_t smem = size_t(kRows + 2 * kpad) * LD * sizeof(T);
+      launch_pdl(fwd_k<T, DH, 64>, gq, kWarps * 32, smem, st, a);
+    }
     return check_launch("sfk_attention_fwd(mma)");
   }
+  if (short32) {
+    constexpr int R = 32, QP = R + 32;
+    const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
+    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
+    return check_launch("sfk_attention_bwd(small32)");
+  }
   if (a.qw <= kRows && a.kw <= kRows) {
-    const size_t smem_s = size_t(4 * kRows + 3 * kRows) * LD * sizeof(T) + size_t(2 * kRows) * 12;
-    launch_pdl(bwd_small_k<T, DH>, dim3(1, a.heads, a.batch), kWarps * 32, smem_s, st, a);
+    constexpr int R = 64, QP = R + 32;
+    const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
+    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
     return check_launch("sfk_attention_bwd(small)");
   }
   const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
