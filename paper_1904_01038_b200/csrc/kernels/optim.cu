@@ -56,28 +56,12 @@ __global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   if (skip && *skip) return;
-  // software-pipelined: the next group's loads are in flight while this
-  // group's (FP64, issue-heavy) update runs
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  float4 p4, m4, v4;
-  uint2 g2;
-  if (q < n4) {
-    p4 = *reinterpret_cast<const float4*>(master + 4 * q);
-    m4 = *reinterpret_cast<const float4*>(m + 4 * q);
-    v4 = *reinterpret_cast<const float4*>(v + 4 * q);
-    g2 = *reinterpret_cast<const uint2*>(grad + 4 * q);
-  }
-  for (; q < n4; q += stride) {
-    const int64_t i = 4 * q, qn = q + stride;
-    float4 pn, mn, vn;
-    uint2 gn;
-    if (qn < n4) {
-      pn = *reinterpret_cast<const float4*>(master + 4 * qn);
-      mn = *reinterpret_cast<const float4*>(m + 4 * qn);
-      vn = *reinterpret_cast<const float4*>(v + 4 * qn);
-      gn = *reinterpret_cast<const uint2*>(grad + 4 * qn);
-    }
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < n4; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = 4 * q;
+    float4 p4 = *reinterpret_cast<const float4*>(master + i);
+    float4 m4 = *reinterpret_cast<const float4*>(m + i);
+    float4 v4 = *reinterpret_cast<const float4*>(v + i);
+    const uint2 g2 = *reinterpret_cast<const uint2*>(grad + i);
     const G* gg = reinterpret_cast<const G*>(&g2);
     float* pp = &p4.x;
     float* mp = &m4.x;
@@ -103,7 +87,6 @@ __global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __
 #pragma unroll
       for (int j = 0; j < 4; ++j) Num<S>::st(shadow + i + j, pp[j]);
     }
-    p4 = pn, m4 = mn, v4 = vn, g2 = gn;
   }
 }
 
