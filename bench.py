@@ -310,6 +310,8 @@ def run_ours(args, cfg):
         "profile_ms_per_step": {k: round(v[0], 3) for k, v in prof.items()},
         "clocks": clk.summary(),
     }
+    if world == 1:
+        line["predicted_scaling"] = predict_scaling(tr, sqf, dev_ms_max / args.steps, cfg["accum"])
     if world == 1 and not args.no_cpu_baseline:
         try:
             thr = ref_threads()
@@ -322,6 +324,27 @@ def run_ours(args, cfg):
             line["cpu_baseline"] = {"value": None, "unit": "tgt_tokens/s", "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {ex}"}
     print(json.dumps(line), flush=True)
+
+
+def predict_scaling(tr, sqf, step_ms, accum, bus_gbs=400.0):
+    """Model, not a measurement: the reference's timeline simulator
+    (simulate_timeline, overlap_accum policy) fed with this run's measured
+    sub-batch time and each gradient bucket's ring all-reduce time at an
+    assumed NCCL bus bandwidth over NVLink 5 (bus_gbs, per direction).
+    Returns the predicted weak-scaling efficiency at 2/4/8 GPUs."""
+    sizes = [e[2] for e in sorted(tr.manifest(), key=lambda e: e[3])]
+    buckets = sqf.bucket_gradients(sizes, 1 << 23)
+    esize = 2
+    sub_ms = step_ms / accum
+    out = {"model": "simulate_timeline overlap_accum, ring all-reduce at %.0f GB/s bus bandwidth (assumed)" % bus_gbs,
+           "sub_batch_ms": round(sub_ms, 3)}
+    for n in (2, 4, 8):
+        comm = [max(1e-6, 2.0 * (n - 1) / n * (b - a) * esize / (bus_gbs * 1e9) * 1e3) for a, b in buckets]
+        rows = "\n".join(f"compute {w} " + " ".join([repr(sub_ms)] * accum) for w in range(n))
+        text = f"workers {n}\naccum {accum}\nmode overlap_accum\n{rows}\nbuckets " + " ".join(map(repr, comm)) + "\n"
+        r = sqf.simulate_timeline(text)
+        out[f"efficiency_{n}gpu"] = round(sub_ms * accum / r["makespan"], 4)
+    return out
 
 
 def main():

@@ -96,6 +96,12 @@ int sqf_checkpoint_info(const char* path, int32_t* version, int64_t* nparams, in
                         int64_t* meta_bytes);
 int sqf_checkpoint_read(const char* path, float* params, float* opt, char* meta, int64_t meta_cap);
 
+/* Data-parallel timeline model (simulate_timeline / format_report,
+ * simulator.cpp:12-229): scenario text (workers, accum, mode
+ * serial_sync|overlap|overlap_accum, compute rows, buckets) in, the report
+ * text ("makespan", "idle <w>", "exposed_comm", "total_compute", %.17g) out. */
+int sqf_simulate_timeline(const char* scenario, char* report, int cap);
+
 /* all-reduce/backward overlap of the last step (config overlap_allreduce; with
  * world 1 only under overlap_simulate): bucket indices in issue order (up to
  * cap written), *early = how many were issued while backward was running.

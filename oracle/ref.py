@@ -108,6 +108,7 @@ def _declare(L):
     s("sqfref_trainer_subbatch_grad", C.c_int, vp, vp, vp, C.c_int, f32, vp, P(StatsC))
     s("sqfref_trainer_evaluate", C.c_int, vp, vp, P(f64), P(f64), P(i64), P(i64))
     s("sqfref_trainer_save", C.c_int, vp, cp)
+    s("sqfref_simulate_timeline", C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, vp, C.c_int)
     s("sqfref_checkpoint_read", C.c_int, cp, P(i32), P(i64), vp, P(i64), vp)
     s("sqfref_checkpoint_meta", C.c_int, cp, cp, vp, C.c_int)
 
@@ -314,6 +315,17 @@ def _kv(overrides):
     ka = (cp * max(1, len(keys)))(*[k.encode() for k in keys])
     va = (cp * max(1, len(vals)))(*[v.encode() for v in vals])
     return ka, va, len(keys)
+
+
+def simulate_timeline(workers, accum, mode, compute, buckets):
+    """The reference's simulate_timeline + format_report (simulator.cpp) on a
+    scenario given as values; returns the report text."""
+    modes = {"serial_sync": 0, "overlap": 1, "overlap_accum": 2}
+    c = np.ascontiguousarray(np.asarray(compute, np.float64).reshape(workers, accum))
+    b = np.ascontiguousarray(np.asarray(buckets, np.float64))
+    buf = C.create_string_buffer(1 << 16)
+    _ck(lib().sqfref_simulate_timeline(workers, accum, modes[mode], _ptr(c), _ptr(b), len(b), buf, 1 << 16))
+    return buf.value.decode()
 
 
 def checkpoint_read(path):

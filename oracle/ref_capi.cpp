@@ -11,10 +11,12 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "seqforge/checkpoint.hpp"
+#include "seqforge/simulator.hpp"
 #include "seqforge/common.hpp"
 #include "seqforge/criterions.hpp"
 #include "seqforge/data.hpp"
@@ -569,6 +571,26 @@ int sqfref_trainer_evaluate(void* h, void* corpus, double* loss, double* nll, in
     *nll = e.nll;
     *ntokens = e.ntokens;
     *ncorrect = e.ncorrect;
+  })
+}
+
+// ---------------------------------------------------------------- timeline model
+// the reference's simulate_timeline + format_report on a scenario given as
+// arrays (its text parser takes a std::istream, which must not be used here:
+// under a Python process with numpy loaded first the iostream facets of the
+// host libstdc++ differ from this library's)
+int sqfref_simulate_timeline(int workers, int accum, int mode, const double* compute, const double* comm, int nb,
+                             char* report, int cap) {
+  GUARD({
+    SimScenario sc;
+    sc.workers = workers;
+    sc.accum = accum;
+    sc.mode = mode == 0 ? SyncMode::SerialSync : mode == 1 ? SyncMode::Overlap : SyncMode::OverlapAccum;
+    for (int w = 0; w < workers; ++w) sc.compute.emplace_back(compute + int64_t(w) * accum, compute + int64_t(w + 1) * accum);
+    sc.comm.assign(comm, comm + nb);
+    const std::string text = format_report(simulate_timeline(sc));
+    if (int(text.size()) + 1 > cap) throw BoundsError("buffer");
+    std::memcpy(report, text.c_str(), text.size() + 1);
   })
 }
 

@@ -165,6 +165,22 @@ def quantize_fp16(x: float) -> float:
     return float(L.sqf_quantize_fp16(x))
 
 
+def simulate_timeline(scenario: str) -> dict:
+    """Timeline model of a data-parallel step (simulator.cpp): scenario text in,
+    {"makespan", "idle": [...], "exposed_comm", "total_compute"} out."""
+    buf = C.create_string_buffer(1 << 16)
+    L.check(L.sqf_simulate_timeline(scenario.encode(), buf, 1 << 16))
+    out = {"idle": []}
+    for line in buf.value.decode().splitlines():
+        f = line.split()
+        if f[0] == "idle":
+            out["idle"].append(float(f[2]))
+        else:
+            out[f[0]] = float(f[1])
+    out["text"] = buf.value.decode()
+    return out
+
+
 def read_checkpoint(path):
     """Raw parse of an SQFG checkpoint: (version, meta dict, params, opt)."""
     v, npar, nopt, mb = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()

@@ -7,6 +7,7 @@
 #include "../../../include/sqf_trainer.h"
 #include "nccl_dyn.hpp"
 #include "checkpoint.hpp"
+#include "simulator.hpp"
 #include "trainer.hpp"
 
 namespace sqf {
@@ -264,6 +265,14 @@ int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h) {
   return T(t)->last_h2d_bytes();
 }
 void* sqf_trainer_stream(void* t) { return static_cast<void*>(T(t)->stream()); }
+
+int sqf_simulate_timeline(const char* scenario, char* report, int cap) {
+  SQF_GUARD({
+    const std::string text = format_report(simulate_timeline(parse_scenario(scenario)));
+    if (int(text.size()) + 1 > cap) throw BoundsError("sqf_simulate_timeline: report buffer too small");
+    std::memcpy(report, text.c_str(), text.size() + 1);
+  })
+}
 
 int sqf_trainer_save(void* t, const char* path) { SQF_GUARD(save_checkpoint(*T(t), path)) }
 
