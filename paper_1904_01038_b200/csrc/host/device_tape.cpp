@@ -7,10 +7,9 @@
 
 namespace sqf {
 
-// Timing experiments only (results are wrong when set): SQF_DEBUG_SKIP is a
-// bit mask of launch classes the tape does not enqueue -- 1 bias grads,
-// 2 LN gamma/beta, 4 wgrad GEMMs, 8 attention backward.
-// SQF_WGRAD_TILE=0 restores the wave-efficiency tile choice for the side-stream GEMMs
+// Measured scheduling knobs (defaults are the measured-best settings; see
+// DESIGN.md §5): SQF_WGRAD_TILE=0 restores the wave-efficiency tile choice for
+// the side-stream weight-gradient GEMMs.
 static int tile_env() {
   static const int v = [] {
     const char* e = std::getenv("SQF_WGRAD_TILE");
@@ -19,20 +18,13 @@ static int tile_env() {
   return v;
 }
 
+// SQF_LN_FUSED=1: one-pass LN backward (dx + gamma/beta partials on the main stream)
 static bool ln_fused_env() {
   static const bool v = [] {
     const char* e = std::getenv("SQF_LN_FUSED");
     return e && std::atoi(e) != 0;
   }();
   return v;
-}
-
-static int debug_skip() {
-  static const int m = [] {
-    const char* v = std::getenv("SQF_DEBUG_SKIP");
-    return v ? std::atoi(v) : 0;
-  }();
-  return m;
 }
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -534,7 +526,6 @@ void DeviceTape::join_side() {
 }
 
 void DeviceTape::bias_grad(const void* dy, int rows, int cols, int64_t ld, void* out) {
-  if (debug_skip() & 1) return;
   // sfk_colsum scratch: min(512 * cols, 4M) floats
   const size_t part_floats = std::min<size_t>(size_t(512) * cols, size_t(4) << 20);
   float* part = static_cast<float*>(arena_.alloc(part_floats * 4));
@@ -611,7 +602,7 @@ void DeviceTape::backward_node(int id) {
       // SQF_LN_FUSED=1: one-pass dx + gamma/beta partials on the main stream
       // (measured slower on C4, 121.1 vs 119.3 ms/step: the longer
       // critical-path kernel costs more than the side-stream pass it saves)
-      if (ln_fused_env() && dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024 && !(debug_skip() & 2)) {
+      if (ln_fused_env() && dtype_ != SFK_F32 && n.cols % 8 == 0 && n.cols <= 1024) {
         // dx and the gamma/beta column partials in one pass over x and dy on
         // the main stream; only the small fold of the partials is side work
         float* lpart = static_cast<float*>(arena_.alloc(size_t(2) * ((n.rows + 15) / 16) * n.cols * 4));
@@ -656,7 +647,7 @@ void DeviceTape::backward_node(int id) {
           cur_ = side_;
         }
         pbegin();
-        if (!(debug_skip() & 2)) sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
+        sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
                                            counters((n.cols + 255) / 256), gptr(n.p0), gptr(n.p1), cur_),
                   "layernorm_bwd_params");
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
@@ -706,10 +697,9 @@ void DeviceTape::backward_node(int id) {
       }
       // 16-bit: the bias gradient rides in the weight-gradient GEMM (its
       // epilogue warps sum dY out of the A tiles in shared memory)
-      const bool fused_db = n.has_bias && dtype_ != SFK_F32 && !(debug_skip() & 16);
+      const bool fused_db = n.has_bias && dtype_ != SFK_F32;
       if (n.has_bias && !fused_db) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
-      if (!(debug_skip() & 4))
-        gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
+      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
              n.p0.cols, SFK_EPI_ACCUM, nullptr, nullptr, 0, nullptr, 0, fused_db ? gptr(n.p1) : nullptr);
       if (n.has_bias) grad_done(n.p1);
       grad_done(n.p0);
@@ -800,7 +790,7 @@ void DeviceTape::backward_node(int id) {
       a.lddv = kn.cols;
       a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
       pbegin();
-      if (!(debug_skip() & 8)) sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
+      sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
       pend(Profiler::AttnBwd, attn_flops(n.batch, n.q_width, n.k_width, n.k_len, n.cols, n.causal, true),
            double(esize_) * n.cols * (4.0 * n.rows + 4.0 * kn.rows));
       launches_ += 2;
