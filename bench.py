@@ -357,8 +357,16 @@ def main():
     ap.add_argument("--ref-max-tokens", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce after backward (C5 'overlap off')")
+    ap.add_argument("--max-tokens", type=int, default=0, help="per-GPU token budget override (C5 sweep)")
+    ap.add_argument("--accum", type=int, default=0, help="update_freq override")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.max_tokens:
+        cfg["max_tokens"] = args.max_tokens
+        cfg["desc"] += f" (max_tokens override {args.max_tokens})"
+    if args.accum:
+        cfg["accum"] = args.accum
+        cfg["desc"] += f" (update_freq override {args.accum})"
     if args.impl == "reference":
         run_reference_arm(args, cfg)
     else:
