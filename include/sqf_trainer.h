@@ -32,6 +32,8 @@ typedef struct sqf_step_stats {
 } sqf_step_stats;
 
 const char* sqf_last_error(void);
+/* status code of the last failure on this thread (for entries returning NULL) */
+int sqf_last_status(void);
 
 /* NCCL unique id (128 bytes) for multi-process data parallelism; rank 0
  * creates it and the launcher broadcasts it (torch.distributed store). */
@@ -48,6 +50,17 @@ void* sqf_trainer_create(const char* arch, const char* const* keys, const char* 
                          const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab,
                          int rank, int world, const void* nccl_id);
 void sqf_trainer_free(void* t);
+
+/* A task made through the registry from the resolved config's "task" key
+ * (Registry::make_task; "translation" = TranslationTask, tasks.cpp:7-33,
+ * reading train_src/train_tgt text and dict_src/dict_tgt or building the
+ * dictionaries with min_count). info gives the dictionary sizes, pair count
+ * and total ids; pairs fills eos-terminated ids, concatenated. */
+void* sqf_task_create(const char* arch, const char* const* keys, const char* const* vals, int n);
+void sqf_task_free(void* t);
+int sqf_task_info(void* t, int32_t* src_vocab, int32_t* tgt_vocab, int32_t* npairs, int64_t* src_tokens,
+                  int64_t* tgt_tokens);
+int sqf_task_pairs(void* t, int32_t* src_len, int32_t* tgt_len, int32_t* src_ids, int32_t* tgt_ids);
 
 /* Trainer::train_one (trainer.cpp:204-208): 0 ok, 1 exhausted */
 int sqf_trainer_train_one(void* t, sqf_step_stats* out);

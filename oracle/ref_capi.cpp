@@ -26,6 +26,7 @@
 #include "seqforge/registry.hpp"
 #include "seqforge/rng.hpp"
 #include "seqforge/tape.hpp"
+#include "seqforge/tasks.hpp"
 #include "seqforge/trainer.hpp"
 
 using namespace seqforge;
@@ -571,6 +572,28 @@ int sqfref_trainer_evaluate(void* h, void* corpus, double* loss, double* nll, in
     *nll = e.nll;
     *ntokens = e.ntokens;
     *ncorrect = e.ncorrect;
+  })
+}
+
+// ---------------------------------------------------------------- translation task
+// the reference's TranslationTask (tasks.cpp:7-33) built from a resolved config;
+// dumps "<src_vocab> <tgt_vocab> <npairs>\n" then one "src ids | tgt ids" line per pair
+int sqfref_task_dump(const char* arch, const char** keys, const char** vals, int n, char* out, int64_t cap) {
+  GUARD({
+    std::vector<std::pair<std::string, std::string>> user;
+    for (int i = 0; i < n; ++i) user.emplace_back(keys[i], vals[i]);
+    Config cfg = oracle_registry().resolve_architecture(arch, user);
+    TranslationTask task(cfg);
+    std::string text = std::to_string(task.source_dict().size()) + " " + std::to_string(task.target_dict().size()) +
+                       " " + std::to_string(task.train_pairs().size()) + "\n";
+    for (const auto& p : task.train_pairs()) {
+      for (int x : p.source) text += std::to_string(x) + " ";
+      text += "|";
+      for (int x : p.target) text += " " + std::to_string(x);
+      text += "\n";
+    }
+    if (int64_t(text.size()) + 1 > cap) throw BoundsError("buffer");
+    std::memcpy(out, text.c_str(), text.size() + 1);
   })
 }
 

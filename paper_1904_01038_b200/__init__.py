@@ -165,6 +165,31 @@ def quantize_fp16(x: float) -> float:
     return float(L.sqf_quantize_fp16(x))
 
 
+def load_task(arch: str, overrides: dict):
+    """The task the config names, made through the registry (e.g. task=translation
+    with train_src/train_tgt files): (src_vocab, tgt_vocab, [(source ids, target ids)])."""
+    k, v, n = _kv(overrides)
+    h = L.sqf_task_create(arch.encode(), k, v, n)
+    if not h:
+        raise L.NativeError(L.sqf_last_status(), L.sqf_last_error().decode())
+    try:
+        sv, tv, npairs, ns, nt = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64(), C.c_int64()
+        L.check(L.sqf_task_info(h, C.byref(sv), C.byref(tv), C.byref(npairs), C.byref(ns), C.byref(nt)))
+        sl = np.zeros(max(1, npairs.value), np.int32)
+        tl = np.zeros(max(1, npairs.value), np.int32)
+        si = np.zeros(max(1, ns.value), np.int32)
+        ti = np.zeros(max(1, nt.value), np.int32)
+        L.check(L.sqf_task_pairs(h, _ptr(sl), _ptr(tl), _ptr(si), _ptr(ti)))
+        pairs, a, b = [], 0, 0
+        for i in range(npairs.value):
+            pairs.append((si[a:a + sl[i]].tolist(), ti[b:b + tl[i]].tolist()))
+            a += sl[i]
+            b += tl[i]
+        return sv.value, tv.value, pairs
+    finally:
+        L.sqf_task_free(h)
+
+
 def simulate_timeline(scenario: str) -> dict:
     """Timeline model of a data-parallel step (simulator.cpp): scenario text in,
     {"makespan", "idle": [...], "exposed_comm", "total_compute"} out."""
@@ -232,7 +257,7 @@ class Trainer:
         else:
             h = L.sqf_trainer_create(arch.encode(), k, v, n, None, None, None, None, 0, 0, 0, rank, world, idbuf)
         if not h:
-            raise L.NativeError(-9, (L.sqf_last_error() or b"").decode())
+            raise L.NativeError(L.sqf_last_status(), (L.sqf_last_error() or b"").decode())
         self._h = h
         self.workers = int(overrides.get("workers", 1))
         self.accum = int(overrides.get("accum", 1))

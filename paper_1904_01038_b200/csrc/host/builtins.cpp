@@ -5,6 +5,7 @@
 // and the tasks. Named architectures add the BASELINE.json configs.
 #include <cmath>
 
+#include "translation.hpp"
 #include "device_tape.hpp"
 #include "plugins.hpp"
 
@@ -570,6 +571,8 @@ void register_builtins(Registry& r) {
   r.register_criterion("label_smoothed_cross_entropy", [](const Config& cfg) -> std::unique_ptr<CriterionBase> {
     return std::make_unique<XentCriterion>(cfg.get_real("label_smoothing"));
   });
+  r.register_task("translation",
+                  [](const Config& cfg) -> std::unique_ptr<TaskBase> { return std::make_unique<TranslationTask>(cfg); });
   r.register_task("synthetic",
                   [](const Config& cfg) -> std::unique_ptr<TaskBase> { return std::make_unique<SyntheticTask>(cfg); });
   r.register_optimizer("sgd", [](const Config&, int64_t) -> std::unique_ptr<OptimizerBase> {

@@ -14,9 +14,14 @@ namespace sqf {
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_code = 0;
 
+int code_of(const std::exception& e);
 int fail(const std::exception& e) {
   g_err = e.what();
+  return g_code = code_of(e);
+}
+int code_of(const std::exception& e) {
   if (dynamic_cast<const ConfigError*>(&e)) return -1;
   if (dynamic_cast<const ShapeError*>(&e)) return -2;
   if (dynamic_cast<const BoundsError*>(&e)) return -3;
@@ -95,6 +100,7 @@ using namespace sqf;
 extern "C" {
 
 const char* sqf_last_error(void) { return g_err.c_str(); }
+int sqf_last_status(void) { return g_code; }
 
 int sqf_nccl_unique_id(void* out128) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
@@ -128,6 +134,46 @@ void* sqf_trainer_create(const char* arch, const char* const* keys, const char* 
 }
 
 void sqf_trainer_free(void* t) { delete T(t); }
+
+void* sqf_task_create(const char* arch, const char* const* keys, const char* const* vals, int n) {
+  try {
+    const Registry& reg = global_registry();
+    Config cfg = reg.resolve_architecture(arch, user_kv(keys, vals, n));
+    return reg.make_task(cfg.get_str("task"), cfg).release();
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+void sqf_task_free(void* t) { delete static_cast<TaskBase*>(t); }
+
+int sqf_task_info(void* t, int32_t* src_vocab, int32_t* tgt_vocab, int32_t* npairs, int64_t* src_tokens,
+                  int64_t* tgt_tokens) {
+  SQF_GUARD({
+    const TaskBase& task = *static_cast<TaskBase*>(t);
+    *src_vocab = task.source_vocab();
+    *tgt_vocab = task.target_vocab();
+    *npairs = int32_t(task.train_pairs().size());
+    int64_t a = 0, b = 0;
+    for (const auto& p : task.train_pairs()) a += int64_t(p.source.size()), b += int64_t(p.target.size());
+    *src_tokens = a;
+    *tgt_tokens = b;
+  })
+}
+
+int sqf_task_pairs(void* t, int32_t* src_len, int32_t* tgt_len, int32_t* src_ids, int32_t* tgt_ids) {
+  SQF_GUARD({
+    const auto& pairs = static_cast<TaskBase*>(t)->train_pairs();
+    int64_t a = 0, b = 0;
+    for (size_t i = 0; i < pairs.size(); ++i) {
+      src_len[i] = int32_t(pairs[i].source.size());
+      tgt_len[i] = int32_t(pairs[i].target.size());
+      for (int x : pairs[i].source) src_ids[a++] = x;
+      for (int x : pairs[i].target) tgt_ids[b++] = x;
+    }
+  })
+}
 
 int sqf_trainer_train_one(void* t, sqf_step_stats* out) {
   try {

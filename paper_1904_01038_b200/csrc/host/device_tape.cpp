@@ -55,6 +55,20 @@ void* Arena::alloc(size_t bytes) {
 }
 
 void Arena::reset() {
+  // A sub-batch that needed more than one chunk means the arena is still
+  // growing: merge everything into one chunk of the combined size, so a
+  // workload settles after a few sub-batches instead of allocating whenever
+  // the (first-fit, forward-only) cursor skips past a chunk. cudaFree waits
+  // for the device, so no in-flight kernel still uses the old chunks.
+  if (chunks_.size() > 1) {
+    size_t total = 0;
+    for (auto& c : chunks_) total += c.size;
+    for (auto& c : chunks_) cuda_check(cudaFree(c.base), "arena cudaFree");
+    chunks_.clear();
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, total), "arena cudaMalloc");
+    chunks_.push_back({static_cast<char*>(p), total, 0});
+  }
   for (auto& c : chunks_) c.used = 0;
   cur_ = 0;
 }

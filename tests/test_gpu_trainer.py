@@ -217,3 +217,22 @@ def test_deal_dispatch_with_prefetch_matches_reference_replay():
             break
     assert steps >= 4
     assert rel(mine.params(), theirs.params()) < 1e-4
+
+
+def test_translation_task_from_files_trains_like_in_memory(tmp_path):
+    """task=translation (text files -> dictionaries -> pairs, tasks.cpp:7-33)
+    feeds the same trainer path as an in-memory corpus of the same pairs."""
+    import paper_1904_01038_b200 as sqf
+    src = ["das haus ist klein", "das haus ist sehr klein", "ein neues haus", "haus haus das ist"] * 12
+    tgt = ["the house is small", "the house is very small", "a new house", "house house the is"] * 12
+    (tmp_path / "t.src").write_text("\n".join(src) + "\n")
+    (tmp_path / "t.tgt").write_text("\n".join(tgt) + "\n")
+    ov = dict(BASE, task="translation", train_src=str(tmp_path / "t.src"), train_tgt=str(tmp_path / "t.tgt"),
+              max_tokens=256, fp16=True)
+    sv, tv, pairs = sqf.load_task("transformer_base_defaults", ov)
+    a = sqf.Trainer("transformer_base_defaults", ov)
+    mem = {k: v for k, v in ov.items() if k not in ("task", "train_src", "train_tgt")}
+    b = sqf.Trainer("transformer_base_defaults", mem, corpus=sqf.Corpus.from_pairs(pairs), src_vocab=sv, tgt_vocab=tv)
+    for _ in range(3):
+        assert a.train_one() == b.train_one()
+    assert np.array_equal(a.params(), b.params())
