@@ -340,7 +340,7 @@ class TransformerModel : public ModelBase {
       x = residual(t, h, l.w2, &l.b2, false, x, site);
     }
     x = t.layer_norm(x, dec_lng_, dec_lnb_);
-    return t.linear(x, out_proj_, nullptr, false);
+    return t.logits(x, out_proj_);
   }
 };
 

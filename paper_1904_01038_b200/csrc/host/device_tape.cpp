@@ -332,6 +332,23 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
   ++launches_;
 }
 
+int DeviceTape::logits(int x, ParamRef w) {
+  const Node& in = nodes_[x];
+  if (in.cols != w.cols) throw ShapeError("matmul_nt: inner dimension mismatch");
+  Node n;
+  n.kind = Kind::Linear;
+  n.in0 = x;
+  n.p0 = w;
+  n.rows = in.rows;
+  n.cols = w.rows;
+  n.ld = dtype_ == SFK_F32 ? n.cols : (int64_t(n.cols) + 7) / 8 * 8;
+  n.out = alloc_elems(int64_t(n.rows) * n.ld);
+  gemm(Profiler::GemmFwd, n.rows, n.cols, in.cols, in.out, in.cols, true, pptr(w), w.cols, true, n.out, n.ld,
+       SFK_EPI_PREROUND);
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
 int DeviceTape::linear(int x, ParamRef w, const ParamRef* bias, bool relu, int residual) {
   const Node& in = nodes_[x];
   if (in.cols != w.cols) throw ShapeError("matmul_nt: inner dimension mismatch");
@@ -346,6 +363,7 @@ int DeviceTape::linear(int x, ParamRef w, const ParamRef* bias, bool relu, int r
   n.relu = relu;
   n.rows = in.rows;
   n.cols = w.rows;
+  n.ld = n.cols;
   if (residual >= 0 && (nodes_[residual].rows != n.rows || nodes_[residual].cols != n.cols))
     throw ShapeError("add: shape mismatch");
   n.out = alloc_elems(int64_t(n.rows) * n.cols);
@@ -493,7 +511,7 @@ void DeviceTape::run_xent(Node& n, float seed, bool with_grad, double* stats_acc
   Node& lg = nodes_[n.in0];
   // the logits buffer becomes its own gradient (dlogits written in place)
   pbegin();
-  sfk_check(sfk_xent_fwd_bwd(dtype_, lg.out, lg.rows, lg.cols, lg.cols, n.gold, kPad, n.eps, seed,
+  sfk_check(sfk_xent_fwd_bwd(dtype_, lg.out, lg.rows, lg.cols, lg.ld ? lg.ld : lg.cols, n.gold, kPad, n.eps, seed,
                              with_grad ? lg.out : nullptr, n.row_out, cur_),
             "xent");
   sfk_check(sfk_xent_reduce(n.row_out, n.rows, stats_acc, cur_), "xent_reduce");
@@ -712,8 +730,9 @@ void DeviceTape::backward_node(int id) {
       // 16-bit: the bias gradient rides in the weight-gradient GEMM (its
       // epilogue warps sum dY out of the A tiles in shared memory)
       const bool fused_db = n.has_bias && dtype_ != SFK_F32;
-      if (n.has_bias && !fused_db) bias_grad(dy, n.rows, n.cols, n.cols, gptr(n.p1));
-      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, n.cols, false, in.out, in.cols, false, gptr(n.p0),
+      const int64_t ldy = n.ld ? n.ld : n.cols;
+      if (n.has_bias && !fused_db) bias_grad(dy, n.rows, n.cols, ldy, gptr(n.p1));
+      gemm(Profiler::GemmWgrad, n.cols, in.cols, n.rows, dy, ldy, false, in.out, in.cols, false, gptr(n.p0),
              n.p0.cols, SFK_EPI_ACCUM, nullptr, nullptr, 0, nullptr, 0, fused_db ? gptr(n.p1) : nullptr);
       if (n.has_bias) grad_done(n.p1);
       grad_done(n.p0);
@@ -746,7 +765,7 @@ void DeviceTape::backward_node(int id) {
         mask = inm.out;
         inm.grad_masked = true;
       }
-      gemm(Profiler::GemmDgrad, n.rows, in.cols, n.cols, dy, n.cols, true, pptr(n.p0), n.p0.cols, false, dx, in.cols,
+      gemm(Profiler::GemmDgrad, n.rows, in.cols, n.cols, dy, ldy, true, pptr(n.p0), n.p0.cols, false, dx, in.cols,
            flags, nullptr, flags == SFK_EPI_RESIDUAL ? acc : nullptr, in.cols, mask, in.cols);
       return;
     }

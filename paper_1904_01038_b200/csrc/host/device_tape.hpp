@@ -125,6 +125,11 @@ class DeviceTape {
   int layer_norm(int x, ParamRef gamma, ParamRef beta);
   // a9 (+a11 bias, a12 relu, a13 residual add): y = [res +] [relu](x W^T [+ b])
   int linear(int x, ParamRef w, const ParamRef* bias, bool relu, int residual = -1);
+  // the output projection: like linear(x, w, nullptr, false) but the logits
+  // rows get a leading dimension rounded up to 8 elements, so a vocabulary of
+  // any size keeps the 16-byte row alignment the tensor-core GEMMs (dgrad,
+  // wgrad read dlogits through TMA) and the vectorised xent need
+  int logits(int x, ParamRef w);
   // a16: q/k/v are column slices [q_col, q_col+d) of node q and [k_col..), [v_col..) of node kv
   int attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
                 int k_width, bool causal, const int32_t* k_len);
@@ -187,6 +192,7 @@ class DeviceTape {
     ParamRef p0{}, p1{};
     bool has_bias = false, relu = false, causal = false;
     int rows = 0, cols = 0;
+    int64_t ld = 0;  // row stride of out/grad (== cols except for padded logits)
     void* out = nullptr;
     void* grad = nullptr;
     bool grad_masked = false;  // relu node: grad already holds d(pre-activation)
