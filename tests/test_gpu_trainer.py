@@ -236,3 +236,36 @@ def test_translation_task_from_files_trains_like_in_memory(tmp_path):
     for _ in range(3):
         assert a.train_one() == b.train_one()
     assert np.array_equal(a.params(), b.params())
+
+
+@pytest.mark.parametrize("ov", [
+    {"max_tokens": 1024, "workers": 2, "accum": 2, "fp16": True, "dropout": 0.1},  # replicas + accumulation + dropout
+    {"max_tokens": 1024, "fp16": True, "share_embeddings": True},                  # tied embeddings on the 16-bit path
+    {"max_tokens": 1024, "workers": 2, "accum": 2, "fp16": True, "dispatch": "deal"},
+])
+def test_fp16_variants_track_reference(ov):
+    """fp16 loss within 1e-2 of the reference's emulated fp16, identical skip
+    decisions, for replica folding, tied embeddings and deal dispatch."""
+    mine, theirs, c = pair("transformer_base_defaults", ov)
+    if ov.get("dispatch") == "deal":
+        import paper_1904_01038_b200 as sqf
+        plan = sqf.make_batches(c, ov["max_tokens"], 0, 1)
+        order = sqf.shuffle_epoch(len(plan), 1, 1)
+        for s in range(3):
+            sub = [[plan[order[s * 4 + w * 2 + a]] for a in range(2)] for w in range(2)]
+            a, b = mine.train_one(), theirs.train_step(sub)
+            assert a["ntokens"] == b["ntokens"] and a["skipped"] == b["skipped"]
+            assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"])
+        return
+    for _ in range(3):
+        a, b = mine.train_one(), theirs.train_one()
+        assert a["ntokens"] == b["ntokens"] and a["skipped"] == b["skipped"]
+        assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"])
+
+
+def test_bf16_dropout_within_1e2_of_reference_fp32():
+    mine, theirs, _ = pair("transformer_base_defaults", {"max_tokens": 1024, "bf16": True, "dropout": 0.1})
+    for _ in range(3):
+        a, b = mine.train_one(), theirs.train_one()
+        assert a["ntokens"] == b["ntokens"]
+        assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"])
