@@ -241,7 +241,7 @@ def test_translation_task_from_files_trains_like_in_memory(tmp_path):
 @pytest.mark.parametrize("ov", [
     {"max_tokens": 1024, "workers": 2, "accum": 2, "fp16": True, "dropout": 0.1},  # replicas + accumulation + dropout
     {"max_tokens": 1024, "fp16": True, "share_embeddings": True},                  # tied embeddings on the 16-bit path
-    {"max_tokens": 1024, "workers": 2, "accum": 2, "fp16": True, "dispatch": "deal"},
+    {"max_tokens": 256, "workers": 2, "accum": 2, "fp16": True, "dispatch": "deal"},
 ])
 def test_fp16_variants_track_reference(ov):
     """fp16 loss within 1e-2 of the reference's emulated fp16, identical skip
@@ -251,7 +251,9 @@ def test_fp16_variants_track_reference(ov):
         import paper_1904_01038_b200 as sqf
         plan = sqf.make_batches(c, ov["max_tokens"], 0, 1)
         order = sqf.shuffle_epoch(len(plan), 1, 1)
-        for s in range(3):
+        nsteps = min(3, len(order) // 4)
+        assert nsteps >= 1
+        for s in range(nsteps):
             sub = [[plan[order[s * 4 + w * 2 + a]] for a in range(2)] for w in range(2)]
             a, b = mine.train_one(), theirs.train_step(sub)
             assert a["ntokens"] == b["ntokens"] and a["skipped"] == b["skipped"]
