@@ -361,26 +361,23 @@ cudaEvent_t Trainer::ovl_event() {
   return ovl_events_[ovl_next_event_++];
 }
 
-int Trainer::bucket_of(int64_t offset) const {
-  auto it = std::upper_bound(bucket_index_.begin(), bucket_index_.end(), std::make_pair(offset, INT32_MAX));
-  if (it == bucket_index_.begin()) throw BoundsError("overlap: offset below the first bucket");
-  --it;
-  return it->second;
-}
 
 // every bucket a gradient write [offset, offset + numel) touches (a stacked
-// parameter group may span several buckets)
+// parameter group may span several buckets); buckets tile the flat vector
 template <typename F>
-static void for_buckets(const std::vector<GradientBucket>& bk, int first, int64_t offset, int64_t numel, F f) {
-  (void)first;
-  for (size_t b = 0; b < bk.size(); ++b)
-    if (bk[b].start < offset + numel && offset < bk[b].end) f(int(b));
+void Trainer::for_buckets(int64_t offset, int64_t numel, F f) const {
+  auto it = std::upper_bound(bucket_index_.begin(), bucket_index_.end(), std::make_pair(offset, INT32_MAX));
+  if (it != bucket_index_.begin()) --it;
+  for (; it != bucket_index_.end() && it->first < offset + numel; ++it) {
+    const GradientBucket& bk = buckets_[size_t(it->second)];
+    if (bk.start < offset + numel && offset < bk.end) f(it->second);
+  }
 }
 
 void Trainer::ovl_begin(const DeviceTape& tape) {
   ovl_remaining_.assign(buckets_.size(), 0);
   for (const auto& w : tape.planned_grad_writes())
-    for_buckets(buckets_, 0, w.first, w.second, [&](int b) { ++ovl_remaining_[size_t(b)]; });
+    for_buckets(w.first, w.second, [&](int b) { ++ovl_remaining_[size_t(b)]; });
   ovl_next_ = 0;
   ovl_next_event_ = 0;
   overlap_log_.clear();
@@ -389,7 +386,7 @@ void Trainer::ovl_begin(const DeviceTape& tape) {
 }
 
 void Trainer::ovl_on_write(int64_t offset, int64_t numel) {
-  for_buckets(buckets_, 0, offset, numel, [&](int b) {
+  for_buckets(offset, numel, [&](int b) {
     if (--ovl_remaining_[size_t(b)] < 0) throw DeviceError("overlap: more gradient writes than planned");
   });
   while (ovl_next_ < int(buckets_.size()) && ovl_remaining_[size_t(ovl_next_)] == 0) {

@@ -186,7 +186,8 @@ class Trainer {
   int overlap_early_ = 0;
   std::vector<std::pair<int64_t, int>> bucket_index_;  // (start, bucket) sorted by start
   cudaEvent_t ovl_event();
-  int bucket_of(int64_t offset) const;
+  template <typename F>
+  void for_buckets(int64_t offset, int64_t numel, F f) const;
   void ovl_begin(const DeviceTape& tape);
   void ovl_on_write(int64_t offset, int64_t numel);
   void ovl_issue(int b);
