@@ -90,6 +90,11 @@ int sqf_trainer_restore(void* t, int64_t step, int32_t epoch, int32_t cursor, do
 /* our kernel launches during the last train_step, and its device time (ms) */
 int64_t sqf_trainer_kernel_launches(void* t);
 float sqf_trainer_last_step_ms(void* t);
+/* The optimizer update of a step runs on a side stream, overlapped with the
+ * next step's forward (which waits per parameter range). flush: make the
+ * trainer stream wait for it and return the device time (ms) from the end of
+ * the last step's main-stream work to that point (timing closure). */
+float sqf_trainer_flush_ms(void* t);
 /* host->device bytes of the last step (returned) and device->host (*d2h) */
 int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h);
 /* CUDA stream the trainer launches on (cudaStream_t) */

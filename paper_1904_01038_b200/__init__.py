@@ -351,6 +351,14 @@ class Trainer:
     def last_step_ms(self) -> float:
         return float(L.sqf_trainer_last_step_ms(self._h))
 
+    def flush_ms(self) -> float:
+        """Wait (on the trainer stream) for the last step's optimizer update,
+        which overlaps the next step; device ms from the step's end to there."""
+        v = float(L.sqf_trainer_flush_ms(self._h))
+        if v < 0:
+            raise L.NativeError(L.sqf_last_status(), L.sqf_last_error().decode())
+        return v
+
     @property
     def last_io_bytes(self):
         """(host->device, device->host) bytes moved by the last step."""

@@ -124,6 +124,7 @@ sqf_trainer_set_injector = _sig("sqf_trainer_set_injector", C.c_int, vp, vp, C.c
 sqf_trainer_restore = _sig("sqf_trainer_restore", C.c_int, vp, i64, i32, i32, f64, i64)
 sqf_trainer_kernel_launches = _sig("sqf_trainer_kernel_launches", i64, vp)
 sqf_trainer_last_step_ms = _sig("sqf_trainer_last_step_ms", f32, vp)
+sqf_trainer_flush_ms = _sig("sqf_trainer_flush_ms", f32, vp)
 sqf_last_status = _sig("sqf_last_status", C.c_int)
 sqf_task_create = _sig("sqf_task_create", vp, cp, P(cp), P(cp), C.c_int)
 sqf_task_free = _sig("sqf_task_free", None, vp)

@@ -385,9 +385,22 @@ class AdamOptimizer : public OptimizerBase {
     ++t_;
     const double bc1 = 1.0 - std::pow(b1_, double(t_));
     const double bc2 = 1.0 - std::pow(b2_, double(t_));
-    sfk_check(sfk_adam(grad_dtype, master, shadow, shadow_dtype, grad, m_, v_, n, lr, b1_, b2_, eps_, bc1, bc2,
-                       prep.scale, prep.unscale ? 1 : 0, prep.ntokens, prep.skip, stream),
-              "adam");
+    if (!prep.ranges) {
+      sfk_check(sfk_adam(grad_dtype, master, shadow, shadow_dtype, grad, m_, v_, n, lr, b1_, b2_, eps_, bc1, bc2,
+                         prep.scale, prep.unscale ? 1 : 0, prep.ntokens, prep.skip, stream),
+                "adam");
+      return;
+    }
+    const size_t gs = grad_dtype == SFK_F32 ? 4 : 2, ss = shadow_dtype == SFK_F32 ? 4 : 2;
+    for (size_t i = 0; i < prep.ranges->size(); ++i) {
+      const auto [off, cnt] = (*prep.ranges)[i];
+      sfk_check(sfk_adam(grad_dtype, master + off, shadow ? static_cast<char*>(shadow) + off * ss : nullptr,
+                         shadow_dtype, static_cast<const char*>(grad) + off * gs, m_ + off, v_ + off, cnt, lr, b1_, b2_,
+                         eps_, bc1, bc2, prep.scale, prep.unscale ? 1 : 0, prep.ntokens, prep.skip, stream),
+                "adam");
+      if (prep.range_done)
+        cuda_check(cudaEventRecord((*prep.range_done)[i], static_cast<cudaStream_t>(stream)), "adam range event");
+    }
   }
   int64_t step_count() const override { return t_; }
   void set_step_count(int64_t t) override { t_ = t; }

@@ -306,6 +306,14 @@ int sqf_trainer_restore(void* t, int64_t step, int32_t epoch, int32_t cursor, do
 
 int64_t sqf_trainer_kernel_launches(void* t) { return T(t)->kernel_launches(); }
 float sqf_trainer_last_step_ms(void* t) { return T(t)->last_step_ms(); }
+float sqf_trainer_flush_ms(void* t) {
+  try {
+    return T(t)->flush_ms();
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1.f;
+  }
+}
 int64_t sqf_trainer_last_io_bytes(void* t, int64_t* d2h) {
   *d2h = T(t)->last_d2h_bytes();
   return T(t)->last_h2d_bytes();

@@ -168,6 +168,10 @@ class DeviceTape {
   // writes a parameter range's gradient contribution is enqueued (on `stream`);
   // the trainer uses it to start bucket all-reduces while backward continues
   using GradHook = std::function<void(int64_t offset, int64_t numel, cudaStream_t stream)>;
+  // called before a launch reads parameters at `offset` on `stream` (the
+  // trainer makes the stream wait for that range's optimizer update)
+  using UseHook = std::function<void(int64_t offset, cudaStream_t stream)>;
+  void set_use_hook(UseHook h) { use_hook_ = std::move(h); }
   void set_grad_hook(GradHook h) { hook_ = std::move(h); }
   // every parameter-gradient write backward() makes, as (offset, numel), in the
   // order the hook will report them
@@ -233,6 +237,7 @@ class DeviceTape {
     return p;
   }
   GradHook hook_;
+  UseHook use_hook_;
   float* ws_main_ = nullptr;
   float* ws_side_ = nullptr;
   int64_t ws_floats_ = 0;
@@ -256,7 +261,10 @@ class DeviceTape {
   }
 
   void* alloc_elems(int64_t n) { return arena_.alloc(size_t(n) * esize_); }
-  void* pptr(const ParamRef& p) const { return static_cast<char*>(params_.compute) + p.offset * esize_; }
+  void* pptr(const ParamRef& p) const {
+    if (use_hook_) use_hook_(p.offset, cur_);
+    return static_cast<char*>(params_.compute) + p.offset * esize_;
+  }
   void* gptr(const ParamRef& p) const { return static_cast<char*>(params_.grad) + p.offset * esize_; }
   // gradient buffer of node `id`: returns {ptr, fresh}; allocates on first use
   std::pair<void*, bool> grad_of(int id);

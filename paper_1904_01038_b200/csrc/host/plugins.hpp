@@ -6,6 +6,8 @@
 // a B200 wants (matmul+bias+relu+residual as one `linear` node).
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <memory>
 #include <span>
@@ -85,6 +87,11 @@ struct GradPrep {
   bool unscale = false;
   float ntokens = 1.0f;
   const int32_t* skip = nullptr;  // device flag; update is a no-op when set
+  // optional: update in these [offset, offset + count) ranges, one launch each,
+  // recording range_done[i] on the stream after range i (the next step's
+  // forward waits per range instead of for the whole update)
+  const std::vector<std::pair<int64_t, int64_t>>* ranges = nullptr;
+  const std::vector<cudaEvent_t>* range_done = nullptr;
 };
 
 class OptimizerBase {

@@ -46,6 +46,11 @@ Trainer::~Trainer() {
   cudaFreeHost(blob_host_);
   cudaFreeHost(readback_host_);
   if (ev0_) cudaEventDestroy(ev0_);
+  for (auto e : adam_range_ev_) cudaEventDestroy(e);
+  for (auto e : adam_done_)
+    if (e) cudaEventDestroy(e);
+  if (ev_checked_) cudaEventDestroy(ev_checked_);
+  if (ev_flush_) cudaEventDestroy(ev_flush_);
   for (auto e : arena_free_)
     if (e) cudaEventDestroy(e);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -129,10 +134,24 @@ void Trainer::init(const Registry& reg) {
   } else {
     cuda_check(cudaMalloc(&compute_, size_t(n_) * 2), "shadow");
   }
-  for (int i = 0; i < local_; ++i) {
+  for (int i = 0; i < 2 * local_; ++i) {
     void* g = nullptr;
     cuda_check(cudaMalloc(&g, size_t(n_) * esize()), "grads");
+    cuda_check(cudaMemset(g, 0, size_t(n_) * esize()), "grads");
     grads_.push_back(g);
+  }
+  // optimizer ranges (~8M elements, 256-aligned) and their events
+  {
+    const char* e = std::getenv("SQF_ADAM_OVERLAP");
+    adam_overlap_ = !(e && std::atoi(e) == 0);
+    const int64_t chunk = int64_t(8) << 20;
+    for (int64_t off = 0; off < n_; off += chunk) adam_ranges_.emplace_back(off, std::min(chunk, n_ - off));
+    adam_range_ev_.resize(adam_ranges_.size());
+    for (auto& ev : adam_range_ev_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    adam_range_wait_.assign(adam_ranges_.size(), 0);
+    for (auto& ev : adam_done_) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_checked_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreate(&ev_flush_), "event");
   }
   const std::vector<float> pe = model_->position_table();
   if (!pe.empty()) {
@@ -160,13 +179,38 @@ const LossScaler& Trainer::scaler() const {
 }
 
 void Trainer::push_params() {
+  join_optimizer();
+  std::fill(adam_range_wait_.begin(), adam_range_wait_.end(), 0);
   std::vector<float> dev(static_cast<size_t>(n_));
   model_->to_device_order(model_->params(), dev);
   cuda_check(cudaMemcpy(master_, dev.data(), size_t(n_) * 4, cudaMemcpyHostToDevice), "params upload");
   rebroadcast();
 }
 
+void Trainer::join_optimizer() {
+  if (side_) cuda_check(cudaStreamSynchronize(side_), "optimizer join");
+}
+
+float Trainer::flush_ms() {
+  for (int k = 0; k < 2; ++k)
+    if (adam_pending_[k]) cuda_check(cudaStreamWaitEvent(stream_, adam_done_[k], 0), "stream wait");
+  cuda_check(cudaEventRecord(ev_flush_, stream_), "event");
+  cuda_check(cudaEventSynchronize(ev_flush_), "flush");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev1_, ev_flush_);
+  return ms;
+}
+
+void Trainer::param_wait(int64_t offset, cudaStream_t s) {
+  const size_t r = size_t(offset / (int64_t(8) << 20));
+  if (r < adam_range_wait_.size() && adam_range_wait_[r]) {
+    cuda_check(cudaStreamWaitEvent(s, adam_range_ev_[r], 0), "stream wait");
+    adam_range_wait_[r] = 0;
+  }
+}
+
 void Trainer::rebroadcast() {
+  join_optimizer();
   // trainer.cpp:149-156: replicas = quantised master; every rank holds the same
   // master (identical reduced grads -> identical updates), so no traffic
   if (compute_ != master_) sfk_check(sfk_cast(master_, compute_, dtype_, n_, stream_), "rebroadcast");
@@ -174,6 +218,7 @@ void Trainer::rebroadcast() {
 }
 
 void Trainer::pull_params() {
+  join_optimizer();
   std::vector<float> dev(static_cast<size_t>(n_));
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   cuda_check(cudaMemcpy(dev.data(), master_, size_t(n_) * 4, cudaMemcpyDeviceToHost), "params download");
@@ -181,14 +226,16 @@ void Trainer::pull_params() {
 }
 
 std::vector<float> Trainer::reduced_grads() {
+  join_optimizer();
+  void* g0 = grads_[size_t(last_gset_ * local_)];
   std::vector<float> devf(static_cast<size_t>(n_));
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   if (dtype_ == SFK_F32) {
-    cuda_check(cudaMemcpy(devf.data(), grads_[0], size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
+    cuda_check(cudaMemcpy(devf.data(), g0, size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
   } else {
     float* tmp = nullptr;
     cuda_check(cudaMalloc(&tmp, size_t(n_) * 4), "grads tmp");
-    sfk_check(sfk_convert(dtype_, grads_[0], SFK_F32, tmp, n_, stream_), "grads convert");
+    sfk_check(sfk_convert(dtype_, g0, SFK_F32, tmp, n_, stream_), "grads convert");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     cuda_check(cudaMemcpy(devf.data(), tmp, size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
     cudaFree(tmp);
@@ -335,8 +382,8 @@ void Trainer::allreduce_grads() {
   // then runs the identical update (no rebroadcast traffic)
   nccl_check(NcclApi::get().GroupStart(), "group");
   for (const auto& b : buckets_)
-    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grads_[0]) + b.start * esize(),
-                             static_cast<char*>(grads_[0]) + b.start * esize(), size_t(b.end - b.start),
+    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grad_buf(0)) + b.start * esize(),
+                             static_cast<char*>(grad_buf(0)) + b.start * esize(), size_t(b.end - b.start),
                              nccl_type(dtype_), ncclSum, comm_, stream_),
                "allreduce grads");
   nccl_check(NcclApi::get().AllReduce(stats_dev_, stats_dev_, 4, ncclFloat64, ncclSum, comm_, stream_), "allreduce stats");
@@ -403,8 +450,8 @@ void Trainer::ovl_issue(int b) {
   cuda_check(cudaStreamWaitEvent(comm_stream_, es, 0), "stream wait");
   const GradientBucket& bk = buckets_[size_t(b)];
   if (world_ > 1)
-    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grads_[0]) + bk.start * esize(),
-                                        static_cast<char*>(grads_[0]) + bk.start * esize(), size_t(bk.end - bk.start),
+    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grad_buf(0)) + bk.start * esize(),
+                                        static_cast<char*>(grad_buf(0)) + bk.start * esize(), size_t(bk.end - bk.start),
                                         nccl_type(dtype_), ncclSum, comm_, comm_stream_),
                "allreduce bucket");
   overlap_log_.push_back(b);
@@ -450,8 +497,13 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   upload(packs, dev);
   cuda_check(cudaMemsetAsync(stats_dev_, 0, 4 * sizeof(double), stream_), "stats zero");
   cuda_check(cudaMemsetAsync(flag_dev_, 0, 4, stream_), "flag zero");
+  // this step's gradient set was last read by the update two steps ago
+  if (adam_pending_[gset_]) {
+    cuda_check(cudaStreamWaitEvent(stream_, adam_done_[gset_], 0), "stream wait");
+    adam_pending_[gset_] = false;
+  }
   for (int lw = 0; lw < local_; ++lw)
-    cuda_check(cudaMemsetAsync(grads_[size_t(lw)], 0, size_t(n_) * esize(), stream_), "grad zero");
+    cuda_check(cudaMemsetAsync(grad_buf(lw), 0, size_t(n_) * esize(), stream_), "grad zero");
   launches_ = 0;
   const bool overlap = overlap_ && local_ == 1 && (world_ > 1 || overlap_sim_) && !dev.empty();
   for (size_t i = 0; i < dev.size(); ++i) {
@@ -461,7 +513,8 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     const int k = int(i & 1);
     if (arena_busy_[k]) cuda_check(cudaStreamWaitEvent(stream_, arena_free_[k], 0), "arena wait");
     arena_[k].reset();
-    DeviceTape tape(arena_[k], DeviceParams{master_, compute_, grads_[size_t(lw)], n_}, dtype_, stream_);
+    DeviceTape tape(arena_[k], DeviceParams{master_, compute_, grad_buf(lw), n_}, dtype_, stream_);
+    tape.set_use_hook([this](int64_t off, cudaStream_t st) { param_wait(off, st); });
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     // a profiling pass serialises everything on the main stream so the
@@ -485,7 +538,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   arena_busy_[0] = arena_busy_[1] = false;  // the last backward joined the side stream
   // in-process replicas fold in index order with re-rounding (trainer.cpp:75-87)
   for (int lw = 1; lw < local_; ++lw) {
-    sfk_check(sfk_accumulate(dtype_, grads_[0], grads_[size_t(lw)], n_, stream_), "replica fold");
+    sfk_check(sfk_accumulate(dtype_, grad_buf(0), grad_buf(lw), n_, stream_), "replica fold");
     ++launches_;
   }
   if (overlap)
@@ -493,22 +546,42 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   else
     allreduce_grads();
   if (prof_) prof_->begin(stream_);
-  sfk_check(sfk_nonfinite(dtype_, grads_[0], n_, flag_dev_, stream_), "overflow check");
+  sfk_check(sfk_nonfinite(dtype_, grad_buf(0), n_, flag_dev_, stream_), "overflow check");
   ++launches_;
 
   const bool injected = fp16_ && injector_ && injector_(stats.step);
   const double lr = scheduler_->lr(stats.step);
   const int64_t t_before = optimizer_->step_count();
+  // The update runs on the side stream in ~8M-element ranges, overlapped
+  // with the next step's forward, which waits per range before it first reads
+  // those parameters; the stats read-back below does not wait for it. (Under
+  // the profiler, and with SQF_ADAM_OVERLAP=0, it stays on the main stream.)
+  const bool adam_side = adam_overlap_ && side_ && !prof_;
   if (!injected) {
     GradPrep prep;
     prep.scale = float(scale);
     prep.unscale = fp16_;
     prep.ntokens = float(stats.ntokens);
     prep.skip = flag_dev_;
-    optimizer_->apply(master_, compute_ == master_ ? nullptr : compute_, dtype_, grads_[0], dtype_, n_, lr, prep,
-                      stream_);
-    ++launches_;
+    cudaStream_t os = stream_;
+    if (adam_side) {
+      cuda_check(cudaEventRecord(ev_checked_, stream_), "event record");
+      cuda_check(cudaStreamWaitEvent(side_, ev_checked_, 0), "stream wait");
+      prep.ranges = &adam_ranges_;
+      prep.range_done = &adam_range_ev_;
+      os = side_;
+    }
+    optimizer_->apply(master_, compute_ == master_ ? nullptr : compute_, dtype_, grad_buf(0), dtype_, n_, lr, prep,
+                      os);
+    launches_ += adam_side ? int64_t(adam_ranges_.size()) : 1;
+    if (adam_side) {
+      std::fill(adam_range_wait_.begin(), adam_range_wait_.end(), 1);
+      cuda_check(cudaEventRecord(adam_done_[gset_], side_), "event record");
+      adam_pending_[gset_] = true;
+    }
   }
+  last_gset_ = gset_;
+  if (adam_side) gset_ ^= 1;
   // overflow check + update: 2 B grad read (check) + 28 B/param update
   if (prof_) prof_->end(stream_, Profiler::Optim, 0, double(n_) * (esize() + (injected ? 0 : 16 + 2 * esize() + 8)));
   // the next deal-mode step's batches are prepared while this one runs
@@ -546,6 +619,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
 
 EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
   // trainer.cpp:275-289: teacher-forced scoring on the fp32 master
+  join_optimizer();
   EvalStats out;
   if (pairs.empty()) return out;
   EpochPlan plan = make_batches(pairs, cfg_.get_int("max_tokens"), std::nullopt, 0);

@@ -56,7 +56,16 @@ class Trainer {
   bool fp16() const { return fp16_; }
   const Config& config() const { return cfg_; }
   ModelBase& model() { return *model_; }
-  OptimizerBase& optimizer() { return *optimizer_; }
+  OptimizerBase& optimizer() {
+    join_optimizer();  // host access to the moments: the update may still run on the side stream
+    return *optimizer_;
+  }
+  // wait (host) for the last optimizer update, which runs on the side stream
+  // overlapped with the next step's forward
+  void join_optimizer();
+  // make the compute stream wait for the last update and return the device
+  // time (ms) from the end of the last step's main-stream work to that point
+  float flush_ms();
   TaskBase& task() { return *task_; }
   const LossScaler& scaler() const;
   const std::vector<GradientBucket>& buckets() const { return buckets_; }
@@ -110,7 +119,9 @@ class Trainer {
   int64_t n_ = 0;
   float* master_ = nullptr;
   void* compute_ = nullptr;        // == master_ in fp32 mode
-  std::vector<void*> grads_;       // one per local replica, compute dtype
+  std::vector<void*> grads_;       // [2 sets][local replicas], compute dtype
+  int gset_ = 0, last_gset_ = 0;   // set this step accumulates into / last completed step's set
+  void* grad_buf(int lw) const { return grads_[size_t(gset_ * local_ + lw)]; }
   float* pe_ = nullptr;
   double* stats_dev_ = nullptr;    // loss, nll, ntokens, ncorrect
   int32_t* flag_dev_ = nullptr;
@@ -126,6 +137,17 @@ class Trainer {
   cudaStream_t side_ = nullptr;        // parameter-gradient stream (wgrad, bias grad)
   std::vector<cudaEvent_t> evpool_;    // ordering events handed to the tapes
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  // optimizer update overlapped with the next forward: per-range events the
+  // forward waits on (once each), and per grad set the event after which the
+  // set may be zeroed again
+  std::vector<std::pair<int64_t, int64_t>> adam_ranges_;
+  std::vector<cudaEvent_t> adam_range_ev_;
+  std::vector<char> adam_range_wait_;
+  cudaEvent_t adam_done_[2] = {nullptr, nullptr};
+  bool adam_pending_[2] = {false, false};
+  cudaEvent_t ev_checked_ = nullptr, ev_flush_ = nullptr;
+  bool adam_overlap_ = true;
+  void param_wait(int64_t offset, cudaStream_t s);
   ncclComm_t comm_ = nullptr;
   // Two activation arenas alternate between sub-batches so the side-stream
   // parameter-gradient work of sub-batch i (which reads its activations) can
