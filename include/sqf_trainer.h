@@ -169,6 +169,41 @@ int sqf_schedule_lr(const char* name, double base, int64_t warmup, double init, 
 /* binary16 RNE round trip (fp16.cpp:22-76) */
 float sqf_quantize_fp16(float x);
 
+/* ---- generation (reference generate.hpp:12-90, generate.cpp:123-480) ----
+ * GenConfig fields; the decoder runs on the device from the fp32 master. */
+typedef struct sqf_gen_config {
+  int32_t beam;
+  int32_t max_len;          /* 0 = 2 * source_len + 8 */
+  int32_t diverse_groups;
+  int32_t topk;
+  double lenpen;
+  double diverse_strength;
+  double temperature;
+  uint64_t seed;
+} sqf_gen_config;
+/* gen_config_from(trainer's resolved config) (generate.cpp:15-26) */
+int sqf_gen_config_default(void* t, sqf_gen_config* out);
+/* mode 0 = beam_search, 1 = diverse_beam_search, 2 = top_k_sample.
+ * source: rows x src_width ids (pad 1), src_lens per row (0 = empty row);
+ * stream_ids: sampling stream per row (NULL = row index). *out receives a
+ * result handle (free with sqf_gen_free). */
+int sqf_generate(void* t, int mode, const int32_t* source, const int32_t* src_lens, int rows, int src_width,
+                 const sqf_gen_config* cfg, const uint64_t* stream_ids, void** out);
+/* number of hypotheses for sentence s */
+int sqf_gen_count(void* g, int s);
+/* hypothesis k of sentence s: *len tokens (cap >= len, else -3), step scores */
+int sqf_gen_hyp(void* g, int s, int k, int32_t* tokens, float* step_scores, int cap, int32_t* len,
+                double* cum_logprob, double* score, int32_t* finish_step, int32_t* finished);
+void sqf_gen_free(void* g);
+/* score_hypothesis (generate.cpp:28-32) */
+int sqf_score_hypothesis(double cum_logprob, int64_t length, double alpha, double* out);
+/* sample_from_topk (generate.cpp:353-383) */
+int sqf_sample_from_topk(const float* logits, int vocab, int k, double temperature, double u, int32_t* out);
+/* batch_for_inference (generate.cpp:459-480): lens of n sources -> groups
+ * (original indices, concatenated in processing order) and group sizes */
+int sqf_batch_for_inference(const int32_t* lens, int n, int64_t max_tokens, int32_t* ngroups, int32_t* sizes,
+                            int32_t* members);
+
 #ifdef __cplusplus
 }
 #endif

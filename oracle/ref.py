@@ -108,6 +108,13 @@ def _declare(L):
     s("sqfref_trainer_subbatch_grad", C.c_int, vp, vp, vp, C.c_int, f32, vp, P(StatsC))
     s("sqfref_trainer_evaluate", C.c_int, vp, vp, P(f64), P(f64), P(i64), P(i64))
     s("sqfref_trainer_save", C.c_int, vp, cp)
+    s("sqfref_generate", C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, f64,
+      f64, f64, C.c_uint64, vp, C.c_int, P(vp))
+    s("sqfref_gen_count", C.c_int, vp, C.c_int)
+    s("sqfref_gen_hyp", C.c_int, vp, C.c_int, C.c_int, vp, vp, C.c_int, P(i32), P(f64), P(f64), P(i32), P(i32))
+    s("sqfref_gen_free", None, vp)
+    s("sqfref_sample_from_topk", C.c_int, vp, C.c_int, C.c_int, f64, f64, P(i32))
+    s("sqfref_batch_for_inference", C.c_int, vp, C.c_int, i64, P(i32), vp, vp)
     s("sqfref_simulate_timeline", C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, vp, C.c_int)
     s("sqfref_checkpoint_read", C.c_int, cp, P(i32), P(i64), vp, P(i64), vp)
     s("sqfref_checkpoint_meta", C.c_int, cp, cp, vp, C.c_int)
@@ -376,6 +383,23 @@ class RefTrainer:
                                             len(sub[0]), C.byref(st)))
         return st.as_dict()
 
+    def generate(self, sources, mode="beam", stream_ids=None, no_cache=False, beam=4, max_len=0,
+                 diverse_groups=1, topk=1, lenpen=0.6, diverse_strength=0.5, temperature=1.0, seed=1):
+        """The reference's beam_search / diverse_beam_search / top_k_sample
+        (generate.hpp:46-90) on this trainer's model (fp32)."""
+        src, lens = _pad_rows(sources)
+        ids = None if stream_ids is None else np.ascontiguousarray(stream_ids, np.uint64)
+        h = C.c_void_p()
+        _ck(lib().sqfref_generate(self.h, {"beam": 0, "diverse": 1, "sample": 2}[mode], _ptr(src), _ptr(lens),
+                                  len(lens), src.shape[1], beam, max_len, diverse_groups, topk, lenpen,
+                                  diverse_strength, temperature, seed, None if ids is None else _ptr(ids),
+                                  int(no_cache), C.byref(h)))
+        try:
+            return [[_read_hyp(lib().sqfref_gen_hyp, h, s, k) for k in range(lib().sqfref_gen_count(h, s))]
+                    for s in range(len(lens))]
+        finally:
+            lib().sqfref_gen_free(h)
+
     def set_injector(self, steps):
         a = np.asarray(list(steps) or [0], np.int64)
         _ck(lib().sqfref_trainer_set_injector(self.h, _ptr(a), len(list(steps))))
@@ -434,3 +458,39 @@ class RefTrainer:
         loss, nll, nt, nc = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
         _ck(lib().sqfref_trainer_evaluate(self.h, rc.h, C.byref(loss), C.byref(nll), C.byref(nt), C.byref(nc)))
         return {"loss": loss.value, "nll": nll.value, "ntokens": nt.value, "ncorrect": nc.value}
+
+
+def sample_from_topk(logits, k, temperature, u):
+    x = np.ascontiguousarray(logits, np.float32)
+    out = C.c_int32()
+    _ck(lib().sqfref_sample_from_topk(_ptr(x), len(x), k, temperature, u, C.byref(out)))
+    return out.value
+
+
+def batch_for_inference(lengths, max_tokens):
+    lens = np.ascontiguousarray(lengths, np.int32)
+    n = len(lens)
+    sizes, members = np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32)
+    ng = C.c_int32()
+    _ck(lib().sqfref_batch_for_inference(_ptr(lens), n, max_tokens, C.byref(ng), _ptr(sizes), _ptr(members)))
+    out, at = [], 0
+    for i in range(ng.value):
+        out.append(members[at:at + sizes[i]].tolist())
+        at += sizes[i]
+    return out
+
+
+def _pad_rows(sources):
+    lens = np.array([len(r) for r in sources], np.int32)
+    src = np.full((len(lens), max(1, int(lens.max()) if len(lens) else 1)), 1, np.int32)
+    for i, r in enumerate(sources):
+        src[i, :len(r)] = r
+    return src, lens
+
+
+def _read_hyp(fn, h, s, k, cap=4096):
+    tok, sc = np.zeros(cap, np.int32), np.zeros(cap, np.float32)
+    n, cum, score, fs, fin = C.c_int32(), C.c_double(), C.c_double(), C.c_int32(), C.c_int32()
+    _ck(fn(h, s, k, _ptr(tok), _ptr(sc), cap, C.byref(n), C.byref(cum), C.byref(score), C.byref(fs), C.byref(fin)))
+    return {"tokens": tok[:n.value].tolist(), "step_scores": sc[:n.value].tolist(), "cum_logprob": cum.value,
+            "score": score.value, "finish_step": fs.value, "finished": bool(fin.value)}

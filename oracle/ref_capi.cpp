@@ -21,6 +21,7 @@
 #include "seqforge/criterions.hpp"
 #include "seqforge/data.hpp"
 #include "seqforge/fp16.hpp"
+#include "seqforge/generate.hpp"
 #include "seqforge/model.hpp"
 #include "seqforge/optim.hpp"
 #include "seqforge/registry.hpp"
@@ -640,6 +641,79 @@ int sqfref_checkpoint_meta(const char* path, const char* key, char* out, int cap
     if (it == raw.meta.end()) throw IntegrityError(std::string("no key ") + key);
     if (int(it->second.size()) + 1 > cap) throw BoundsError("buffer");
     std::memcpy(out, it->second.c_str(), it->second.size() + 1);
+  })
+}
+
+// ---------------------------------------------------------------- generation
+// generate.hpp:46-90 on the trainer's model; mode 0 beam, 1 diverse, 2 sample
+int sqfref_generate(void* h, int mode, const int32_t* source, const int32_t* src_lens, int rows, int src_width,
+                    int beam, int max_len, int groups, int topk, double lenpen, double strength,
+                    double temperature, uint64_t seed, const uint64_t* stream_ids, int no_cache, void** out) {
+  GUARD({
+    const auto& model = dynamic_cast<const TransformerModel&>(static_cast<TrainerBox*>(h)->tr->model());
+    MiniBatch b;
+    b.rows = rows;
+    b.src_width = src_width;
+    b.source.assign(source, source + static_cast<size_t>(rows) * src_width);
+    b.src_lens.assign(src_lens, src_lens + rows);
+    GenConfig g;
+    g.beam = beam;
+    g.max_len = max_len;
+    g.diverse_groups = groups;
+    g.topk = topk;
+    g.lenpen = lenpen;
+    g.diverse_strength = strength;
+    g.temperature = temperature;
+    g.seed = seed;
+    g.no_cache = no_cache != 0;
+    auto res = std::make_unique<std::vector<std::vector<Hypothesis>>>();
+    if (mode == 0) {
+      *res = beam_search(model, b, g);
+    } else if (mode == 1) {
+      *res = diverse_beam_search(model, b, g);
+    } else {
+      std::vector<uint64_t> ids;
+      if (stream_ids) ids.assign(stream_ids, stream_ids + rows);
+      for (Hypothesis& x : top_k_sample(model, b, g, ids)) res->push_back({std::move(x)});
+    }
+    *out = res.release();
+  })
+}
+int sqfref_gen_count(void* g, int s) {
+  return static_cast<int>((*static_cast<std::vector<std::vector<Hypothesis>>*>(g))[static_cast<size_t>(s)].size());
+}
+int sqfref_gen_hyp(void* g, int s, int k, int32_t* tokens, float* steps, int cap, int32_t* len, double* cum,
+                   double* score, int32_t* finish_step, int32_t* finished) {
+  const Hypothesis& x = (*static_cast<std::vector<std::vector<Hypothesis>>*>(g))[static_cast<size_t>(s)]
+                                                                                [static_cast<size_t>(k)];
+  *len = static_cast<int32_t>(x.tokens.size());
+  if (*len > cap) return -3;
+  for (int i = 0; i < *len; ++i) {
+    tokens[i] = x.tokens[static_cast<size_t>(i)];
+    steps[i] = x.step_scores[static_cast<size_t>(i)];
+  }
+  *cum = x.cum_logprob;
+  *score = x.score;
+  *finish_step = x.finish_step;
+  *finished = x.finished ? 1 : 0;
+  return 0;
+}
+void sqfref_gen_free(void* g) { delete static_cast<std::vector<std::vector<Hypothesis>>*>(g); }
+int sqfref_sample_from_topk(const float* logits, int vocab, int k, double temperature, double u, int32_t* out) {
+  GUARD({ *out = sample_from_topk(logits, vocab, k, temperature, u); })
+}
+int sqfref_batch_for_inference(const int32_t* lens, int n, int64_t max_tokens, int32_t* ngroups, int32_t* sizes,
+                               int32_t* members) {
+  GUARD({
+    std::vector<std::vector<int>> src(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) src[static_cast<size_t>(i)].assign(static_cast<size_t>(lens[i]), 4);
+    auto groups = batch_for_inference(src, max_tokens);
+    *ngroups = static_cast<int32_t>(groups.size());
+    int64_t at = 0;
+    for (size_t i = 0; i < groups.size(); ++i) {
+      sizes[i] = static_cast<int32_t>(groups[i].size());
+      for (int m : groups[i]) members[at++] = m;
+    }
   })
 }
 

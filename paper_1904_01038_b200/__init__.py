@@ -291,6 +291,32 @@ class Trainer:
                                        C.byref(nc)))
         return EvalStats(loss.value, nll.value, nt.value, nc.value)
 
+    # ---- generation (reference generate.hpp:46-90; decoder on the device)
+    def gen_config(self) -> dict:
+        """gen_config_from(the resolved config) (generate.cpp:15-26)."""
+        g = L.GenConfigC()
+        L.check(L.sqf_gen_config_default(self._h, C.byref(g)))
+        return {f: getattr(g, f) for f, _ in L.GenConfigC._fields_}
+
+    def generate(self, sources, mode: str = "beam", stream_ids=None, **cfg) -> list:
+        """beam_search / diverse_beam_search / top_k_sample over source id rows
+        (eos-terminated lists; [] = empty row). Returns one list of Hypothesis per
+        sentence (one element for mode="sample")."""
+        modes = {"beam": 0, "diverse": 1, "sample": 2}
+        if mode not in modes:
+            raise ValueError(f"unknown generation mode {mode!r}")
+        g = L.GenConfigC(**{**self.gen_config(), **cfg})
+        src, lens = _pad_rows(sources)
+        ids = None if stream_ids is None else np.ascontiguousarray(stream_ids, np.uint64)
+        h = C.c_void_p()
+        L.check(L.sqf_generate(self._h, modes[mode], _ptr(src), _ptr(lens), len(lens), src.shape[1], C.byref(g),
+                               None if ids is None else _ptr(ids), C.byref(h)))
+        try:
+            return [[_read_hyp(L.sqf_gen_hyp, h, s, k) for k in range(L.sqf_gen_count(h, s))]
+                    for s in range(len(lens))]
+        finally:
+            L.sqf_gen_free(h)
+
     # ---- state
     @property
     def num_params(self) -> int:
@@ -401,3 +427,61 @@ class Trainer:
                 break
             out[name.decode()] = (ms.value, fl.value, by.value, n.value)
         return out
+
+
+# ---- generation helpers (reference generate.hpp)
+@dataclass
+class Hypothesis:
+    tokens: list
+    step_scores: list
+    cum_logprob: float
+    score: float
+    finish_step: int
+    finished: bool
+
+
+def _pad_rows(sources):
+    lens = np.array([len(r) for r in sources], np.int32)
+    width = max(1, int(lens.max()) if len(lens) else 1)
+    src = np.full((len(lens), width), 1, np.int32)  # pad id 1
+    for i, r in enumerate(sources):
+        src[i, :len(r)] = r
+    return src, lens
+
+
+def _read_hyp(fn, h, s, k, cap=4096):
+    tok = np.zeros(cap, np.int32)
+    sc = np.zeros(cap, np.float32)
+    n, cum, score, fs, fin = C.c_int32(), C.c_double(), C.c_double(), C.c_int32(), C.c_int32()
+    st = fn(h, s, k, _ptr(tok), _ptr(sc), cap, C.byref(n), C.byref(cum), C.byref(score), C.byref(fs), C.byref(fin))
+    if st != 0:
+        raise RuntimeError(f"generation: reading hypothesis failed ({st})")
+    return Hypothesis(tok[:n.value].tolist(), sc[:n.value].tolist(), cum.value, score.value, fs.value,
+                      bool(fin.value))
+
+
+def score_hypothesis(cum_logprob: float, length: int, alpha: float) -> float:
+    out = C.c_double()
+    L.check(L.sqf_score_hypothesis(cum_logprob, length, alpha, C.byref(out)))
+    return out.value
+
+
+def sample_from_topk(logits, k: int, temperature: float, u: float) -> int:
+    x = np.ascontiguousarray(logits, np.float32)
+    out = C.c_int32()
+    L.check(L.sqf_sample_from_topk(_ptr(x), len(x), k, temperature, u, C.byref(out)))
+    return out.value
+
+
+def batch_for_inference(lengths, max_tokens: int) -> list:
+    lens = np.ascontiguousarray(lengths, np.int32)
+    n = len(lens)
+    sizes = np.zeros(max(n, 1), np.int32)
+    members = np.zeros(max(n, 1), np.int32)
+    ng = C.c_int32()
+    L.check(L.sqf_batch_for_inference(_ptr(lens), n, max_tokens, C.byref(ng), _ptr(sizes), _ptr(members)))
+    out, at = [], 0
+    for i in range(ng.value):
+        out.append(members[at:at + sizes[i]].tolist())
+        at += sizes[i]
+    return out

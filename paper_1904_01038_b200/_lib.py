@@ -185,3 +185,21 @@ def cstrs(items):
     for i, s in enumerate(items):
         arr[i] = s.encode() if isinstance(s, str) else s
     return arr
+
+# ---- generation (include/sqf_trainer.h, reference generate.hpp)
+
+
+class GenConfigC(C.Structure):
+    _fields_ = [("beam", i32), ("max_len", i32), ("diverse_groups", i32), ("topk", i32), ("lenpen", f64),
+                ("diverse_strength", f64), ("temperature", f64), ("seed", u64)]
+
+
+sqf_gen_config_default = _sig("sqf_gen_config_default", C.c_int, vp, P(GenConfigC))
+sqf_generate = _sig("sqf_generate", C.c_int, vp, C.c_int, vp, vp, C.c_int, C.c_int, P(GenConfigC), vp, P(vp))
+sqf_gen_count = _sig("sqf_gen_count", C.c_int, vp, C.c_int)
+sqf_gen_hyp = _sig("sqf_gen_hyp", C.c_int, vp, C.c_int, C.c_int, vp, vp, C.c_int, P(i32), P(f64), P(f64), P(i32),
+                   P(i32))
+sqf_gen_free = _sig("sqf_gen_free", None, vp)
+sqf_score_hypothesis = _sig("sqf_score_hypothesis", C.c_int, f64, i64, f64, P(f64))
+sqf_sample_from_topk = _sig("sqf_sample_from_topk", C.c_int, vp, C.c_int, C.c_int, f64, f64, P(i32))
+sqf_batch_for_inference = _sig("sqf_batch_for_inference", C.c_int, vp, C.c_int, i64, P(i32), vp, vp)

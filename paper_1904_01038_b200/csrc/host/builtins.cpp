@@ -60,6 +60,7 @@ class TransformerModel : public ModelBase {
   int max_positions() const override { return max_pos_; }
   std::unique_ptr<ModelBase> clone() const override { return std::make_unique<TransformerModel>(*this); }
   void set_train_step(int64_t s) override { train_step_ = s; }
+  void set_inference(bool on) override { inference_ = on; }
 
   std::vector<float> position_table() const override {
     std::vector<float> pe(size_t(max_pos_) * d_);
@@ -96,6 +97,7 @@ class TransformerModel : public ModelBase {
 
   int src_vocab_, tgt_vocab_, d_, heads_, ffn_, max_pos_, enc_n_, dec_n_;
   float dropout_;
+  bool inference_ = false;  // generation: no dropout sites
   bool share_;
   uint64_t seed_;
   int64_t train_step_ = 0;
@@ -287,14 +289,14 @@ class TransformerModel : public ModelBase {
   // model.cpp:156-163: dropout site n of the step draws from stream
   // kStreamDropoutBase | (train_step << 8) | n; sites count in recording order
   int maybe_dropout(DeviceTape& t, int x, int& site, int residual = -1) const {
-    if (dropout_ <= 0.0f) return x;
+    if (dropout_ <= 0.0f || inference_) return x;
     const uint64_t stream = (uint64_t(1) << 32) | (uint64_t(train_step_) << 8) | uint64_t(site++);
     return t.dropout(x, dropout_, seed_, stream, residual);
   }
   // x + dropout(linear(in)): the residual add rides in the GEMM epilogue when
   // there is no dropout, else in the dropout kernel (model.cpp:218-224)
   int residual(DeviceTape& t, int in, const ParamRef& w, const ParamRef* b, bool relu, int x, int& site) const {
-    if (dropout_ <= 0.0f) return t.linear(in, w, b, relu, x);
+    if (dropout_ <= 0.0f || inference_) return t.linear(in, w, b, relu, x);
     return maybe_dropout(t, t.linear(in, w, b, relu), site, x);
   }
 

@@ -7,6 +7,7 @@
 #include "../../../include/sqf_trainer.h"
 #include "nccl_dyn.hpp"
 #include "checkpoint.hpp"
+#include "generate.hpp"
 #include "simulator.hpp"
 #include "trainer.hpp"
 
@@ -518,5 +519,95 @@ int sqf_schedule_lr(const char* name, double base, int64_t warmup, double init, 
 }
 
 float sqf_quantize_fp16(float x) { return quantize_fp16(x); }
+
+int sqf_gen_config_default(void* t, sqf_gen_config* out) {
+  SQF_GUARD({
+    GenConfig g = gen_config_from(T(t)->config());
+    *out = sqf_gen_config{g.beam, g.max_len, g.diverse_groups, g.topk, g.lenpen, g.diverse_strength,
+                          g.temperature, g.seed};
+  })
+}
+
+int sqf_generate(void* t, int mode, const int32_t* source, const int32_t* src_lens, int rows, int src_width,
+                 const sqf_gen_config* c, const uint64_t* stream_ids, void** out) {
+  SQF_GUARD({
+    if (mode < 0 || mode > 2) throw ConfigError("generation: mode must be 0 (beam), 1 (diverse) or 2 (sample)");
+    if (rows < 1 || src_width < 0) throw ShapeError("generation: batch has no rows");
+    MiniBatch b;
+    b.rows = rows;
+    b.src_width = src_width;
+    b.source.assign(source, source + size_t(rows) * src_width);
+    b.src_lens.assign(src_lens, src_lens + rows);
+    for (int s = 0; s < rows; ++s)
+      if (src_lens[s] < 0 || src_lens[s] > src_width) throw ShapeError("generation: source length out of range");
+    GenConfig g;
+    g.beam = c->beam;
+    g.max_len = c->max_len;
+    g.diverse_groups = c->diverse_groups;
+    g.topk = c->topk;
+    g.lenpen = c->lenpen;
+    g.diverse_strength = c->diverse_strength;
+    g.temperature = c->temperature;
+    g.seed = c->seed;
+    auto res = std::make_unique<std::vector<std::vector<Hypothesis>>>();
+    if (mode == 0) {
+      *res = beam_search(*T(t), b, g);
+    } else if (mode == 1) {
+      *res = diverse_beam_search(*T(t), b, g);
+    } else {
+      std::vector<uint64_t> ids;
+      if (stream_ids) ids.assign(stream_ids, stream_ids + rows);
+      for (Hypothesis& h : top_k_sample(*T(t), b, g, ids)) res->push_back({std::move(h)});
+    }
+    *out = res.release();
+  })
+}
+
+int sqf_gen_count(void* g, int s) {
+  auto& r = *static_cast<std::vector<std::vector<Hypothesis>>*>(g);
+  if (s < 0 || size_t(s) >= r.size()) return -3;
+  return int(r[size_t(s)].size());
+}
+
+int sqf_gen_hyp(void* g, int s, int k, int32_t* tokens, float* step_scores, int cap, int32_t* len,
+                double* cum_logprob, double* score, int32_t* finish_step, int32_t* finished) {
+  SQF_GUARD({
+    auto& r = *static_cast<std::vector<std::vector<Hypothesis>>*>(g);
+    const Hypothesis& h = r.at(size_t(s)).at(size_t(k));
+    *len = int32_t(h.tokens.size());
+    if (int(h.tokens.size()) > cap) throw BoundsError("generation: token buffer too small");
+    std::copy(h.tokens.begin(), h.tokens.end(), tokens);
+    std::copy(h.step_scores.begin(), h.step_scores.end(), step_scores);
+    *cum_logprob = h.cum_logprob;
+    *score = h.score;
+    *finish_step = h.finish_step;
+    *finished = h.finished ? 1 : 0;
+  })
+}
+
+void sqf_gen_free(void* g) { delete static_cast<std::vector<std::vector<Hypothesis>>*>(g); }
+
+int sqf_score_hypothesis(double cum_logprob, int64_t length, double alpha, double* out) {
+  SQF_GUARD({ *out = score_hypothesis(cum_logprob, length, alpha); })
+}
+
+int sqf_sample_from_topk(const float* logits, int vocab, int k, double temperature, double u, int32_t* out) {
+  SQF_GUARD({ *out = sample_from_topk(logits, vocab, k, temperature, u); })
+}
+
+int sqf_batch_for_inference(const int32_t* lens, int n, int64_t max_tokens, int32_t* ngroups, int32_t* sizes,
+                            int32_t* members) {
+  SQF_GUARD({
+    std::vector<std::vector<int>> src(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) src[size_t(i)].assign(size_t(lens[i]), 0);
+    auto groups = batch_for_inference(src, max_tokens);
+    *ngroups = int32_t(groups.size());
+    int64_t at = 0;
+    for (size_t i = 0; i < groups.size(); ++i) {
+      sizes[i] = int32_t(groups[i].size());
+      for (int m : groups[i]) members[at++] = m;
+    }
+  })
+}
 
 }  // extern "C"

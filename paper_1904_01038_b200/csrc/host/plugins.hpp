@@ -54,6 +54,8 @@ class ModelBase {
   virtual int max_positions() const = 0;
   virtual std::unique_ptr<ModelBase> clone() const = 0;
   virtual void set_train_step(int64_t) {}
+  // generation decodes without dropout (generate.cpp)
+  virtual void set_inference(bool) {}
   // canonical -> device permutation helpers (host vectors)
   void to_device_order(std::span<const float> canonical, std::span<float> device) const;
   void to_canonical_order(std::span<const float> device, std::span<float> canonical) const;

@@ -646,3 +646,38 @@ EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
 }
 
 }  // namespace sqf
+
+namespace sqf {
+
+std::vector<float> Trainer::last_position_logits(const MiniBatch& mb) {
+  // reference generate.cpp:86-120 (recompute_logits): decode every row's full
+  // prefix and keep the final position's logits; the decoder runs on the
+  // device from the fp32 master, only R x V floats come back
+  join_optimizer();
+  const int V = model_->target_vocab();
+  const int R = mb.rows, T = mb.tgt_width;
+  std::vector<PackedBatch> packs{PackedBatch::pack(mb)};
+  std::vector<DeviceBatch> dev;
+  upload(packs, dev);
+  arena_[0].reset();
+  model_->set_inference(true);
+  std::vector<float> out(size_t(R) * V);
+  try {
+    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    tape.set_counters(counters_, kCounters, &counter_cursor_);
+    const int lg = model_->forward_to_logits(tape, dev[0]);
+    if (tape.rows(lg) != R * T || tape.cols(lg) != V) throw ShapeError("generation: logits shape");
+    const float* base = static_cast<const float*>(tape.out(lg)) + size_t(T - 1) * V;
+    cuda_check(cudaMemcpy2DAsync(out.data(), size_t(V) * 4, base, size_t(T) * V * 4, size_t(V) * 4, R,
+                                 cudaMemcpyDeviceToHost, stream_),
+               "logits D2H");
+    cuda_check(cudaDeviceSynchronize(), "generation sync");
+  } catch (...) {
+    model_->set_inference(false);
+    throw;
+  }
+  model_->set_inference(false);
+  return out;
+}
+
+}  // namespace sqf

@@ -46,6 +46,10 @@ class Trainer {
   std::optional<StepStats> train_one();
   StepStats train_step(const std::vector<std::vector<MiniBatch>>& sub);
   EvalStats evaluate(const std::vector<SequencePair>& pairs);
+  // generation support (generate.cpp): teacher-forced decoder pass of `mb` on
+  // the fp32 master; returns the logits of each row's last target position,
+  // rows x target_vocab, row-major (reference generate.cpp:86-120)
+  std::vector<float> last_position_logits(const MiniBatch& mb);
 
   int64_t step() const { return step_; }
   int epoch() const { return epoch_; }
