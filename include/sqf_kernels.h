@@ -261,6 +261,12 @@ int sfk_sgd(int grad_dtype, float* master, void* shadow, int shadow_dtype,
 int sfk_accumulate(int dtype, void* dst, const void* src, int64_t n, void* stream);
 /* shadow = q(master) (trainer.cpp:149-156) */
 int sfk_cast(const float* src, void* dst, int dst_dtype, int64_t n, void* stream);
+
+/* K/V-cache reorder of the incremental decoder (model.cpp:540-557):
+ * dst[m][r] = src[m][idx[r]] for nmat matrices of `rows` rows of row_bytes
+ * (mat_bytes apart); 16-byte multiples, out of place. */
+int sfk_gather_rows(const void* src, void* dst, const int32_t* idx, int rows, int64_t row_bytes, int nmat,
+                    int64_t mat_bytes, void* stream);
 /* dst = src converted (any dtype pair) */
 int sfk_convert(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n,
                 void* stream);

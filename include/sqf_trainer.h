@@ -170,7 +170,8 @@ int sqf_schedule_lr(const char* name, double base, int64_t warmup, double init, 
 float sqf_quantize_fp16(float x);
 
 /* ---- generation (reference generate.hpp:12-90, generate.cpp:123-480) ----
- * GenConfig fields; the decoder runs on the device from the fp32 master. */
+ * GenConfig fields; the decoder runs on the device from the fp32 master,
+ * incrementally with per-layer K/V caches unless no_cache. */
 typedef struct sqf_gen_config {
   int32_t beam;
   int32_t max_len;          /* 0 = 2 * source_len + 8 */
@@ -180,6 +181,8 @@ typedef struct sqf_gen_config {
   double diverse_strength;
   double temperature;
   uint64_t seed;
+  int32_t no_cache;         /* 1 = re-decode the full prefix each step (reference oracle mode) */
+  int32_t _pad;
 } sqf_gen_config;
 /* gen_config_from(trainer's resolved config) (generate.cpp:15-26) */
 int sqf_gen_config_default(void* t, sqf_gen_config* out);

@@ -82,6 +82,60 @@ class TransformerModel : public ModelBase {
     return decode(tape, b, enc, site);
   }
 
+  int decoder_layers() const override { return dec_n_; }
+  int model_dim() const override { return d_; }
+
+  int encode_cross_kv(DeviceTape& t, const DeviceBatch& b) const override {
+    if (b.src_width > max_pos_)
+      throw CapacityError("transformer: source length " + std::to_string(b.src_width) + " exceeds max_positions " +
+                          std::to_string(max_pos_));
+    if (!pe_dev_) throw ConfigError("transformer: position table not uploaded");
+    if (dec_.empty()) throw ConfigError("transformer: no decoder layers");
+    int site = 0;
+    return t.linear(encode(t, b, site), cross_kv_w_, &cross_kv_b_, false);
+  }
+
+  // model.cpp:466-538 (forward_decoder_step): the decoder of decode() for one
+  // position, self-attention over the cached keys/values of positions 0..pos
+  int decode_step(DeviceTape& t, const int32_t* ids, int rows, int pos, void* self_cache, int cap,
+                  const void* cross, int src_width, const int32_t* self_len,
+                  const int32_t* src_len) const override {
+    if (pos >= max_pos_ || pos >= cap)
+      throw CapacityError("transformer: decoding position " + std::to_string(pos) + " exceeds max_positions " +
+                          std::to_string(max_pos_));
+    if (!pe_dev_) throw ConfigError("transformer: position table not uploaded");
+    const size_t es = t.dtype() == SFK_F32 ? 4 : 2;
+    const size_t kv_row = size_t(2) * d_ * es, layer_bytes = size_t(rows) * cap * kv_row;
+    // width 1: the row's position is the table row the pointer starts at
+    int x = t.embedding(tgt_embed_, ids, rows, 1, std::sqrt(float(d_)), pe_dev_ + size_t(pos) * d_,
+                        DeviceBatch::Segs{});
+    const int ckv = t.external(cross, rows * src_width, 2 * d_ * dec_n_);
+    int li = 0;
+    for (const Layer& l : dec_) {
+      const int z = t.layer_norm(x, l.ln1g, l.ln1b);
+      const ParamRef bqkv = l.self.bqkv();
+      const int qkv = t.linear(z, l.self.wqkv(), &bqkv, false);
+      char* cache = static_cast<char*>(self_cache) + size_t(li) * layer_bytes;
+      cuda_check(cudaMemcpy2DAsync(cache + size_t(pos) * kv_row, size_t(cap) * kv_row,
+                                   static_cast<const char*>(t.out(qkv)) + size_t(d_) * es, size_t(3) * d_ * es,
+                                   kv_row, size_t(rows), cudaMemcpyDeviceToDevice, t.stream()),
+                 "kv cache append");
+      const int kv = t.external(cache, rows * cap, 2 * d_);
+      const int a = t.attention(qkv, 0, kv, 0, d_, d_, heads_, rows, 1, cap, false, self_len);
+      x = t.linear(a, l.self.wo, &l.self.bo, false, x);
+      const int z2 = t.layer_norm(x, l.ln2g, l.ln2b);
+      const int cq = t.linear(z2, l.cross.wq, &l.cross.bq, false);
+      const int kc = 2 * d_ * li++;
+      const int ca = t.attention(cq, 0, ckv, kc, kc + d_, d_, heads_, rows, 1, src_width, false, src_len);
+      x = t.linear(ca, l.cross.wo, &l.cross.bo, false, x);
+      const int z3 = t.layer_norm(x, l.ln3g, l.ln3b);
+      const int h = t.linear(z3, l.w1, &l.b1, true);
+      x = t.linear(h, l.w2, &l.b2, false, x);
+    }
+    x = t.layer_norm(x, dec_lng_, dec_lnb_);
+    return t.logits(x, out_proj_);
+  }
+
  private:
   struct Attn {
     ParamRef wq, wk, wv, wo, bq, bk, bv, bo;

@@ -385,6 +385,17 @@ double attn_flops(int batch, int qw, int kw, const int32_t* /*k_len device*/, in
 }
 }  // namespace
 
+int DeviceTape::external(const void* data, int rows, int cols) {
+  Node n;
+  n.kind = Kind::External;
+  n.rows = rows;
+  n.cols = cols;
+  n.ld = cols;
+  n.out = const_cast<void*>(data);
+  nodes_.push_back(n);
+  return int(nodes_.size()) - 1;
+}
+
 int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
                           int k_width, bool causal, const int32_t* k_len) {
   if (heads <= 0 || d % heads != 0) throw ShapeError("attention: d_model not divisible by heads");
@@ -785,6 +796,8 @@ void DeviceTape::backward_node(int id) {
       ++launches_;
       return;
     }
+    case Kind::External:
+      break;
     case Kind::Attention: {
       const Node& qn = nodes_[n.in0];
       const Node& kn = nodes_[n.in1];

@@ -114,7 +114,7 @@ struct DeviceParams {
 
 class DeviceTape {
  public:
-  enum class Kind { Embedding, LayerNorm, Linear, Attention, Xent, Dropout };
+  enum class Kind { Embedding, LayerNorm, Linear, Attention, Xent, Dropout, External };
 
   DeviceTape(Arena& arena, const DeviceParams& params, int dtype, cudaStream_t stream);
 
@@ -133,6 +133,10 @@ class DeviceTape {
   // a16: q/k/v are column slices [q_col, q_col+d) of node q and [k_col..), [v_col..) of node kv
   int attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
                 int k_width, bool causal, const int32_t* k_len);
+  // a leaf over caller-owned device memory (rows x cols, row-major, tape
+  // dtype): the incremental decoder's K/V caches; never differentiated
+  int external(const void* data, int rows, int cols);
+  cudaStream_t stream() const { return stream_; }
   // a18: records the loss node; stats are produced when backward()/finish() runs
   int softmax_xent(int logits, const int32_t* gold, float epsilon);
   // Tape::dropout (tape.cpp:109-121) with the mask drawn from RngStream(seed,

@@ -5,9 +5,9 @@
 // the reference's selection rules (candidate order, stable ties, eos banking,
 // admissible early stop, final n-best order) so hypotheses match it.
 //
-// Decoding here is the reference's cache-free mode (GenConfig::no_cache,
-// generate.cpp:86-120, which the reference tests bitwise-equal to its cached
-// decoder, test_generate.cpp:268-297): every step re-decodes each live prefix.
+// Decoding: by default incremental, with per-layer K/V caches on the device
+// (reorder = a row gather kernel); no_cache selects the reference's cache-free
+// mode (generate.cpp:86-120), which re-decodes every live prefix per step.
 #pragma once
 
 #include <cstdint>
@@ -29,6 +29,7 @@ struct GenConfig {
   int topk = 1;
   double temperature = 1.0;
   uint64_t seed = 1;
+  bool no_cache = false;  // re-decode the full prefix each step (generate.hpp:21)
 };
 
 // generate.cpp:15-26

@@ -56,6 +56,23 @@ class ModelBase {
   virtual void set_train_step(int64_t) {}
   // generation decodes without dropout (generate.cpp)
   virtual void set_inference(bool) {}
+  // incremental decoding on the device (reference model.cpp:315-557).
+  // encode_cross_kv: encoder + every decoder layer's cross K/V, one node of
+  // rows b*src_width+j, cols layers*2d ([k|v] per layer)
+  virtual int encode_cross_kv(DeviceTape&, const DeviceBatch&) const {
+    throw ConfigError("model: no incremental decoder");
+  }
+  // one target position `pos` for `rows` hypotheses (ids: device [rows]).
+  // self_cache: layers consecutive [rows*cap x 2d] (k|v) matrices, the new
+  // position's k/v stored at row r*cap+pos; cross: [rows*src_width x
+  // layers*2d]; self_len [rows] = pos+1; src_len [rows]. Returns the logits node.
+  virtual int decode_step(DeviceTape&, const int32_t* /*ids*/, int /*rows*/, int /*pos*/, void* /*self_cache*/,
+                          int /*cap*/, const void* /*cross*/, int /*src_width*/, const int32_t* /*self_len*/,
+                          const int32_t* /*src_len*/) const {
+    throw ConfigError("model: no incremental decoder");
+  }
+  virtual int decoder_layers() const { return 0; }
+  virtual int model_dim() const { return 0; }
   // canonical -> device permutation helpers (host vectors)
   void to_device_order(std::span<const float> canonical, std::span<float> device) const;
   void to_canonical_order(std::span<const float> device, std::span<float> canonical) const;

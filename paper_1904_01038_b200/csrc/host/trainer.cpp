@@ -681,3 +681,113 @@ std::vector<float> Trainer::last_position_logits(const MiniBatch& mb) {
 }
 
 }  // namespace sqf
+
+namespace sqf {
+
+void Trainer::inc_begin(const MiniBatch& src, const std::vector<int>& row_sentence, int cap) {
+  // model.cpp:315-465 (forward_encoder + make_incremental_state): the encoder
+  // and every layer's cross K/V once per batch, rows replicated per hypothesis
+  join_optimizer();
+  inc_.reset();
+  const int R = int(row_sentence.size()), S = src.src_width;
+  if (R < 1 || cap < 1 || S < 1) throw ShapeError("incremental state: empty");
+  auto st = std::make_unique<IncState>();
+  st->rows = R;
+  st->src_width = S;
+  st->cap = cap;
+  st->layers = model_->decoder_layers();
+  st->d = model_->model_dim();
+  const size_t kv_row = size_t(2) * st->d * 4, layer_bytes = size_t(R) * cap * kv_row;
+  const size_t cross_row = size_t(S) * st->layers * kv_row;
+  for (auto& p : st->self) cuda_check(cudaMalloc(&p, layer_bytes * st->layers), "kv cache");
+  cuda_check(cudaMemsetAsync(st->self[0], 0, layer_bytes * st->layers, stream_), "kv cache zero");
+  cuda_check(cudaMalloc(&st->cross, cross_row * R), "cross cache");
+  cuda_check(cudaMalloc(&st->idx, size_t(4) * R * 4), "decoder indices");
+
+  MiniBatch mb;
+  mb.rows = src.rows;
+  mb.src_width = S;
+  mb.tgt_width = 1;
+  mb.source = src.source;
+  mb.src_lens = src.src_lens;
+  mb.target_in.assign(size_t(src.rows), kBos);
+  mb.target_out.assign(size_t(src.rows), kPad);
+  mb.tgt_lens.assign(size_t(src.rows), 1);
+  std::vector<PackedBatch> packs{PackedBatch::pack(mb)};
+  std::vector<DeviceBatch> dev;
+  upload(packs, dev);
+  arena_[0].reset();
+  std::vector<int32_t> h(size_t(4) * R, 0);
+  for (int r = 0; r < R; ++r) {
+    h[size_t(2) * R + r] = std::max(1, src.src_lens.at(size_t(row_sentence[r])));  // empty rows: a pad key
+    h[size_t(3) * R + r] = row_sentence[r];
+  }
+  cuda_check(cudaMemcpyAsync(st->idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream_), "indices H2D");
+  model_->set_inference(true);
+  try {
+    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    tape.set_counters(counters_, kCounters, &counter_cursor_);
+    const int ckv = model_->encode_cross_kv(tape, dev[0]);
+    sfk_check(sfk_gather_rows(tape.out(ckv), st->cross, st->idx + size_t(3) * R, R, int64_t(cross_row), 1,
+                              int64_t(cross_row) * R, stream_),
+              "cross cache gather");
+    cuda_check(cudaStreamSynchronize(stream_), "incremental state sync");
+  } catch (...) {
+    model_->set_inference(false);
+    throw;
+  }
+  model_->set_inference(false);
+  inc_ = std::move(st);
+}
+
+std::vector<float> Trainer::inc_step(const std::vector<int>& last, int pos) {
+  if (!inc_) throw ConfigError("incremental decoding: no state (inc_begin first)");
+  IncState& st = *inc_;
+  const int R = st.rows, V = model_->target_vocab();
+  if (int(last.size()) != R) throw ShapeError("incremental decoding: one token per row");
+  std::vector<int32_t> h(size_t(2) * R);
+  for (int r = 0; r < R; ++r) {
+    h[size_t(r)] = last[size_t(r)];
+    h[size_t(R) + r] = pos + 1;
+  }
+  cuda_check(cudaMemcpyAsync(st.idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream_), "step H2D");
+  arena_[0].reset();
+  std::vector<float> out(size_t(R) * V);
+  model_->set_inference(true);
+  try {
+    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    tape.set_counters(counters_, kCounters, &counter_cursor_);
+    const int lg = model_->decode_step(tape, st.idx, R, pos, st.self[st.cur], st.cap, st.cross, st.src_width,
+                                       st.idx + R, st.idx + size_t(2) * R);
+    cuda_check(cudaMemcpyAsync(out.data(), tape.out(lg), out.size() * 4, cudaMemcpyDeviceToHost, stream_),
+               "step logits D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "step sync");
+  } catch (...) {
+    model_->set_inference(false);
+    throw;
+  }
+  model_->set_inference(false);
+  return out;
+}
+
+void Trainer::inc_reorder(const std::vector<int>& order) {
+  // model.cpp:540-557: new row r = old row order[r], every layer's K/V
+  if (!inc_) throw ConfigError("incremental decoding: no state (inc_begin first)");
+  IncState& st = *inc_;
+  const int R = st.rows;
+  if (int(order.size()) != R) throw ShapeError("reorder: one source row per row");
+  std::vector<int32_t> h(order.begin(), order.end());
+  for (int v : h)
+    if (v < 0 || v >= R) throw BoundsError("reorder: row index out of range");
+  cuda_check(cudaMemcpyAsync(st.idx + size_t(3) * R, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream_),
+             "order H2D");
+  const int64_t row = int64_t(st.cap) * 2 * st.d * 4;
+  sfk_check(sfk_gather_rows(st.self[st.cur], st.self[st.cur ^ 1], st.idx + size_t(3) * R, R, row, st.layers,
+                            row * R, stream_),
+            "kv cache reorder");
+  st.cur ^= 1;
+}
+
+void Trainer::inc_end() { inc_.reset(); }
+
+}  // namespace sqf

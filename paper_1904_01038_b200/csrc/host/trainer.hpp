@@ -50,6 +50,16 @@ class Trainer {
   // the fp32 master; returns the logits of each row's last target position,
   // rows x target_vocab, row-major (reference generate.cpp:86-120)
   std::vector<float> last_position_logits(const MiniBatch& mb);
+  // incremental decoding (reference make_incremental_state /
+  // forward_decoder_step / reorder_incremental_state, model.cpp:315-557):
+  // K/V caches of `rows` hypotheses live on the device; row r decodes
+  // sentence row_sentence[r] of `src` (only source fields used); positions
+  // up to cap-1. step returns rows x target_vocab logits; reorder gathers
+  // cache rows (new row r = old row order[r]).
+  void inc_begin(const MiniBatch& src, const std::vector<int>& row_sentence, int cap);
+  std::vector<float> inc_step(const std::vector<int>& last_tokens, int pos);
+  void inc_reorder(const std::vector<int>& order);
+  void inc_end();
 
   int64_t step() const { return step_; }
   int epoch() const { return epoch_; }
@@ -105,6 +115,21 @@ class Trainer {
   int overlap_early() const { return overlap_early_; }
 
  private:
+  struct IncState {
+    int rows = 0, src_width = 0, cap = 0, layers = 0, d = 0;
+    void* self[2] = {nullptr, nullptr};  // double-buffered [layers][rows*cap][2d]
+    int cur = 0;
+    void* cross = nullptr;               // [rows*src_width][layers*2d]
+    int32_t* idx = nullptr;              // device: ids[rows] | self_len[rows] | src_len[rows] | order[rows]
+    ~IncState() {
+      cudaFree(self[0]);
+      cudaFree(self[1]);
+      cudaFree(cross);
+      cudaFree(idx);
+    }
+  };
+  std::unique_ptr<IncState> inc_;
+
   Config cfg_;
   std::unique_ptr<TaskBase> task_;
   std::unique_ptr<ModelBase> model_;

@@ -116,11 +116,12 @@ def test_gen_config_defaults(trained):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("no_cache", [False, True])
 @pytest.mark.parametrize("beam,lenpen", [(4, 0.6), (1, 0.0), (5, 1.0)])
-def test_beam_search_matches_reference(trained, beam, lenpen):
+def test_beam_search_matches_reference(trained, beam, lenpen, no_cache):
     mine, theirs, c = trained
     src = sources(c, range(0, 12))
-    a = mine.generate(src, "beam", beam=beam, lenpen=lenpen)
+    a = mine.generate(src, "beam", beam=beam, lenpen=lenpen, no_cache=no_cache)
     b = theirs.generate(src, "beam", beam=beam, lenpen=lenpen)
     assert len(a) == len(b)
     for hs, rs in zip(a, b):
@@ -150,8 +151,8 @@ def test_diverse_beam_search_matches_reference(trained):
 def test_top_k_sampling_matches_reference(trained):
     mine, theirs, c = trained
     src = sources(c, range(40, 50))
-    for topk, temp in ((1, 1.0), (5, 0.8), (20, 1.5)):
-        a = mine.generate(src, "sample", topk=topk, temperature=temp, seed=11)
+    for (topk, temp), nc in zip(((1, 1.0), (5, 0.8), (20, 1.5), (5, 0.8)), (False, False, False, True)):
+        a = mine.generate(src, "sample", topk=topk, temperature=temp, seed=11, no_cache=nc)
         b = theirs.generate(src, "sample", topk=topk, temperature=temp, seed=11)
         for (h,), (r,) in zip(a, b):
             same(h, r)
@@ -189,3 +190,19 @@ def test_empty_row_and_length_caps(trained):
         for h, r in zip(hs, rs):
             assert len(h.tokens) <= 2 and h.tokens[-1] == 2
             same(h, r)
+
+
+@pytest.mark.gpu
+def test_incremental_decoder_agrees_with_recomputed(trained):
+    """The device K/V-cache decoder (gather reorder) against the cache-free
+    re-decode of every prefix on the same device (test_generate.cpp:268-297)."""
+    mine, _, c = trained
+    src = sources(c, range(80, 90)) + [[]]
+    for mode, kw in (("beam", {"beam": 4}), ("diverse", {"beam": 4, "diverse_groups": 2}),
+                     ("sample", {"topk": 8, "seed": 5})):
+        a = mine.generate(src, mode, **kw)
+        b = mine.generate(src, mode, no_cache=True, **kw)
+        for hs, rs in zip(a, b):
+            assert [h.tokens for h in hs] == [r.tokens for r in rs], mode
+            for h, r in zip(hs, rs):
+                assert np.max(np.abs(np.subtract(h.step_scores, r.step_scores))) <= 1e-5
