@@ -182,7 +182,8 @@ typedef struct sqf_gen_config {
   double temperature;
   uint64_t seed;
   int32_t no_cache;         /* 1 = re-decode the full prefix each step (reference oracle mode) */
-  int32_t _pad;
+  int32_t host_select;      /* 1 = rank all rows x V candidates on the host instead of
+                               sfk_beam_topk on the device (testing) */
 } sqf_gen_config;
 /* gen_config_from(trainer's resolved config) (generate.cpp:15-26) */
 int sqf_gen_config_default(void* t, sqf_gen_config* out);

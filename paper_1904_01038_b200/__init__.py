@@ -296,7 +296,7 @@ class Trainer:
         """gen_config_from(the resolved config) (generate.cpp:15-26)."""
         g = L.GenConfigC()
         L.check(L.sqf_gen_config_default(self._h, C.byref(g)))
-        return {f: getattr(g, f) for f, _ in L.GenConfigC._fields_ if f != "_pad"}
+        return {f: getattr(g, f) for f, _ in L.GenConfigC._fields_}
 
     def generate(self, sources, mode: str = "beam", stream_ids=None, **cfg) -> list:
         """beam_search / diverse_beam_search / top_k_sample over source id rows

@@ -191,7 +191,7 @@ def cstrs(items):
 
 class GenConfigC(C.Structure):
     _fields_ = [("beam", i32), ("max_len", i32), ("diverse_groups", i32), ("topk", i32), ("lenpen", f64),
-                ("diverse_strength", f64), ("temperature", f64), ("seed", u64), ("no_cache", i32), ("_pad", i32)]
+                ("diverse_strength", f64), ("temperature", f64), ("seed", u64), ("no_cache", i32), ("host_select", i32)]
 
 
 sqf_gen_config_default = _sig("sqf_gen_config_default", C.c_int, vp, P(GenConfigC))

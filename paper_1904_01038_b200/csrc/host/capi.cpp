@@ -524,7 +524,7 @@ int sqf_gen_config_default(void* t, sqf_gen_config* out) {
   SQF_GUARD({
     GenConfig g = gen_config_from(T(t)->config());
     *out = sqf_gen_config{g.beam, g.max_len, g.diverse_groups, g.topk, g.lenpen, g.diverse_strength,
-                          g.temperature, g.seed, g.no_cache ? 1 : 0, 0};
+                          g.temperature, g.seed, g.no_cache ? 1 : 0, g.host_select ? 1 : 0};
   })
 }
 
@@ -550,6 +550,7 @@ int sqf_generate(void* t, int mode, const int32_t* source, const int32_t* src_le
     g.temperature = c->temperature;
     g.seed = c->seed;
     g.no_cache = c->no_cache != 0;
+    g.host_select = c->host_select != 0;
     auto res = std::make_unique<std::vector<std::vector<Hypothesis>>>();
     if (mode == 0) {
       *res = beam_search(*T(t), b, g);

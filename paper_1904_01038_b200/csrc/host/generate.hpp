@@ -30,6 +30,7 @@ struct GenConfig {
   double temperature = 1.0;
   uint64_t seed = 1;
   bool no_cache = false;  // re-decode the full prefix each step (generate.hpp:21)
+  bool host_select = false;  // B200: rank all rows x V candidates on the host (testing)
 };
 
 // generate.cpp:15-26

@@ -740,10 +740,10 @@ void Trainer::inc_begin(const MiniBatch& src, const std::vector<int>& row_senten
   inc_ = std::move(st);
 }
 
-std::vector<float> Trainer::inc_step(const std::vector<int>& last, int pos) {
+void Trainer::inc_run(const std::vector<int>& last, int pos, const std::function<void(DeviceTape&, int)>& consume) {
   if (!inc_) throw ConfigError("incremental decoding: no state (inc_begin first)");
   IncState& st = *inc_;
-  const int R = st.rows, V = model_->target_vocab();
+  const int R = st.rows;
   if (int(last.size()) != R) throw ShapeError("incremental decoding: one token per row");
   std::vector<int32_t> h(size_t(2) * R);
   for (int r = 0; r < R; ++r) {
@@ -752,21 +752,65 @@ std::vector<float> Trainer::inc_step(const std::vector<int>& last, int pos) {
   }
   cuda_check(cudaMemcpyAsync(st.idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream_), "step H2D");
   arena_[0].reset();
-  std::vector<float> out(size_t(R) * V);
   model_->set_inference(true);
   try {
     DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     const int lg = model_->decode_step(tape, st.idx, R, pos, st.self[st.cur], st.cap, st.cross, st.src_width,
                                        st.idx + R, st.idx + size_t(2) * R);
-    cuda_check(cudaMemcpyAsync(out.data(), tape.out(lg), out.size() * 4, cudaMemcpyDeviceToHost, stream_),
-               "step logits D2H");
+    consume(tape, lg);
     cuda_check(cudaStreamSynchronize(stream_), "step sync");
   } catch (...) {
     model_->set_inference(false);
     throw;
   }
   model_->set_inference(false);
+}
+
+std::vector<float> Trainer::inc_step(const std::vector<int>& last, int pos) {
+  const int V = model_->target_vocab();
+  std::vector<float> out(last.size() * size_t(V));
+  inc_run(last, pos, [&](DeviceTape& tape, int lg) {
+    cuda_check(cudaMemcpyAsync(out.data(), tape.out(lg), out.size() * 4, cudaMemcpyDeviceToHost, stream_),
+               "step logits D2H");
+  });
+  return out;
+}
+
+Trainer::BeamCands Trainer::inc_step_topk(const std::vector<int>& last, int pos, const std::vector<double>& cum,
+                                          int kk) {
+  if (!inc_) throw ConfigError("incremental decoding: no state (inc_begin first)");
+  IncState& st = *inc_;
+  const int R = st.rows, V = model_->target_vocab();
+  kk = std::min(kk, V);
+  if (int(cum.size()) != R) throw ShapeError("incremental decoding: one cumulative score per row");
+  if (!st.cum) cuda_check(cudaMalloc(&st.cum, size_t(R) * 8), "beam cum");
+  if (st.cands_kk < kk) {
+    cudaFree(st.cands);
+    st.cands = nullptr;
+    cuda_check(cudaMalloc(&st.cands, size_t(R) * (2 + 2 * size_t(kk)) * 4), "beam candidates");
+    st.cands_kk = kk;
+  }
+  cuda_check(cudaMemcpyAsync(st.cum, cum.data(), size_t(R) * 8, cudaMemcpyHostToDevice, stream_), "cum H2D");
+  BeamCands out;
+  out.kk = kk;
+  out.lse.resize(size_t(R));
+  out.eos_lp.resize(size_t(R));
+  out.tok.resize(size_t(R) * kk);
+  out.lp.resize(size_t(R) * kk);
+  float* lse = static_cast<float*>(st.cands);
+  float* eos_lp = lse + R;
+  int32_t* tok = reinterpret_cast<int32_t*>(eos_lp + R);
+  float* lp = reinterpret_cast<float*>(tok + size_t(R) * kk);
+  inc_run(last, pos, [&](DeviceTape& tape, int lg) {
+    sfk_check(sfk_beam_topk(static_cast<const float*>(tape.out(lg)), V, R, V, st.cum, kk, kEos, lse, eos_lp, tok, lp,
+                            stream_),
+              "beam_topk");
+    cuda_check(cudaMemcpyAsync(out.lse.data(), lse, size_t(R) * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaMemcpyAsync(out.eos_lp.data(), eos_lp, size_t(R) * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaMemcpyAsync(out.tok.data(), tok, size_t(R) * kk * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaMemcpyAsync(out.lp.data(), lp, size_t(R) * kk * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+  });
   return out;
 }
 

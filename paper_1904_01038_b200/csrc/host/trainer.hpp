@@ -58,6 +58,15 @@ class Trainer {
   // cache rows (new row r = old row order[r]).
   void inc_begin(const MiniBatch& src, const std::vector<int>& row_sentence, int cap);
   std::vector<float> inc_step(const std::vector<int>& last_tokens, int pos);
+  // the same step with candidate selection on the device (sfk_beam_topk):
+  // per row lse, eos log-prob and the kk best (token, log-prob) under
+  // key = cum[r] + lp, best first -- rows x kk values come back, not rows x V
+  struct BeamCands {
+    int kk = 0;
+    std::vector<float> lse, eos_lp, lp;
+    std::vector<int32_t> tok;
+  };
+  BeamCands inc_step_topk(const std::vector<int>& last_tokens, int pos, const std::vector<double>& cum, int kk);
   void inc_reorder(const std::vector<int>& order);
   void inc_end();
 
@@ -121,7 +130,12 @@ class Trainer {
     int cur = 0;
     void* cross = nullptr;               // [rows*src_width][layers*2d]
     int32_t* idx = nullptr;              // device: ids[rows] | self_len[rows] | src_len[rows] | order[rows]
+    double* cum = nullptr;               // device [rows]
+    void* cands = nullptr;               // device: lse | eos_lp | tok[rows*kk] | lp[rows*kk]
+    int cands_kk = 0;
     ~IncState() {
+      cudaFree(cum);
+      cudaFree(cands);
       cudaFree(self[0]);
       cudaFree(self[1]);
       cudaFree(cross);
@@ -129,6 +143,7 @@ class Trainer {
     }
   };
   std::unique_ptr<IncState> inc_;
+  void inc_run(const std::vector<int>& last, int pos, const std::function<void(DeviceTape&, int)>& consume);
 
   Config cfg_;
   std::unique_ptr<TaskBase> task_;

@@ -202,7 +202,9 @@ def test_incremental_decoder_agrees_with_recomputed(trained):
                      ("sample", {"topk": 8, "seed": 5})):
         a = mine.generate(src, mode, **kw)
         b = mine.generate(src, mode, no_cache=True, **kw)
-        for hs, rs in zip(a, b):
-            assert [h.tokens for h in hs] == [r.tokens for r in rs], mode
-            for h, r in zip(hs, rs):
-                assert np.max(np.abs(np.subtract(h.step_scores, r.step_scores))) <= 1e-5
+        h_sel = mine.generate(src, mode, host_select=True, **kw)
+        for other in (b, h_sel):
+            for hs, rs in zip(a, other):
+                assert [h.tokens for h in hs] == [r.tokens for r in rs], mode
+                for h, r in zip(hs, rs):
+                    assert np.max(np.abs(np.subtract(h.step_scores, r.step_scores))) <= 1e-5
