@@ -268,12 +268,12 @@ int sfk_cast(const float* src, void* dst, int dst_dtype, int64_t n, void* stream
 int sfk_gather_rows(const void* src, void* dst, const int32_t* idx, int rows, int64_t row_bytes, int nmat,
                     int64_t mat_bytes, void* stream);
 
-/* Beam candidate selection (generate.cpp:220-262) per fp32 logits row:
+/* Beam candidate selection (generate.cpp:220-262) per logits row (dtype):
  * lse[r], eos_lp[r] = logit[eos] - lse, and the kk best tokens under
  * key = cum[r] + (logit - lse) descending, token ascending on ties
  * (tok/lp: rows x kk, best first). */
-int sfk_beam_topk(const float* logits, int64_t ld, int rows, int vocab, const double* cum, int kk, int eos,
-                  float* lse, float* eos_lp, int32_t* tok, float* lp, void* stream);
+int sfk_beam_topk(int dtype, const void* logits, int64_t ld, int rows, int vocab, const double* cum, int kk,
+                  int eos, float* lse, float* eos_lp, int32_t* tok, float* lp, void* stream);
 /* dst = src converted (any dtype pair) */
 int sfk_convert(int src_dtype, const void* src, int dst_dtype, void* dst, int64_t n,
                 void* stream);

@@ -170,8 +170,9 @@ int sqf_schedule_lr(const char* name, double base, int64_t warmup, double init, 
 float sqf_quantize_fp16(float x);
 
 /* ---- generation (reference generate.hpp:12-90, generate.cpp:123-480) ----
- * GenConfig fields; the decoder runs on the device from the fp32 master,
- * incrementally with per-layer K/V caches unless no_cache. */
+ * GenConfig fields; the decoder runs on the device from the trainer's compute
+ * weights (fp32 master, or the fp16/bf16 shadow), incrementally with per-layer
+ * K/V caches unless no_cache. */
 typedef struct sqf_gen_config {
   int32_t beam;
   int32_t max_len;          /* 0 = 2 * source_len + 8 */

@@ -1,7 +1,8 @@
 // Sequence generation over the B200 trainer's model (reference
 // include/seqforge/generate.hpp, src/generate.cpp): beam search, diverse beam
 // search, top-k sampling, inference batching. The decoder runs on the device
-// (Trainer::last_position_logits, fp32 master, sm_100a kernels); the host keeps
+// (Trainer::inc_* / last_position_logits, the trainer's compute weights:
+// fp32 master, or the fp16/bf16 shadow on the tensor-core kernels); the host keeps
 // the reference's selection rules (candidate order, stable ties, eos banking,
 // admissible early stop, final n-best order) so hypotheses match it.
 //

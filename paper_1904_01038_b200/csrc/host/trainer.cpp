@@ -649,6 +649,16 @@ EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
 
 namespace sqf {
 
+int64_t Trainer::logits_ld(int V) const { return dtype_ == SFK_F32 ? V : (int64_t(V) + 7) / 8 * 8; }
+
+const float* Trainer::logits_as_f32(const void* logits, int64_t n) {
+  // 16-bit decoding: widen the logits once on the device (arena scratch)
+  if (dtype_ == SFK_F32) return static_cast<const float*>(logits);
+  float* f = static_cast<float*>(arena_[0].alloc(size_t(n) * 4));
+  sfk_check(sfk_convert(dtype_, logits, SFK_F32, f, n, stream_), "logits widen");
+  return f;
+}
+
 std::vector<float> Trainer::last_position_logits(const MiniBatch& mb) {
   // reference generate.cpp:86-120 (recompute_logits): decode every row's full
   // prefix and keep the final position's logits; the decoder runs on the
@@ -663,13 +673,14 @@ std::vector<float> Trainer::last_position_logits(const MiniBatch& mb) {
   model_->set_inference(true);
   std::vector<float> out(size_t(R) * V);
   try {
-    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    DeviceTape tape(arena_[0], DeviceParams{master_, compute_, nullptr, n_}, dtype_, stream_);
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     const int lg = model_->forward_to_logits(tape, dev[0]);
     if (tape.rows(lg) != R * T || tape.cols(lg) != V) throw ShapeError("generation: logits shape");
-    const float* base = static_cast<const float*>(tape.out(lg)) + size_t(T - 1) * V;
-    cuda_check(cudaMemcpy2DAsync(out.data(), size_t(V) * 4, base, size_t(T) * V * 4, size_t(V) * 4, R,
-                                 cudaMemcpyDeviceToHost, stream_),
+    const int64_t ld = logits_ld(V);
+    const float* f = logits_as_f32(tape.out(lg), int64_t(R) * T * ld);
+    cuda_check(cudaMemcpy2DAsync(out.data(), size_t(V) * 4, f + size_t(T - 1) * ld, size_t(T) * ld * 4,
+                                 size_t(V) * 4, R, cudaMemcpyDeviceToHost, stream_),
                "logits D2H");
     cuda_check(cudaDeviceSynchronize(), "generation sync");
   } catch (...) {
@@ -697,7 +708,8 @@ void Trainer::inc_begin(const MiniBatch& src, const std::vector<int>& row_senten
   st->cap = cap;
   st->layers = model_->decoder_layers();
   st->d = model_->model_dim();
-  const size_t kv_row = size_t(2) * st->d * 4, layer_bytes = size_t(R) * cap * kv_row;
+  st->es = dtype_ == SFK_F32 ? 4 : 2;
+  const size_t kv_row = size_t(2) * st->d * st->es, layer_bytes = size_t(R) * cap * kv_row;
   const size_t cross_row = size_t(S) * st->layers * kv_row;
   for (auto& p : st->self) cuda_check(cudaMalloc(&p, layer_bytes * st->layers), "kv cache");
   cuda_check(cudaMemsetAsync(st->self[0], 0, layer_bytes * st->layers, stream_), "kv cache zero");
@@ -725,7 +737,7 @@ void Trainer::inc_begin(const MiniBatch& src, const std::vector<int>& row_senten
   cuda_check(cudaMemcpyAsync(st->idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream_), "indices H2D");
   model_->set_inference(true);
   try {
-    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    DeviceTape tape(arena_[0], DeviceParams{master_, compute_, nullptr, n_}, dtype_, stream_);
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     const int ckv = model_->encode_cross_kv(tape, dev[0]);
     sfk_check(sfk_gather_rows(tape.out(ckv), st->cross, st->idx + size_t(3) * R, R, int64_t(cross_row), 1,
@@ -754,7 +766,7 @@ void Trainer::inc_run(const std::vector<int>& last, int pos, const std::function
   arena_[0].reset();
   model_->set_inference(true);
   try {
-    DeviceTape tape(arena_[0], DeviceParams{master_, master_, nullptr, n_}, SFK_F32, stream_);
+    DeviceTape tape(arena_[0], DeviceParams{master_, compute_, nullptr, n_}, dtype_, stream_);
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     const int lg = model_->decode_step(tape, st.idx, R, pos, st.self[st.cur], st.cap, st.cross, st.src_width,
                                        st.idx + R, st.idx + size_t(2) * R);
@@ -771,7 +783,10 @@ std::vector<float> Trainer::inc_step(const std::vector<int>& last, int pos) {
   const int V = model_->target_vocab();
   std::vector<float> out(last.size() * size_t(V));
   inc_run(last, pos, [&](DeviceTape& tape, int lg) {
-    cuda_check(cudaMemcpyAsync(out.data(), tape.out(lg), out.size() * 4, cudaMemcpyDeviceToHost, stream_),
+    const int64_t ld = logits_ld(V), R = int64_t(last.size());
+    const float* f = logits_as_f32(tape.out(lg), R * ld);
+    cuda_check(cudaMemcpy2DAsync(out.data(), size_t(V) * 4, f, size_t(ld) * 4, size_t(V) * 4, size_t(R),
+                                 cudaMemcpyDeviceToHost, stream_),
                "step logits D2H");
   });
   return out;
@@ -803,7 +818,7 @@ Trainer::BeamCands Trainer::inc_step_topk(const std::vector<int>& last, int pos,
   int32_t* tok = reinterpret_cast<int32_t*>(eos_lp + R);
   float* lp = reinterpret_cast<float*>(tok + size_t(R) * kk);
   inc_run(last, pos, [&](DeviceTape& tape, int lg) {
-    sfk_check(sfk_beam_topk(static_cast<const float*>(tape.out(lg)), V, R, V, st.cum, kk, kEos, lse, eos_lp, tok, lp,
+    sfk_check(sfk_beam_topk(dtype_, tape.out(lg), logits_ld(V), R, V, st.cum, kk, kEos, lse, eos_lp, tok, lp,
                             stream_),
               "beam_topk");
     cuda_check(cudaMemcpyAsync(out.lse.data(), lse, size_t(R) * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
@@ -825,7 +840,7 @@ void Trainer::inc_reorder(const std::vector<int>& order) {
     if (v < 0 || v >= R) throw BoundsError("reorder: row index out of range");
   cuda_check(cudaMemcpyAsync(st.idx + size_t(3) * R, h.data(), h.size() * 4, cudaMemcpyHostToDevice, stream_),
              "order H2D");
-  const int64_t row = int64_t(st.cap) * 2 * st.d * 4;
+  const int64_t row = int64_t(st.cap) * 2 * st.d * st.es;
   sfk_check(sfk_gather_rows(st.self[st.cur], st.self[st.cur ^ 1], st.idx + size_t(3) * R, R, row, st.layers,
                             row * R, stream_),
             "kv cache reorder");

@@ -126,6 +126,7 @@ class Trainer {
  private:
   struct IncState {
     int rows = 0, src_width = 0, cap = 0, layers = 0, d = 0;
+    size_t es = 4;                       // cache element size (decoding dtype)
     void* self[2] = {nullptr, nullptr};  // double-buffered [layers][rows*cap][2d]
     int cur = 0;
     void* cross = nullptr;               // [rows*src_width][layers*2d]
@@ -143,6 +144,8 @@ class Trainer {
     }
   };
   std::unique_ptr<IncState> inc_;
+  int64_t logits_ld(int V) const;
+  const float* logits_as_f32(const void* logits, int64_t n);
   void inc_run(const std::vector<int>& last, int pos, const std::function<void(DeviceTape&, int)>& consume);
 
   Config cfg_;

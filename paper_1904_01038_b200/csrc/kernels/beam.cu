@@ -1,5 +1,5 @@
 // Device-side candidate selection for beam search (reference
-// generate.cpp:220-262): per decoder row, the log-partition lse, the eos
+// generate.cpp:220-262): per decoder row (fp32 / fp16 / bf16 logits), the log-partition lse, the eos
 // log-probability, and the kk best continuations under the reference's order
 // -- key = cum (double) + lp (float), lp = logit - lse, key descending, token
 // ascending on ties -- so the host merges rows * kk candidates instead of
@@ -32,18 +32,20 @@ __device__ __forceinline__ Best warp_best(Best b) {
   return b;
 }
 
-__global__ void __launch_bounds__(kThreads) beam_topk_k(const float* __restrict__ logits, int64_t ld, int V,
+template <typename T>
+__global__ void __launch_bounds__(kThreads) beam_topk_k(const T* __restrict__ logits, int64_t ld, int V,
                                                        const double* __restrict__ cum, int kk, int eos,
                                                        float* __restrict__ lse_out, float* __restrict__ eos_lp,
                                                        int32_t* __restrict__ tok_out, float* __restrict__ lp_out) {
   const int row = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float* x = logits + int64_t(row) * ld;
+  const T* xr = logits + int64_t(row) * ld;
+  auto x = [xr](int v) { return Num<T>::ld(xr + v); };
   __shared__ float red[kThreads / 32];
   __shared__ Best bred[kThreads / 32];
   __shared__ Best prev;
 
   float m = -FLT_MAX;
-  for (int v = threadIdx.x; v < V; v += kThreads) m = fmaxf(m, x[v]);
+  for (int v = threadIdx.x; v < V; v += kThreads) m = fmaxf(m, x(v));
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) red[warp] = m;
   __syncthreads();
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const float* __restrict_
   for (int w = 1; w < kThreads / 32; ++w) m = fmaxf(m, red[w]);
   __syncthreads();
   float s = 0.f;
-  for (int v = threadIdx.x; v < V; v += kThreads) s += expf(x[v] - m);
+  for (int v = threadIdx.x; v < V; v += kThreads) s += expf(x(v) - m);
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) red[warp] = s;
   __syncthreads();
@@ -61,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const float* __restrict_
   const double c = cum[row];
   if (threadIdx.x == 0) {
     lse_out[row] = lse;
-    eos_lp[row] = x[eos] - lse;
+    eos_lp[row] = x(eos) - lse;
     prev = Best{DBL_MAX, -1};
   }
   __syncthreads();
@@ -70,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const float* __restrict_
     const Best p = prev;
     Best b{-DBL_MAX, 0x7fffffff};
     for (int v = threadIdx.x; v < V; v += kThreads) {
-      const Best cnd{c + double(x[v] - lse), v};
+      const Best cnd{c + double(x(v) - lse), v};
       if (before(p, cnd) && before(cnd, b)) b = cnd;
     }
     b = warp_best(b);
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const float* __restrict_
         if (before(bred[i], w)) w = bred[i];
       const int t = w.tok < V ? w.tok : eos;  // non-finite row: nothing ranks
       tok_out[int64_t(row) * kk + j] = t;
-      lp_out[int64_t(row) * kk + j] = x[t] - lse;
+      lp_out[int64_t(row) * kk + j] = x(t) - lse;
       prev = w;
     }
     __syncthreads();
@@ -94,14 +96,16 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const float* __restrict_
 
 using namespace sfk;
 
-extern "C" int sfk_beam_topk(const float* logits, int64_t ld, int rows, int vocab, const double* cum, int kk, int eos,
-                             float* lse, float* eos_lp, int32_t* tok, float* lp, void* stream) {
+extern "C" int sfk_beam_topk(int dtype, const void* logits, int64_t ld, int rows, int vocab, const double* cum, int kk,
+                             int eos, float* lse, float* eos_lp, int32_t* tok, float* lp, void* stream) {
   if (rows < 0 || vocab < 1 || kk < 1 || kk > vocab || ld < vocab || eos < 0 || eos >= vocab ||
       (rows && (!logits || !cum || !lse || !eos_lp || !tok || !lp))) {
     set_error("sfk_beam_topk: bad arguments (1 <= kk <= vocab, eos < vocab)");
     return SFK_EINVAL;
   }
   if (rows == 0) return SFK_OK;
-  beam_topk_k<<<rows, kThreads, 0, as_stream(stream)>>>(logits, ld, vocab, cum, kk, eos, lse, eos_lp, tok, lp);
+  SFK_DISPATCH(dtype, T,
+               beam_topk_k<T><<<rows, kThreads, 0, as_stream(stream)>>>(static_cast<const T*>(logits), ld, vocab, cum,
+                                                                       kk, eos, lse, eos_lp, tok, lp));
   return check_launch("sfk_beam_topk");
 }

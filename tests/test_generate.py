@@ -208,3 +208,30 @@ def test_incremental_decoder_agrees_with_recomputed(trained):
                 assert [h.tokens for h in hs] == [r.tokens for r in rs], mode
                 for h, r in zip(hs, rs):
                     assert np.max(np.abs(np.subtract(h.step_scores, r.step_scores))) <= 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec,tol", [("fp16", 2e-2), ("bf16", 5e-2)])
+def test_16bit_decoding_tracks_reference_fp32(trained, prec, tol):
+    """Decoding from the fp16/bf16 shadow on the tensor-core kernels (the
+    paper's FP16 inference) against the reference's fp32 beam search: the
+    reference has no 16-bit decoder, so tokens may differ where candidates are
+    within 16-bit rounding of each other -- most best hypotheses agree and
+    their scores are within the north star's 16-bit tolerance."""
+    import paper_1904_01038_b200 as sqf
+    _, theirs, c = trained
+    m16 = sqf.Trainer("transformer_base_defaults", dict(BASE, max_tokens=1024, **{prec: True}), corpus=c,
+                      src_vocab=1000, tgt_vocab=1000)
+    m16.set_params(theirs.params())
+    src = sources(c, range(0, 16))
+    a = m16.generate(src, "beam", beam=4)
+    b = theirs.generate(src, "beam", beam=4)
+    agree = [x[0].tokens == y[0]["tokens"] for x, y in zip(a, b)]
+    assert sum(agree) >= 12, agree
+    for x, y, ok in zip(a, b, agree):
+        if ok:
+            assert abs(x[0].score - y[0]["score"]) <= tol * max(1.0, abs(y[0]["score"]))
+    nc = m16.generate(src, "beam", beam=4, no_cache=True)
+    assert sum(x[0].tokens == y[0].tokens for x, y in zip(a, nc)) >= 14
+    s = m16.generate(src + [[]], "sample", topk=5, seed=2)
+    assert s[-1][0].tokens == [2] and all(h[0].tokens[-1] == 2 for h in s)

@@ -21,13 +21,15 @@ def main():
     ap.add_argument("--beam", type=int, default=4)
     ap.add_argument("--max-len", type=int, default=0)
     ap.add_argument("--ref-sentences", type=int, default=4)
+    ap.add_argument("--precision", choices=["fp32", "fp16", "bf16"], default="fp32")
     args = ap.parse_args()
     import paper_1904_01038_b200 as sqf
     c = sqf.synthetic_corpus(max(args.sentences, 64), args.vocab, args.vocab, 1.1, 1)
     ov = {"max_tokens": 1024, "seed": 1}
-    tr = sqf.Trainer(args.arch, ov, corpus=c, src_vocab=args.vocab, tgt_vocab=args.vocab)
+    tov = dict(ov, **({args.precision: True} if args.precision != "fp32" else {}))
+    tr = sqf.Trainer(args.arch, tov, corpus=c, src_vocab=args.vocab, tgt_vocab=args.vocab)
     src = [list(c.pair(i)[0]) for i in range(args.sentences)]
-    out = {"workload": f"{args.arch} beam {args.beam}, {args.sentences} sentences, V={args.vocab}, fp32 master"}
+    out = {"workload": f"{args.arch} beam {args.beam}, {args.sentences} sentences, V={args.vocab}, {args.precision} weights"}
     tr.generate(src[:2], "beam", beam=args.beam, max_len=args.max_len)  # warm-up
     for name, nc in (("incremental", False), ("recompute", True)):
         t0 = time.perf_counter()
