@@ -490,3 +490,51 @@ def test_gemm_fused_bias_grad(dtype, shape, pair):
     torch.testing.assert_close(outs[0][0].double(), want_w, rtol=tol, atol=tol * k ** 0.5)
     torch.testing.assert_close(outs[0][1].double(), want_b, rtol=tol, atol=tol * k ** 0.5)
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+# ---------------------------------------------------------------- generation kernels
+
+def test_gather_rows_reorders_every_matrix():
+    lib = L()
+    rows, row_elems, nmat = 37, 96, 5
+    src = torch.randn(nmat, rows, row_elems, device="cuda")
+    dst = torch.empty_like(src)
+    idx = torch.randint(0, rows, (rows,), device="cuda", dtype=torch.int32)
+    lib.check(lib.sfk_gather_rows(ptr(src), ptr(dst), ptr(idx), rows, row_elems * 4, nmat, rows * row_elems * 4,
+                                  stream()), kernel=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src[:, idx.long()])
+    assert lib.sfk_gather_rows(ptr(src), ptr(src), ptr(idx), rows, row_elems * 4, nmat, 0, stream()) != 0
+
+
+@pytest.mark.parametrize("dt,V,kk", [(0, 1000, 8), (1, 32768, 8), (2, 5000, 10), (0, 7, 7)])
+def test_beam_topk_order_and_values(dt, V, kk):
+    """sfk_beam_topk against a host ranking of every candidate: key = cum +
+    (logit - lse) descending, token ascending on ties (generate.cpp:246-249);
+    ties are forced by repeating logit values."""
+    lib = L()
+    rows = 12
+    g = torch.Generator(device="cuda").manual_seed(dt * 7 + kk)
+    logits = (torch.randn(rows, V, device="cuda", generator=g) * 3).to(TDT[dt])
+    logits[:, 1::3] = logits[:, 0:1]  # many exact ties in every row
+    ld = V
+    cum = torch.randn(rows, device="cuda", dtype=torch.float64, generator=g) * 10
+    lse = torch.empty(rows, device="cuda")
+    eos_lp = torch.empty(rows, device="cuda")
+    tok = torch.empty(rows, kk, device="cuda", dtype=torch.int32)
+    lp = torch.empty(rows, kk, device="cuda")
+    lib.check(lib.sfk_beam_topk(dt, ptr(logits), ld, rows, V, ptr(cum), kk, 2, ptr(lse), ptr(eos_lp), ptr(tok),
+                                ptr(lp), stream()), kernel=True)
+    torch.cuda.synchronize()
+    x = logits.float().cpu().numpy()
+    c = cum.cpu().numpy()
+    want_lse = np.log(np.exp(x.astype(np.float64) - x.max(1, keepdims=True)).sum(1)) + x.max(1)
+    np.testing.assert_allclose(lse.cpu().numpy(), want_lse, rtol=0, atol=1e-4)
+    got_lse = lse.cpu().numpy()
+    np.testing.assert_allclose(eos_lp.cpu().numpy(), x[:, 2] - got_lse, atol=1e-6)
+    for r in range(rows):
+        lpr = (x[r] - got_lse[r]).astype(np.float32)
+        key = c[r] + lpr.astype(np.float64)
+        order = sorted(range(V), key=lambda v: (-key[v], v))[:kk]
+        assert tok[r].cpu().tolist() == order, r
+        np.testing.assert_array_equal(lp[r].cpu().numpy(), lpr[order])
