@@ -817,15 +817,18 @@ Trainer::BeamCands Trainer::inc_step_topk(const std::vector<int>& last, int pos,
   float* eos_lp = lse + R;
   int32_t* tok = reinterpret_cast<int32_t*>(eos_lp + R);
   float* lp = reinterpret_cast<float*>(tok + size_t(R) * kk);
+  std::vector<uint32_t> host(size_t(R) * (2 + 2 * size_t(kk)));
   inc_run(last, pos, [&](DeviceTape& tape, int lg) {
     sfk_check(sfk_beam_topk(dtype_, tape.out(lg), logits_ld(V), R, V, st.cum, kk, kEos, lse, eos_lp, tok, lp,
                             stream_),
               "beam_topk");
-    cuda_check(cudaMemcpyAsync(out.lse.data(), lse, size_t(R) * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
-    cuda_check(cudaMemcpyAsync(out.eos_lp.data(), eos_lp, size_t(R) * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
-    cuda_check(cudaMemcpyAsync(out.tok.data(), tok, size_t(R) * kk * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
-    cuda_check(cudaMemcpyAsync(out.lp.data(), lp, size_t(R) * kk * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    // lse | eos_lp | tok | lp are contiguous: one read-back per position
+    cuda_check(cudaMemcpyAsync(host.data(), lse, host.size() * 4, cudaMemcpyDeviceToHost, stream_), "candidates D2H");
   });
+  std::memcpy(out.lse.data(), host.data(), size_t(R) * 4);
+  std::memcpy(out.eos_lp.data(), host.data() + R, size_t(R) * 4);
+  std::memcpy(out.tok.data(), host.data() + 2 * size_t(R), size_t(R) * kk * 4);
+  std::memcpy(out.lp.data(), host.data() + 2 * size_t(R) + size_t(R) * kk, size_t(R) * kk * 4);
   return out;
 }
 
