@@ -235,3 +235,29 @@ def test_16bit_decoding_tracks_reference_fp32(trained, prec, tol):
     assert sum(x[0].tokens == y[0].tokens for x, y in zip(a, nc)) >= 14
     s = m16.generate(src + [[]], "sample", topk=5, seed=2)
     assert s[-1][0].tokens == [2] and all(h[0].tokens[-1] == 2 for h in s)
+
+
+@pytest.mark.gpu
+def test_saturated_beam_enumerates_every_hypothesis():
+    """test_generate.cpp:150-220: with V = 6 (5 non-eos continuations) and a
+    length cap of 3, a beam of 31 banks every finished sequence (1 + 5 + 25);
+    the B200 list equals the reference's, order included."""
+    import itertools
+
+    import paper_1904_01038_b200 as sqf
+    c = corpus(40, 6)
+    ov = dict(BASE, max_tokens=256)
+    theirs = ref.RefTrainer("tiny_transformer", dict(ov, max_positions=256), c, 6, 6)
+    for _ in range(5):
+        theirs.train_one()
+    mine = sqf.Trainer("tiny_transformer", dict(ov, max_positions=256), corpus=c, src_vocab=6, tgt_vocab=6)
+    mine.set_params(theirs.params())
+    src = sources(c, range(2))
+    for no_cache in (False, True):
+        a = mine.generate(src, "beam", beam=31, max_len=3, lenpen=0.6, no_cache=no_cache)
+        b = theirs.generate(src, "beam", beam=31, max_len=3, lenpen=0.6)
+        for hs, rs in zip(a, b):
+            want = {tuple(p) + (2,) for n in range(3) for p in itertools.product([0, 1, 3, 4, 5], repeat=n)}
+            assert len(hs) == 31 and {tuple(h.tokens) for h in hs} == want
+            for h, r in zip(hs, rs):
+                same(h, r)
