@@ -271,7 +271,8 @@ int sfk_gather_rows(const void* src, void* dst, const int32_t* idx, int rows, in
 /* Beam candidate selection (generate.cpp:220-262) per logits row (dtype):
  * lse[r], eos_lp[r] = logit[eos] - lse, and the kk best tokens under
  * key = cum[r] + (logit - lse) descending, token ascending on ties
- * (tok/lp: rows x kk, best first). */
+ * (tok/lp: rows x kk, best first). cum == NULL: rank by the raw logit
+ * (descending, token ascending) and return raw logits in lp (top-k sampling). */
 int sfk_beam_topk(int dtype, const void* logits, int64_t ld, int rows, int vocab, const double* cum, int kk,
                   int eos, float* lse, float* eos_lp, int32_t* tok, float* lp, void* stream);
 /* dst = src converted (any dtype pair) */

@@ -798,7 +798,8 @@ Trainer::BeamCands Trainer::inc_step_topk(const std::vector<int>& last, int pos,
   IncState& st = *inc_;
   const int R = st.rows, V = model_->target_vocab();
   kk = std::min(kk, V);
-  if (int(cum.size()) != R) throw ShapeError("incremental decoding: one cumulative score per row");
+  const bool raw = cum.empty();
+  if (!raw && int(cum.size()) != R) throw ShapeError("incremental decoding: one cumulative score per row");
   if (!st.cum) cuda_check(cudaMalloc(&st.cum, size_t(R) * 8), "beam cum");
   if (st.cands_kk < kk) {
     cudaFree(st.cands);
@@ -806,7 +807,7 @@ Trainer::BeamCands Trainer::inc_step_topk(const std::vector<int>& last, int pos,
     cuda_check(cudaMalloc(&st.cands, size_t(R) * (2 + 2 * size_t(kk)) * 4), "beam candidates");
     st.cands_kk = kk;
   }
-  cuda_check(cudaMemcpyAsync(st.cum, cum.data(), size_t(R) * 8, cudaMemcpyHostToDevice, stream_), "cum H2D");
+  if (!raw) cuda_check(cudaMemcpyAsync(st.cum, cum.data(), size_t(R) * 8, cudaMemcpyHostToDevice, stream_), "cum H2D");
   BeamCands out;
   out.kk = kk;
   out.lse.resize(size_t(R));
@@ -819,7 +820,8 @@ Trainer::BeamCands Trainer::inc_step_topk(const std::vector<int>& last, int pos,
   float* lp = reinterpret_cast<float*>(tok + size_t(R) * kk);
   std::vector<uint32_t> host(size_t(R) * (2 + 2 * size_t(kk)));
   inc_run(last, pos, [&](DeviceTape& tape, int lg) {
-    sfk_check(sfk_beam_topk(dtype_, tape.out(lg), logits_ld(V), R, V, st.cum, kk, kEos, lse, eos_lp, tok, lp,
+    sfk_check(sfk_beam_topk(dtype_, tape.out(lg), logits_ld(V), R, V, raw ? nullptr : st.cum, kk, kEos, lse, eos_lp,
+                            tok, lp,
                             stream_),
               "beam_topk");
     // lse | eos_lp | tok | lp are contiguous: one read-back per position

@@ -66,6 +66,7 @@ class Trainer {
     std::vector<float> lse, eos_lp, lp;
     std::vector<int32_t> tok;
   };
+  // empty cum: rank raw logits instead and return them in lp (sampling)
   BeamCands inc_step_topk(const std::vector<int>& last_tokens, int pos, const std::vector<double>& cum, int kk);
   void inc_reorder(const std::vector<int>& order);
   void inc_end();

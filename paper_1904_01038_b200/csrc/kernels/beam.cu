@@ -6,6 +6,8 @@
 // rows * V (V = 32k for the WMT models). One CTA per row; kk passes over the
 // row, each taking the best candidate strictly after the previous one in that
 // total order (no membership sets). The row stays in L2 between passes.
+// With cum == nullptr (top-k sampling, generate.cpp:353-383) the order is the
+// raw logit descending, token ascending, and lp returns the raw logits.
 #include <cfloat>
 
 #include "common.cuh"
@@ -60,7 +62,8 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const T* __restrict__ lo
   s = 0.f;
   for (int w = 0; w < kThreads / 32; ++w) s += red[w];
   const float lse = m + logf(s);
-  const double c = cum[row];
+  const bool raw = cum == nullptr;  // sampling: rank raw logits, return them
+  const double c = raw ? 0.0 : cum[row];
   if (threadIdx.x == 0) {
     lse_out[row] = lse;
     eos_lp[row] = x(eos) - lse;
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const T* __restrict__ lo
     const Best p = prev;
     Best b{-DBL_MAX, 0x7fffffff};
     for (int v = threadIdx.x; v < V; v += kThreads) {
-      const Best cnd{c + double(x(v) - lse), v};
+      const Best cnd{raw ? double(x(v)) : c + double(x(v) - lse), v};
       if (before(p, cnd) && before(cnd, b)) b = cnd;
     }
     b = warp_best(b);
@@ -84,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const T* __restrict__ lo
         if (before(bred[i], w)) w = bred[i];
       const int t = w.tok < V ? w.tok : eos;  // non-finite row: nothing ranks
       tok_out[int64_t(row) * kk + j] = t;
-      lp_out[int64_t(row) * kk + j] = x(t) - lse;
+      lp_out[int64_t(row) * kk + j] = raw ? x(t) : x(t) - lse;
       prev = w;
     }
     __syncthreads();
@@ -99,7 +102,7 @@ using namespace sfk;
 extern "C" int sfk_beam_topk(int dtype, const void* logits, int64_t ld, int rows, int vocab, const double* cum, int kk,
                              int eos, float* lse, float* eos_lp, int32_t* tok, float* lp, void* stream) {
   if (rows < 0 || vocab < 1 || kk < 1 || kk > vocab || ld < vocab || eos < 0 || eos >= vocab ||
-      (rows && (!logits || !cum || !lse || !eos_lp || !tok || !lp))) {
+      (rows && (!logits || !lse || !eos_lp || !tok || !lp))) {
     set_error("sfk_beam_topk: bad arguments (1 <= kk <= vocab, eos < vocab)");
     return SFK_EINVAL;
   }

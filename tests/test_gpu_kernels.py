@@ -538,3 +538,25 @@ def test_beam_topk_order_and_values(dt, V, kk):
         order = sorted(range(V), key=lambda v: (-key[v], v))[:kk]
         assert tok[r].cpu().tolist() == order, r
         np.testing.assert_array_equal(lp[r].cpu().numpy(), lpr[order])
+
+
+@pytest.mark.parametrize("dt,V,kk", [(0, 1000, 5), (1, 32768, 20)])
+def test_topk_raw_mode_for_sampling(dt, V, kk):
+    """cum == NULL: rank by the raw logit (ties to the lower id, as
+    sample_from_topk's stable sort, generate.cpp:360-365) and return raw logits."""
+    lib = L()
+    rows = 6
+    g = torch.Generator(device="cuda").manual_seed(11 + dt)
+    logits = (torch.randn(rows, V, device="cuda", generator=g) * 2).to(TDT[dt])
+    logits[:, 5::7] = logits[:, 3:4]
+    lse, eos_lp, lp = (torch.empty(rows, device="cuda") for _ in range(3))
+    tok = torch.empty(rows, kk, device="cuda", dtype=torch.int32)
+    lp = torch.empty(rows, kk, device="cuda")
+    lib.check(lib.sfk_beam_topk(dt, ptr(logits), V, rows, V, None, kk, 2, ptr(lse), ptr(eos_lp), ptr(tok), ptr(lp),
+                                stream()), kernel=True)
+    torch.cuda.synchronize()
+    x = logits.float().cpu().numpy()
+    for r in range(rows):
+        order = sorted(range(V), key=lambda v: (-x[r, v], v))[:kk]
+        assert tok[r].cpu().tolist() == order
+        np.testing.assert_array_equal(lp[r].cpu().numpy(), x[r, order])
