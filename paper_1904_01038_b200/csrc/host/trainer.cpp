@@ -711,8 +711,13 @@ void Trainer::inc_begin(const MiniBatch& src, const std::vector<int>& row_senten
   st->es = dtype_ == SFK_F32 ? 4 : 2;
   const size_t kv_row = size_t(2) * st->d * st->es, layer_bytes = size_t(R) * cap * kv_row;
   const size_t cross_row = size_t(S) * st->layers * kv_row;
-  for (auto& p : st->self) cuda_check(cudaMalloc(&p, layer_bytes * st->layers), "kv cache");
-  cuda_check(cudaMemsetAsync(st->self[0], 0, layer_bytes * st->layers, stream_), "kv cache zero");
+  // both halves zeroed: the tensor-core attention loads whole key tiles and
+  // masks positions >= k_len in the scores, so unwritten cache rows must
+  // hold finite values (0 * NaN would poison P.V)
+  for (auto& p : st->self) {
+    cuda_check(cudaMalloc(&p, layer_bytes * st->layers), "kv cache");
+    cuda_check(cudaMemsetAsync(p, 0, layer_bytes * st->layers, stream_), "kv cache zero");
+  }
   cuda_check(cudaMalloc(&st->cross, cross_row * R), "cross cache");
   cuda_check(cudaMalloc(&st->idx, size_t(4) * R * 4), "decoder indices");
 
