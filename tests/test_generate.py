@@ -261,3 +261,22 @@ def test_saturated_beam_enumerates_every_hypothesis():
             assert len(hs) == 31 and {tuple(h.tokens) for h in hs} == want
             for h, r in zip(hs, rs):
                 same(h, r)
+
+
+@pytest.mark.gpu
+def test_generation_between_steps_leaves_training_unchanged():
+    """Decoding mid-run (after an update whose Adam pass overlaps the next
+    forward) must not perturb training: same losses, bitwise, as a twin
+    trainer that never generated."""
+    import paper_1904_01038_b200 as sqf
+    c = corpus(120, 1000)
+    ov = dict(BASE, max_tokens=1024, fp16=True)
+    a = sqf.Trainer("transformer_base_defaults", ov, corpus=c, src_vocab=1000, tgt_vocab=1000)
+    b = sqf.Trainer("transformer_base_defaults", ov, corpus=c, src_vocab=1000, tgt_vocab=1000)
+    src = sources(c, range(5))
+    for step in range(4):
+        x, y = a.train_one(), b.train_one()
+        assert x == y, step
+        a.generate(src, "beam", beam=3)
+        a.generate(src, "sample", topk=4)
+    np.testing.assert_array_equal(a.params(), b.params())
