@@ -264,9 +264,10 @@ int sfk_cast(const float* src, void* dst, int dst_dtype, int64_t n, void* stream
 
 /* K/V-cache reorder of the incremental decoder (model.cpp:540-557):
  * dst[m][r] = src[m][idx[r]] for nmat matrices of `rows` rows of row_bytes
- * (mat_bytes apart); 16-byte multiples, out of place. */
-int sfk_gather_rows(const void* src, void* dst, const int32_t* idx, int rows, int64_t row_bytes, int nmat,
-                    int64_t mat_bytes, void* stream);
+ * (mat_bytes apart), moving the first copy_bytes of each row; 16-byte
+ * multiples, out of place. */
+int sfk_gather_rows(const void* src, void* dst, const int32_t* idx, int rows, int64_t row_bytes,
+                    int64_t copy_bytes, int nmat, int64_t mat_bytes, void* stream);
 
 /* Beam candidate selection (generate.cpp:220-262) per logits row (dtype):
  * lse[r], eos_lp[r] = logit[eos] - lse, and the kk best tokens under

@@ -203,6 +203,6 @@ sqf_gen_free = _sig("sqf_gen_free", None, vp)
 sqf_score_hypothesis = _sig("sqf_score_hypothesis", C.c_int, f64, i64, f64, P(f64))
 sqf_sample_from_topk = _sig("sqf_sample_from_topk", C.c_int, vp, C.c_int, C.c_int, f64, f64, P(i32))
 sqf_batch_for_inference = _sig("sqf_batch_for_inference", C.c_int, vp, C.c_int, i64, P(i32), vp, vp)
-sfk_gather_rows = _sig("sfk_gather_rows", C.c_int, vp, vp, vp, C.c_int, i64, C.c_int, i64, vp)
+sfk_gather_rows = _sig("sfk_gather_rows", C.c_int, vp, vp, vp, C.c_int, i64, i64, C.c_int, i64, vp)
 sfk_beam_topk = _sig("sfk_beam_topk", C.c_int, C.c_int, vp, i64, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp,
                      vp, vp)

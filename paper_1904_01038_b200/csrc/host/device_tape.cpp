@@ -319,8 +319,9 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
     const char* v = std::getenv("SQF_GEMM_STREAM_K");  // 0 off (default), 1 auto, 2 force
     return v ? std::atoi(v) : 0;
   }();
-  if (ws && ctr_base_ && sk_mode > 0) {
-    g.stream_k = sk_mode > 1 ? 1 : 0;
+  const int sk = sk_override_ ? sk_override_ : sk_mode;
+  if (ws && ctr_base_ && sk > 0) {
+    g.stream_k = sk > 1 ? 1 : 0;
     g.workspace = ws;
     g.workspace_floats = ws_floats_;
     g.n_counters = 2 * 148;

@@ -182,6 +182,9 @@ class DeviceTape {
   std::vector<std::pair<int64_t, int64_t>> planned_grad_writes() const;
   cudaStream_t side_stream() const { return side_; }
   // stream-K GEMM workspaces, one per stream (concurrent GEMMs must not share)
+  // 2 = force stream-K on every eligible GEMM (decoding: M = a few dozen
+  // rows, so plain tiles would leave most SMs idle); 0 = SQF_GEMM_STREAM_K
+  void set_stream_k(int mode) { sk_override_ = mode; }
   void set_gemm_workspace(float* main_ws, float* side_ws, int64_t floats) {
     ws_main_ = main_ws;
     ws_side_ = side_ws;
@@ -225,6 +228,7 @@ class DeviceTape {
   Arena& arena_;
   DeviceParams params_;
   int dtype_;
+  int sk_override_ = 0;
   size_t esize_;
   cudaStream_t stream_;
   std::vector<Node> nodes_;

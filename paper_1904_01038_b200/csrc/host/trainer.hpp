@@ -127,6 +127,7 @@ class Trainer {
  private:
   struct IncState {
     int rows = 0, src_width = 0, cap = 0, layers = 0, d = 0;
+    int filled = 0;                      // cache positions written so far (reorder copies these)
     size_t es = 4;                       // cache element size (decoding dtype)
     void* self[2] = {nullptr, nullptr};  // double-buffered [layers][rows*cap][2d]
     int cur = 0;

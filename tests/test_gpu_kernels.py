@@ -500,11 +500,18 @@ def test_gather_rows_reorders_every_matrix():
     src = torch.randn(nmat, rows, row_elems, device="cuda")
     dst = torch.empty_like(src)
     idx = torch.randint(0, rows, (rows,), device="cuda", dtype=torch.int32)
-    lib.check(lib.sfk_gather_rows(ptr(src), ptr(dst), ptr(idx), rows, row_elems * 4, nmat, rows * row_elems * 4,
-                                  stream()), kernel=True)
+    lib.check(lib.sfk_gather_rows(ptr(src), ptr(dst), ptr(idx), rows, row_elems * 4, row_elems * 4, nmat,
+                                  rows * row_elems * 4, stream()), kernel=True)
     torch.cuda.synchronize()
     assert torch.equal(dst, src[:, idx.long()])
-    assert lib.sfk_gather_rows(ptr(src), ptr(src), ptr(idx), rows, row_elems * 4, nmat, 0, stream()) != 0
+    # prefix copy: only the first 40 elements of each row move
+    dst2 = torch.zeros_like(src)
+    lib.check(lib.sfk_gather_rows(ptr(src), ptr(dst2), ptr(idx), rows, row_elems * 4, 40 * 4, nmat,
+                                  rows * row_elems * 4, stream()), kernel=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dst2[..., :40], src[:, idx.long(), :40]) and not dst2[..., 40:].any()
+    assert lib.sfk_gather_rows(ptr(src), ptr(src), ptr(idx), rows, row_elems * 4, row_elems * 4, nmat, 0,
+                               stream()) != 0
 
 
 @pytest.mark.parametrize("dt,V,kk", [(0, 1000, 8), (1, 32768, 8), (2, 5000, 10), (0, 7, 7)])
