@@ -437,7 +437,7 @@ class AdamOptimizer : public OptimizerBase {
   void apply(float* master, void* shadow, int shadow_dtype, const void* grad, int grad_dtype, int64_t n, double lr,
              const GradPrep& prep, void* stream) override {
     if (n != n_) throw ShapeError("adam: moment/parameter length mismatch");
-    ensure();
+    ensure(static_cast<cudaStream_t>(stream));
     ++t_;
     const double bc1 = 1.0 - std::pow(b1_, double(t_));
     const double bc2 = 1.0 - std::pow(b2_, double(t_));
@@ -463,6 +463,8 @@ class AdamOptimizer : public OptimizerBase {
   std::vector<std::pair<std::string, std::vector<float>>> state_blobs() const override {
     std::vector<float> m(size_t(n_), 0.f), v(size_t(n_), 0.f);
     if (m_) {
+      // the update may still be running on a trainer stream: join the device
+      cuda_check(cudaDeviceSynchronize(), "adam state");
       cuda_check(cudaMemcpy(m.data(), m_, size_t(n_) * 4, cudaMemcpyDeviceToHost), "adam state");
       cuda_check(cudaMemcpy(v.data(), v_, size_t(n_) * 4, cudaMemcpyDeviceToHost), "adam state");
     }
@@ -470,7 +472,10 @@ class AdamOptimizer : public OptimizerBase {
   }
   void load_state_blobs(const std::vector<std::pair<std::string, std::vector<float>>>& blobs) override {
     bool gm = false, gv = false;
-    ensure();
+    // no pending update may land after the load; the legacy-stream copies
+    // below are joined before any trainer stream reads the moments
+    cuda_check(cudaDeviceSynchronize(), "adam load");
+    ensure(nullptr);
     for (const auto& [name, data] : blobs) {
       if (data.size() != size_t(n_)) throw IntegrityError("adam: moment size mismatch");
       if (name == "adam.m") {
@@ -483,6 +488,7 @@ class AdamOptimizer : public OptimizerBase {
         throw IntegrityError("adam: unknown state blob '" + name + "'");
       }
     }
+    cuda_check(cudaDeviceSynchronize(), "adam load");
     if (!gm || !gv) throw IntegrityError("adam: missing moment blobs");
   }
 
@@ -492,12 +498,15 @@ class AdamOptimizer : public OptimizerBase {
   int64_t t_ = 0;
   float* m_ = nullptr;
   float* v_ = nullptr;
-  void ensure() {
+  // zeroed on the stream the first update runs on (or joined when called
+  // outside a step), so the update never reads uncleared moments
+  void ensure(cudaStream_t s) {
     if (m_) return;
     cuda_check(cudaMalloc(&m_, size_t(std::max<int64_t>(n_, 1)) * 4), "adam m");
     cuda_check(cudaMalloc(&v_, size_t(std::max<int64_t>(n_, 1)) * 4), "adam v");
-    cuda_check(cudaMemset(m_, 0, size_t(n_) * 4), "adam m");
-    cuda_check(cudaMemset(v_, 0, size_t(n_) * 4), "adam v");
+    cuda_check(cudaMemsetAsync(m_, 0, size_t(n_) * 4, s), "adam m");
+    cuda_check(cudaMemsetAsync(v_, 0, size_t(n_) * 4, s), "adam v");
+    if (!s) cuda_check(cudaDeviceSynchronize(), "adam zero");
   }
 };
 

@@ -172,9 +172,9 @@ class DeviceTape {
   // writes a parameter range's gradient contribution is enqueued (on `stream`);
   // the trainer uses it to start bucket all-reduces while backward continues
   using GradHook = std::function<void(int64_t offset, int64_t numel, cudaStream_t stream)>;
-  // called before a launch reads parameters at `offset` on `stream` (the
+  // called before a launch reads parameters [offset, offset + numel) on `stream` (the
   // trainer makes the stream wait for that range's optimizer update)
-  using UseHook = std::function<void(int64_t offset, cudaStream_t stream)>;
+  using UseHook = std::function<void(int64_t offset, int64_t numel, cudaStream_t stream)>;
   void set_use_hook(UseHook h) { use_hook_ = std::move(h); }
   void set_grad_hook(GradHook h) { hook_ = std::move(h); }
   // every parameter-gradient write backward() makes, as (offset, numel), in the
@@ -270,7 +270,7 @@ class DeviceTape {
 
   void* alloc_elems(int64_t n) { return arena_.alloc(size_t(n) * esize_); }
   void* pptr(const ParamRef& p) const {
-    if (use_hook_) use_hook_(p.offset, cur_);
+    if (use_hook_) use_hook_(p.offset, int64_t(p.rows) * p.cols, cur_);
     return static_cast<char*>(params_.compute) + p.offset * esize_;
   }
   void* gptr(const ParamRef& p) const { return static_cast<char*>(params_.grad) + p.offset * esize_; }

@@ -134,10 +134,13 @@ void Trainer::init(const Registry& reg) {
   } else {
     cuda_check(cudaMalloc(&compute_, size_t(n_) * 2), "shadow");
   }
+  // Every upload/clear below is ordered on stream_ (a non-blocking stream
+  // does not order against the legacy stream, and a pageable cudaMemcpy H2D
+  // may return before its DMA lands), then joined once at the end of init.
   for (int i = 0; i < 2 * local_; ++i) {
     void* g = nullptr;
     cuda_check(cudaMalloc(&g, size_t(n_) * esize()), "grads");
-    cuda_check(cudaMemset(g, 0, size_t(n_) * esize()), "grads");
+    cuda_check(cudaMemsetAsync(g, 0, size_t(n_) * esize(), stream_), "grads");
     grads_.push_back(g);
   }
   // optimizer ranges (~8M elements, 256-aligned) and their events
@@ -156,7 +159,8 @@ void Trainer::init(const Registry& reg) {
   const std::vector<float> pe = model_->position_table();
   if (!pe.empty()) {
     cuda_check(cudaMalloc(&pe_, pe.size() * 4), "pe");
-    cuda_check(cudaMemcpy(pe_, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice), "pe upload");
+    cuda_check(cudaMemcpyAsync(pe_, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice, stream_), "pe upload");
+    cuda_check(cudaStreamSynchronize(stream_), "pe upload");
     set_model_position_table(*model_, pe_);
   }
   cuda_check(cudaMalloc(&stats_dev_, 4 * sizeof(double)), "stats");
@@ -168,7 +172,8 @@ void Trainer::init(const Registry& reg) {
     gemm_ws_floats_ = int64_t(sms) * 2 * 128 * 256;
     cuda_check(cudaMalloc(&gemm_ws_, size_t(gemm_ws_floats_) * 2 * 4), "gemm workspace");
   }
-  cuda_check(cudaMemset(counters_, 0, size_t(kCounters) * 4), "counters");
+  cuda_check(cudaMemsetAsync(counters_, 0, size_t(kCounters) * 4, stream_), "counters");
+  cuda_check(cudaMemsetAsync(flag_dev_, 0, 16, stream_), "flag");
   cuda_check(cudaMallocHost(&readback_host_, 64), "readback");
   push_params();
 }
@@ -183,7 +188,8 @@ void Trainer::push_params() {
   std::fill(adam_range_wait_.begin(), adam_range_wait_.end(), 0);
   std::vector<float> dev(static_cast<size_t>(n_));
   model_->to_device_order(model_->params(), dev);
-  cuda_check(cudaMemcpy(master_, dev.data(), size_t(n_) * 4, cudaMemcpyHostToDevice), "params upload");
+  // on stream_, so the shadow cast in rebroadcast() reads the uploaded master
+  cuda_check(cudaMemcpyAsync(master_, dev.data(), size_t(n_) * 4, cudaMemcpyHostToDevice, stream_), "params upload");
   rebroadcast();
 }
 
@@ -201,12 +207,17 @@ float Trainer::flush_ms() {
   return ms;
 }
 
-void Trainer::param_wait(int64_t offset, cudaStream_t s) {
-  const size_t r = size_t(offset / (int64_t(8) << 20));
-  if (r < adam_range_wait_.size() && adam_range_wait_[r]) {
-    cuda_check(cudaStreamWaitEvent(s, adam_range_ev_[r], 0), "stream wait");
-    adam_range_wait_[r] = 0;
-  }
+void Trainer::param_wait(int64_t offset, int64_t numel, cudaStream_t s) {
+  // a parameter may straddle optimizer ranges (the 32k x 1024 embeddings span
+  // four): wait for every range that holds one of its elements
+  if (numel <= 0) return;
+  const int64_t chunk = int64_t(8) << 20;
+  const size_t r0 = size_t(offset / chunk), r1 = size_t((offset + numel - 1) / chunk);
+  for (size_t r = r0; r <= r1 && r < adam_range_wait_.size(); ++r)
+    if (adam_range_wait_[r]) {
+      cuda_check(cudaStreamWaitEvent(s, adam_range_ev_[r], 0), "stream wait");
+      adam_range_wait_[r] = 0;
+    }
 }
 
 void Trainer::rebroadcast() {
@@ -221,7 +232,8 @@ void Trainer::pull_params() {
   join_optimizer();
   std::vector<float> dev(static_cast<size_t>(n_));
   cuda_check(cudaStreamSynchronize(stream_), "sync");
-  cuda_check(cudaMemcpy(dev.data(), master_, size_t(n_) * 4, cudaMemcpyDeviceToHost), "params download");
+  cuda_check(cudaMemcpyAsync(dev.data(), master_, size_t(n_) * 4, cudaMemcpyDeviceToHost, stream_), "params download");
+  cuda_check(cudaStreamSynchronize(stream_), "params download");
   model_->to_canonical_order(dev, model_->params());
 }
 
@@ -231,13 +243,15 @@ std::vector<float> Trainer::reduced_grads() {
   std::vector<float> devf(static_cast<size_t>(n_));
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   if (dtype_ == SFK_F32) {
-    cuda_check(cudaMemcpy(devf.data(), g0, size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
+    cuda_check(cudaMemcpyAsync(devf.data(), g0, size_t(n_) * 4, cudaMemcpyDeviceToHost, stream_), "grads download");
+    cuda_check(cudaStreamSynchronize(stream_), "grads download");
   } else {
     float* tmp = nullptr;
     cuda_check(cudaMalloc(&tmp, size_t(n_) * 4), "grads tmp");
     sfk_check(sfk_convert(dtype_, g0, SFK_F32, tmp, n_, stream_), "grads convert");
     cuda_check(cudaStreamSynchronize(stream_), "sync");
-    cuda_check(cudaMemcpy(devf.data(), tmp, size_t(n_) * 4, cudaMemcpyDeviceToHost), "grads download");
+    cuda_check(cudaMemcpyAsync(devf.data(), tmp, size_t(n_) * 4, cudaMemcpyDeviceToHost, stream_), "grads download");
+    cuda_check(cudaStreamSynchronize(stream_), "grads download");
     cudaFree(tmp);
   }
   std::vector<float> out(static_cast<size_t>(n_));
@@ -496,12 +510,15 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   cuda_check(cudaEventRecord(ev0_, stream_), "event");
   upload(packs, dev);
   cuda_check(cudaMemsetAsync(stats_dev_, 0, 4 * sizeof(double), stream_), "stats zero");
-  cuda_check(cudaMemsetAsync(flag_dev_, 0, 4, stream_), "flag zero");
-  // this step's gradient set was last read by the update two steps ago
+  // this step's gradient set (and its overflow flag) was last read by the
+  // update two steps ago; the previous step's update may still be running on
+  // the side stream and reads the other set's flag, so clearing this one is safe
   if (adam_pending_[gset_]) {
     cuda_check(cudaStreamWaitEvent(stream_, adam_done_[gset_], 0), "stream wait");
     adam_pending_[gset_] = false;
   }
+  int32_t* flag_d = flag_dev_ + gset_;
+  cuda_check(cudaMemsetAsync(flag_d, 0, 4, stream_), "flag zero");
   for (int lw = 0; lw < local_; ++lw)
     cuda_check(cudaMemsetAsync(grad_buf(lw), 0, size_t(n_) * esize(), stream_), "grad zero");
   launches_ = 0;
@@ -514,7 +531,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     if (arena_busy_[k]) cuda_check(cudaStreamWaitEvent(stream_, arena_free_[k], 0), "arena wait");
     arena_[k].reset();
     DeviceTape tape(arena_[k], DeviceParams{master_, compute_, grad_buf(lw), n_}, dtype_, stream_);
-    tape.set_use_hook([this](int64_t off, cudaStream_t st) { param_wait(off, st); });
+    tape.set_use_hook([this](int64_t off, int64_t n, cudaStream_t st) { param_wait(off, n, st); });
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     // a profiling pass serialises everything on the main stream so the
@@ -546,7 +563,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   else
     allreduce_grads();
   if (prof_) prof_->begin(stream_);
-  sfk_check(sfk_nonfinite(dtype_, grad_buf(0), n_, flag_dev_, stream_), "overflow check");
+  sfk_check(sfk_nonfinite(dtype_, grad_buf(0), n_, flag_d, stream_), "overflow check");
   ++launches_;
 
   const bool injected = fp16_ && injector_ && injector_(stats.step);
@@ -562,7 +579,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     prep.scale = float(scale);
     prep.unscale = fp16_;
     prep.ntokens = float(stats.ntokens);
-    prep.skip = flag_dev_;
+    prep.skip = flag_d;
     cudaStream_t os = stream_;
     if (adam_side) {
       cuda_check(cudaEventRecord(ev_checked_, stream_), "event record");
@@ -589,7 +606,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     prefetch_ = std::async(std::launch::async, [this, e = epoch_, p = pos_, o = order_] { return plan_deal(e, p, o); });
   char* rb = static_cast<char*>(readback_host_);
   cuda_check(cudaMemcpyAsync(rb, stats_dev_, 4 * sizeof(double), cudaMemcpyDeviceToHost, stream_), "stats D2H");
-  cuda_check(cudaMemcpyAsync(rb + 32, flag_dev_, 4, cudaMemcpyDeviceToHost, stream_), "flag D2H");
+  cuda_check(cudaMemcpyAsync(rb + 32, flag_d, 4, cudaMemcpyDeviceToHost, stream_), "flag D2H");
   cuda_check(cudaEventRecord(ev1_, stream_), "event");
   cuda_check(cudaStreamSynchronize(stream_), "step sync");
   cudaEventElapsedTime(&last_ms_, ev0_, ev1_);
@@ -637,7 +654,8 @@ EvalStats Trainer::evaluate(const std::vector<SequencePair>& pairs) {
     cuda_check(cudaStreamSynchronize(stream_), "eval sync");  // staging buffer reuse
   }
   double st[4];
-  cuda_check(cudaMemcpy(st, stats_dev_, sizeof st, cudaMemcpyDeviceToHost), "eval D2H");
+  cuda_check(cudaMemcpyAsync(st, stats_dev_, sizeof st, cudaMemcpyDeviceToHost, stream_), "eval D2H");
+  cuda_check(cudaStreamSynchronize(stream_), "eval D2H");
   out.loss = st[0];
   out.nll = st[1];
   out.ntokens = int64_t(st[2]);

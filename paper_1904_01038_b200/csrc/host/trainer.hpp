@@ -196,7 +196,7 @@ class Trainer {
   bool adam_pending_[2] = {false, false};
   cudaEvent_t ev_checked_ = nullptr, ev_flush_ = nullptr;
   bool adam_overlap_ = true;
-  void param_wait(int64_t offset, cudaStream_t s);
+  void param_wait(int64_t offset, int64_t numel, cudaStream_t s);
   ncclComm_t comm_ = nullptr;
   // Two activation arenas alternate between sub-batches so the side-stream
   // parameter-gradient work of sub-batch i (which reads its activations) can
