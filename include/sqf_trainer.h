@@ -51,6 +51,22 @@ void* sqf_trainer_create(const char* arch, const char* const* keys, const char* 
                          int rank, int world, const void* nccl_id);
 void sqf_trainer_free(void* t);
 
+/* The gradient exchange between data-parallel ranks (the reference's
+ * all_reduce, trainer.cpp:75-87, across processes). sqf_trainer_create uses
+ * NCCL (nccl_id from sqf_nccl_unique_id). sqf_trainer_create_host_collective
+ * instead hands every bucket (and the 4-double step statistics) to `fn` as a
+ * pinned host copy to be summed in place over all ranks -- a test/tooling
+ * backend (e.g. torch.distributed gloo) that runs the same N>1 trainer path
+ * without NCCL. fn returns 0 on success. dtype codes: */
+enum sqf_coll_dtype { SQF_COLL_F32 = 0, SQF_COLL_F16 = 1, SQF_COLL_BF16 = 2, SQF_COLL_F64 = 3 };
+typedef int (*sqf_host_allreduce_fn)(void* buf, int64_t count, int dtype, void* user);
+void* sqf_trainer_create_host_collective(const char* arch, const char* const* keys, const char* const* vals, int n,
+                                         const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
+                                         const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab,
+                                         int rank, int world, sqf_host_allreduce_fn fn, void* user);
+/* "nccl", "host" or "none" (world 1) */
+const char* sqf_trainer_collective(void* t);
+
 /* A task made through the registry from the resolved config's "task" key
  * (Registry::make_task; "translation" = TranslationTask, tasks.cpp:7-33,
  * reading train_src/train_tgt text and dict_src/dict_tgt or building the

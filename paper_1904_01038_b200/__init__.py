@@ -233,6 +233,23 @@ class EvalStats:
     ncorrect: int
 
 
+_COLL_NP = {L.COLL_F32: np.float32, L.COLL_F16: np.float16, L.COLL_BF16: np.uint16, L.COLL_F64: np.float64}
+
+
+def _host_allreduce_trampoline(fn):
+    def cb(buf, count, dtype, _user):
+        try:
+            arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)), shape=(count * np.dtype(
+                _COLL_NP[dtype]).itemsize,)).view(_COLL_NP[dtype])
+            fn(arr, dtype)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported as a status through the C ABI
+            import traceback
+            traceback.print_exc()
+            return 1
+    return cb
+
+
 class Trainer:
     """Drop-in for the reference's Trainer (trainer.hpp:80-125) on B200.
 
@@ -244,18 +261,24 @@ class Trainer:
 
     def __init__(self, arch: str, overrides: dict | None = None, corpus: Corpus | None = None,
                  src_vocab: int = 0, tgt_vocab: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, host_allreduce=None):
         overrides = dict(overrides or {})
         self.overrides = overrides
         k, v, n = _kv(overrides)
         self.corpus = corpus
-        idbuf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
         if corpus is not None:
-            h = L.sqf_trainer_create(arch.encode(), k, v, n, _ptr(corpus.src_len), _ptr(corpus.tgt_len),
-                                     _ptr(corpus.src_ids), _ptr(corpus.tgt_ids), corpus.npairs, src_vocab,
-                                     tgt_vocab, rank, world, idbuf)
+            task = (_ptr(corpus.src_len), _ptr(corpus.tgt_len), _ptr(corpus.src_ids), _ptr(corpus.tgt_ids),
+                    corpus.npairs, src_vocab, tgt_vocab)
         else:
-            h = L.sqf_trainer_create(arch.encode(), k, v, n, None, None, None, None, 0, 0, 0, rank, world, idbuf)
+            task = (None, None, None, None, 0, 0, 0)
+        if host_allreduce is not None:
+            # host_allreduce(array) sums a numpy view of the buffer in place
+            # over all ranks (e.g. torch.distributed gloo); tests/tooling only
+            self._coll_cb = L.HOST_ALLREDUCE_FN(_host_allreduce_trampoline(host_allreduce))
+            h = L.sqf_trainer_create_host_collective(arch.encode(), k, v, n, *task, rank, world, self._coll_cb, None)
+        else:
+            idbuf = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id else None
+            h = L.sqf_trainer_create(arch.encode(), k, v, n, *task, rank, world, idbuf)
         if not h:
             raise L.NativeError(L.sqf_last_status(), (L.sqf_last_error() or b"").decode())
         self._h = h
@@ -269,6 +292,10 @@ class Trainer:
 
     def __del__(self):
         self.close()
+
+    @property
+    def collective(self) -> str:
+        return L.sqf_trainer_collective(self._h).decode()
 
     # ---- the hot path
     def train_one(self):

@@ -106,6 +106,12 @@ sqf_last_error = _sig("sqf_last_error", cp)
 sqf_nccl_unique_id = _sig("sqf_nccl_unique_id", C.c_int, vp)
 sqf_trainer_create = _sig("sqf_trainer_create", vp, cp, P(cp), P(cp), C.c_int, vp, vp, vp, vp, C.c_int, C.c_int,
                           C.c_int, C.c_int, C.c_int, vp)
+HOST_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, vp, i64, C.c_int, vp)
+COLL_F32, COLL_F16, COLL_BF16, COLL_F64 = 0, 1, 2, 3
+sqf_trainer_create_host_collective = _sig("sqf_trainer_create_host_collective", vp, cp, P(cp), P(cp), C.c_int, vp,
+                                          vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          HOST_ALLREDUCE_FN, vp)
+sqf_trainer_collective = _sig("sqf_trainer_collective", cp, vp)
 sqf_trainer_free = _sig("sqf_trainer_free", None, vp)
 sqf_trainer_train_one = _sig("sqf_trainer_train_one", C.c_int, vp, P(StepStats))
 sqf_trainer_train_step = _sig("sqf_trainer_train_step", C.c_int, vp, vp, vp, P(StepStats))

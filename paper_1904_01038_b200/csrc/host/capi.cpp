@@ -1,6 +1,7 @@
 // C ABI (include/sqf_trainer.h) over the host trainer. Exceptions never cross
 // the boundary: they become the reference's error classes as status codes.
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 
@@ -114,10 +115,10 @@ int sqf_nccl_unique_id(void* out128) {
   return 0;
 }
 
-void* sqf_trainer_create(const char* arch, const char* const* keys, const char* const* vals, int n,
-                         const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
-                         const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab, int rank, int world,
-                         const void* nccl_id) {
+static void* create_trainer(const char* arch, const char* const* keys, const char* const* vals, int n,
+                            const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
+                            const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab, int rank, int world,
+                            const std::function<std::unique_ptr<Collective>()>& coll) {
   try {
     const Registry& reg = global_registry();
     Config cfg = reg.resolve_architecture(arch, user_kv(keys, vals, n));
@@ -125,14 +126,35 @@ void* sqf_trainer_create(const char* arch, const char* const* keys, const char* 
     if (npairs > 0)
       task = std::make_unique<MemoryTask>(unpack_pairs(npairs, src_len, tgt_len, src_ids, tgt_ids), src_vocab,
                                           tgt_vocab);
-    ncclUniqueId id;
-    if (nccl_id) std::memcpy(&id, nccl_id, sizeof id);
-    return new Trainer(cfg, reg, std::move(task), rank, world, nccl_id ? &id : nullptr);
+    return new Trainer(cfg, reg, std::move(task), rank, world, world > 1 ? coll() : nullptr);
   } catch (const std::exception& e) {
     fail(e);
     return nullptr;
   }
 }
+
+void* sqf_trainer_create(const char* arch, const char* const* keys, const char* const* vals, int n,
+                         const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
+                         const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab, int rank, int world,
+                         const void* nccl_id) {
+  return create_trainer(arch, keys, vals, n, src_len, tgt_len, src_ids, tgt_ids, npairs, src_vocab, tgt_vocab, rank,
+                        world, [&]() -> std::unique_ptr<Collective> {
+                          if (!nccl_id) throw ConfigError("trainer: world > 1 needs an NCCL unique id");
+                          ncclUniqueId id;
+                          std::memcpy(&id, nccl_id, sizeof id);
+                          return make_nccl_collective(rank, world, id);
+                        });
+}
+
+void* sqf_trainer_create_host_collective(const char* arch, const char* const* keys, const char* const* vals, int n,
+                                         const int32_t* src_len, const int32_t* tgt_len, const int32_t* src_ids,
+                                         const int32_t* tgt_ids, int npairs, int src_vocab, int tgt_vocab, int rank,
+                                         int world, sqf_host_allreduce_fn fn, void* user) {
+  return create_trainer(arch, keys, vals, n, src_len, tgt_len, src_ids, tgt_ids, npairs, src_vocab, tgt_vocab, rank,
+                        world, [&] { return make_host_collective(fn, user); });
+}
+
+const char* sqf_trainer_collective(void* t) { return t ? T(t)->collective() : "none"; }
 
 void sqf_trainer_free(void* t) { delete T(t); }
 

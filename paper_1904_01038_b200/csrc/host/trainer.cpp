@@ -1,6 +1,5 @@
 #include "trainer.hpp"
 
-#include "nccl_dyn.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -11,29 +10,17 @@ namespace sqf {
 
 void set_model_position_table(ModelBase& m, const float* dev);
 
-namespace {
-void nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw DeviceError(std::string(what) + ": " + NcclApi::get().GetErrorString(r));
-}
-ncclDataType_t nccl_type(int dtype) {
-  return dtype == SFK_F32 ? ncclFloat32 : dtype == SFK_F16 ? ncclFloat16 : ncclBfloat16;
-}
-}  // namespace
-
 Trainer::Trainer(const Config& cfg, const Registry& reg, std::unique_ptr<TaskBase> task, int rank, int world,
-                 const ncclUniqueId* nccl_id)
-    : cfg_(cfg), task_(std::move(task)), rank_(rank), world_(world) {
+                 std::unique_ptr<Collective> coll)
+    : cfg_(cfg), task_(std::move(task)), rank_(rank), world_(world), coll_(std::move(coll)) {
   if (world_ < 1 || rank_ < 0 || rank_ >= world_) throw ConfigError("trainer: bad rank/world");
+  if (world_ > 1 && !coll_) throw ConfigError("trainer: world > 1 needs a collective (NCCL unique id)");
   if (!task_) task_ = reg.make_task(cfg_.get_str("task"), cfg_);
-  if (world_ > 1) {
-    if (!nccl_id) throw ConfigError("trainer: world > 1 needs an NCCL unique id");
-    nccl_check(NcclApi::get().CommInitRank(&comm_, world_, *nccl_id, rank_), "ncclCommInitRank");
-  }
   init(reg);
 }
 
 Trainer::~Trainer() {
-  if (comm_) NcclApi::get().CommDestroy(comm_);
+  coll_.reset();
   cudaFree(master_);
   if (compute_ != master_) cudaFree(compute_);
   for (void* g : grads_) cudaFree(g);
@@ -394,14 +381,11 @@ void Trainer::allreduce_grads() {
   // bucketed all-reduce over NVLink, buckets in reverse device order (the
   // order backward completes them); same sum on every rank, so every rank
   // then runs the identical update (no rebroadcast traffic)
-  nccl_check(NcclApi::get().GroupStart(), "group");
+  coll_->group_start();
   for (const auto& b : buckets_)
-    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grad_buf(0)) + b.start * esize(),
-                             static_cast<char*>(grad_buf(0)) + b.start * esize(), size_t(b.end - b.start),
-                             nccl_type(dtype_), ncclSum, comm_, stream_),
-               "allreduce grads");
-  nccl_check(NcclApi::get().AllReduce(stats_dev_, stats_dev_, 4, ncclFloat64, ncclSum, comm_, stream_), "allreduce stats");
-  nccl_check(NcclApi::get().GroupEnd(), "group");
+    coll_->all_reduce(static_cast<char*>(grad_buf(0)) + b.start * esize(), size_t(b.end - b.start), dtype_, stream_);
+  coll_->all_reduce(stats_dev_, 4, SQF_COLL_F64, stream_);
+  coll_->group_end();
 }
 
 // ---------------------------------------------------------------- overlap
@@ -464,10 +448,8 @@ void Trainer::ovl_issue(int b) {
   cuda_check(cudaStreamWaitEvent(comm_stream_, es, 0), "stream wait");
   const GradientBucket& bk = buckets_[size_t(b)];
   if (world_ > 1)
-    nccl_check(NcclApi::get().AllReduce(static_cast<char*>(grad_buf(0)) + bk.start * esize(),
-                                        static_cast<char*>(grad_buf(0)) + bk.start * esize(), size_t(bk.end - bk.start),
-                                        nccl_type(dtype_), ncclSum, comm_, comm_stream_),
-               "allreduce bucket");
+    coll_->all_reduce(static_cast<char*>(grad_buf(0)) + bk.start * esize(), size_t(bk.end - bk.start), dtype_,
+                      comm_stream_);
   overlap_log_.push_back(b);
 }
 
@@ -477,9 +459,7 @@ void Trainer::ovl_finish() {
   cudaEvent_t em = ovl_event();
   cuda_check(cudaEventRecord(em, stream_), "event record");
   cuda_check(cudaStreamWaitEvent(comm_stream_, em, 0), "stream wait");
-  if (world_ > 1)
-    nccl_check(NcclApi::get().AllReduce(stats_dev_, stats_dev_, 4, ncclFloat64, ncclSum, comm_, comm_stream_),
-               "allreduce stats");
+  if (world_ > 1) coll_->all_reduce(stats_dev_, 4, SQF_COLL_F64, comm_stream_);
   cudaEvent_t done = ovl_event();
   cuda_check(cudaEventRecord(done, comm_stream_), "event record");
   cuda_check(cudaStreamWaitEvent(stream_, done, 0), "stream wait");

@@ -17,6 +17,7 @@
 #include <memory>
 #include <optional>
 
+#include "collective.hpp"
 #include "device_tape.hpp"
 #include "plugins.hpp"
 
@@ -38,9 +39,10 @@ struct EvalStats {
 
 class Trainer {
  public:
-  // task == nullptr: the task is made through the registry from cfg["task"]
+  // task == nullptr: the task is made through the registry from cfg["task"];
+  // world > 1 needs the collective that joins the ranks (NCCL in production)
   Trainer(const Config& cfg, const Registry& reg, std::unique_ptr<TaskBase> task, int rank = 0, int world = 1,
-          const ncclUniqueId* nccl_id = nullptr);
+          std::unique_ptr<Collective> coll = nullptr);
   ~Trainer();
 
   std::optional<StepStats> train_one();
@@ -108,6 +110,7 @@ class Trainer {
   cudaStream_t stream() const { return stream_; }
   int rank() const { return rank_; }
   int world() const { return world_; }
+  const char* collective() const { return coll_ ? coll_->name() : "none"; }
   // timing hook: events recorded on the compute stream around the last step
   float last_step_ms() const { return last_ms_; }
   // host<->device bytes of the last step (packed batch ids up; stats + flag down)
@@ -197,7 +200,7 @@ class Trainer {
   cudaEvent_t ev_checked_ = nullptr, ev_flush_ = nullptr;
   bool adam_overlap_ = true;
   void param_wait(int64_t offset, int64_t numel, cudaStream_t s);
-  ncclComm_t comm_ = nullptr;
+  std::unique_ptr<Collective> coll_;
   // Two activation arenas alternate between sub-batches so the side-stream
   // parameter-gradient work of sub-batch i (which reads its activations) can
   // run under the forward of sub-batch i+1; arena k is reused only after the
