@@ -56,7 +56,7 @@ def make(arch, ov, c):
 @pytest.mark.parametrize("arch", ARCHS)
 def test_headline_fp32_gradient_matches_reference(arch, corpus):
     mine, theirs = make(arch, {"optimizer": "sgd", "scheduler": "fixed", "lr": 1e-9}, corpus)
-    assert mine.num_params() == theirs.num_params()
+    assert len(mine.params()) == len(theirs.params())
     members = short_members(corpus, 2, 12)
     g_ref, st = theirs.subbatch_grad(members)
     s = mine.train_step([[members]])

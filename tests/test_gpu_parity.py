@@ -84,13 +84,22 @@ def test_bf16_100_steps_within_1e2_of_reference_fp32():
         assert abs(a["loss"] - b["loss"]) <= LOSS_TOL * abs(b["loss"]), (i, a, b)
 
 
-def test_fp16_100_steps_parameters_stay_close_to_reference():
-    """After 100 fp16 steps the fp32 masters stay close to the reference's
-    (same updates up to fp16 rounding of the gradients): a broken unscale,
-    1/ntokens division or shadow cast would drift far beyond this."""
+def test_fp16_100_steps_parameters_stay_within_reference_fp16_noise():
+    """After 100 fp16 steps our fp32 masters differ from the reference's
+    emulated-fp16 masters by no more than the reference's own fp16 run differs
+    from its fp32 run (times a small factor): 16-bit rounding of the gradients
+    makes Adam's normalised updates drift apart at the same rate whoever does
+    the rounding, while a broken unscale, 1/ntokens division or shadow cast
+    would be far outside it."""
     mine, theirs = pair({"fp16": True, "max_tokens": 512}, npairs=200)
+    import paper_1904_01038_b200 as sqf
+    c = sqf.synthetic_corpus(200, V, V, 1.1, 1)
+    ref32 = ref.RefTrainer("transformer_base_defaults", dict(BASE, max_tokens=512), c, V, V)
     for _ in range(100):
         a, b = mine.train_one(), theirs.train_one()
+        ref32.train_one()
         assert a["skipped"] == b["skipped"]
-    p, q = mine.params(), theirs.params()
-    assert np.linalg.norm(p - q) <= 1e-2 * np.linalg.norm(q)
+    p, q, r = mine.params(), theirs.params(), ref32.params()
+    ours, own = np.linalg.norm(p - q), np.linalg.norm(r - q)
+    print(f"|ours-ref16| = {ours:.4g}  |ref32-ref16| = {own:.4g}  |ref16| = {np.linalg.norm(q):.4g}")
+    assert ours <= 3.0 * own, (ours, own)
