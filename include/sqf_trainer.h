@@ -146,7 +146,13 @@ int sqf_trainer_overlap_log(void* t, int32_t* order, int cap, int32_t* early);
  * accumulated per-class totals: class 0..9 = gemm_fwd, gemm_dgrad,
  * gemm_wgrad, attn_fwd, attn_bwd, layernorm, xent, embed, bias_grad, optim.
  * Returns the class name, or NULL past the last class. */
+/* on: 0 off, 1 serialised per-launch timing, 2 timeline of the concurrent
+ * schedule (see sqf_trainer_timeline) */
 int sqf_trainer_set_profile(void* t, int on);
+/* timeline mode: launches of the last step as [stream, class, t0 ms, t1 ms]
+ * relative to the step start (stream 0 main, 1 side, 2 comm); returns the
+ * count (writes at most cap rows) */
+int sqf_trainer_timeline(void* t, float* out, int cap);
 const char* sqf_trainer_profile(void* t, int cls, double* ms, double* flops, double* bytes, int64_t* launches);
 
 /* ---------------- host-side boundary pieces (no GPU needed) --------------- */

@@ -441,8 +441,17 @@ class Trainer:
     def stream(self) -> int:
         return int(L.sqf_trainer_stream(self._h) or 0)
 
-    def set_profile(self, on: bool = True):
+    def set_profile(self, on=True):
+        """True/1: serialised per-launch timing; 2: timeline of the concurrent schedule."""
         L.check(L.sqf_trainer_set_profile(self._h, int(on)))
+
+    def timeline(self):
+        """Timeline mode: the last step's launches as rows (stream, class, t0_ms, t1_ms);
+        stream 0 = main, 1 = side (parameter gradients, optimizer), 2 = comm."""
+        n = L.sqf_trainer_timeline(self._h, None, 0)
+        out = np.zeros((max(n, 1), 4), np.float32)
+        L.sqf_trainer_timeline(self._h, out.ctypes.data, n)
+        return out[:n]
 
     def profile(self):
         """Per kernel class: {name: (ms, flops, bytes, launches)} accumulated since set_profile."""

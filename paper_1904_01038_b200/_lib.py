@@ -146,6 +146,7 @@ sqf_trainer_last_io_bytes = _sig("sqf_trainer_last_io_bytes", i64, vp, P(i64))
 sqf_trainer_stream = _sig("sqf_trainer_stream", vp, vp)
 sqf_trainer_set_profile = _sig("sqf_trainer_set_profile", C.c_int, vp, C.c_int)
 sqf_trainer_profile = _sig("sqf_trainer_profile", cp, vp, C.c_int, P(f64), P(f64), P(f64), P(i64))
+sqf_trainer_timeline = _sig("sqf_trainer_timeline", C.c_int, vp, vp, C.c_int)
 
 # ---- host boundary pieces
 sqf_synthetic_corpus = _sig("sqf_synthetic_corpus", C.c_int, C.c_int, C.c_int, C.c_int, f64, u64, vp, vp, vp, vp,

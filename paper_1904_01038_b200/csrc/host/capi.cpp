@@ -394,7 +394,21 @@ int sqf_trainer_overlap_log(void* t, int32_t* order, int cap, int32_t* early) {
   return n;
 }
 
-int sqf_trainer_set_profile(void* t, int on) { SQF_GUARD(T(t)->set_profile(on != 0)) }
+int sqf_trainer_set_profile(void* t, int on) { SQF_GUARD(T(t)->set_profile(on)) }
+
+int sqf_trainer_timeline(void* t, float* out, int cap) {
+  Profiler* p = T(t)->profiler();
+  if (!p) return 0;
+  const int n = int(p->spans.size());
+  for (int i = 0; i < n && i < cap; ++i) {
+    const auto& s = p->spans[size_t(i)];
+    out[4 * i] = float(s.stream);
+    out[4 * i + 1] = float(s.cat);
+    out[4 * i + 2] = s.t0;
+    out[4 * i + 3] = s.t1;
+  }
+  return n;
+}
 
 const char* sqf_trainer_profile(void* t, int cls, double* ms, double* flops, double* bytes, int64_t* launches) {
   Profiler* p = T(t)->profiler();

@@ -103,13 +103,26 @@ void Profiler::begin(cudaStream_t s) {
 void Profiler::end(cudaStream_t s, int cat, double fl, double by) {
   cudaEvent_t b = get();
   cuda_check(cudaEventRecord(b, s), "profiler record");
-  pending_.push_back({open_, b, cat, fl, by});
+  pending_.push_back({open_, b, cat, fl, by, s});
+}
+void Profiler::mark_base(cudaStream_t s) {
+  base_ = get();
+  cuda_check(cudaEventRecord(base_, s), "profiler record");
 }
 void Profiler::collect() {
   for (const Rec& r : pending_) {
     cuda_check(cudaEventSynchronize(r.b), "profiler sync");
     float t = 0.f;
     cuda_check(cudaEventElapsedTime(&t, r.a, r.b), "profiler elapsed");
+    if (base_) {
+      int si = 0;
+      while (si < int(streams.size()) && streams[size_t(si)] != r.s) ++si;
+      if (si == int(streams.size())) streams.push_back(r.s);
+      float t0 = 0.f, t1 = 0.f;
+      cuda_check(cudaEventElapsedTime(&t0, base_, r.a), "profiler elapsed");
+      cuda_check(cudaEventElapsedTime(&t1, base_, r.b), "profiler elapsed");
+      spans.push_back({si, r.cat, t0, t1});
+    }
     ms[r.cat] += t;
     flops[r.cat] += r.flops;
     bytes[r.cat] += r.bytes;
@@ -117,9 +130,12 @@ void Profiler::collect() {
   }
   pending_.clear();
   next_ = 0;
+  base_ = nullptr;
 }
 void Profiler::reset() {
   pending_.clear();
+  spans.clear();
+  base_ = nullptr;
   next_ = 0;
   for (int c = 0; c < kCats; ++c) ms[c] = flops[c] = bytes[c] = 0, count[c] = 0;
 }

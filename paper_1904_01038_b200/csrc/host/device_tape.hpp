@@ -91,13 +91,26 @@ class Profiler {
   void reset();
   double ms[kCats] = {}, flops[kCats] = {}, bytes[kCats] = {};
   int64_t count[kCats] = {};
+  // Timeline mode: the trainer keeps its concurrent schedule (side stream,
+  // overlapped optimizer) and every launch's [start, end] is kept relative to
+  // the base event of the step (ms), with the stream it ran on.
+  bool concurrent = false;
+  struct Span {
+    int stream, cat;
+    float t0, t1;
+  };
+  std::vector<Span> spans;
+  std::vector<cudaStream_t> streams;  // index = Span::stream
+  void mark_base(cudaStream_t s);
 
  private:
   struct Rec {
     cudaEvent_t a, b;
     int cat;
     double flops, bytes;
+    cudaStream_t s;
   };
+  cudaEvent_t base_ = nullptr;
   std::vector<cudaEvent_t> pool_;
   size_t next_ = 0;
   std::vector<Rec> pending_;

@@ -488,6 +488,10 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   // upload this rank's packed sub-batches in one copy
   std::vector<DeviceBatch> dev;
   cuda_check(cudaEventRecord(ev0_, stream_), "event");
+  if (prof_ && prof_->concurrent) {
+    prof_->spans.clear();
+    prof_->mark_base(stream_);
+  }
   upload(packs, dev);
   cuda_check(cudaMemsetAsync(stats_dev_, 0, 4 * sizeof(double), stream_), "stats zero");
   // this step's gradient set (and its overflow flag) was last read by the
@@ -516,7 +520,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     // a profiling pass serialises everything on the main stream so the
     // per-launch event windows measure each kernel alone (no concurrency)
-    if (!prof_) tape.set_side_stream(side_, &evpool_);
+    if (!prof_ || prof_->concurrent) tape.set_side_stream(side_, &evpool_);
     tape.set_gemm_workspace(gemm_ws_, gemm_ws_ + gemm_ws_floats_, gemm_ws_floats_);
     CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
     if (overlap && i + 1 == dev.size()) {
@@ -553,7 +557,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   // with the next step's forward, which waits per range before it first reads
   // those parameters; the stats read-back below does not wait for it. (Under
   // the profiler, and with SQF_ADAM_OVERLAP=0, it stays on the main stream.)
-  const bool adam_side = adam_overlap_ && side_ && !prof_;
+  const bool adam_side = adam_overlap_ && side_ && (!prof_ || prof_->concurrent);
   if (!injected) {
     GradPrep prep;
     prep.scale = float(scale);

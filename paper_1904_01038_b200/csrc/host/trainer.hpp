@@ -117,9 +117,15 @@ class Trainer {
   int64_t last_h2d_bytes() const { return h2d_bytes_; }
   int64_t last_d2h_bytes() const { return 36; }
   // per-launch event profiling of subsequent steps (bench roofline evidence)
-  void set_profile(bool on) {
-    if (on && !prof_) prof_ = std::make_unique<Profiler>();
-    if (!on) prof_.reset();
+  // mode 0 off, 1 serialised per-launch timing (every launch alone on the
+  // main stream), 2 timeline of the concurrent schedule
+  void set_profile(int mode) {
+    if (mode && !prof_) prof_ = std::make_unique<Profiler>();
+    if (!mode) prof_.reset();
+    if (prof_) {
+      prof_->concurrent = mode == 2;
+      prof_->streams = {stream_, side_, comm_stream_};
+    }
   }
   Profiler* profiler() { return prof_.get(); }
   // all-reduce/backward overlap of the last step: bucket indices in issue
