@@ -172,8 +172,11 @@ __global__ void __launch_bounds__(128) embed_bwd_fold_v(const int4* __restrict__
 
 constexpr int kMaxCh = 4;  // d <= 32 lanes * 4 chunks * 8 = 1024
 
+// One warp per row. Every global load of the row (x, gamma, beta) is issued
+// up front, so a warp pays one memory round trip before its reductions; 4 rows
+// per 128-thread block keep the grid fine-grained.
 template <typename T>
-__global__ void __launch_bounds__(256) ln_fwd_v(const T* __restrict__ x, int rows, int d, const T* __restrict__ g,
+__global__ void __launch_bounds__(128) ln_fwd_v(const T* __restrict__ x, int rows, int d, const T* __restrict__ g,
                                                const T* __restrict__ b, T* __restrict__ y,
                                                float2* __restrict__ stats) {
   SFK_PDL_WAIT();
@@ -181,13 +184,23 @@ __global__ void __launch_bounds__(256) ln_fwd_v(const T* __restrict__ x, int row
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (r >= rows) return;
   const T* xr = x + int64_t(r) * d;
+  uint4 xu[kMaxCh], gu[kMaxCh], bu[kMaxCh];
+#pragma unroll
+  for (int i = 0; i < kMaxCh; ++i) {
+    const int c = (lane + 32 * i) * 8;
+    if (c < d) {
+      xu[i] = *reinterpret_cast<const uint4*>(xr + c);
+      gu[i] = __ldg(reinterpret_cast<const uint4*>(g + c));
+      bu[i] = __ldg(reinterpret_cast<const uint4*>(b + c));
+    }
+  }
   float v[kMaxCh][8];
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < kMaxCh; ++i) {
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
-      V8<T>::load(xr + c, v[i]);
+      V8<T>::unpack(xu[i], v[i]);
 #pragma unroll
       for (int e = 0; e < 8; ++e) s += v[i][e];
     }
@@ -212,8 +225,8 @@ __global__ void __launch_bounds__(256) ln_fwd_v(const T* __restrict__ x, int row
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
       float gg[8], bb[8], o[8];
-      V8<T>::load(g + c, gg);
-      V8<T>::load(b + c, bb);
+      V8<T>::unpack(gu[i], gg);
+      V8<T>::unpack(bu[i], bb);
 #pragma unroll
       for (int e = 0; e < 8; ++e)
         o[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[i][e], mean), rstd), gg[e]), bb[e]);
@@ -459,10 +472,11 @@ __global__ void colsum_partial_v(const T* __restrict__ x, int rows, int n, int64
 // path) is one warp per row with no column state; the gamma/beta gradients
 // (parameter work, run on the side stream) are a column reduction over rows.
 template <typename T>
-__global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T* __restrict__ dy, int rows, int d,
+__global__ void __launch_bounds__(128) ln_dx_v(const T* __restrict__ x, const T* __restrict__ dy, int rows, int d,
                                               const T* __restrict__ g, const float2* __restrict__ stats,
                                               T* dx, const T* acc) {
-  // acc: nullptr (dx = contribution), dx (in place) or another buffer (out of place)
+  // acc: nullptr (dx = contribution), dx (in place) or another buffer (out of place).
+  // All loads of the row (x, dy, acc, gamma, stats) are issued before any math.
   const int accumulate = acc != nullptr;
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
@@ -470,7 +484,7 @@ __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T*
   if (r >= rows) return;
   const float2 st = stats[r];
   const float inv_n = __fdiv_rn(1.0f, float(d));
-  uint4 xr[kMaxCh], gr[kMaxCh], dxo[kMaxCh];
+  uint4 xr[kMaxCh], gr[kMaxCh], dxo[kMaxCh], gu[kMaxCh];
 #pragma unroll
   for (int i = 0; i < kMaxCh; ++i) {
     const int c = (lane + 32 * i) * 8;
@@ -478,6 +492,7 @@ __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T*
       xr[i] = *reinterpret_cast<const uint4*>(x + int64_t(r) * d + c);
       gr[i] = *reinterpret_cast<const uint4*>(dy + int64_t(r) * d + c);
       if (accumulate) dxo[i] = *reinterpret_cast<const uint4*>(acc + int64_t(r) * d + c);
+      gu[i] = __ldg(reinterpret_cast<const uint4*>(g + c));
     }
   }
   float s1 = 0.f, s2 = 0.f;
@@ -486,7 +501,7 @@ __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T*
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
       float gg[8], xh[8], gy[8];
-      V8<T>::load(g + c, gg);
+      V8<T>::unpack(gu[i], gg);
       V8<T>::unpack(xr[i], xh);
       V8<T>::unpack(gr[i], gy);
 #pragma unroll
@@ -505,7 +520,7 @@ __global__ void __launch_bounds__(256) ln_dx_v(const T* __restrict__ x, const T*
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
       float gg[8], xh[8], gy[8], o[8];
-      V8<T>::load(g + c, gg);
+      V8<T>::unpack(gu[i], gg);
       V8<T>::unpack(xr[i], xh);
       V8<T>::unpack(gr[i], gy);
       if (accumulate) V8<T>::unpack(dxo[i], o);
@@ -876,13 +891,13 @@ int embed_bwd_chunked_vec(int dtype, const int32_t* chunks, int nchunks, const i
 int ln_fwd_vec(int dtype, const void* x, int rows, int d, const void* g, const void* b, void* y, float* stats,
                cudaStream_t s) {
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(y) || !al16(g) || !al16(b)) return SFK_EUNSUP;
-  const int blocks = (rows + 7) / 8;
+  const int blocks = (rows + 3) / 4;
   if (dtype == SFK_F16)
-    launch_pdl(vec::ln_fwd_v<__half>, blocks, 256, 0, s, static_cast<const __half*>(x), rows, d,
+    launch_pdl(vec::ln_fwd_v<__half>, blocks, 128, 0, s, static_cast<const __half*>(x), rows, d,
                                                  static_cast<const __half*>(g), static_cast<const __half*>(b),
                                                  static_cast<__half*>(y), reinterpret_cast<float2*>(stats));
   else
-    launch_pdl(vec::ln_fwd_v<__nv_bfloat16>, blocks, 256, 0, s, 
+    launch_pdl(vec::ln_fwd_v<__nv_bfloat16>, blocks, 128, 0, s, 
         static_cast<const __nv_bfloat16*>(x), rows, d, static_cast<const __nv_bfloat16*>(g),
         static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(y), reinterpret_cast<float2*>(stats));
   return check_launch("sfk_layernorm_fwd(vec)");
@@ -1168,13 +1183,13 @@ int ln_dx_acc_vec(int dtype, const void* x, const void* dy, int rows, int d, con
                   const void* acc, void* dx, cudaStream_t s) {
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy) || !al16(dx) || !al16(g) || (acc && !al16(acc)))
     return SFK_EUNSUP;
-  const int blocks = (rows + 7) / 8;
+  const int blocks = (rows + 3) / 4;
   if (dtype == SFK_F16)
-    launch_pdl(vec::ln_dx_v<__half>, dim3(blocks), dim3(256), 0, s, static_cast<const __half*>(x),
+    launch_pdl(vec::ln_dx_v<__half>, dim3(blocks), dim3(128), 0, s, static_cast<const __half*>(x),
                static_cast<const __half*>(dy), rows, d, static_cast<const __half*>(g),
                reinterpret_cast<const float2*>(stats), static_cast<__half*>(dx), static_cast<const __half*>(acc));
   else
-    launch_pdl(vec::ln_dx_v<__nv_bfloat16>, dim3(blocks), dim3(256), 0, s, static_cast<const __nv_bfloat16*>(x),
+    launch_pdl(vec::ln_dx_v<__nv_bfloat16>, dim3(blocks), dim3(128), 0, s, static_cast<const __nv_bfloat16*>(x),
                static_cast<const __nv_bfloat16*>(dy), rows, d, static_cast<const __nv_bfloat16*>(g),
                reinterpret_cast<const float2*>(stats), static_cast<__nv_bfloat16*>(dx),
                static_cast<const __nv_bfloat16*>(acc));
