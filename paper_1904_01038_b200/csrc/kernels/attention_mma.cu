@@ -47,6 +47,14 @@ struct MmaT<__nv_bfloat16> {
   }
 };
 
+// 2^x on the SFU, flushing subnormal results to zero (probabilities that
+// small are zero in every 16-bit output anyway)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
@@ -115,7 +123,10 @@ __device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.cau
 
 // ------------------------------------------------------------------ forward
 // R = query rows per CTA (64: 4 warps; 32: 2 warps for short sentences)
-template <typename T, int DH, int R>
+// KC = keys per chunk: 32 when every key span fits (short sentences), else 64.
+// Scores are kept in log2 units (s * sc * log2 e) so each probability is one
+// subtract and one SFU exp2; the saved max is converted back to natural units.
+template <typename T, int DH, int R, int KC>
 __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
@@ -126,7 +137,7 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   const int len = a.causal ? a.kw : a.klen[b];
   // keys any row of this block can see
   const int nk = a.causal ? min(a.kw, min(q0 + R, a.qw)) : len;
-  const int nk_pad = (nk + 63) & ~63;
+  const int nk_pad = (nk + KC - 1) / KC * KC;
   T* Qs = reinterpret_cast<T*>(smem);
   T* Ks = Qs + R * LD;
   T* Vs = Ks + nk_pad * LD;
@@ -146,19 +157,20 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 1;
   const int lim_b = row_b < a.qw ? (a.causal ? row_b + 1 : len) : 1;
   const int warp_keys = a.causal ? min(a.qw, q0 + r0 + 16) : len;
-  const float l2e = 1.4426950408889634f;
+  const float c2 = a.sc * 1.4426950408889634f;  // natural score -> log2 units
   float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
   float o[DH / 8][4];
 #pragma unroll
   for (int i = 0; i < DH / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  for (int kc = 0; kc < warp_keys; kc += 64) {
-    float s[8][4];
+  constexpr int NT = KC / 8;
+  for (int kc = 0; kc < warp_keys; kc += KC) {
+    float s[NT][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
+    for (int i = 0; i < NT; ++i) s[i][0] = s[i][1] = s[i][2] = s[i][3] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < 8; nt += 2) {
+      for (int nt = 0; nt < NT; nt += 2) {
         uint32_t bb[4];
         load_b_nk<T>(bb, Ks, LD, kc + nt * 8, ks * 16, lane);
         MmaT<T>::mma(s[nt], qa[ks], bb[0], bb[1]);
@@ -166,12 +178,12 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
       }
     float mx_a = m_a, mx_b = m_b;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = kc + nt * 8 + 2 * tq + e;
-        s[nt][e] = j < lim_a ? s[nt][e] * a.sc : -INFINITY;
-        s[nt][2 + e] = j < lim_b ? s[nt][2 + e] * a.sc : -INFINITY;
+        s[nt][e] = j < lim_a ? s[nt][e] * c2 : -INFINITY;
+        s[nt][2 + e] = j < lim_b ? s[nt][2 + e] * c2 : -INFINITY;
         mx_a = fmaxf(mx_a, s[nt][e]);
         mx_b = fmaxf(mx_b, s[nt][2 + e]);
       }
@@ -180,16 +192,16 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
       mx_a = fmaxf(mx_a, __shfl_xor_sync(0xffffffffu, mx_a, off));
       mx_b = fmaxf(mx_b, __shfl_xor_sync(0xffffffffu, mx_b, off));
     }
-    const float al_a = exp2f((m_a - mx_a) * l2e), al_b = exp2f((m_b - mx_b) * l2e);
+    const float al_a = ex2(m_a - mx_a), al_b = ex2(m_b - mx_b);
     m_a = mx_a;
     m_b = mx_b;
     float rs_a = 0.f, rs_b = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      s[nt][0] = exp2f((s[nt][0] - m_a) * l2e);
-      s[nt][1] = exp2f((s[nt][1] - m_a) * l2e);
-      s[nt][2] = exp2f((s[nt][2] - m_b) * l2e);
-      s[nt][3] = exp2f((s[nt][3] - m_b) * l2e);
+    for (int nt = 0; nt < NT; ++nt) {
+      s[nt][0] = ex2(s[nt][0] - m_a);
+      s[nt][1] = ex2(s[nt][1] - m_a);
+      s[nt][2] = ex2(s[nt][2] - m_b);
+      s[nt][3] = ex2(s[nt][3] - m_b);
       rs_a += s[nt][0] + s[nt][1];
       rs_b += s[nt][2] + s[nt][3];
     }
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
       o[i][3] *= al_b;
     }
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {  // 16 keys per k-step
+    for (int kk = 0; kk < NT / 2; ++kk) {  // 16 keys per k-step
       uint32_t pa[4] = {MmaT<T>::pack(s[2 * kk][0], s[2 * kk][1]), MmaT<T>::pack(s[2 * kk][2], s[2 * kk][3]),
                         MmaT<T>::pack(s[2 * kk + 1][0], s[2 * kk + 1][1]),
                         MmaT<T>::pack(s[2 * kk + 1][2], s[2 * kk + 1][3])};
@@ -231,9 +243,10 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
     if (row_b < a.qw)
       *reinterpret_cast<uint32_t*>(out + (qrow0 + row_b) * a.ldout + c) = MmaT<T>::pack(o[nt][2] * ib, o[nt][3] * ib);
   }
-  if (tq == 0) {
-    if (row_a < a.qw) a.stats[(qrow0 + row_a) * a.heads + h] = make_float2(m_a, ia);
-    if (row_b < a.qw) a.stats[(qrow0 + row_b) * a.heads + h] = make_float2(m_b, ib);
+  if (tq == 0) {  // max back in natural units (the saved-stats contract)
+    const float ln2 = 0.6931471805599453f;
+    if (row_a < a.qw) a.stats[(qrow0 + row_a) * a.heads + h] = make_float2(m_a * ln2, ia);
+    if (row_b < a.qw) a.stats[(qrow0 + row_b) * a.heads + h] = make_float2(m_b * ln2, ib);
   }
 }
 
@@ -294,7 +307,7 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
   const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 0;
   const int lim_b = row_b < a.qw ? (a.causal ? row_b + 1 : len) : 0;
   const int warp_keys = a.causal ? min(a.qw, q0 + r0 + 16) : len;
-  const float l2e = 1.4426950408889634f;
+  const float l2e = 1.4426950408889634f, c2 = a.sc * l2e;
   float dq[DH / 8][4];
 #pragma unroll
   for (int i = 0; i < DH / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
@@ -321,8 +334,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = kc + nt * 8 + 2 * tq + e;
-        const float pa = j < lim_a ? exp2f((s[nt][e] * a.sc - st_a.x) * l2e) * st_a.y : 0.f;
-        const float pb = j < lim_b ? exp2f((s[nt][2 + e] * a.sc - st_b.x) * l2e) * st_b.y : 0.f;
+        const float pa = j < lim_a ? ex2(s[nt][e] * c2 - st_a.x * l2e) * st_a.y : 0.f;
+        const float pb = j < lim_b ? ex2(s[nt][2 + e] * c2 - st_b.x * l2e) * st_b.y : 0.f;
         s[nt][e] = pa * (dp[nt][e] - D_a);
         s[nt][2 + e] = pb * (dp[nt][2 + e] - D_b);
       }
@@ -406,7 +419,7 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
       load_a<T>(ka[ks], Ks, LD, r0, ks * 16, lane);
       load_a<T>(va[ks], Vs, LD, r0, ks * 16, lane);
     }
-    const float l2e = 1.4426950408889634f;
+    const float l2e = 1.4426950408889634f, c2 = a.sc * l2e;
     // causal: queries before this warp's first key never see it
     const int qbeg = a.causal ? ((k0 + r0 - qstart) & ~15) : 0;
     for (int qc = qbeg; qc < nq; qc += NC) {
@@ -440,8 +453,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
           const bool qok = qi < nq;
           const bool va_ok = qok && key_a < a.kw && (a.causal ? key_a <= t : key_a < len);
           const bool vb_ok = qok && key_b < a.kw && (a.causal ? key_b <= t : key_b < len);
-          const float pa = va_ok ? exp2f((s[nt][e] * a.sc - st.x) * l2e) * st.y : 0.f;
-          const float pb = vb_ok ? exp2f((s[nt][2 + e] * a.sc - st.x) * l2e) * st.y : 0.f;
+          const float pa = va_ok ? ex2(s[nt][e] * c2 - st.x * l2e) * st.y : 0.f;
+          const float pb = vb_ok ? ex2(s[nt][2 + e] * c2 - st.x * l2e) * st.y : 0.f;
           p[nt][e] = pa;
           p[nt][2 + e] = pb;
           s[nt][e] = pa * (dp[nt][e] - D);
@@ -527,7 +540,7 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
   stage_wait();
   __syncthreads();
   const int r0 = warp * 16;
-  const float l2e = 1.4426950408889634f;
+  const float l2e = 1.4426950408889634f, c2 = a.sc * l2e;
   // ---- phase 1: D and dQ for query rows r0..r0+15
   if (r0 < a.qw) {
     const int row_a = r0 + g, row_b = row_a + 8;
@@ -583,8 +596,8 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int j = kc + nt * 8 + 2 * tq + e;
-          const float pa = j < lim_a ? exp2f((s[nt][e] * a.sc - st_a.x) * l2e) * st_a.y : 0.f;
-          const float pb = j < lim_b ? exp2f((s[nt][2 + e] * a.sc - st_b.x) * l2e) * st_b.y : 0.f;
+          const float pa = j < lim_a ? ex2(s[nt][e] * c2 - st_a.x * l2e) * st_a.y : 0.f;
+          const float pb = j < lim_b ? ex2(s[nt][2 + e] * c2 - st_b.x * l2e) * st_b.y : 0.f;
           s[nt][e] = pa * (dp[nt][e] - D_a);
           s[nt][2 + e] = pb * (dp[nt][2 + e] - D_b);
         }
@@ -663,8 +676,8 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
           const bool qok = t < nq;
           const bool va_ok = qok && key_a < a.kw && (a.causal ? key_a <= t : key_a < len);
           const bool vb_ok = qok && key_b < a.kw && (a.causal ? key_b <= t : key_b < len);
-          const float pa = va_ok ? exp2f((s[nt][e] * a.sc - st.x) * l2e) * st.y : 0.f;
-          const float pb = vb_ok ? exp2f((s[nt][2 + e] * a.sc - st.x) * l2e) * st.y : 0.f;
+          const float pa = va_ok ? ex2(s[nt][e] * c2 - st.x * l2e) * st.y : 0.f;
+          const float pb = vb_ok ? ex2(s[nt][2 + e] * c2 - st.x * l2e) * st.y : 0.f;
           p[nt][e] = pa;
           p[nt][2 + e] = pb;
           s[nt][e] = pa * (dp[nt][e] - D);
@@ -745,8 +758,10 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   const int kpad = (a.kw + 63) & ~63, qpad = ((a.qw + 63) & ~63) + 64;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(fwd_k<T, DH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(fwd_k<T, DH, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dq_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_small_k<T, DH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -757,12 +772,21 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   // sentences of <= 32 positions: 32-row CTAs of 2 warps, so no warp idles
   const bool short32 = a.qw <= 32 && (bwd ? a.kw <= 32 : true);
   if (!bwd) {
+    // every key span within 32: 32-key chunks (no work on a padded half)
+    const bool k32 = a.kw <= 32;
+    const size_t kp = k32 ? 32 : kpad;
     if (short32) {
-      const size_t smem = size_t(32 + 2 * kpad) * LD * sizeof(T);
-      launch_pdl(fwd_k<T, DH, 32>, dim3(1, a.heads, a.batch), 64, smem, st, a);
+      const size_t smem = size_t(32 + 2 * kp) * LD * sizeof(T);
+      if (k32)
+        launch_pdl(fwd_k<T, DH, 32, 32>, dim3(1, a.heads, a.batch), 64, smem, st, a);
+      else
+        launch_pdl(fwd_k<T, DH, 32, 64>, dim3(1, a.heads, a.batch), 64, smem, st, a);
     } else {
-      const size_t smem = size_t(kRows + 2 * kpad) * LD * sizeof(T);
-      launch_pdl(fwd_k<T, DH, 64>, gq, kWarps * 32, smem, st, a);
+      const size_t smem = size_t(kRows + 2 * kp) * LD * sizeof(T);
+      if (k32)
+        launch_pdl(fwd_k<T, DH, 64, 32>, gq, kWarps * 32, smem, st, a);
+      else
+        launch_pdl(fwd_k<T, DH, 64, 64>, gq, kWarps * 32, smem, st, a);
     }
     return check_launch("sfk_attention_fwd(mma)");
   }

@@ -18,28 +18,54 @@ __global__ void nonfinite_k(const T* __restrict__ g, int64_t n, int32_t* flag) {
   if (bad && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// Per-update constants. Division by the update's constants (loss scale,
+// token count, bias corrections) uses the correctly rounded reciprocal and
+// one FMA correction (Markstein): q = RN(a*y), r = a - b*q (exact by FMA),
+// RN(q + r*y) is the correctly rounded a/b when y = RN(1/b) -- the same bits
+// as a true division at a fraction of its cost. Only the per-element
+// division by sqrt(vhat) + eps and the square root stay full IEEE ops.
+struct AdamConst {
+  double lr, b1, b2, eps, bc1, bc2, rbc1, rbc2;
+  float scale, rscale, ntok, rntok;
+  int unscale;
+};
+
+__device__ __forceinline__ double div_by(double a, double b, double rb) {
+  const double q = __dmul_rn(a, rb);
+  return __fma_rn(__fma_rn(-b, q, a), rb, q);
+}
+__device__ __forceinline__ float div_by(float a, float b, float rb) {
+  const float q = __fmul_rn(a, rb);
+  return __fmaf_rn(__fmaf_rn(-b, q, a), rb, q);
+}
+
+// one element: returns the new master value; m, v updated in place
+// (optim.cpp:48-66 evaluation order, explicit _rn ops: no contraction)
+__device__ __forceinline__ float adam_elem(const AdamConst& c, float p, float& m, float& v, float gf) {
+  if (c.unscale) gf = div_by(gf, c.scale, c.rscale);
+  gf = div_by(gf, c.ntok, c.rntok);
+  const double g = gf;
+  const double mm = __dadd_rn(__dmul_rn(c.b1, double(m)), __dmul_rn(1.0 - c.b1, g));
+  const double vv = __dadd_rn(__dmul_rn(c.b2, double(v)), __dmul_rn(__dmul_rn(1.0 - c.b2, g), g));
+  m = float(mm);
+  v = float(vv);
+  const double mhat = div_by(double(m), c.bc1, c.rbc1);
+  const double vhat = div_by(double(v), c.bc2, c.rbc2);
+  return float(__dsub_rn(double(p), __ddiv_rn(__dmul_rn(c.lr, mhat), __dadd_rn(__dsqrt_rn(vhat), c.eps))));
+}
+
 template <typename G, typename S>
 __global__ void adam_k(float* __restrict__ master, S* __restrict__ shadow, const G* __restrict__ grad,
-                       float* __restrict__ m, float* __restrict__ v, int64_t n, double lr, double b1, double b2,
-                       double eps, double bc1, double bc2, float scale, int unscale, float ntok,
+                       float* __restrict__ m, float* __restrict__ v, int64_t n, const AdamConst c,
                        const int32_t* __restrict__ skip) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   if (skip && *skip) return;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    float gf = Num<G>::ld(grad + i);
-    if (unscale) gf = __fdiv_rn(gf, scale);
-    gf = __fdiv_rn(gf, ntok);
-    const double g = gf;
-    // explicit _rn ops: no FMA contraction, same evaluation order as optim.cpp:53-56
-    const double mm = __dadd_rn(__dmul_rn(b1, double(m[i])), __dmul_rn(1.0 - b1, g));
-    const double vv = __dadd_rn(__dmul_rn(b2, double(v[i])), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
-    const float mf = float(mm), vf = float(vv);
-    m[i] = mf;
-    v[i] = vf;
-    const double mhat = __ddiv_rn(double(mf), bc1);
-    const double vhat = __ddiv_rn(double(vf), bc2);
-    const float p = float(__dsub_rn(double(master[i]), __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps))));
+    float mi = m[i], vi = v[i];
+    const float p = adam_elem(c, master[i], mi, vi, Num<G>::ld(grad + i));
+    m[i] = mi;
+    v[i] = vi;
     master[i] = p;
     if (shadow) Num<S>::st(shadow + i, p);
   }
@@ -50,9 +76,8 @@ __global__ void adam_k(float* __restrict__ master, S* __restrict__ shadow, const
 template <typename G, typename S>
 __global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __restrict__ shadow,
                                                const G* __restrict__ grad, float* __restrict__ m,
-                                               float* __restrict__ v, int64_t n4, double lr, double b1, double b2,
-                                               double eps, double bc1, double bc2, float scale, int unscale,
-                                               float ntok, const int32_t* __restrict__ skip) {
+                                               float* __restrict__ v, int64_t n4, const AdamConst c,
+                                               const int32_t* __restrict__ skip) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   if (skip && *skip) return;
@@ -67,19 +92,7 @@ __global__ void __launch_bounds__(256) adam4_k(float* __restrict__ master, S* __
     float* mp = &m4.x;
     float* vp = &v4.x;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float gf = Num<G>::ld(gg + j);
-      if (unscale) gf = __fdiv_rn(gf, scale);
-      gf = __fdiv_rn(gf, ntok);
-      const double g = gf;
-      const double mm = __dadd_rn(__dmul_rn(b1, double(mp[j])), __dmul_rn(1.0 - b1, g));
-      const double vv = __dadd_rn(__dmul_rn(b2, double(vp[j])), __dmul_rn(__dmul_rn(1.0 - b2, g), g));
-      mp[j] = float(mm);
-      vp[j] = float(vv);
-      const double mhat = __ddiv_rn(double(mp[j]), bc1);
-      const double vhat = __ddiv_rn(double(vp[j]), bc2);
-      pp[j] = float(__dsub_rn(double(pp[j]), __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps))));
-    }
+    for (int j = 0; j < 4; ++j) pp[j] = adam_elem(c, pp[j], mp[j], vp[j], Num<G>::ld(gg + j));
     *reinterpret_cast<float4*>(master + i) = p4;
     *reinterpret_cast<float4*>(m + i) = m4;
     *reinterpret_cast<float4*>(v + i) = v4;
@@ -157,18 +170,18 @@ extern "C" int sfk_adam(int grad_dtype, float* master, void* shadow, int shadow_
                                                              reinterpret_cast<uintptr_t>(m) |
                                                              reinterpret_cast<uintptr_t>(v)) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(grad) & 7) == 0;
+  AdamConst c{lr, b1, b2, eps, bc1, bc2, 1.0 / bc1, 1.0 / bc2, scale, 1.0f / scale, ntokens, 1.0f / ntokens,
+               unscale};
   if (vec) {
     const int64_t n4 = n / 4;
     SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
-                  launch_pdl(adam4_k<G, S>, grid_for(n4), 256, 0, as_stream(stream), 
-                      master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n4, lr, b1, b2, eps, bc1,
-                      bc2, scale, unscale, ntokens, skip));
+                  launch_pdl(adam4_k<G, S>, grid_for(n4), 256, 0, as_stream(stream),
+                      master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n4, c, skip));
     return check_launch("sfk_adam(vec)");
   }
   SFK_DISPATCH2(grad_dtype, G, shadow_dtype, S,
-                launch_pdl(adam_k<G, S>, grid_for(n), 256, 0, as_stream(stream), 
-                    master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n, lr, b1, b2, eps, bc1, bc2,
-                    scale, unscale, ntokens, skip));
+                launch_pdl(adam_k<G, S>, grid_for(n), 256, 0, as_stream(stream),
+                    master, static_cast<S*>(shadow), static_cast<const G*>(grad), m, v, n, c, skip));
   return check_launch("sfk_adam");
 }
 

@@ -248,15 +248,23 @@ def test_attention_matches_reference(fp16, batch, qw, kw, heads, dh, causal):
         np.testing.assert_allclose(got.float().cpu().numpy(), want, rtol=rt, atol=rt * 4)
 
 
-def test_adam_bit_exact_with_reference():
+@pytest.mark.parametrize("n,scale,ntok,lr,t,seed", [(10000, 512.0, 3333.0, 7e-4, 5, 3),
+                                                   (1 << 20, 128.0, 51239.0, 5e-4, 1, 4),
+                                                   (1 << 20, 0.5, 430117.0, 1e-3, 977, 5),
+                                                   (1 << 20, 2.0 ** -14, 7.0, 2e-3, 40000, 6)])
+def test_adam_bit_exact_with_reference(n, scale, ntok, lr, t, seed):
+    """The fused unscale + 1/ntokens + Adam kernel against the reference's
+    double-math update (optim.cpp:48-66): bit-identical master, moments and
+    16-bit shadow over a million elements whose gradients and moments span
+    many orders of magnitude (the constant divisions use a reciprocal plus one
+    FMA correction, which must round exactly like a true division)."""
     lib = L()
-    rng = np.random.default_rng(3)
-    n = 10000
+    rng = np.random.default_rng(seed)
     p = rng.standard_normal(n).astype(np.float32)
-    g = ref.quantize_array(rng.standard_normal(n).astype(np.float32) * 512)
-    m = (rng.standard_normal(n) * 0.01).astype(np.float32)
-    v = (rng.random(n) * 0.01).astype(np.float32)
-    scale, ntok, lr, t = 512.0, 3333.0, 7e-4, 5
+    mag = 10.0 ** rng.uniform(-6, 3, n)
+    g = ref.quantize_array((rng.standard_normal(n) * mag).astype(np.float32))
+    m = (rng.standard_normal(n) * 10.0 ** rng.uniform(-9, -1, n)).astype(np.float32)
+    v = (rng.random(n) * 10.0 ** rng.uniform(-14, -1, n)).astype(np.float32)
     g_pre = ((g / np.float32(scale)).astype(np.float32) / np.float32(ntok)).astype(np.float32)
     want_p, want_m, want_v = ref.adam(p, g_pre, m, v, t - 1, lr)
     tp, tm, tv = (torch.tensor(a, device="cuda") for a in (p, m, v))
