@@ -19,6 +19,18 @@ static int tile_env() {
 }
 
 // SQF_LN_FUSED=1: one-pass LN backward (dx + gamma/beta partials on the main stream)
+// SQF_ABLATE (measurement only, results are wrong): bit mask of kernel
+// classes whose launches are skipped, to read each class's share of the real
+// concurrent step from the step-time difference. 1 LN fwd, 2 LN dx, 4 LN
+// gamma/beta, 8 attention fwd, 16 attention bwd, 32 xent.
+int ablate_mask() {
+  static const int m = [] {
+    const char* e = std::getenv("SQF_ABLATE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+
 static bool ln_fused_env() {
   static const bool v = [] {
     const char* e = std::getenv("SQF_LN_FUSED");
@@ -274,6 +286,7 @@ int DeviceTape::layer_norm(int x, ParamRef gamma, ParamRef beta) {
   n.out = alloc_elems(int64_t(n.rows) * n.cols);
   n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * 8));
   pbegin();
+  if (!(ablate_mask() & 1))
   sfk_check(sfk_layernorm_fwd(dtype_, in.out, n.rows, n.cols, pptr(gamma), pptr(beta), n.out, n.stats, cur_),
             "layernorm_fwd");
   pend(Profiler::LayerNorm, 0, double(n.rows) * (2.0 * n.cols * esize_ + 8));
@@ -455,7 +468,7 @@ int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d,
   a.ldo = d;
   a.stats = n.stats;
   pbegin();
-  sfk_check(sfk_attention_fwd(&a, cur_), "attention_fwd");
+  if (!(ablate_mask() & 8)) sfk_check(sfk_attention_fwd(&a, cur_), "attention_fwd");
   pend(Profiler::AttnFwd, attn_flops(batch, q_width, k_width, k_len, d, causal, false),
        double(esize_) * d * (2.0 * n.rows + 2.0 * kn.rows));
   ++launches_;
@@ -539,6 +552,7 @@ void DeviceTape::run_xent(Node& n, float seed, bool with_grad, double* stats_acc
   Node& lg = nodes_[n.in0];
   // the logits buffer becomes its own gradient (dlogits written in place)
   pbegin();
+  if (!(ablate_mask() & 32))
   sfk_check(sfk_xent_fwd_bwd(dtype_, lg.out, lg.rows, lg.cols, lg.ld ? lg.ld : lg.cols, n.gold, kPad, n.eps, seed,
                              with_grad ? lg.out : nullptr, n.row_out, cur_),
             "xent");
@@ -707,6 +721,7 @@ void DeviceTape::backward_node(int id) {
           cur_ = side_;
         }
         pbegin();
+        if (!(ablate_mask() & 4))
         sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
                                            counters((n.cols + 255) / 256), gptr(n.p0), gptr(n.p1), cur_),
                   "layernorm_bwd_params");
@@ -721,6 +736,7 @@ void DeviceTape::backward_node(int id) {
           cur_ = stream_;
         }
         pbegin();
+        if (!(ablate_mask() & 2))
         sfk_check(sfk_layernorm_bwd_dx_acc(dtype_, in.out, n.grad, n.rows, n.cols, pptr(n.p0), n.stats, acc, dxw,
                                            cur_),
                   "layernorm_bwd_dx");
@@ -853,7 +869,7 @@ void DeviceTape::backward_node(int id) {
       a.lddv = kn.cols;
       a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
       pbegin();
-      sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
+      if (!(ablate_mask() & 16)) sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
       pend(Profiler::AttnBwd, attn_flops(n.batch, n.q_width, n.k_width, n.k_len, n.cols, n.causal, true),
            double(esize_) * n.cols * (4.0 * n.rows + 4.0 * kn.rows));
       launches_ += 2;
