@@ -9,6 +9,7 @@
 namespace sqf {
 
 void set_model_position_table(ModelBase& m, const float* dev);
+int ablate_mask();  // device_tape.cpp: SQF_ABLATE measurement knob
 
 Trainer::Trainer(const Config& cfg, const Registry& reg, std::unique_ptr<TaskBase> task, int rank, int world,
                  std::unique_ptr<Collective> coll)
@@ -563,7 +564,9 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     prep.scale = float(scale);
     prep.unscale = fp16_;
     prep.ntokens = float(stats.ntokens);
-    prep.skip = flag_d;
+    // (SQF_ABLATE: results are garbage by design; never skip so the step
+    // keeps its full shape)
+    prep.skip = ablate_mask() ? nullptr : flag_d;
     cudaStream_t os = stream_;
     if (adam_side) {
       cuda_check(cudaEventRecord(ev_checked_, stream_), "event record");
@@ -596,7 +599,7 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
   cudaEventElapsedTime(&last_ms_, ev0_, ev1_);
   if (prof_) prof_->collect();
   const double* st = reinterpret_cast<const double*>(rb);
-  const int32_t flag = *reinterpret_cast<const int32_t*>(rb + 32);
+  const int32_t flag = ablate_mask() ? 0 : *reinterpret_cast<const int32_t*>(rb + 32);
   stats.loss = st[0];
   stats.nll = st[1];
   stats.ncorrect = int64_t(st[3]);

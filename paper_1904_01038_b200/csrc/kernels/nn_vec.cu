@@ -714,8 +714,15 @@ __global__ void __launch_bounds__(512) xent_v(const T* __restrict__ logits, int 
     if (tid == 0) reinterpret_cast<float4*>(row_out)[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
+  // log2 domain: every exponential is one FFMA + one SFU ex2 (ftz: terms
+  // below 2^-126 of the row max contribute nothing at fp32 precision anyway)
   const float L2E = 1.4426950408889634f;
-  float m = -INFINITY, s = 0.f;
+  auto ex2 = [](float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  };
+  float m = -INFINITY, s = 0.f, sf = 0.f;  // sf: sum of logits (label-smoothing term)
   int mi = 0x7fffffff;
   // four 16-byte loads in flight per thread before any of them is consumed
   for (int ch0 = tid; ch0 < nch; ch0 += 4 * blockDim.x) {
@@ -739,12 +746,16 @@ __global__ void __launch_bounds__(512) xent_v(const T* __restrict__ logits, int 
       for (int e = 1; e < 8; ++e)
         if (f[e] > cm) cm = f[e], ci = e;
       if (cm > m) {
-        s *= exp2f((m - cm) * L2E);
+        s *= ex2((m - cm) * L2E);
         m = cm;
         mi = ch * 8 + ci;
       }
+      const float nml = -m * L2E;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += exp2f((f[e] - m) * L2E);
+      for (int e = 0; e < 8; ++e) {
+        s += ex2(fmaf(f[e], L2E, nml));
+        sf += f[e];
+      }
     }
   }
   // (max, sum, first argmax) combine
@@ -782,24 +793,29 @@ __global__ void __launch_bounds__(512) xent_v(const T* __restrict__ logits, int 
   const int amax = ri[0];
   __syncthreads();
   const float uni = __fdiv_rn(eps, float(V)), on = __fadd_rn(1.0f - eps, uni);
-  float sm = 0.f;
-  for (int ch = tid; ch < nch; ch += blockDim.x) {
-    float f[8], o[8];
-    V8<T>::unpack(xrow[ch], f);
+  if (dst) {
+    const float nll2 = -lse * L2E;
+    const int gch = gid / 8;
+    for (int ch = tid; ch < nch; ch += blockDim.x) {
+      float f[8], o[8];
+      V8<T>::unpack(xrow[ch], f);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float p = exp2f((f[e] - lse) * L2E);
-      o[e] = __fmul_rn(seed, __fsub_rn(p, ch * 8 + e == gid ? on : uni));
-      sm += __fsub_rn(lse, f[e]);
+      for (int e = 0; e < 8; ++e) o[e] = __fmul_rn(seed, __fsub_rn(ex2(fmaf(f[e], L2E, nll2)), uni));
+      if (ch == gch) {  // the gold column's target is (1 - eps) + eps / V
+        const int e = gid % 8;
+        o[e] = __fmul_rn(seed, __fsub_rn(ex2(fmaf(f[e], L2E, nll2)), on));
+      }
+      V8<T>::store(dst + ch * 8, o);
     }
-    if (dst) V8<T>::store(dst + ch * 8, o);
   }
-  sm = warp_sum(sm);
+  // sum over v of (lse - l_v) = V * lse - sum l_v
+  float sm = warp_sum(sf);
   if (lane == 0) rs[wid] = sm;
   __syncthreads();
   if (tid == 0) {
-    float tot = 0.f;
-    for (int w = 0; w < nw; ++w) tot += rs[w];
+    float tsf = 0.f;
+    for (int w = 0; w < nw; ++w) tsf += rs[w];
+    const float tot = __fsub_rn(__fmul_rn(float(V), lse), tsf);
     float gl[8];
     V8<T>::unpack(xrow[gid / 8], gl);
     const float nll = __fsub_rn(lse, gl[gid % 8]);
