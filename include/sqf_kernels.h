@@ -180,6 +180,23 @@ int sfk_layernorm_bwd_dx_part(int dtype, const void* x, const void* dy, int rows
                               float* part, int* nparts, void* stream);
 int sfk_layernorm_bwd_fold(int dtype, const float* part, int nparts, int d, void* dgamma,
                            void* dbeta, void* stream);
+/* gamma/beta gradients in two steps, so the per-node work is one lean pass and
+ * the folds of many LayerNorm nodes share one launch:
+ * sfk_layernorm_bwd_params_partial: block b of *nparts (<= 148) sums its row
+ * chunk of dy*xhat and dy into part[b][0|1][d] (fixed order); part holds
+ * >= 2*148*d floats. sfk_layernorm_bwd_params_fold: for every job, in block
+ * order, dgamma = q(dgamma + sum_b part[b][0]), dbeta = q(dbeta + sum_b part[b][1]). */
+int sfk_layernorm_bwd_params_partial(int dtype, const void* x, const void* dy, int rows, int d,
+                                     const float* stats, float* part, int* nparts, void* stream);
+typedef struct {
+  const float* part;
+  void* dgamma;
+  void* dbeta;
+  int nparts;
+  int d;
+} sfk_ln_fold_job;
+enum { SFK_LN_FOLD_MAX_JOBS = 48 };
+int sfk_layernorm_bwd_params_fold(int dtype, const sfk_ln_fold_job* jobs, int njobs, void* stream);
 /* (counters: >= ceil(d/256) zeroed int32 slots, re-armed to 0 by the kernel,
  * selects the single-launch form; NULL falls back to partial + fold launches) */
 

@@ -83,6 +83,9 @@ sfk_layernorm_bwd_dx_acc = _sig("sfk_layernorm_bwd_dx_acc", C.c_int, C.c_int, vp
                                 vp, vp)
 sfk_layernorm_bwd_dx_part = _sig("sfk_layernorm_bwd_dx_part", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp,
                                  vp, C.c_int, vp, P(C.c_int), vp)
+sfk_layernorm_bwd_params_partial = _sig("sfk_layernorm_bwd_params_partial", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
+                                        vp, vp, P(C.c_int), vp)
+sfk_layernorm_bwd_params_fold = _sig("sfk_layernorm_bwd_params_fold", C.c_int, C.c_int, vp, C.c_int, vp)
 sfk_layernorm_bwd_fold = _sig("sfk_layernorm_bwd_fold", C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp)
 sfk_layernorm_bwd_params = _sig("sfk_layernorm_bwd_params", C.c_int, C.c_int, vp, vp, C.c_int, C.c_int, vp, vp, vp,
                                 vp, vp, vp)

@@ -574,7 +574,31 @@ void DeviceTape::backward(int loss_node, float seed, double* stats_acc, bool joi
   if (n.kind != Kind::Xent) throw ShapeError("backward: loss node must be a softmax_xent node");
   run_xent(n, seed, true, stats_acc);
   for (int i = loss_node - 1; i >= 0; --i) backward_node(i);
+  if (!ln_folds_.empty()) {
+    // the partials were written on the side stream (or the main stream when
+    // there is none): fold them there, behind everything already enqueued
+    if (side_) cur_ = side_;
+    flush_ln_folds();
+    if (side_) {
+      cudaEvent_t done = event();
+      cuda_check(cudaEventRecord(done, side_), "event record");
+      side_last_ = done;
+      cur_ = stream_;
+    }
+  }
   if (join) join_side();
+}
+
+void DeviceTape::flush_ln_folds() {
+  if (ln_folds_.empty()) return;
+  pbegin();
+  sfk_check(sfk_layernorm_bwd_params_fold(dtype_, ln_folds_.data(), int(ln_folds_.size()), cur_),
+            "layernorm_bwd_params_fold");
+  double bytes = 0;
+  for (const auto& j : ln_folds_) bytes += double(j.nparts) * j.d * 8.0;
+  pend(Profiler::LayerNorm, 0, bytes);
+  ++launches_;
+  ln_folds_.clear();
 }
 
 cudaEvent_t DeviceTape::event() {
@@ -720,12 +744,18 @@ void DeviceTape::backward_node(int id) {
           cuda_check(cudaStreamWaitEvent(side_, ready, 0), "stream wait");
           cur_ = side_;
         }
+        // column partials now; the folds of all LayerNorm nodes of the
+        // sub-batch share one launch at the end of backward (per node when a
+        // gradient hook needs each parameter's completion in order)
         pbegin();
+        int nparts = 0;
         if (!(ablate_mask() & 4))
-        sfk_check(sfk_layernorm_bwd_params(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part,
-                                           counters((n.cols + 255) / 256), gptr(n.p0), gptr(n.p1), cur_),
-                  "layernorm_bwd_params");
+          sfk_check(sfk_layernorm_bwd_params_partial(dtype_, in.out, n.grad, n.rows, n.cols, n.stats, part, &nparts,
+                                                     cur_),
+                    "layernorm_bwd_params_partial");
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * 2.0);
+        if (nparts > 0) ln_folds_.push_back({part, gptr(n.p0), gptr(n.p1), nparts, n.cols});
+        if (hook_ || ln_folds_.size() == size_t(SFK_LN_FOLD_MAX_JOBS)) flush_ln_folds();
         grad_done(n.p0);
         grad_done(n.p1);
         if (side_ && !ln_main) {
@@ -741,7 +771,7 @@ void DeviceTape::backward_node(int id) {
                                            cur_),
                   "layernorm_bwd_dx");
         pend(Profiler::LayerNorm, 0, double(n.rows) * n.cols * esize_ * (acc ? 4.0 : 3.0));
-        launches_ += 3;
+        launches_ += 2;
         return;
       }
       pbegin();

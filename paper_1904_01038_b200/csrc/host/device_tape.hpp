@@ -295,6 +295,8 @@ class DeviceTape {
   // making the main stream wait for it.
   std::pair<void*, const void*> acc_target(int id);
   void backward_node(int id);
+  std::vector<sfk_ln_fold_job> ln_folds_;  // LayerNorm gamma/beta folds not yet launched
+  void flush_ln_folds();
   void run_xent(Node& n, float seed, bool with_grad, double* stats_acc);
   void gemm(int cat, int m, int n, int k, const void* a, int64_t lda, bool a_kmajor, const void* b, int64_t ldb,
             bool b_kmajor, void* c, int64_t ldc, int flags, const void* bias = nullptr, const void* res = nullptr,

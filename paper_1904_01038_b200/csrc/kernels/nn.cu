@@ -358,6 +358,8 @@ int ln_dx_acc_vec(int, const void*, const void*, int, int, const void*, const fl
 int ln_dx_part_vec(int, const void*, const void*, int, int, const void*, const float*, void*, int, float*, int*,
                    cudaStream_t);
 int fold2_vec(int, const float*, int, int, void*, void*, cudaStream_t);
+int ln_gb_partial_vec(int, const void*, const void*, int, int, const float*, float*, int*, cudaStream_t);
+int ln_gb_fold_vec(int, const sfk_ln_fold_job*, int, cudaStream_t);
 int colred_launch(int, bool, const void*, const void*, const float*, int, int, int64_t, float*, int32_t*, void*, void*,
                   cudaStream_t);
 int xent_vec(int, void*, int, int, int64_t, const int32_t*, int, float, float, void*, float*, cudaStream_t);
@@ -397,6 +399,22 @@ extern "C" int sfk_layernorm_bwd_fold(int dtype, const float* part, int nparts, 
   if (nparts == 0) return SFK_OK;
   const int e = sfk::fold2_vec(dtype, part, nparts, d, dgamma, dbeta, sfk::as_stream(stream));
   if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_fold: needs 16-bit data");
+  return e;
+}
+
+extern "C" int sfk_layernorm_bwd_params_partial(int dtype, const void* x, const void* dy, int rows, int d,
+                                                const float* stats, float* part, int* nparts, void* stream) {
+  *nparts = 0;
+  if (rows == 0) return SFK_OK;
+  const int e = sfk::ln_gb_partial_vec(dtype, x, dy, rows, d, stats, part, nparts, sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_params_partial: needs 16-bit data, d % 8 == 0, d <= 1024");
+  return e;
+}
+
+extern "C" int sfk_layernorm_bwd_params_fold(int dtype, const sfk_ln_fold_job* jobs, int njobs, void* stream) {
+  const int e = sfk::ln_gb_fold_vec(dtype, jobs, njobs, sfk::as_stream(stream));
+  if (e == SFK_EUNSUP) sfk::set_error("sfk_layernorm_bwd_params_fold: needs 16-bit data");
+  if (e == SFK_EINVAL) sfk::set_error("sfk_layernorm_bwd_params_fold: too many jobs");
   return e;
 }
 

@@ -689,6 +689,112 @@ __global__ void __launch_bounds__(128) ln_dgb_partial_v(const T* __restrict__ x,
   *reinterpret_cast<float4*>(ob + 4) = make_float4(pb[4], pb[5], pb[6], pb[7]);
 }
 
+// LayerNorm gamma/beta partials: block b sums rows [b*rpb, (b+1)*rpb) of
+// dy*xhat (gamma) and dy (beta). Warp w takes rows w, w+8, ... two at a time
+// (all loads of both rows in flight), every lane keeps the column sums of its
+// d/256 16-byte chunks, and the 8 warp sums are combined in warp order through
+// shared memory into part[b][0|1][d]. Fixed association: deterministic.
+template <typename T>
+__global__ void __launch_bounds__(256) ln_gb_part_k(const T* __restrict__ x, const T* __restrict__ dy,
+                                                   const float2* __restrict__ stats, int rows, int d, int rpb,
+                                                   float* __restrict__ part) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  extern __shared__ float red[];  // [8][d]
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
+  float pg[kMaxCh][8], pb[kMaxCh][8];
+#pragma unroll
+  for (int i = 0; i < kMaxCh; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) pg[i][e] = pb[i][e] = 0.f;
+  for (int r = r0 + warp; r < r1; r += 16) {
+    const bool two = r + 8 < r1;
+    uint4 xu[2][kMaxCh], gu[2][kMaxCh];
+    float2 st[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (j == 1 && !two) break;
+      const int64_t row = r + 8 * j;
+      st[j] = stats[row];
+#pragma unroll
+      for (int i = 0; i < kMaxCh; ++i) {
+        const int c = (lane + 32 * i) * 8;
+        if (c < d) {
+          xu[j][i] = *reinterpret_cast<const uint4*>(x + row * d + c);
+          gu[j][i] = *reinterpret_cast<const uint4*>(dy + row * d + c);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (j == 1 && !two) break;
+#pragma unroll
+      for (int i = 0; i < kMaxCh; ++i) {
+        const int c = (lane + 32 * i) * 8;
+        if (c < d) {
+          float xh[8], gy[8];
+          V8<T>::unpack(xu[j][i], xh);
+          V8<T>::unpack(gu[j][i], gy);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            pg[i][e] += gy[e] * __fmul_rn(__fsub_rn(xh[e], st[j].x), st[j].y);
+            pb[i][e] += gy[e];
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+#pragma unroll
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+      if (c < d) {
+        float* o = red + warp * d + c;
+        const float(&src)[8] = v == 0 ? pg[i] : pb[i];
+        *reinterpret_cast<float4*>(o) = make_float4(src[0], src[1], src[2], src[3]);
+        *reinterpret_cast<float4*>(o + 4) = make_float4(src[4], src[5], src[6], src[7]);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w * d + c];
+      part[(int64_t(blockIdx.x) * 2 + v) * d + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// Batched fold of gamma/beta partials for many LayerNorm nodes: block
+// (chunk, vec, job) owns 256 columns of one vector of one job; each thread
+// sums its column over the job's partials in block order (eight loads in
+// flight), then out = q(out + sum).
+struct LnFoldBatch {
+  sfk_ln_fold_job job[SFK_LN_FOLD_MAX_JOBS];
+};
+template <typename T>
+__global__ void __launch_bounds__(256) ln_gb_fold_k(const __grid_constant__ LnFoldBatch B) {
+  SFK_PDL_WAIT();
+  SFK_PDL_LAUNCH();
+  const sfk_ln_fold_job& jb = B.job[blockIdx.z];
+  const int v = blockIdx.y, c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= jb.d) return;
+  const float* p = jb.part + int64_t(v) * jb.d + c;
+  const int64_t stride = int64_t(2) * jb.d;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int b = 0;
+  for (; b + 8 <= jb.nparts; b += 8)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += __ldcg(p + (b + u) * stride);
+  for (; b < jb.nparts; ++b) acc[0] += __ldcg(p + b * stride);
+  const float t = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  T* o = static_cast<T*>(v == 0 ? jb.dgamma : jb.dbeta) + c;
+  Num<T>::st(o, Num<T>::ld(o) + t);
+}
+
 // Fused label-smoothed cross entropy fwd+bwd for one vocabulary row per
 // block (tape.cpp:259-290, 481-502): the row is staged in shared memory with
 // 16-byte loads; pass 1 computes max / first argmax / sum-exp online,
@@ -1181,6 +1287,48 @@ int ln_dx_part_vec(int dtype, const void* x, const void* dy, int rows, int d, co
                static_cast<const __nv_bfloat16*>(dy), rows, d, static_cast<const __nv_bfloat16*>(g),
                reinterpret_cast<const float2*>(stats), static_cast<__nv_bfloat16*>(dx), accumulate, part, nblk);
   return check_launch("sfk_layernorm_bwd_dx_part(vec)");
+}
+
+int ln_gb_partial_vec(int dtype, const void* x, const void* dy, int rows, int d, const float* stats, float* part,
+                      int* nparts, cudaStream_t s) {
+  if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(dy)) return SFK_EUNSUP;
+  int nb = std::min(148, std::max(1, rows / 16));
+  const int rpb = (rows + nb - 1) / nb;
+  nb = (rows + rpb - 1) / rpb;
+  *nparts = nb;
+  const size_t smem = size_t(8) * d * sizeof(float);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(vec::ln_gb_part_k<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(vec::ln_gb_part_k<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cfg = true;
+  }
+  auto st = reinterpret_cast<const float2*>(stats);
+  if (dtype == SFK_F16)
+    launch_pdl(vec::ln_gb_part_k<__half>, dim3(nb), dim3(256), smem, s, static_cast<const __half*>(x),
+               static_cast<const __half*>(dy), st, rows, d, rpb, part);
+  else
+    launch_pdl(vec::ln_gb_part_k<__nv_bfloat16>, dim3(nb), dim3(256), smem, s, static_cast<const __nv_bfloat16*>(x),
+               static_cast<const __nv_bfloat16*>(dy), st, rows, d, rpb, part);
+  return check_launch("sfk_layernorm_bwd_params_partial");
+}
+
+int ln_gb_fold_vec(int dtype, const sfk_ln_fold_job* jobs, int njobs, cudaStream_t s) {
+  if (dtype == SFK_F32) return SFK_EUNSUP;
+  if (njobs <= 0) return SFK_OK;
+  if (njobs > SFK_LN_FOLD_MAX_JOBS) return SFK_EINVAL;
+  vec::LnFoldBatch B{};
+  int dmax = 0;
+  for (int j = 0; j < njobs; ++j) {
+    B.job[j] = jobs[j];
+    dmax = std::max(dmax, jobs[j].d);
+  }
+  const dim3 grid((dmax + 255) / 256, 2, njobs);
+  if (dtype == SFK_F16)
+    launch_pdl(vec::ln_gb_fold_k<__half>, grid, dim3(256), 0, s, B);
+  else
+    launch_pdl(vec::ln_gb_fold_k<__nv_bfloat16>, grid, dim3(256), 0, s, B);
+  return check_launch("sfk_layernorm_bwd_params_fold");
 }
 
 int fold2_vec(int dtype, const float* part, int nparts, int d, void* dgamma, void* dbeta, cudaStream_t s) {

@@ -575,3 +575,49 @@ def test_topk_raw_mode_for_sampling(dt, V, kk):
         order = sorted(range(V), key=lambda v: (-x[r, v], v))[:kk]
         assert tok[r].cpu().tolist() == order
         np.testing.assert_array_equal(lp[r].cpu().numpy(), x[r, order])
+
+
+class LnFoldJob(C.Structure):
+    _fields_ = [("part", C.c_void_p), ("dgamma", C.c_void_p), ("dbeta", C.c_void_p), ("nparts", C.c_int),
+                ("d", C.c_int)]
+
+
+@pytest.mark.parametrize("dt", [1, 2])
+def test_layernorm_params_partial_and_batched_fold_match_reference(dt):
+    """gamma/beta gradients as the trainer computes them: one partial pass per
+    LayerNorm node, then a single fold launch for several nodes (different
+    widths and row counts), each gradient accumulated q(old + sum) into a
+    non-zero buffer -- against the reference's layer_norm backward
+    (tape.cpp:383-418), summed over rows."""
+    lib = L()
+    rng = np.random.default_rng(11)
+    jobs, want, outs, keep = [], [], [], []
+    for rows, d in ((3584, 1024), (1234, 512), (37, 64), (900, 1024)):
+        x = ref.quantize_array((rng.standard_normal((rows, d)) * 2 + 0.5).astype(np.float32))
+        gm = ref.quantize_array((1 + 0.1 * rng.standard_normal(d)).astype(np.float32))
+        bt = ref.quantize_array((0.1 * rng.standard_normal(d)).astype(np.float32))
+        dy = ref.quantize_array(rng.standard_normal((rows, d)).astype(np.float32))
+        _, _, dg, db = ref.layer_norm(x, gm, bt, dy, False)
+        g0 = ref.quantize_array((0.5 * rng.standard_normal(d)).astype(np.float32))
+        b0 = ref.quantize_array((0.5 * rng.standard_normal(d)).astype(np.float32))
+        tx, tg, tb, tdy = (torch.tensor(a, device="cuda").to(TDT[dt]) for a in (x, gm, bt, dy))
+        ty, stats = torch.zeros_like(tx), torch.zeros(rows, 2, device="cuda")
+        lib.check(lib.sfk_layernorm_fwd(dt, ptr(tx), rows, d, ptr(tg), ptr(tb), ptr(ty), ptr(stats), stream()), True)
+        part = torch.full((2 * 148 * d,), float("nan"), device="cuda")
+        npart = C.c_int()
+        lib.check(lib.sfk_layernorm_bwd_params_partial(dt, ptr(tx), ptr(tdy), rows, d, ptr(stats), ptr(part),
+                                                       C.byref(npart), stream()), True)
+        assert 1 <= npart.value <= 148
+        og, ob = torch.tensor(g0, device="cuda").to(TDT[dt]), torch.tensor(b0, device="cuda").to(TDT[dt])
+        jobs.append(LnFoldJob(part.data_ptr(), og.data_ptr(), ob.data_ptr(), npart.value, d))
+        want.append((g0.astype(np.float64) + dg, b0.astype(np.float64) + db))
+        outs.append((og, ob))
+        keep += [tx, tdy, stats, part]
+    arr = (LnFoldJob * len(jobs))(*jobs)
+    lib.check(lib.sfk_layernorm_bwd_params_fold(dt, arr, len(jobs), stream()), True)
+    torch.cuda.synchronize()
+    rt = 4e-3 if dt == 1 else 1.6e-2
+    for (og, ob), (wg, wb), j in zip(outs, want, jobs):
+        sc = np.sqrt(j.nparts * 1.0)
+        np.testing.assert_allclose(og.float().cpu().numpy(), wg, rtol=rt, atol=rt * 10 * sc)
+        np.testing.assert_allclose(ob.float().cpu().numpy(), wb, rtol=rt, atol=rt * 10 * sc)

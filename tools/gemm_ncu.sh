@@ -7,6 +7,7 @@ for spec in ${2:-"big8k:256:1 fwd_ffn1:256:1 fwd_out:256:1"}; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 3 -c 1 -o $O/${name}_$tile_$pair \
     python tools/gemm_one.py $name $tile $pair > $O/${name}.log 2>&1
   ncu -i $O/${name}_$tile_$pair.ncu-rep --page raw --csv > $O/${name}.raw.csv 2>/dev/null
+  rm -f $O/${name}_$tile_$pair.ncu-rep
   python - "$O/${name}.raw.csv" "$name" <<'PY'
 import csv, sys
 rows = list(csv.reader(open(sys.argv[1])))

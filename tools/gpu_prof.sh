@@ -10,6 +10,7 @@ for ks in $KS; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:"^$k\$" -s $s -c 2 -o $O/$k \
     python tools/step_once.py --accum 2 --warmup 1 > $O/$k.log 2>&1
   ncu -i $O/$k.ncu-rep --page raw --csv > $O/$k.raw.csv 2>/dev/null
+  ncu -i $O/$k.ncu-rep --page source --csv > $O/$k.source.csv 2>/dev/null; rm -f $O/$k.ncu-rep
   python tools/ncu_summary.py $O/$k.raw.csv >> $O/summary.txt 2>&1
 done
 cat $O/summary.txt
