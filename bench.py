@@ -141,9 +141,10 @@ def reference_sample(cfg, threads, max_tokens, steps, warmup):
     each running train_one on its own batch stream of the same synthetic workload."""
     os.environ["SEQFORGE_LOG"] = "quiet"  # the reference warns per oversized singleton
     from oracle import ref
-    import paper_1904_01038_b200 as sqf
     V = cfg["vocab"]
-    corpus = sqf.synthetic_corpus(4000, V, V, 1.1, 1)
+    # the same corpus as the GPU arm, drawn through the reference's own RngStream
+    # (the product library is never loaded on this arm)
+    corpus = ref.synthetic_corpus(4000, V, V, 1.1, 1)
     ov = {"max_tokens": max_tokens, "fp16": cfg["prec"] == "fp16", "seed": 1, "max_epochs": 1000}
     trainers = [None] * threads
 
@@ -183,6 +184,19 @@ def ref_threads():
     return max(1, min(n, int(os.environ.get("SQF_REF_THREADS", "8"))))
 
 
+def host_cpu():
+    """(CPU model, logical CPUs) of the box the reference arm runs on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
 def run_reference_arm(args, cfg):
     rank, world, _ = dist_setup()
     if rank != 0:
@@ -198,7 +212,7 @@ def run_reference_arm(args, cfg):
             "impl": "reference",
             "config": {"workload": cfg["desc"] + f" (CPU sample at max_tokens {mt})", "arch": cfg["arch"]},
             "cpu_baseline": {"value": value, "unit": "tgt_tokens/s", "cores": thr, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": host_cpu()[0], "nproc": host_cpu()[1]},
             "e2e": {"value": value, "unit": "tgt_tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -226,10 +240,14 @@ def run_ours(args, cfg):
     corpus = sqf.synthetic_corpus(npairs, V, V, 1.1, 1)
     ov = {"max_tokens": cfg["max_tokens"], "accum": cfg["accum"], "workers": world, "dispatch": "deal",
           "fp16": cfg["prec"] == "fp16", "bf16": cfg["prec"] == "bf16", "seed": 1, "max_epochs": 1000,
-          "warmup": 4000, "lr": 5e-4, "bucket_threshold": 1 << 23, "overlap_allreduce": not args.no_overlap,
-          # gradients are un-normalised token sums in fp16 until after the all-reduce
-          # (trainer.cpp:264-265); at ~57k tokens per update the scale settles near 1
-          "fp16_init_scale": 1.0, "fp16_min_scale": 2.0 ** -14}
+          "warmup": 4000, "lr": 5e-4, "bucket_threshold": 1 << 23, "overlap_allreduce": not args.no_overlap}
+    # The reference's scaler defaults (128 / window 256 / floor 2^-5,
+    # registry.cpp:205-208) unless overridden: gradients are un-normalised token
+    # sums until after the all-reduce (trainer.cpp:264-265), so at ~51k tokens
+    # per update the warm-up skips a few steps while the scale settles.
+    if args.fp16_init_scale:
+        ov["fp16_init_scale"] = args.fp16_init_scale
+        ov["fp16_min_scale"] = 2.0 ** -14
     tr = sqf.Trainer(cfg["arch"], ov, corpus=corpus, src_vocab=V, tgt_vocab=V, rank=rank, world=world,
                      nccl_id=nccl_id)
     # warm-up: at least W steps, and until the dynamic loss scale has settled
@@ -298,7 +316,8 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["desc"], "arch": cfg["arch"], "max_tokens_per_gpu": cfg["max_tokens"],
                    "update_freq": cfg["accum"], "dispatch": "deal", "global_batch_tokens": tokens // args.steps,
                    "parallelism": f"dp{world}", "l2": "inputs > L2 (weights+grads+Adam state+activations, GBs)",
-                   "skipped_steps": skipped,
+                   "skipped_steps": skipped, "loss_scale": tr.scaler()[0] if cfg["prec"] == "fp16" else None,
+                   "warmup_steps_run": done,
                    "allreduce": ("bucketed NCCL, overlapped with the last backward" if not args.no_overlap
                                  else "bucketed NCCL after backward") if world > 1 else "none (1 GPU)"},
         "e2e": {"value": e2e, "unit": "tgt_tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 36},
@@ -321,6 +340,7 @@ def run_ours(args, cfg):
             v, tok, sec = reference_sample(cfg, thr, args.ref_max_tokens, 1, 0)
             line["cpu_baseline"] = {
                 "value": v, "unit": "tgt_tokens/s", "cores": thr, "kind": "reference",
+                "cpu_model": host_cpu()[0], "nproc": host_cpu()[1],
                 "sample": f"{thr} threads x 1 train_one of {cfg['arch']} at max_tokens={args.ref_max_tokens} "
                           f"({tok} target tokens, {sec:.1f} s) with the reference built from its sources"}
         except Exception as ex:  # the GPU number stands on its own
@@ -362,6 +382,8 @@ def main():
     ap.add_argument("--no-overlap", action="store_true", help="all-reduce after backward (C5 'overlap off')")
     ap.add_argument("--max-tokens", type=int, default=0, help="per-GPU token budget override (C5 sweep)")
     ap.add_argument("--accum", type=int, default=0, help="update_freq override")
+    ap.add_argument("--fp16-init-scale", type=float, default=0.0,
+                    help="start the loss scale here (and lower its floor to 2^-14) instead of the reference defaults")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.max_tokens:

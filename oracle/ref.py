@@ -77,6 +77,7 @@ def _declare(L):
     s("sqfref_rng_below", None, u64, u64, u64, u64, C.c_int, vp)
     s("sqfref_positional_row", None, C.c_int, C.c_int, vp)
     s("sqfref_corpus_create", vp, C.c_int, vp, vp, vp, vp)
+    s("sqfref_synthetic_corpus", C.c_int, C.c_int, C.c_int, C.c_int, f64, u64, u64, vp, vp, vp, vp, vp, vp)
     s("sqfref_corpus_free", None, vp)
     s("sqfref_make_batches", C.c_int, vp, i64, C.c_int, u64, P(i32), vp, vp)
     s("sqfref_shuffle_epoch", C.c_int, C.c_int, u64, C.c_int, vp)
@@ -128,6 +129,28 @@ def _ck(status):
     if status < 0:
         raise RefError(f"reference error {status}: {lib().sqfref_last_error().decode()}")
     return status
+
+
+class OracleCorpus:
+    """A corpus with the product Corpus's fields (src_len, tgt_len, src_ids,
+    tgt_ids, npairs), generated without the product library."""
+
+    def __init__(self, sl, tl, si, ti):
+        self.src_len, self.tgt_len, self.src_ids, self.tgt_ids = sl, tl, si, ti
+        self.npairs = len(sl)
+
+
+def synthetic_corpus(npairs, src_vocab, tgt_vocab, zipf_s=1.1, seed=1, stream=4242):
+    """SURVEY §8(d) generator on the reference's RngStream (ref_capi.cpp); equal
+    to paper_1904_01038_b200.synthetic_corpus (tests/test_boundary.py)."""
+    sl, tl = np.zeros(npairs, np.int32), np.zeros(npairs, np.int32)
+    st, tt = C.c_int64(), C.c_int64()
+    _ck(lib().sqfref_synthetic_corpus(npairs, src_vocab, tgt_vocab, zipf_s, seed, stream, _ptr(sl), _ptr(tl), None,
+                                      None, C.byref(st), C.byref(tt)))
+    si, ti = np.zeros(max(st.value, 1), np.int32), np.zeros(max(tt.value, 1), np.int32)
+    _ck(lib().sqfref_synthetic_corpus(npairs, src_vocab, tgt_vocab, zipf_s, seed, stream, _ptr(sl), _ptr(tl),
+                                      _ptr(si), _ptr(ti), C.byref(st), C.byref(tt)))
+    return OracleCorpus(sl, tl, si[:st.value], ti[:tt.value])
 
 
 class RefCorpus:

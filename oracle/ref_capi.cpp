@@ -1,3 +1,5 @@
+#include <algorithm>
+#include <cmath>
 // TEST INFRASTRUCTURE ONLY — never linked into, loaded by or called from the
 // product path. This file is a thin C-ABI shim over the *unmodified* C++
 // reference (seqforge, /root/reference/proj) so Python tests can use the
@@ -202,6 +204,54 @@ void* sqfref_corpus_create(int npairs, const int32_t* src_len, const int32_t* tg
   return c;
 }
 void sqfref_corpus_free(void* c) { delete static_cast<Corpus*>(c); }
+
+// The synthetic WMT-shaped corpus of SURVEY §8(d) (the benchmark's input
+// specification, not reference code) drawn from the reference's own RngStream,
+// so the CPU reference arm never loads the product library: lengths
+// clamp(round(exp(3.1 + 0.6 z)), 1, 200) and clamp(round(ls (1 + 0.1 z')), 1, 200),
+// ids by inverse CDF of Zipf(s) over [4, V), eos appended. Two-pass like the
+// product call: ids == NULL only reports the lengths and totals.
+int sqfref_synthetic_corpus(int npairs, int src_vocab, int tgt_vocab, double zipf_s, uint64_t seed,
+                            uint64_t stream, int32_t* src_len, int32_t* tgt_len, int32_t* src_ids, int32_t* tgt_ids,
+                            int64_t* src_total, int64_t* tgt_total) {
+  if (npairs < 0 || src_vocab <= 4 || tgt_vocab <= 4) return -1;
+  auto cdf_of = [&](int vocab) {
+    std::vector<double> c(static_cast<size_t>(vocab - 4));
+    double run = 0.0;
+    for (size_t k = 0; k < c.size(); ++k) c[k] = run += zipf_s > 0 ? std::pow(double(k + 1), -zipf_s) : 1.0;
+    for (double& x : c) x /= run;
+    return c;
+  };
+  const std::vector<double> sc = cdf_of(src_vocab), tc = cdf_of(tgt_vocab);
+  RngStream rng(seed, stream);
+  auto id_of = [&](const std::vector<double>& c) {
+    const size_t k = size_t(std::upper_bound(c.begin(), c.end(), rng.next_double()) - c.begin());
+    return int32_t(4 + std::min(k, c.size() - 1));
+  };
+  auto len_of = [](double x) { return int32_t(std::clamp(std::round(x), 1.0, 200.0)); };
+  int64_t so = 0, to = 0;
+  for (int i = 0; i < npairs; ++i) {
+    const int32_t ls = len_of(std::exp(3.1 + 0.6 * rng.next_normal()));
+    const int32_t lt = len_of(double(ls) * (1.0 + 0.1 * rng.next_normal()));
+    src_len[i] = ls + 1;
+    tgt_len[i] = lt + 1;
+    for (int32_t j = 0; j < ls; ++j) {
+      const int32_t t = id_of(sc);
+      if (src_ids) src_ids[so + j] = t;
+    }
+    for (int32_t j = 0; j < lt; ++j) {
+      const int32_t t = id_of(tc);
+      if (tgt_ids) tgt_ids[to + j] = t;
+    }
+    if (src_ids) src_ids[so + ls] = 2;  // eos
+    if (tgt_ids) tgt_ids[to + lt] = 2;
+    so += ls + 1;
+    to += lt + 1;
+  }
+  *src_total = so;
+  *tgt_total = to;
+  return 0;
+}
 
 // make_batches (data.cpp:115-161): returns batch count; sizes/members are
 // written into caller buffers of capacity npairs.

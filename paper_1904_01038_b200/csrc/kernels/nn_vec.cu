@@ -689,28 +689,30 @@ __global__ void __launch_bounds__(128) ln_dgb_partial_v(const T* __restrict__ x,
   *reinterpret_cast<float4*>(ob + 4) = make_float4(pb[4], pb[5], pb[6], pb[7]);
 }
 
-// LayerNorm gamma/beta partials: block b sums rows [b*rpb, (b+1)*rpb) of
-// dy*xhat (gamma) and dy (beta). Warp w takes rows w, w+8, ... two at a time
-// (all loads of both rows in flight), every lane keeps the column sums of its
-// d/256 16-byte chunks, and the 8 warp sums are combined in warp order through
-// shared memory into part[b][0|1][d]. Fixed association: deterministic.
+// LayerNorm gamma/beta partials: block (b, s) sums rows [b*rpb, (b+1)*rpb) of
+// dy*xhat (gamma) and dy (beta) over the 512-column slice s. Warp w takes rows
+// w, w+8, ... two at a time (all loads of both rows in flight), every lane keeps
+// the column sums of its two 16-byte chunks, and the 8 warp sums are combined
+// in warp order through shared memory into part[b][0|1][d]. Fixed
+// association: deterministic.
+constexpr int kGbCh = 2;  // 16-byte chunks per lane: 32 lanes x 2 x 8 = 512 columns
 template <typename T>
 __global__ void __launch_bounds__(256) ln_gb_part_k(const T* __restrict__ x, const T* __restrict__ dy,
                                                    const float2* __restrict__ stats, int rows, int d, int rpb,
                                                    float* __restrict__ part) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
-  extern __shared__ float red[];  // [8][d]
+  __shared__ __align__(16) float red[8][512];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
-  float pg[kMaxCh][8], pb[kMaxCh][8];
+  const int r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb), c0 = blockIdx.y * 512;
+  float pg[kGbCh][8], pb[kGbCh][8];
 #pragma unroll
-  for (int i = 0; i < kMaxCh; ++i)
+  for (int i = 0; i < kGbCh; ++i)
 #pragma unroll
     for (int e = 0; e < 8; ++e) pg[i][e] = pb[i][e] = 0.f;
   for (int r = r0 + warp; r < r1; r += 16) {
     const bool two = r + 8 < r1;
-    uint4 xu[2][kMaxCh], gu[2][kMaxCh];
+    uint4 xu[2][kGbCh], gu[2][kGbCh];
     float2 st[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -718,8 +720,8 @@ __global__ void __launch_bounds__(256) ln_gb_part_k(const T* __restrict__ x, con
       const int64_t row = r + 8 * j;
       st[j] = stats[row];
 #pragma unroll
-      for (int i = 0; i < kMaxCh; ++i) {
-        const int c = (lane + 32 * i) * 8;
+      for (int i = 0; i < kGbCh; ++i) {
+        const int c = c0 + (lane + 32 * i) * 8;
         if (c < d) {
           xu[j][i] = *reinterpret_cast<const uint4*>(x + row * d + c);
           gu[j][i] = *reinterpret_cast<const uint4*>(dy + row * d + c);
@@ -730,8 +732,8 @@ __global__ void __launch_bounds__(256) ln_gb_part_k(const T* __restrict__ x, con
     for (int j = 0; j < 2; ++j) {
       if (j == 1 && !two) break;
 #pragma unroll
-      for (int i = 0; i < kMaxCh; ++i) {
-        const int c = (lane + 32 * i) * 8;
+      for (int i = 0; i < kGbCh; ++i) {
+        const int c = c0 + (lane + 32 * i) * 8;
         if (c < d) {
           float xh[8], gy[8];
           V8<T>::unpack(xu[j][i], xh);
@@ -745,33 +747,35 @@ __global__ void __launch_bounds__(256) ln_gb_part_k(const T* __restrict__ x, con
       }
     }
   }
+  const int width = min(512, d - c0);
 #pragma unroll
   for (int v = 0; v < 2; ++v) {
 #pragma unroll
-    for (int i = 0; i < kMaxCh; ++i) {
-      const int c = (lane + 32 * i) * 8;
-      if (c < d) {
-        float* o = red + warp * d + c;
+    for (int i = 0; i < kGbCh; ++i) {
+      const int cl = (lane + 32 * i) * 8;
+      if (cl < width) {
+        float* o = &red[warp][cl];
         const float(&src)[8] = v == 0 ? pg[i] : pb[i];
         *reinterpret_cast<float4*>(o) = make_float4(src[0], src[1], src[2], src[3]);
         *reinterpret_cast<float4*>(o + 4) = make_float4(src[4], src[5], src[6], src[7]);
       }
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    for (int cl = threadIdx.x; cl < width; cl += blockDim.x) {
       float t = 0.f;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) t += red[w * d + c];
-      part[(int64_t(blockIdx.x) * 2 + v) * d + c] = t;
+      for (int w = 0; w < 8; ++w) t += red[w][cl];
+      part[(int64_t(blockIdx.x) * 2 + v) * d + c0 + cl] = t;
     }
     __syncthreads();
   }
 }
 
-// Batched fold of gamma/beta partials for many LayerNorm nodes: block
-// (chunk, vec, job) owns 256 columns of one vector of one job; each thread
-// sums its column over the job's partials in block order (eight loads in
-// flight), then out = q(out + sum).
+// Batched fold of gamma/beta partials for many LayerNorm nodes. Block
+// (chunk, vec, job) owns 32 columns of one vector of one job; warp w sums the
+// contiguous partial range [w*P/8, (w+1)*P/8) for its lane's column (all loads
+// independent), the 8 warp sums are added in warp order, then
+// out = q(out + sum). Fixed association: deterministic.
 struct LnFoldBatch {
   sfk_ln_fold_job job[SFK_LN_FOLD_MAX_JOBS];
 };
@@ -779,20 +783,33 @@ template <typename T>
 __global__ void __launch_bounds__(256) ln_gb_fold_k(const __grid_constant__ LnFoldBatch B) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
+  __shared__ float red[8][32];
   const sfk_ln_fold_job& jb = B.job[blockIdx.z];
-  const int v = blockIdx.y, c = blockIdx.x * 256 + threadIdx.x;
-  if (c >= jb.d) return;
-  const float* p = jb.part + int64_t(v) * jb.d + c;
-  const int64_t stride = int64_t(2) * jb.d;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int b = 0;
-  for (; b + 8 <= jb.nparts; b += 8)
+  const int v = blockIdx.y, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c = blockIdx.x * 32 + lane;
+  if (blockIdx.x * 32 >= jb.d) return;
+  const int p0 = warp * jb.nparts / 8, p1 = (warp + 1) * jb.nparts / 8;
+  float acc = 0.f;
+  if (c < jb.d) {
+    const float* p = jb.part + int64_t(v) * jb.d + c;
+    const int64_t stride = int64_t(2) * jb.d;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    int q = p0;
+    for (; q + 4 <= p1; q += 4)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] += __ldcg(p + (b + u) * stride);
-  for (; b < jb.nparts; ++b) acc[0] += __ldcg(p + b * stride);
-  const float t = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-  T* o = static_cast<T*>(v == 0 ? jb.dgamma : jb.dbeta) + c;
-  Num<T>::st(o, Num<T>::ld(o) + t);
+      for (int u = 0; u < 4; ++u) a[u] += __ldcg(p + (q + u) * stride);
+    for (; q < p1; ++q) a[0] += __ldcg(p + q * stride);
+    acc = (a[0] + a[1]) + (a[2] + a[3]);
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && c < jb.d) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    T* o = static_cast<T*>(v == 0 ? jb.dgamma : jb.dbeta) + c;
+    Num<T>::st(o, Num<T>::ld(o) + t);
+  }
 }
 
 // Fused label-smoothed cross entropy fwd+bwd for one vocabulary row per
@@ -1296,19 +1313,13 @@ int ln_gb_partial_vec(int dtype, const void* x, const void* dy, int rows, int d,
   const int rpb = (rows + nb - 1) / nb;
   nb = (rows + rpb - 1) / rpb;
   *nparts = nb;
-  const size_t smem = size_t(8) * d * sizeof(float);
-  static bool cfg = false;
-  if (!cfg) {
-    cudaFuncSetAttribute(vec::ln_gb_part_k<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cudaFuncSetAttribute(vec::ln_gb_part_k<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    cfg = true;
-  }
+  const dim3 grid(nb, (d + 511) / 512);
   auto st = reinterpret_cast<const float2*>(stats);
   if (dtype == SFK_F16)
-    launch_pdl(vec::ln_gb_part_k<__half>, dim3(nb), dim3(256), smem, s, static_cast<const __half*>(x),
+    launch_pdl(vec::ln_gb_part_k<__half>, grid, dim3(256), 0, s, static_cast<const __half*>(x),
                static_cast<const __half*>(dy), st, rows, d, rpb, part);
   else
-    launch_pdl(vec::ln_gb_part_k<__nv_bfloat16>, dim3(nb), dim3(256), smem, s, static_cast<const __nv_bfloat16*>(x),
+    launch_pdl(vec::ln_gb_part_k<__nv_bfloat16>, grid, dim3(256), 0, s, static_cast<const __nv_bfloat16*>(x),
                static_cast<const __nv_bfloat16*>(dy), st, rows, d, rpb, part);
   return check_launch("sfk_layernorm_bwd_params_partial");
 }
@@ -1323,7 +1334,7 @@ int ln_gb_fold_vec(int dtype, const sfk_ln_fold_job* jobs, int njobs, cudaStream
     B.job[j] = jobs[j];
     dmax = std::max(dmax, jobs[j].d);
   }
-  const dim3 grid((dmax + 255) / 256, 2, njobs);
+  const dim3 grid((dmax + 31) / 32, 2, njobs);
   if (dtype == SFK_F16)
     launch_pdl(vec::ln_gb_fold_k<__half>, grid, dim3(256), 0, s, B);
   else

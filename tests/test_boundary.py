@@ -141,3 +141,14 @@ def test_registry_errors_surface_as_reference_classes():
     with pytest.raises(sqf.NativeError) as e:
         sqf.model_init("tiny_transformer", {"nonexistent_key": 1})
     assert e.value.kind == "ConfigError"
+
+
+def test_oracle_side_corpus_equals_product_corpus():
+    """The bench's CPU reference arm builds its corpus from the oracle
+    (reference RngStream) without loading the product library: it must be the
+    product's synthetic corpus, id for id."""
+    for npairs, sv, tv, s in ((500, 1000, 1000, 1.1), (300, 32768, 32768, 1.1), (50, 10000, 8000, 0.0)):
+        a = sqf.synthetic_corpus(npairs, sv, tv, s, 1)
+        b = ref.synthetic_corpus(npairs, sv, tv, s, 1)
+        for f in ("src_len", "tgt_len", "src_ids", "tgt_ids"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
