@@ -94,14 +94,20 @@ __device__ __forceinline__ void load_b_kn(uint32_t (&b)[4], const T* s, int ld, 
 // stage_wait() + __syncthreads().
 template <typename T, int DH>
 __device__ __forceinline__ void stage(T* s, int lds, const T* g, int64_t ldg, int r0, int n, int rows_pad, int dh) {
-  constexpr int V = 8;  // 16-byte vectors
-  const int vpr = DH / V;
-  for (int i = threadIdx.x; i < rows_pad * vpr; i += blockDim.x) {
-    const int r = i / vpr, c = (i % vpr) * V;
-    const bool ok = r < n && c < dh;
-    const T* src = ok ? g + int64_t(r0 + r) * ldg + c : g;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(s + r * lds + c)), "l"(src),
-                 "r"(ok ? 16 : 0)
+  // thread t always copies 16-byte column chunk t % VPR of rows t / VPR,
+  // t / VPR + step, ...: pointers advance by a constant (no per-chunk index math)
+  constexpr int VPR = DH / 8;
+  const int step = int(blockDim.x) / VPR;  // blockDim.x is a multiple of VPR (64/128 threads, VPR <= 16)
+  const int c = (int(threadIdx.x) % VPR) * 8;
+  int r = int(threadIdx.x) / VPR;
+  const bool cok = c < dh;
+  const T* src = g + int64_t(r0 + r) * ldg + c;
+  const int64_t sstep = int64_t(step) * ldg;
+  uint32_t dst = su32(s + r * lds + c);
+  const uint32_t dstep = uint32_t(step * lds * int(sizeof(T)));
+  for (; r < rows_pad; r += step, src += sstep, dst += dstep) {
+    const bool ok = cok && r < n;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(ok ? src : g), "r"(ok ? 16 : 0)
                  : "memory");
   }
 }
@@ -233,15 +239,26 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
   l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
   const float ia = 1.0f / l_a, ib = 1.0f / l_b;
-  T* out = static_cast<T*>(a.out) + h * a.dh;
+  // the warp's Q rows are consumed (fragments are in registers): stage its
+  // 16 x DH output there and write whole 16-byte row chunks
+  T* Os = Qs + r0 * LD;
 #pragma unroll
   for (int nt = 0; nt < DH / 8; ++nt) {
     const int c = nt * 8 + 2 * tq;
-    if (c >= a.dh) continue;
-    if (row_a < a.qw)
-      *reinterpret_cast<uint32_t*>(out + (qrow0 + row_a) * a.ldout + c) = MmaT<T>::pack(o[nt][0] * ia, o[nt][1] * ia);
-    if (row_b < a.qw)
-      *reinterpret_cast<uint32_t*>(out + (qrow0 + row_b) * a.ldout + c) = MmaT<T>::pack(o[nt][2] * ib, o[nt][3] * ib);
+    *reinterpret_cast<uint32_t*>(Os + g * LD + c) = MmaT<T>::pack(o[nt][0] * ia, o[nt][1] * ia);
+    *reinterpret_cast<uint32_t*>(Os + (g + 8) * LD + c) = MmaT<T>::pack(o[nt][2] * ib, o[nt][3] * ib);
+  }
+  __syncwarp();
+  {
+    T* out = static_cast<T*>(a.out) + h * a.dh;
+    constexpr int VPR = DH / 8;
+#pragma unroll
+    for (int k = 0; k < 16 * VPR / 32; ++k) {
+      const int idx = k * 32 + lane, rr = idx / VPR, cc = (idx % VPR) * 8;
+      const int row = q0 + r0 + rr;
+      if (row < a.qw && cc < a.dh)
+        *reinterpret_cast<uint4*>(out + (qrow0 + row) * a.ldout + cc) = *reinterpret_cast<const uint4*>(Os + rr * LD + cc);
+    }
   }
   if (tq == 0) {  // max back in natural units (the saved-stats contract)
     const float ln2 = 0.6931471805599453f;
