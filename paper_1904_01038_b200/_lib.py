@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsqf_b200.so")
+LIB_PATH = os.environ.get("SQF_LIB") or os.path.join(_HERE, "_lib", "libsqf_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -116,6 +116,7 @@ sqf_trainer_create_host_collective = _sig("sqf_trainer_create_host_collective", 
                                           HOST_ALLREDUCE_FN, vp)
 sqf_trainer_collective = _sig("sqf_trainer_collective", cp, vp)
 sqf_trainer_free = _sig("sqf_trainer_free", None, vp)
+sfk_debug_gemm_trace = _sig("sfk_debug_gemm_trace", C.c_int, vp)
 sqf_trainer_train_one = _sig("sqf_trainer_train_one", C.c_int, vp, P(StepStats))
 sqf_trainer_train_step = _sig("sqf_trainer_train_step", C.c_int, vp, vp, vp, P(StepStats))
 sqf_trainer_evaluate = _sig("sqf_trainer_evaluate", C.c_int, vp, vp, C.c_int, P(f64), P(f64), P(i64), P(i64))

@@ -103,6 +103,20 @@ __global__ void __launch_bounds__(256) gemm_simt(const T* __restrict__ a, int64_
 // ------------------------------------------------------------------ tcgen05
 namespace tc {
 constexpr int BM = 128, BK = 64;
+
+// Debug timeline of one pair-GEMM launch (SFK_GEMM_TRACE builds only):
+// %globaltimer (ns) at fixed points of CTA 0 and of the last CTA.
+#ifdef SFK_GEMM_TRACE
+__device__ unsigned long long g_trace[2][12];
+__device__ __forceinline__ void trace(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (blockIdx.x == 0) g_trace[0][slot] = t;
+  if (blockIdx.x == gridDim.x - 1) g_trace[1][slot] = t;
+}
+#else
+__device__ __forceinline__ void trace(int) {}
+#endif
 constexpr int kEpiWarps = 8, kThreads = 64 + 32 * kEpiWarps;  // producer, MMA, 8 epilogue warps
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
@@ -856,6 +870,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) trace(0);  // entry
   if (threadIdx.x == 32) {  // pull both TMA descriptors in while the prologue runs
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
@@ -882,8 +897,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace(1);  // prologue done (barriers, TMEM, cluster sync)
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
+  if (threadIdx.x == 0) trace(2);  // predecessor complete
 
   const int num_m = (M + PM - 1) / PM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
@@ -908,6 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (btile) bias_pend |= 1u << s;
           if (leader) mbar_expect_tx(&full[s], 2 * C::STAGE);
+          if (it == 0) trace(3);  // first TMA issued
           const uint32_t lbar = saddr(&full[s]) & 0xFEFFFFFFu;  // the leader CTA's barrier
           uint8_t* a_dst = smem + s * C::STAGE;
           uint8_t* b_dst = a_dst + C::A_BYTES;
@@ -942,6 +960,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % C::STAGES;
           mbar_wait(&full[s], (it / C::STAGES) & 1);
           fence_after();
+          if (it == 0) trace(4);  // first stage landed
           const uint32_t a_addr = saddr(smem + s * C::STAGE);
           const uint32_t b_addr = a_addr + C::A_BYTES;
 #pragma unroll
@@ -953,6 +972,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit_pair(&empty[s]);
         }
         umma_commit_pair(&tfull[buf]);
+        trace(5);  // last MMA of a tile issued
       }
     }
   } else {
@@ -970,7 +990,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       it += kblocks;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
+      if (threadIdx.x == 64) trace(6);  // accumulators ready
       epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
+      if (threadIdx.x == 64) trace(7);  // epilogue of this warp done
       fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -981,11 +1003,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace(8);  // all warps done
   cluster_sync();
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS));
   }
+  if (threadIdx.x == 32) trace(9);  // TMEM released
 }
 
 // ---------------------------------------------------------------- host side
@@ -1179,6 +1203,16 @@ int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) 
 }  // namespace tc
 
 }  // namespace sfk
+
+// debug builds (SFK_GEMM_TRACE): the last pair-GEMM launch's timeline, 2 x 12 ns stamps
+extern "C" int sfk_debug_gemm_trace(unsigned long long* out) {
+#ifdef SFK_GEMM_TRACE
+  return cudaMemcpyFromSymbol(out, sfk::tc::g_trace, sizeof(sfk::tc::g_trace)) == cudaSuccess ? SFK_OK : SFK_EINVAL;
+#else
+  (void)out;
+  return SFK_EUNSUP;
+#endif
+}
 
 extern "C" int sfk_gemm(const sfk_gemm_args* g, void* stream) {
   using namespace sfk;

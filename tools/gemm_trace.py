@@ -1,0 +1,39 @@
+"""Device timeline of single pair-GEMM launches (trace build: SQF_LIB=.../trace/libsqf_b200.so):
+%globaltimer stamps of CTA 0 and the last CTA relative to CTA 0's entry."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1904_01038_b200 import _lib as L  # noqa: E402
+
+NAMES = ["entry", "prologue", "pdl_wait", "tma0", "stage0", "mma_end", "acc_ready", "epi_done", "all_done", "tmem_free"]
+
+
+def trace(m, n, k, prev=None):
+    dt = torch.float16
+    a = torch.randn(m * k, device="cuda").to(dt)
+    b = torch.randn(n * k, device="cuda").to(dt)
+    c = torch.zeros(m * n, device="cuda").to(dt)
+    args = L.GemmArgs(m=m, n=n, k=k, dtype=1, a=a.data_ptr(), lda=k, a_kmajor=1, b=b.data_ptr(), ldb=k, b_kmajor=1,
+                      c=c.data_ptr(), ldc=n, flags=0, tile_n=256, pair=1)
+    st = torch.cuda.current_stream()
+    for rep in range(3):
+        L.check(L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream)), True)
+        L.check(L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream)), True)  # back to back: the second is traced
+        torch.cuda.synchronize()
+    out = np.zeros(24, np.uint64)
+    L.check(L.sfk_debug_gemm_trace(out.ctypes.data), True)
+    t = out.reshape(2, 12).astype(np.int64)
+    base = t[0, 0]
+    print(f"M={m} N={n} K={k}")
+    for r, who in enumerate(("cta0", "last")):
+        print("  " + who + ": " + " ".join(f"{NAMES[i]}={(t[r, i] - base) / 1e3:.2f}" for i in range(10)))
+
+
+for n, k in ((1024, 512), (1024, 1024), (1024, 4096), (4096, 1024)):
+    trace(3584, n, k)
