@@ -107,7 +107,7 @@ constexpr int BM = 128, BK = 64;
 // Debug timeline of one pair-GEMM launch (SFK_GEMM_TRACE builds only):
 // %globaltimer (ns) at fixed points of CTA 0 and of the last CTA.
 #ifdef SFK_GEMM_TRACE
-__device__ unsigned long long g_trace[2][12];
+__device__ unsigned long long g_trace[2][24];
 __device__ __forceinline__ void trace(int slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -439,6 +439,147 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, int w
     }
     __syncwarp();
   }
+}
+
+// ------------------------------------------------- epilogue with TMA stores
+// Each thread owns one accumulator row (its TMEM lane): it loads that row's
+// side inputs for a 32-column chunk directly (bias is a warp-wide broadcast),
+// applies the fused epilogue, packs to 16 bits and writes the 64-byte row
+// segment into the warp's 128B-swizzled 32 x 64 staging tile; one lane then
+// stores the whole tile with a TMA bulk store (out-of-range rows/columns are
+// clipped by the tensor map). No per-element global stores, no transpose
+// through shared memory. FL >= 0: the epilogue flags are compile-time.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 8 16-bit values at p[col..col+8) of a row, bounds-checked against n (rare slow path at the right edge)
+template <typename T>
+__device__ __forceinline__ uint4 ld_row8(const T* p, int col, int n, bool ok) {
+  if (!ok) return make_uint4(0, 0, 0, 0);
+  if (col + 8 <= n) return *reinterpret_cast<const uint4*>(p + col);
+  uint16_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int j = 0; j < 8 && col + j < n; ++j) h[j] = reinterpret_cast<const uint16_t*>(p)[col + j];
+  return make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16), h[4] | (uint32_t(h[5]) << 16),
+                    h[6] | (uint32_t(h[7]) << 16));
+}
+
+template <int FL, typename T>
+__device__ __forceinline__ uint4 epi_pack8(const Epi& e, const uint32_t* acc, const uint4& side, const uint4& side2,
+                                           const uint4& bias) {
+  const int fl = FL >= 0 ? FL : e.flags;
+  float x[8], s1[8], s2[8], bf[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = __uint_as_float(acc[j]);
+  auto unpack = [](const uint4& u, float (&f)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 t = Pack<T>::unpack(w[j]);
+      f[2 * j] = t.x;
+      f[2 * j + 1] = t.y;
+    }
+  };
+  if (fl & SFK_EPI_ACCUM) {
+    unpack(side, s1);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = s1[j] + x[j];
+  } else {
+    if (fl & SFK_EPI_PREROUND)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = Num<T>::rnd(x[j]);
+    if (fl & SFK_EPI_BIAS) {
+      unpack(bias, bf);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = Num<T>::rnd(x[j] + bf[j]);
+    }
+    if (fl & SFK_EPI_RELU)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = x[j] > 0.0f ? x[j] : 0.0f;
+    if (fl & SFK_EPI_MASK) {
+      unpack(side2, s2);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = s2[j] > 0.0f ? Num<T>::rnd(x[j]) : 0.0f;
+    }
+    if (fl & SFK_EPI_RESIDUAL) {
+      unpack(side, s1);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = Num<T>::rnd(s1[j] + x[j]);
+    }
+  }
+  return make_uint4(Pack<T>::two(x[0], x[1]), Pack<T>::two(x[2], x[3]), Pack<T>::two(x[4], x[5]),
+                    Pack<T>::two(x[6], x[7]));
+}
+
+// stage: this warp's 4 KB staging tile (1024-aligned, shared::cta address)
+template <int BN, int FL, typename T>
+__device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMap* cmap, uint32_t tacc, int warp,
+                                                  int lane, uint32_t stage, int64_t m0, int n0, int M, int N) {
+  const int quarter = warp & 3, half = (warp - 2) >> 2;
+  const int fl = FL >= 0 ? FL : e.flags;
+  const uint32_t lane_base = tacc + (uint32_t(quarter * 32) << 16);
+  const int64_t row = m0 + quarter * 32 + lane;
+  const bool rok = row < M;
+  const T* side_row = nullptr;
+  if (fl & SFK_EPI_ACCUM) side_row = static_cast<const T*>(e.c) + row * e.ldc;
+  else if (fl & SFK_EPI_RESIDUAL) side_row = static_cast<const T*>(e.res) + row * e.ldr;
+  const T* mask_row = (fl & SFK_EPI_MASK) && !(fl & SFK_EPI_ACCUM) ? static_cast<const T*>(e.mask) + row * e.ldm
+                                                                    : nullptr;
+  const T* bias = (fl & SFK_EPI_BIAS) && !(fl & SFK_EPI_ACCUM) ? static_cast<const T*>(e.bias) : nullptr;
+  int nblk = (N - n0 + 63) / 64;
+  if (nblk > BN / 64) nblk = BN / 64;
+  const uint32_t my_row = stage + uint32_t(lane) * 128u;
+  uint32_t r[32];
+  if (half < nblk) tmem_ld32_issue(lane_base + half * 64, r);
+#pragma unroll 1
+  for (int b = half; b < nblk; b += 2) {
+#pragma unroll 1
+    for (int sub = 0; sub < 2; ++sub) {
+      const int col0 = n0 + b * 64 + sub * 32;
+      tmem_ld_wait(r);
+      uint32_t v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = r[j];
+      // next TMEM chunk in flight while this one runs its epilogue
+      if (sub == 0) tmem_ld32_issue(lane_base + b * 64 + 32, r);
+      else if (b + 2 < nblk) tmem_ld32_issue(lane_base + (b + 2) * 64, r);
+      uint4 sd[4], sd2[4], bs[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        sd[g] = side_row ? ld_row8(side_row, col0 + 8 * g, N, rok) : make_uint4(0, 0, 0, 0);
+        sd2[g] = mask_row ? ld_row8(mask_row, col0 + 8 * g, N, rok) : make_uint4(0, 0, 0, 0);
+        bs[g] = bias ? ld_row8(bias, col0 + 8 * g, N, true) : make_uint4(0, 0, 0, 0);
+      }
+      if (sub == 0 && b > half) {
+        // the previous tile's bulk store must have read the staging tile
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+      }
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint4 o = epi_pack8<FL, T>(e, v + 8 * g, sd[g], sd2[g], bs[g]);
+        const uint32_t chunk = uint32_t((sub * 4 + g) ^ (lane & 7));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(my_row + chunk * 16u), "r"(o.x), "r"(o.y),
+                     "r"(o.z), "r"(o.w)
+                     : "memory");
+      }
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(cmap, stage, n0 + b * 64, int(m0) + quarter * 32);
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_read0();
+  __syncwarp();
 }
 
 // ---------------------------------------------------------- stream-K schedule
@@ -852,16 +993,22 @@ __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar, uint32_t cta) {
       : "memory");
 }
 
-template <int BN, bool A_MN, bool B_MN, typename T>
+// FL >= 0: epilogue flags fixed at compile time (the hot combinations);
+// tma_store: the epilogue writes C through TMA bulk stores (tcm) -- needs a
+// 16-byte aligned C with ldc % 8 == 0, else the per-thread store epilogue runs
+template <int BN, bool A_MN, bool B_MN, int FL, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Epi e, int M,
-             int N, int K, int vec_ok, void* bias_grad) {
+    gemm_tc2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+             const __grid_constant__ CUtensorMap tcm, const Epi e, int M, int N, int K, int vec_ok, int tma_store,
+             void* bias_grad) {
   using C = Cfg2<BN>;
   constexpr int PM = 256;      // rows per pair tile
   constexpr int HB = BN / 2;   // B rows staged by each CTA
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  // [stages][epilogue staging: 8 warps x 4 KB, 1024-aligned][barriers]
+  uint8_t* stg_region = smem + C::STAGES * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_region + kEpiWarps * kStgFloats * 4);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -976,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
+    float* stg = reinterpret_cast<float*>(stg_region) + (warp - 2) * kStgFloats;
     int t = 0, it = 0;
     for (int tile = pair; tile < tiles; tile += npairs, ++t) {
       const int buf = t & 1;
@@ -991,7 +1138,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
       if (threadIdx.x == 64) trace(6);  // accumulators ready
-      epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
+      if (tma_store)
+        epilogue_tile_tma<BN, FL, T>(e, &tcm, tmem_base + buf * BN, warp, lane, saddr(stg), m0, n0, M, N);
+      else
+        epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
       if (threadIdx.x == 64) trace(7);  // epilogue of this warp done
       fence_before();
       __syncwarp();
@@ -1001,6 +1151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (tma_store && warp >= 2 && lane == 0) bulk_wait0();  // C written before the CTA retires
   fence_before();
   __syncthreads();
   if (threadIdx.x == 0) trace(8);  // all warps done
@@ -1084,10 +1235,10 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
   return check_launch("sfk_gemm(tcgen05)");
 }
 
-template <int BN, bool A_MN, bool B_MN, typename T>
+template <int BN, bool A_MN, bool B_MN, int FL, typename T>
 int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   using C = Cfg2<BN>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tcm;
   bool ok = A_MN ? make_map(&ta, g->dtype, g->a, g->m, g->k, g->lda, 64)
                  : make_map(&ta, g->dtype, g->a, g->k, g->m, g->lda, 128);
   ok = ok && (B_MN ? make_map(&tb, g->dtype, g->b, g->n, g->k, g->ldb, 64)
@@ -1096,10 +1247,13 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
     set_error("sfk_gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
     return SFK_EINVAL;
   }
+  // C through TMA bulk stores: 32-row x 64-column boxes, 128B swizzle
+  const bool tma_store = vec_ok && make_map(&tcm, g->dtype, g->c, g->n, g->m, g->ldc, 32);
+  if (!tma_store) tcm = ta;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_tc2<BN, A_MN, B_MN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_tc2<BN, A_MN, B_MN, FL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM) != cudaSuccess)
       return check_launch("sfk_gemm: smem attribute");
     attr_set = true;
   }
@@ -1119,7 +1273,8 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, gemm_tc2<BN, A_MN, B_MN, T>, ta, tb, e, g->m, g->n, g->k, vec_ok ? 1 : 0, g->bias_grad);
+  cudaLaunchKernelEx(&cfg, gemm_tc2<BN, A_MN, B_MN, FL, T>, ta, tb, tcm, e, g->m, g->n, g->k, vec_ok ? 1 : 0,
+                     tma_store ? 1 : 0, g->bias_grad);
   return check_launch("sfk_gemm(tcgen05 pair)");
 }
 
@@ -1177,16 +1332,38 @@ int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) 
   const int bn = skt > 0 ? 256 : g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
   if (g->pair > 0) {
-#define SFK_TC2(BNV)                                                    \
-  switch (layout) {                                                     \
-    case 0: return launch2<BNV, false, false, T>(g, e, vec_ok, s);      \
-    case 1: return launch2<BNV, false, true, T>(g, e, vec_ok, s);       \
-    case 3: return launch2<BNV, true, true, T>(g, e, vec_ok, s);        \
-    default: return launch2<BNV, true, false, T>(g, e, vec_ok, s);      \
+    // compile-time epilogues for the combinations the training step uses:
+    // forward (K-major x K-major): preround [+bias [+relu | +residual]] or
+    // +residual; activation gradient (K-major x MN-major): plain, accumulate,
+    // residual, relu mask; weight gradient (MN-major x MN-major): accumulate
+    constexpr int P = SFK_EPI_PREROUND, B = SFK_EPI_BIAS, RL = SFK_EPI_RELU, RS = SFK_EPI_RESIDUAL,
+                  MK = SFK_EPI_MASK, AC = SFK_EPI_ACCUM;
+    const int f = g->flags;
+#define SFK_TC2_FL(BNV, AM, BMN, FLV) return launch2<BNV, AM, BMN, FLV, T>(g, e, vec_ok, s)
+#define SFK_TC2(BNV)                                                                        \
+  switch (layout) {                                                                         \
+    case 0:                                                                                 \
+      if (f == P) SFK_TC2_FL(BNV, false, false, P);                                         \
+      if (f == (P | B)) SFK_TC2_FL(BNV, false, false, P | B);                               \
+      if (f == (P | B | RL)) SFK_TC2_FL(BNV, false, false, P | B | RL);                     \
+      if (f == (P | B | RS)) SFK_TC2_FL(BNV, false, false, P | B | RS);                     \
+      if (f == (P | RS)) SFK_TC2_FL(BNV, false, false, P | RS);                             \
+      SFK_TC2_FL(BNV, false, false, -1);                                                    \
+    case 1:                                                                                 \
+      if (f == 0) SFK_TC2_FL(BNV, false, true, 0);                                          \
+      if (f == AC) SFK_TC2_FL(BNV, false, true, AC);                                        \
+      if (f == RS) SFK_TC2_FL(BNV, false, true, RS);                                        \
+      if (f == MK) SFK_TC2_FL(BNV, false, true, MK);                                        \
+      SFK_TC2_FL(BNV, false, true, -1);                                                     \
+    case 3:                                                                                 \
+      if (f == AC) SFK_TC2_FL(BNV, true, true, AC);                                         \
+      SFK_TC2_FL(BNV, true, true, -1);                                                      \
+    default: SFK_TC2_FL(BNV, true, false, -1);                                              \
   }
     if (bn == 256) { SFK_TC2(256) }
     SFK_TC2(128)
 #undef SFK_TC2
+#undef SFK_TC2_FL
   }
 #define SFK_TC(BNV)                                                         \
   switch (layout) {                                                         \

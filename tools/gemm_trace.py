@@ -26,13 +26,16 @@ def trace(m, n, k, prev=None):
         L.check(L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream)), True)
         L.check(L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream)), True)  # back to back: the second is traced
         torch.cuda.synchronize()
-    out = np.zeros(24, np.uint64)
+    out = np.zeros(48, np.uint64)
     L.check(L.sfk_debug_gemm_trace(out.ctypes.data), True)
-    t = out.reshape(2, 12).astype(np.int64)
+    t = out.reshape(2, 24).astype(np.int64)
     base = t[0, 0]
     print(f"M={m} N={n} K={k}")
     for r, who in enumerate(("cta0", "last")):
         print("  " + who + ": " + " ".join(f"{NAMES[i]}={(t[r, i] - base) / 1e3:.2f}" for i in range(10)))
+        if r == 0:
+            print("    warp2 chunk0: " + " ".join(f"{n}={(t[0, 10 + i] - base) / 1e3:.2f}" for i, n in enumerate(
+                ["ld_done", "staged", "next_ld", "sync", "stores", "sync2", "c2_end", "c4_end", "c6_end"])))
 
 
 for n, k in ((1024, 512), (1024, 1024), (1024, 4096), (4096, 1024)):
