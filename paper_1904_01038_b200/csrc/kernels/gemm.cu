@@ -522,6 +522,28 @@ __device__ __forceinline__ uint4 epi_pack8(const Epi& e, const uint32_t* acc, co
 template <int BN, int FL, typename T>
 __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMap* cmap, uint32_t tacc, int warp,
                                                   int lane, uint32_t stage, int64_t m0, int n0, int M, int N) {
+  if constexpr (FL < 0) {
+    // runtime flags: branch once to a compile-time epilogue (the generic
+    // per-element branching costs ~2.5x the epilogue time)
+    constexpr int P = SFK_EPI_PREROUND, B = SFK_EPI_BIAS, RL = SFK_EPI_RELU, RS = SFK_EPI_RESIDUAL,
+                  MK = SFK_EPI_MASK, AC = SFK_EPI_ACCUM;
+#define SFK_EPI_CASE(V) \
+  case V: return epilogue_tile_tma<BN, V, T>(e, cmap, tacc, warp, lane, stage, m0, n0, M, N);
+    switch (e.flags) {
+      SFK_EPI_CASE(0)
+      SFK_EPI_CASE(P)
+      SFK_EPI_CASE(P | B)
+      SFK_EPI_CASE(P | B | RL)
+      SFK_EPI_CASE(P | B | RS)
+      SFK_EPI_CASE(P | RS)
+      SFK_EPI_CASE(AC)
+      SFK_EPI_CASE(RS)
+      SFK_EPI_CASE(MK)
+      SFK_EPI_CASE(P | B | RL | RS)
+      default: break;
+    }
+#undef SFK_EPI_CASE
+  }
   const int quarter = warp & 3, half = (warp - 2) >> 2;
   const int fl = FL >= 0 ? FL : e.flags;
   const uint32_t lane_base = tacc + (uint32_t(quarter * 32) << 16);
@@ -544,6 +566,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMa
     for (int sub = 0; sub < 2; ++sub) {
       const int col0 = n0 + b * 64 + sub * 32;
       tmem_ld_wait(r);
+      if (warp == 2 && lane == 0 && b * 2 + sub < 8) trace(10 + b * 2 + sub);  // chunk's TMEM data in registers
       uint32_t v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = r[j];
@@ -577,6 +600,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMa
       tma_store_2d(cmap, stage, n0 + b * 64, int(m0) + quarter * 32);
       bulk_commit();
     }
+    if (warp == 2 && lane == 0 && b < 4) trace(18 + b);  // block's bulk store issued
   }
   if (lane == 0) bulk_wait_read0();
   __syncwarp();

@@ -20,7 +20,7 @@ def trace(m, n, k, prev=None):
     b = torch.randn(n * k, device="cuda").to(dt)
     c = torch.zeros(m * n, device="cuda").to(dt)
     args = L.GemmArgs(m=m, n=n, k=k, dtype=1, a=a.data_ptr(), lda=k, a_kmajor=1, b=b.data_ptr(), ldb=k, b_kmajor=1,
-                      c=c.data_ptr(), ldc=n, flags=0, tile_n=256, pair=1)
+                      c=c.data_ptr(), ldc=n, flags=int(os.environ.get('GT_FLAGS', '1')), tile_n=256, pair=1)
     st = torch.cuda.current_stream()
     for rep in range(3):
         L.check(L.sfk_gemm(C.byref(args), C.c_void_p(st.cuda_stream)), True)
@@ -34,8 +34,8 @@ def trace(m, n, k, prev=None):
     for r, who in enumerate(("cta0", "last")):
         print("  " + who + ": " + " ".join(f"{NAMES[i]}={(t[r, i] - base) / 1e3:.2f}" for i in range(10)))
         if r == 0:
-            print("    warp2 chunk0: " + " ".join(f"{n}={(t[0, 10 + i] - base) / 1e3:.2f}" for i, n in enumerate(
-                ["ld_done", "staged", "next_ld", "sync", "stores", "sync2", "c2_end", "c4_end", "c6_end"])))
+            print("    warp2 chunk ld done: " + " ".join(f"c{i}={(t[0, 10 + i] - base) / 1e3:.2f}" for i in range(8))
+                  + "  block stores: " + " ".join(f"b{i}={(t[0, 18 + i] - base) / 1e3:.2f}" for i in range(4)))
 
 
 for n, k in ((1024, 512), (1024, 1024), (1024, 4096), (4096, 1024)):
