@@ -349,7 +349,13 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
     return v ? std::atoi(v) : 0;
   }();
   const int sk = sk_override_ ? sk_override_ : sk_mode;
-  if (ws && ctr_base_ && sk > 0) {
+  // CTA-pair GEMMs split the last wave stream-K style when that pays
+  // (sfk_gemm decides per shape; SQF_PAIR_SK=0 turns it off)
+  static const int pair_sk = [] {
+    const char* v = std::getenv("SQF_PAIR_SK");
+    return v ? std::atoi(v) : 1;
+  }();
+  if (ws && ctr_base_ && (sk > 0 || (g.pair > 0 && pair_sk))) {
     g.stream_k = sk > 1 ? 1 : 0;
     g.workspace = ws;
     g.workspace_floats = ws_floats_;

@@ -518,17 +518,25 @@ __device__ __forceinline__ uint4 epi_pack8(const Epi& e, const uint32_t* acc, co
                     Pack<T>::two(x[6], x[7]));
 }
 
+// Stream-K fix-up source for epilogue_tile_tma: the tile's fp32 partial
+// accumulators, [128 rows][BN] per contributing unit, summed in unit order.
+struct WsSum {
+  const float* slot[8];
+  int n = 0;  // 0: read the accumulators from TMEM instead
+};
+
 // stage: this warp's 4 KB staging tile (1024-aligned, shared::cta address)
 template <int BN, int FL, typename T>
 __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMap* cmap, uint32_t tacc, int warp,
-                                                  int lane, uint32_t stage, int64_t m0, int n0, int M, int N) {
+                                                  int lane, uint32_t stage, int64_t m0, int n0, int M, int N,
+                                                  const WsSum& ws = WsSum{}) {
   if constexpr (FL < 0) {
     // runtime flags: branch once to a compile-time epilogue (the generic
     // per-element branching costs ~2.5x the epilogue time)
     constexpr int P = SFK_EPI_PREROUND, B = SFK_EPI_BIAS, RL = SFK_EPI_RELU, RS = SFK_EPI_RESIDUAL,
                   MK = SFK_EPI_MASK, AC = SFK_EPI_ACCUM;
 #define SFK_EPI_CASE(V) \
-  case V: return epilogue_tile_tma<BN, V, T>(e, cmap, tacc, warp, lane, stage, m0, n0, M, N);
+  case V: return epilogue_tile_tma<BN, V, T>(e, cmap, tacc, warp, lane, stage, m0, n0, M, N, ws);
     switch (e.flags) {
       SFK_EPI_CASE(0)
       SFK_EPI_CASE(P)
@@ -559,20 +567,39 @@ __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMa
   if (nblk > BN / 64) nblk = BN / 64;
   const uint32_t my_row = stage + uint32_t(lane) * 128u;
   uint32_t r[32];
-  if (half < nblk) tmem_ld32_issue(lane_base + half * 64, r);
+  const bool from_ws = ws.n > 0;
+  if (half < nblk && !from_ws) tmem_ld32_issue(lane_base + half * 64, r);
 #pragma unroll 1
   for (int b = half; b < nblk; b += 2) {
 #pragma unroll 1
     for (int sub = 0; sub < 2; ++sub) {
       const int col0 = n0 + b * 64 + sub * 32;
-      tmem_ld_wait(r);
-      if (warp == 2 && lane == 0 && b * 2 + sub < 8) trace(10 + b * 2 + sub);  // chunk's TMEM data in registers
       uint32_t v[32];
+      if (from_ws) {
+        // this thread's row segment of every partial, summed in unit order
+        const int off = (quarter * 32 + lane) * BN + b * 64 + sub * 32;
+        float acc[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = r[j];
-      // next TMEM chunk in flight while this one runs its epilogue
-      if (sub == 0) tmem_ld32_issue(lane_base + b * 64 + 32, r);
-      else if (b + 2 < nblk) tmem_ld32_issue(lane_base + (b + 2) * 64, r);
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int u = 0; u < ws.n; ++u) {
+          const float4* src = reinterpret_cast<const float4*>(ws.slot[u] + off);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 x = __ldcg(src + q);
+            acc[4 * q] += x.x, acc[4 * q + 1] += x.y, acc[4 * q + 2] += x.z, acc[4 * q + 3] += x.w;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc[j]);
+      } else {
+        tmem_ld_wait(r);
+        if (warp == 2 && lane == 0 && b * 2 + sub < 8) trace(10 + b * 2 + sub);  // chunk's TMEM data in registers
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = r[j];
+        // next TMEM chunk in flight while this one runs its epilogue
+        if (sub == 0) tmem_ld32_issue(lane_base + b * 64 + 32, r);
+        else if (b + 2 < nblk) tmem_ld32_issue(lane_base + (b + 2) * 64, r);
+      }
       uint4 sd[4], sd2[4], bs[4];
 #pragma unroll
       for (int g = 0; g < 4; ++g) {
@@ -607,6 +634,30 @@ __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMa
 }
 
 // ---------------------------------------------------------- stream-K schedule
+// Pair stream-K partial: this CTA's 128 x BN fp32 accumulators (TMEM) to a
+// workspace slot, row-major; each thread writes its own row's chunks.
+template <int BN>
+__device__ __forceinline__ void store_partial_rows(uint32_t tacc, int warp, int lane, float* slot) {
+  const int quarter = warp & 3, half = (warp - 2) >> 2;
+  const uint32_t lane_base = tacc + (uint32_t(quarter * 32) << 16);
+  float* row = slot + size_t(quarter * 32 + lane) * BN;
+  uint32_t r[32];
+  tmem_ld32_issue(lane_base + half * 32, r);
+#pragma unroll 1
+  for (int ch = half; ch < BN / 32; ch += 2) {
+    tmem_ld_wait(r);
+    float4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      v[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                         __uint_as_float(r[4 * j + 3]));
+    if (ch + 2 < BN / 32) tmem_ld32_issue(lane_base + (ch + 2) * 32, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) __stcg(reinterpret_cast<float4*>(row + ch * 32) + j, v[j]);
+  }
+}
+
+
 // Work of a persistent CTA b (of G): first its share of the stream-K region
 // -- tiles [0, sk_tiles) flattened to sk_tiles*kblocks k-block iterations and
 // cut into G equal contiguous ranges, so a range may start/end inside a tile --
@@ -624,7 +675,9 @@ struct Sched {
   int64_t tsk, it0, it1, it;
   int dp;
   __device__ __forceinline__ Sched(int tiles_, int kblocks_, int sk_tiles_)
-      : tiles(tiles_), kblocks(kblocks_), G(int(gridDim.x)), b(int(blockIdx.x)), sk_tiles(sk_tiles_) {
+      : Sched(tiles_, kblocks_, sk_tiles_, int(gridDim.x), int(blockIdx.x)) {}
+  __device__ __forceinline__ Sched(int tiles_, int kblocks_, int sk_tiles_, int G_, int b_)
+      : tiles(tiles_), kblocks(kblocks_), G(G_), b(b_), sk_tiles(sk_tiles_) {
     tsk = int64_t(sk_tiles) * kblocks;
     it0 = int64_t(b) * tsk / G;
     it1 = int64_t(b + 1) * tsk / G;
@@ -1024,7 +1077,12 @@ template <int BN, bool A_MN, bool B_MN, int FL, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc2(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
              const __grid_constant__ CUtensorMap tcm, const Epi e, int M, int N, int K, int vec_ok, int tma_store,
-             void* bias_grad) {
+             const Sk sk) {
+  // stream-K (sk.sk_tiles > 0, tma_store only): the k-iterations of the first
+  // sk_tiles tiles are cut evenly over all pairs; a pair whose range covers a
+  // tile only in part parks its fp32 accumulators in sk.ws and the last
+  // arriving part sums them in k order and runs the epilogue (deterministic)
+  void* bias_grad = sk.bias_grad;
   using C = Cfg2<BN>;
   constexpr int PM = 256;      // rows per pair tile
   constexpr int HB = BN / 2;   // B rows staged by each CTA
@@ -1076,16 +1134,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_m = (M + PM - 1) / PM, num_n = (N + BN - 1) / BN;
   const int tiles = num_m * num_n, kblocks = (K + BK - 1) / BK;
   const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+  const int sk_tiles = tma_store ? sk.sk_tiles : 0;
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;
+      int it = 0, tile, kb0, kb1;
       uint32_t bias_pend = 0, bias_ph = 0;  // per stage: a bias-tile read outstanding / its bsum phase
-      for (int tile = pair; tile < tiles; tile += npairs) {
+      Sched sc(tiles, kblocks, sk_tiles, npairs, pair);
+      while (sc.next(tile, kb0, kb1)) {
         const int m0 = (tile % num_m) * PM + 128 * int(rank);
         const int n0 = (tile / num_m) * BN + HB * int(rank);
         const bool btile = A_MN && bias_grad && tile / num_m == 0;
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -1121,13 +1181,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (uint32_t(A_MN) << 15) |
                              (uint32_t(B_MN) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(PM >> 4) << 24);
-      int it = 0, t = 0;
-      for (int tile = pair; tile < tiles; tile += npairs, ++t) {
+      int it = 0, t = 0, tile, kb0, kb1;
+      Sched sc(tiles, kblocks, sk_tiles, npairs, pair);
+      for (; sc.next(tile, kb0, kb1); ++t) {
         const int buf = t & 1;
         mbar_wait(&tempty[buf], ((t >> 1) & 1) ^ 1);
         fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           mbar_wait(&full[s], (it / C::STAGES) & 1);
           fence_after();
@@ -1138,7 +1199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = A_MN ? smem_desc(a_addr + k * 2048, 8192, 1024) : smem_desc(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc(b_addr + k * 2048, 8192, 1024) : smem_desc(b_addr + k * 32, 16, 1024);
-            umma_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            umma_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit_pair(&empty[s]);
         }
@@ -1148,30 +1209,69 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     float* stg = reinterpret_cast<float*>(stg_region) + (warp - 2) * kStgFloats;
-    int t = 0, it = 0;
-    for (int tile = pair; tile < tiles; tile += npairs, ++t) {
+    volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    int t = 0, it = 0, tile, kb0, kb1;
+    Sched sc(tiles, kblocks, sk_tiles, npairs, pair);
+    for (; sc.next(tile, kb0, kb1); ++t) {
       const int buf = t & 1;
       const int m0 = (tile % num_m) * PM + 128 * int(rank), n0 = (tile / num_m) * BN;
       // fused bias gradient: each CTA sums its own 128-row half of A; the
       // pair's MMA commit on empty[s] (multicast to both CTAs) says the stage
-      // is complete and still unrecycled
+      // is complete and still unrecycled (never combined with stream-K)
       if (A_MN && bias_grad && n0 == 0)
-        bias_grad_tile<T, C::STAGES, C::STAGE>(smem, empty, bsum, it, kblocks, warp, lane, stg,
+        bias_grad_tile<T, C::STAGES, C::STAGE>(smem, empty, bsum, it, kb1 - kb0, warp, lane, stg,
                                                static_cast<T*>(bias_grad), m0, M);
-      it += kblocks;
+      it += kb1 - kb0;
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
       if (threadIdx.x == 64) trace(6);  // accumulators ready
-      if (tma_store)
-        epilogue_tile_tma<BN, FL, T>(e, &tcm, tmem_base + buf * BN, warp, lane, saddr(stg), m0, n0, M, N);
-      else
-        epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
-      if (threadIdx.x == 64) trace(7);  // epilogue of this warp done
-      fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(&tempty[buf]);
-        else mbar_arrive_cta(&tempty[buf], 0);
+      if (kb0 == 0 && kb1 == kblocks) {
+        if (tma_store)
+          epilogue_tile_tma<BN, FL, T>(e, &tcm, tmem_base + buf * BN, warp, lane, saddr(stg), m0, n0, M, N);
+        else
+          epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
+        if (threadIdx.x == 64) trace(7);  // epilogue of this warp done
+        fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[buf]);
+          else mbar_arrive_cta(&tempty[buf], 0);
+        }
+      } else {
+        // stream-K part: park this CTA's accumulators in its slot (0: the
+        // pair's first unit, 1: its last), release TMEM, count the arrival
+        const int slot = int64_t(tile) * kblocks <= sc.it0 ? 0 : 1;
+        const size_t slot_floats = size_t(128) * BN;
+        store_partial_rows<BN>(tmem_base + buf * BN, warp, lane,
+                               sk.ws + ((size_t(pair) * 2 + rank) * 2 + slot) * slot_floats);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[buf]);
+          else mbar_arrive_cta(&tempty[buf], 0);
+        }
+        __threadfence();
+        epi_bar();
+        const int64_t i_beg = int64_t(tile) * kblocks, i_end = i_beg + kblocks;
+        const int c0 = int(((i_beg + 1) * sc.G + sc.tsk - 1) / sc.tsk) - 1;
+        const int c1 = int((i_end * sc.G + sc.tsk - 1) / sc.tsk) - 1;
+        if (threadIdx.x == 64) {
+          const int old = atomicAdd(sk.flags + 2 * tile + int(rank), 1);
+          const bool last = old == c1 - c0;
+          if (last) sk.flags[2 * tile + int(rank)] = 0;  // every part has arrived: re-arm
+          *last_flag = last ? 1 : 0;
+        }
+        epi_bar();
+        if (*last_flag) {
+          __threadfence();
+          WsSum ws;
+          for (int c = c0; c <= c1 && ws.n < 8; ++c) {
+            const int sl = i_beg <= sc.start_of(c) ? 0 : 1;
+            ws.slot[ws.n++] = sk.ws + ((size_t(c) * 2 + rank) * 2 + sl) * slot_floats;
+          }
+          epilogue_tile_tma<BN, FL, T>(e, &tcm, 0, warp, lane, saddr(stg), m0, n0, M, N, ws);
+        }
+        epi_bar();  // last_flag is reused by the next unit
       }
     }
   }
@@ -1259,6 +1359,29 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
   return check_launch("sfk_gemm(tcgen05)");
 }
 
+// Stream-K plan for the pair kernel: the stream-K region in tiles (0 = plain
+// data-parallel). Used when the last wave of 256 x BN tiles would leave pairs
+// idle for a sizeable share of the run and the k-loop is long enough to split;
+// never with the fused bias gradient (it assumes whole tiles). stream_k < 0 or
+// no workspace disables it.
+int pick_stream_k2(const sfk_gemm_args* g, int tiles, int bn) {
+  if (g->stream_k < 0 || !g->workspace || !g->counters || g->bias_grad) return 0;
+  const int G = num_sms_cached() / 2;
+  if (g->workspace_floats < int64_t(G) * 4 * 128 * bn) return 0;
+  const int kb = (g->k + BK - 1) / BK;
+  if (kb < 8 || tiles % G == 0) return 0;
+  const int sk_tiles = tiles < G ? tiles : tiles % G + G;
+  if (2 * sk_tiles > g->n_counters) return 0;
+  // a tile must not be cut into more than 8 parts (the fix-up's slot list)
+  const int64_t per_pair = int64_t(sk_tiles) * kb / G;
+  if (per_pair < 1 || (kb + per_pair - 1) / per_pair + 1 > 8) return 0;
+  // data-parallel rounds vs stream-K share (in k-blocks per pair) plus a
+  // fix-up allowance of ~3 k-blocks; split only for a >= 10% gain
+  const double dp = double((tiles + G - 1) / G) * kb;
+  const double skc = double(tiles) * kb / G + 3.0;
+  return skc < 0.9 * dp ? sk_tiles : 0;
+}
+
 template <int BN, bool A_MN, bool B_MN, int FL, typename T>
 int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   using C = Cfg2<BN>;
@@ -1282,7 +1405,15 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
     attr_set = true;
   }
   const int tiles = ((g->m + 255) / 256) * ((g->n + BN - 1) / BN);
-  const int pairs = tiles < num_sms_cached() / 2 ? tiles : num_sms_cached() / 2;
+  int pairs = tiles < num_sms_cached() / 2 ? tiles : num_sms_cached() / 2;
+  Sk sk{nullptr, nullptr, 0, g->bias_grad};
+  if (tma_store) {
+    const int skt = pick_stream_k2(g, tiles, BN);
+    if (skt > 0) {
+      sk = Sk{g->workspace, g->counters, skt, nullptr};
+      pairs = num_sms_cached() / 2;
+    }
+  }
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
@@ -1298,7 +1429,7 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, gemm_tc2<BN, A_MN, B_MN, FL, T>, ta, tb, tcm, e, g->m, g->n, g->k, vec_ok ? 1 : 0,
-                     tma_store ? 1 : 0, g->bias_grad);
+                     tma_store ? 1 : 0, sk);
   return check_launch("sfk_gemm(tcgen05 pair)");
 }
 
