@@ -621,3 +621,23 @@ def test_layernorm_params_partial_and_batched_fold_match_reference(dt):
         sc = np.sqrt(j.nparts * 1.0)
         np.testing.assert_allclose(og.float().cpu().numpy(), wg, rtol=rt, atol=rt * 10 * sc)
         np.testing.assert_allclose(ob.float().cpu().numpy(), wb, rtol=rt, atol=rt * 10 * sc)
+
+
+@pytest.mark.parametrize("dtype", [1, 2])
+@pytest.mark.parametrize("tile_n", [256, 128])
+@pytest.mark.parametrize("layout,flags", [((True, True), 1 | 2 | 16), ((True, True), 1 | 2 | 4), ((True, False), 0),
+                                          ((True, False), 32), ((True, False), 8), ((False, False), 32)])
+@pytest.mark.parametrize("shape", [(3584, 1024, 1024), (3584, 1024, 4096), (3584, 3072, 1024), (3584, 4096, 1024),
+                                   (1024, 1024, 3584), (3000, 1000, 2000)])
+def test_gemm_pair_stream_k(dtype, tile_n, layout, flags, shape):
+    """CTA-pair GEMM with the auto stream-K split of the last wave (fp32
+    partials per CTA, summed in k order by the last arriving part, TMA-store
+    epilogue) against fp64; deterministic, counters re-armed."""
+    ws = sk_workspace()
+    m, n, k = shape
+    got, want = run_gemm(m, n, k, dtype, *layout, flags=flags, seed=5, stream_k=0, ws=ws, pair=1, tile_n=tile_n)
+    tol = (4e-3 if dtype == 1 else 2e-2)
+    torch.testing.assert_close(got, want, rtol=tol, atol=tol * max(1.0, k ** 0.5 * 0.25))
+    assert int(ws[1].abs().sum()) == 0
+    again, _ = run_gemm(m, n, k, dtype, *layout, flags=flags, seed=5, stream_k=0, ws=ws, pair=1, tile_n=tile_n)
+    assert torch.equal(got, again)
