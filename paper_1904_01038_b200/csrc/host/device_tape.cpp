@@ -349,11 +349,12 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
     return v ? std::atoi(v) : 0;
   }();
   const int sk = sk_override_ ? sk_override_ : sk_mode;
-  // CTA-pair GEMMs split the last wave stream-K style when that pays
-  // (sfk_gemm decides per shape; SQF_PAIR_SK=0 turns it off)
+  // SQF_PAIR_SK=1: CTA-pair GEMMs may split the last wave stream-K style
+  // (sfk_gemm decides per shape). Off by default: measured slower on every
+  // C4 shape so far (fp32 partial round trips cost more than the idle tail)
   static const int pair_sk = [] {
     const char* v = std::getenv("SQF_PAIR_SK");
-    return v ? std::atoi(v) : 1;
+    return v ? std::atoi(v) : 0;
   }();
   if (ws && ctr_base_ && (sk > 0 || (g.pair > 0 && pair_sk))) {
     g.stream_k = sk > 1 ? 1 : 0;
