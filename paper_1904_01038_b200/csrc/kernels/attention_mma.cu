@@ -47,6 +47,21 @@ struct MmaT<__nv_bfloat16> {
   }
 };
 
+// 8 consecutive 16-bit values from shared memory (16-byte aligned) as floats
+template <typename T>
+__device__ __forceinline__ void vec_ld8(const T* p, float (&f)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 t;
+    if constexpr (std::is_same<T, __half>::value) t = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+    else t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+
 // 2^x on the SFU, flushing subnormal results to zero (probabilities that
 // small are zero in every 16-bit output anyway)
 __device__ __forceinline__ float ex2(float x) {
@@ -298,11 +313,31 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
   float D_a = 0.f, D_b = 0.f;
   {
     const T* O = static_cast<const T*>(a.o) + h * a.dh;
-    for (int c = tq; c < a.dh; c += 4) {
-      if (row_a < a.qw)
-        D_a += Num<T>::ld(Gs + (r0 + g) * LD + c) * Num<T>::ld(O + (qrow0 + row_a) * a.ldo + c);
-      if (row_b < a.qw)
-        D_b += Num<T>::ld(Gs + (r0 + g + 8) * LD + c) * Num<T>::ld(O + (qrow0 + row_b) * a.ldo + c);
+    if (a.dh % 32 == 0) {
+      // each lane of a quad: a contiguous quarter of the row, 16-byte loads
+      const int qw = a.dh / 4;
+      for (int c = tq * qw; c < (tq + 1) * qw; c += 8) {
+        float g8[8], o8[8];
+        if (row_a < a.qw) {
+          vec_ld8<T>(Gs + (r0 + g) * LD + c, g8);
+          vec_ld8<T>(O + (qrow0 + row_a) * a.ldo + c, o8);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) D_a += g8[j] * o8[j];
+        }
+        if (row_b < a.qw) {
+          vec_ld8<T>(Gs + (r0 + g + 8) * LD + c, g8);
+          vec_ld8<T>(O + (qrow0 + row_b) * a.ldo + c, o8);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) D_b += g8[j] * o8[j];
+        }
+      }
+    } else {
+      for (int c = tq; c < a.dh; c += 4) {
+        if (row_a < a.qw)
+          D_a += Num<T>::ld(Gs + (r0 + g) * LD + c) * Num<T>::ld(O + (qrow0 + row_a) * a.ldo + c);
+        if (row_b < a.qw)
+          D_b += Num<T>::ld(Gs + (r0 + g + 8) * LD + c) * Num<T>::ld(O + (qrow0 + row_b) * a.ldo + c);
+      }
     }
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 1);
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 2);
@@ -562,11 +597,29 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
   if (r0 < a.qw) {
     const int row_a = r0 + g, row_b = row_a + 8;
     float D_a = 0.f, D_b = 0.f;
-    // rows past qw are zero-filled in Gs/Os, so their D is 0
+    // rows past qw are zero-filled in Gs/Os, so their D is 0; each lane of a
+    // quad takes a contiguous quarter of the row (16-byte shared loads)
+    if constexpr (DH % 32 == 0) {
+      constexpr int QW = DH / 4;  // columns per lane
 #pragma unroll
-    for (int c = tq; c < DH; c += 4) {
-      D_a += Num<T>::ld(Gs + row_a * LD + c) * Num<T>::ld(Os + row_a * LD + c);
-      D_b += Num<T>::ld(Gs + row_b * LD + c) * Num<T>::ld(Os + row_b * LD + c);
+      for (int c = tq * QW; c < (tq + 1) * QW; c += 8) {
+        float ga[8], oa[8], gb[8], ob[8];
+        vec_ld8<T>(Gs + row_a * LD + c, ga);
+        vec_ld8<T>(Os + row_a * LD + c, oa);
+        vec_ld8<T>(Gs + row_b * LD + c, gb);
+        vec_ld8<T>(Os + row_b * LD + c, ob);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          D_a += ga[j] * oa[j];
+          D_b += gb[j] * ob[j];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = tq; c < DH; c += 4) {
+        D_a += Num<T>::ld(Gs + row_a * LD + c) * Num<T>::ld(Os + row_a * LD + c);
+        D_b += Num<T>::ld(Gs + row_b * LD + c) * Num<T>::ld(Os + row_b * LD + c);
+      }
     }
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 1);
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 2);
