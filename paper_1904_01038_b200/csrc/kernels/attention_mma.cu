@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
   stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0) + qstart, nq, nq_pad, a.dh);
   for (int i = threadIdx.x; i < nq_pad; i += blockDim.x) {
     const bool ok = i < nq;
-    St[i] = ok ? a.stats[(qrow0 + qstart + i) * a.heads + h] : make_float2(0.f, 0.f);
+    const float2 sv = ok ? a.stats[(qrow0 + qstart + i) * a.heads + h] : make_float2(0.f, 0.f);
+    St[i] = make_float2(sv.x * 1.4426950408889634f, sv.y);  // max in log2 units
     Ds[i] = ok ? a.dsum[(qrow0 + qstart + i) * a.heads + h] : 0.f;
   }
   stage_wait();
@@ -505,8 +506,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
           const bool qok = qi < nq;
           const bool va_ok = qok && key_a < a.kw && (a.causal ? key_a <= t : key_a < len);
           const bool vb_ok = qok && key_b < a.kw && (a.causal ? key_b <= t : key_b < len);
-          const float pa = va_ok ? ex2(s[nt][e] * c2 - st.x * l2e) * st.y : 0.f;
-          const float pb = vb_ok ? ex2(s[nt][2 + e] * c2 - st.x * l2e) * st.y : 0.f;
+          const float pa = va_ok ? ex2(s[nt][e] * c2 - st.x) * st.y : 0.f;
+          const float pb = vb_ok ? ex2(s[nt][2 + e] * c2 - st.x) * st.y : 0.f;
           p[nt][e] = pa;
           p[nt][2 + e] = pb;
           s[nt][e] = pa * (dp[nt][e] - D);
@@ -586,7 +587,8 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
   stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), a.kw, R, a.dh);
   stage<T, DH>(Os, LD, static_cast<const T*>(a.o) + h * a.dh, a.ldo, int(qrow0), a.qw, R, a.dh);
   for (int i = threadIdx.x; i < QP; i += blockDim.x) {
-    St[i] = i < a.qw ? a.stats[(qrow0 + i) * a.heads + h] : make_float2(0.f, 0.f);
+    const float2 sv = i < a.qw ? a.stats[(qrow0 + i) * a.heads + h] : make_float2(0.f, 0.f);
+    St[i] = make_float2(sv.x * 1.4426950408889634f, sv.y);  // max in log2 units
     Ds[i] = 0.f;
   }
   stage_wait();
@@ -666,8 +668,8 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int j = kc + nt * 8 + 2 * tq + e;
-          const float pa = j < lim_a ? ex2(s[nt][e] * c2 - st_a.x * l2e) * st_a.y : 0.f;
-          const float pb = j < lim_b ? ex2(s[nt][2 + e] * c2 - st_b.x * l2e) * st_b.y : 0.f;
+          const float pa = j < lim_a ? ex2(s[nt][e] * c2 - st_a.x) * st_a.y : 0.f;
+          const float pb = j < lim_b ? ex2(s[nt][2 + e] * c2 - st_b.x) * st_b.y : 0.f;
           s[nt][e] = pa * (dp[nt][e] - D_a);
           s[nt][2 + e] = pb * (dp[nt][2 + e] - D_b);
         }
@@ -717,6 +719,8 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
       load_a<T>(va[ks], Vs, LD, r0, ks * 16, lane);
     }
     const int qbeg = a.causal ? (r0 & ~15) : 0;
+    const bool ka_ok = key_a < a.kw && (a.causal || key_a < len);
+    const bool kb_ok = key_b < a.kw && (a.causal || key_b < len);
     for (int qc = qbeg; qc < nq; qc += NC) {
       float s[NC / 8][4], dp[NC / 8][4];
 #pragma unroll
@@ -743,11 +747,11 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
           const int t = qc + nt * 8 + 2 * tq + e;
           const float2 st = St[t];
           const float D = Ds[t];
-          const bool qok = t < nq;
-          const bool va_ok = qok && key_a < a.kw && (a.causal ? key_a <= t : key_a < len);
-          const bool vb_ok = qok && key_b < a.kw && (a.causal ? key_b <= t : key_b < len);
-          const float pa = va_ok ? ex2(s[nt][e] * c2 - st.x * l2e) * st.y : 0.f;
-          const float pb = vb_ok ? ex2(s[nt][2 + e] * c2 - st.x * l2e) * st.y : 0.f;
+          // key predicates hoisted (ka_ok/kb_ok), only the query index varies
+          const bool va_ok = t < nq && ka_ok && (!a.causal || key_a <= t);
+          const bool vb_ok = t < nq && kb_ok && (!a.causal || key_b <= t);
+          const float pa = va_ok ? ex2(s[nt][e] * c2 - st.x) * st.y : 0.f;
+          const float pb = vb_ok ? ex2(s[nt][2 + e] * c2 - st.x) * st.y : 0.f;
           p[nt][e] = pa;
           p[nt][2 + e] = pb;
           s[nt][e] = pa * (dp[nt][e] - D);

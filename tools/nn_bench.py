@@ -42,6 +42,11 @@ def main():
     t = timeit(lambda: L.sfk_layernorm_bwd_fused(1, p(x), p(dy), R, d, p(g), p(st), p(dx), 1, p(part), None, p(dg),
                                                  p(db), s))
     print(f"ln_bwd      {t:7.1f} us  {4 * mb / t * 1e-3:6.2f} TB/s")
+    t = timeit(lambda: L.sfk_layernorm_bwd_dx_acc(1, p(x), p(dy), R, d, p(g), p(st), p(dx), p(dx), s))
+    print(f"ln_dx(acc)  {t:7.1f} us  {4 * mb / t * 1e-3:6.2f} TB/s  (reads x, dy, acc; writes dx)")
+    npart = C.c_int()
+    t = timeit(lambda: L.sfk_layernorm_bwd_params_partial(1, p(x), p(dy), R, d, p(st), p(part), C.byref(npart), s))
+    print(f"ln_gb_part  {t:7.1f} us  {2 * mb / t * 1e-3:6.2f} TB/s  ({npart.value} partials)")
     for n in (1024, 3072, 4096, 32768):
         a = torch.randn(R, n, device="cuda").half()
         o = torch.zeros(n, device="cuda").half()
