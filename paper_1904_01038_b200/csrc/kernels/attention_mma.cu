@@ -421,12 +421,12 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
 
 // ------------------------------------------------------------------ backward: dK, dV
 template <typename T, int DH>
-__global__ void __launch_bounds__(kWarps * 32) bwd_dkv_k(Args a) {
+__global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
-  constexpr int NC = DH >= 128 ? 32 : 64;  // query columns per chunk (register budget)
+  constexpr int NC = DH >= 64 ? 32 : 64;  // query columns per chunk (register budget: 3 CTAs per SM at DH 64)
   const int b = blockIdx.z, h = blockIdx.y, k0 = blockIdx.x * kRows;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];

@@ -559,18 +559,32 @@ __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMa
       const int col0 = n0 + b * 64 + sub * 32;
       uint32_t v[32];
       if (from_ws) {
-        // this thread's row segment of every partial, summed in unit order
-        const int off = (quarter * 32 + lane) * BN + b * 64 + sub * 32;
+        // this thread's row of every partial, summed in unit order; partials
+        // are stored [chunk][float4 j][row] so each warp load is 512
+        // contiguous bytes (see store_partial_rows)
+        const int ch = b * 2 + sub, row = quarter * 32 + lane;
         float acc[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-        for (int u = 0; u < ws.n; ++u) {
-          const float4* src = reinterpret_cast<const float4*>(ws.slot[u] + off);
+        float4 x[8];
+        {
+          const float4* src = reinterpret_cast<const float4*>(ws.slot[0]) + size_t(ch) * 8 * 128 + row;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 x = __ldcg(src + q);
-            acc[4 * q] += x.x, acc[4 * q + 1] += x.y, acc[4 * q + 2] += x.z, acc[4 * q + 3] += x.w;
+          for (int q = 0; q < 8; ++q) x[q] = __ldcg(src + q * 128);
+        }
+        for (int u = 0; u < ws.n; ++u) {
+          float4 y[8];
+          if (u + 1 < ws.n) {  // next part's loads in flight while this one is added
+            const float4* src = reinterpret_cast<const float4*>(ws.slot[u + 1]) + size_t(ch) * 8 * 128 + row;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) y[q] = __ldcg(src + q * 128);
           }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            acc[4 * q] += x[q].x, acc[4 * q + 1] += x[q].y, acc[4 * q + 2] += x[q].z, acc[4 * q + 3] += x[q].w;
+          if (u + 1 < ws.n)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x[q] = y[q];
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(acc[j]);
@@ -619,11 +633,13 @@ __device__ __forceinline__ void epilogue_tile_tma(const Epi& e, const CUtensorMa
 // ---------------------------------------------------------- stream-K schedule
 // Pair stream-K partial: this CTA's 128 x BN fp32 accumulators (TMEM) to a
 // workspace slot, row-major; each thread writes its own row's chunks.
+// Layout [chunk of 32 columns][float4 j][row]: for a fixed (chunk, j) the 32
+// lanes (rows) write 512 contiguous bytes.
 template <int BN>
 __device__ __forceinline__ void store_partial_rows(uint32_t tacc, int warp, int lane, float* slot) {
   const int quarter = warp & 3, half = (warp - 2) >> 2;
   const uint32_t lane_base = tacc + (uint32_t(quarter * 32) << 16);
-  float* row = slot + size_t(quarter * 32 + lane) * BN;
+  float4* rowp = reinterpret_cast<float4*>(slot) + quarter * 32 + lane;
   uint32_t r[32];
   tmem_ld32_issue(lane_base + half * 32, r);
 #pragma unroll 1
@@ -636,7 +652,7 @@ __device__ __forceinline__ void store_partial_rows(uint32_t tacc, int warp, int 
                          __uint_as_float(r[4 * j + 3]));
     if (ch + 2 < BN / 32) tmem_ld32_issue(lane_base + (ch + 2) * 32, r);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) __stcg(reinterpret_cast<float4*>(row + ch * 32) + j, v[j]);
+    for (int j = 0; j < 8; ++j) __stcg(rowp + (size_t(ch) * 8 + j) * 128, v[j]);
   }
 }
 
@@ -1227,6 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const size_t slot_floats = size_t(128) * BN;
         store_partial_rows<BN>(tmem_base + buf * BN, warp, lane,
                                sk.ws + ((size_t(pair) * 2 + rank) * 2 + slot) * slot_floats);
+        if (threadIdx.x == 64) trace(11);  // partial stored (this warp)
         fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -1252,7 +1269,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int sl = i_beg <= sc.start_of(c) ? 0 : 1;
             ws.slot[ws.n++] = sk.ws + ((size_t(c) * 2 + rank) * 2 + sl) * slot_floats;
           }
+          if (threadIdx.x == 64) trace(22);  // last part: fix-up starts
           epilogue_tile_tma<BN, FL, T>(e, &tcm, 0, warp, lane, saddr(stg), m0, n0, M, N, ws);
+          if (threadIdx.x == 64) trace(23);  // fix-up epilogue done
         }
         epi_bar();  // last_flag is reused by the next unit
       }

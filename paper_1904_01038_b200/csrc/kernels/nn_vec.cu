@@ -172,68 +172,105 @@ __global__ void __launch_bounds__(128) embed_bwd_fold_v(const int4* __restrict__
 
 constexpr int kMaxCh = 4;  // d <= 32 lanes * 4 chunks * 8 = 1024
 
-// One warp per row. Every global load of the row (x, gamma, beta) is issued
-// up front, so a warp pays one memory round trip before its reductions; 4 rows
-// per 128-thread block keep the grid fine-grained.
+// One warp per two rows (rows w and w + rows_per_block/2 of the block). Every
+// global load of both rows and of gamma/beta is issued up front, so a warp
+// pays one memory round trip, gamma/beta are fetched once per two rows, and
+// the two rows' reductions interleave.
+constexpr int kLnFwdRows = 2;
 template <typename T>
 __global__ void __launch_bounds__(128) ln_fwd_v(const T* __restrict__ x, int rows, int d, const T* __restrict__ g,
                                                const T* __restrict__ b, T* __restrict__ y,
                                                float2* __restrict__ stats) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  const T* xr = x + int64_t(r) * d;
-  uint4 xu[kMaxCh], gu[kMaxCh], bu[kMaxCh];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  const int r0 = blockIdx.x * nw * kLnFwdRows + warp;
+  if (r0 >= rows) return;
+  int rr[kLnFwdRows];
+  bool ok[kLnFwdRows];
+#pragma unroll
+  for (int k = 0; k < kLnFwdRows; ++k) {
+    rr[k] = r0 + k * nw;
+    ok[k] = rr[k] < rows;
+  }
+  uint4 xu[kLnFwdRows][kMaxCh], gu[kMaxCh], bu[kMaxCh];
 #pragma unroll
   for (int i = 0; i < kMaxCh; ++i) {
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
-      xu[i] = *reinterpret_cast<const uint4*>(xr + c);
+#pragma unroll
+      for (int k = 0; k < kLnFwdRows; ++k)
+        if (ok[k]) xu[k][i] = *reinterpret_cast<const uint4*>(x + int64_t(rr[k]) * d + c);
       gu[i] = __ldg(reinterpret_cast<const uint4*>(g + c));
       bu[i] = __ldg(reinterpret_cast<const uint4*>(b + c));
     }
   }
-  float v[kMaxCh][8];
-  float s = 0.f;
+  float mean[kLnFwdRows], rstd[kLnFwdRows];
+  {
+    float sm[kLnFwdRows];
 #pragma unroll
-  for (int i = 0; i < kMaxCh; ++i) {
-    const int c = (lane + 32 * i) * 8;
-    if (c < d) {
-      V8<T>::unpack(xu[i], v[i]);
+    for (int k = 0; k < kLnFwdRows; ++k) {
+      sm[k] = 0.f;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += v[i][e];
+      for (int i = 0; i < kMaxCh; ++i) {
+        const int c = (lane + 32 * i) * 8;
+        if (c < d && ok[k]) {
+          float v[8];
+          V8<T>::unpack(xu[k][i], v);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sm[k] += v[e];
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kLnFwdRows; ++k) mean[k] = __fdiv_rn(warp_sum(sm[k]), float(d));
+    float q[kLnFwdRows];
+#pragma unroll
+    for (int k = 0; k < kLnFwdRows; ++k) {
+      q[k] = 0.f;
+#pragma unroll
+      for (int i = 0; i < kMaxCh; ++i) {
+        const int c = (lane + 32 * i) * 8;
+        if (c < d && ok[k]) {
+          float v[8];
+          V8<T>::unpack(xu[k][i], v);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float t = __fsub_rn(v[e], mean[k]);
+            q[k] = __fadd_rn(q[k], __fmul_rn(t, t));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kLnFwdRows; ++k) {
+      const float var = __fdiv_rn(warp_sum(q[k]), float(d));
+      rstd[k] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
     }
   }
-  const float mean = __fdiv_rn(warp_sum(s), float(d));
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < kMaxCh; ++i) {
-    const int c = (lane + 32 * i) * 8;
-    if (c < d)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float t = __fsub_rn(v[i][e], mean);
-        q = __fadd_rn(q, __fmul_rn(t, t));
-      }
-  }
-  const float var = __fdiv_rn(warp_sum(q), float(d));
-  const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
-  T* yr = y + int64_t(r) * d;
 #pragma unroll
   for (int i = 0; i < kMaxCh; ++i) {
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
-      float gg[8], bb[8], o[8];
+      float gg[8], bb[8];
       V8<T>::unpack(gu[i], gg);
       V8<T>::unpack(bu[i], bb);
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        o[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[i][e], mean), rstd), gg[e]), bb[e]);
-      V8<T>::store(yr + c, o);
+      for (int k = 0; k < kLnFwdRows; ++k) {
+        if (!ok[k]) continue;
+        float v[8], o[8];
+        V8<T>::unpack(xu[k][i], v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          o[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[e], mean[k]), rstd[k]), gg[e]), bb[e]);
+        V8<T>::store(y + int64_t(rr[k]) * d + c, o);
+      }
     }
   }
-  if (lane == 0) stats[r] = make_float2(mean, rstd);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < kLnFwdRows; ++k)
+      if (ok[k]) stats[rr[k]] = make_float2(mean[k], rstd[k]);
 }
 
 // 8 warps per block over a contiguous row chunk; per-block column partials
@@ -1030,7 +1067,7 @@ int embed_bwd_chunked_vec(int dtype, const int32_t* chunks, int nchunks, const i
 int ln_fwd_vec(int dtype, const void* x, int rows, int d, const void* g, const void* b, void* y, float* stats,
                cudaStream_t s) {
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(y) || !al16(g) || !al16(b)) return SFK_EUNSUP;
-  const int blocks = (rows + 3) / 4;
+  const int blocks = (rows + 4 * vec::kLnFwdRows - 1) / (4 * vec::kLnFwdRows);
   if (dtype == SFK_F16)
     launch_pdl(vec::ln_fwd_v<__half>, blocks, 128, 0, s, static_cast<const __half*>(x), rows, d,
                                                  static_cast<const __half*>(g), static_cast<const __half*>(b),
