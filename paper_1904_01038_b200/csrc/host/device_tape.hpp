@@ -150,6 +150,12 @@ class DeviceTape {
   // dtype): the incremental decoder's K/V caches; never differentiated
   int external(const void* data, int rows, int cols);
   cudaStream_t stream() const { return stream_; }
+  // backward on another stream than the forward was recorded on (the caller
+  // orders the two streams); no side-stream work may be pending
+  void set_main_stream(cudaStream_t s) {
+    stream_ = s;
+    cur_ = s;
+  }
   // a18: records the loss node; stats are produced when backward()/finish() runs
   int softmax_xent(int logits, const int32_t* gold, float epsilon);
   // Tape::dropout (tape.cpp:109-121) with the mask drawn from RngStream(seed,

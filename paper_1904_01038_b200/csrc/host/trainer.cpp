@@ -45,6 +45,12 @@ Trainer::~Trainer() {
   if (stream_) cudaStreamDestroy(stream_);
   if (side_) cudaStreamDestroy(side_);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  if (fwd_stream_) cudaStreamDestroy(fwd_stream_);
+  if (ev_upload_) cudaEventDestroy(ev_upload_);
+  for (auto e : fwd_done_)
+    if (e) cudaEventDestroy(e);
+  for (auto e : main_done_)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ovl_events_) cudaEventDestroy(e);
   for (cudaEvent_t e : evpool_) cudaEventDestroy(e);
 }
@@ -113,6 +119,14 @@ void Trainer::init(const Registry& reg) {
   cuda_check(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, p_main), "stream");
   cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, p_side), "side stream");
   cuda_check(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, p_comm), "comm stream");
+  cuda_check(cudaStreamCreateWithPriority(&fwd_stream_, cudaStreamNonBlocking, lo), "forward stream");
+  {
+    const char* e = std::getenv("SQF_FWD_AHEAD");
+    fwd_ahead_ = !(e && std::atoi(e) == 0);
+  }
+  cuda_check(cudaEventCreateWithFlags(&ev_upload_, cudaEventDisableTiming), "event");
+  for (auto& e : fwd_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  for (auto& e : main_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreate(&ev0_), "event");
   for (auto& e : arena_free_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreate(&ev1_), "event");
@@ -158,7 +172,8 @@ void Trainer::init(const Registry& reg) {
     int sms = sfk_num_sms();
     if (sms <= 0) sms = 148;
     gemm_ws_floats_ = int64_t(sms) * 2 * 128 * 256;
-    cuda_check(cudaMalloc(&gemm_ws_, size_t(gemm_ws_floats_) * 2 * 4), "gemm workspace");
+    // [main | side | forward-ahead] stream-K workspaces
+    cuda_check(cudaMalloc(&gemm_ws_, size_t(gemm_ws_floats_) * 3 * 4), "gemm workspace");
   }
   cuda_check(cudaMemsetAsync(counters_, 0, size_t(kCounters) * 4, stream_), "counters");
   cuda_check(cudaMemsetAsync(flag_dev_, 0, 16, stream_), "flag");
@@ -508,34 +523,68 @@ StepStats Trainer::run_step(const std::vector<std::vector<MiniBatch>>& sub, std:
     cuda_check(cudaMemsetAsync(grad_buf(lw), 0, size_t(n_) * esize(), stream_), "grad zero");
   launches_ = 0;
   const bool overlap = overlap_ && local_ == 1 && (world_ > 1 || overlap_sim_) && !dev.empty();
-  for (size_t i = 0; i < dev.size(); ++i) {
+  // Forward-ahead: sub-batch i+1's forward is enqueued on fwd_stream_ before
+  // sub-batch i's backward, so the two run concurrently (the forward needs
+  // only the weights, which do not change inside a step); the backward of
+  // i+1 then continues on the main stream. Results are identical either way.
+  const bool ahead = fwd_ahead_ && fwd_stream_ && (!prof_ || prof_->concurrent) && dev.size() > 1;
+  cudaStream_t fs = ahead ? fwd_stream_ : stream_;
+  if (ahead) {
+    cuda_check(cudaEventRecord(ev_upload_, stream_), "event record");  // batch upload, zeroed grads
+    cuda_check(cudaStreamWaitEvent(fs, ev_upload_, 0), "stream wait");
+  }
+  std::unique_ptr<DeviceTape> tapes[2];
+  CriterionOutput outs[2];
+  auto forward = [&](size_t i) {
     const int lw = which[i].first, a = which[i].second;
     const int w = rank_ * local_ + lw;
     model_->set_train_step(step_ * workers_ * accum_ + int64_t(w) * accum_ + a);
     const int k = int(i & 1);
-    if (arena_busy_[k]) cuda_check(cudaStreamWaitEvent(stream_, arena_free_[k], 0), "arena wait");
+    if (arena_busy_[k]) {
+      // the arena's previous sub-batch: its side-stream work and (when the
+      // forward runs on its own stream) its main-stream backward
+      cuda_check(cudaStreamWaitEvent(fs, arena_free_[k], 0), "arena wait");
+      if (ahead) cuda_check(cudaStreamWaitEvent(fs, main_done_[k], 0), "arena wait");
+    }
     arena_[k].reset();
-    DeviceTape tape(arena_[k], DeviceParams{master_, compute_, grad_buf(lw), n_}, dtype_, stream_);
+    tapes[k] = std::make_unique<DeviceTape>(arena_[k], DeviceParams{master_, compute_, grad_buf(lw), n_}, dtype_, fs);
+    DeviceTape& tape = *tapes[k];
     tape.set_use_hook([this](int64_t off, int64_t n, cudaStream_t st) { param_wait(off, n, st); });
     tape.set_profiler(prof_.get());
     tape.set_counters(counters_, kCounters, &counter_cursor_);
     // a profiling pass serialises everything on the main stream so the
     // per-launch event windows measure each kernel alone (no concurrency)
     if (!prof_ || prof_->concurrent) tape.set_side_stream(side_, &evpool_);
-    tape.set_gemm_workspace(gemm_ws_, gemm_ws_ + gemm_ws_floats_, gemm_ws_floats_);
-    CriterionOutput out = criterion_->compute(*model_, dev[i], tape);
+    float* ws_fwd = ahead ? gemm_ws_ + 2 * gemm_ws_floats_ : gemm_ws_;
+    tape.set_gemm_workspace(ws_fwd, gemm_ws_ + gemm_ws_floats_, gemm_ws_floats_);
+    outs[k] = criterion_->compute(*model_, dev[i], tape);
+    if (ahead) cuda_check(cudaEventRecord(fwd_done_[k], fs), "event record");
+  };
+  if (ahead) forward(0);
+  for (size_t i = 0; i < dev.size(); ++i) {
+    const int k = int(i & 1);
+    if (!ahead) forward(i);
+    else if (i + 1 < dev.size()) forward(i + 1);
+    DeviceTape& tape = *tapes[k];
+    if (ahead) {
+      cuda_check(cudaStreamWaitEvent(stream_, fwd_done_[k], 0), "stream wait");
+      tape.set_main_stream(stream_);
+      tape.set_gemm_workspace(gemm_ws_, gemm_ws_ + gemm_ws_floats_, gemm_ws_floats_);
+    }
     if (overlap && i + 1 == dev.size()) {
       ovl_begin(tape);
       tape.set_grad_hook([this](int64_t off, int64_t n, cudaStream_t) { ovl_on_write(off, n); });
     }
     // the loss-scale multiply is the backward seed (trainer.cpp:237-239)
     const bool last = i + 1 == dev.size();
-    tape.backward(out.loss_node, float(scale), stats_dev_, last);
+    tape.backward(outs[k].loss_node, float(scale), stats_dev_, last);
     if (!last) {
       cuda_check(cudaEventRecord(arena_free_[k], side_), "event record");
+      if (ahead) cuda_check(cudaEventRecord(main_done_[k], stream_), "event record");
       arena_busy_[k] = true;
     }
     launches_ += tape.launches();
+    tapes[k].reset();
   }
   arena_busy_[0] = arena_busy_[1] = false;  // the last backward joined the side stream
   // in-process replicas fold in index order with re-rounding (trainer.cpp:75-87)

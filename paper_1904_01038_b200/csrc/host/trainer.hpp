@@ -256,6 +256,11 @@ class Trainer {
   // ---- bucketed all-reduce overlapped with the last sub-batch's backward
   bool overlap_ = true, overlap_sim_ = false;
   cudaStream_t comm_stream_ = nullptr;
+  // forward-ahead (SQF_FWD_AHEAD, default on): the next sub-batch's forward
+  // on its own stream, concurrent with this sub-batch's backward
+  cudaStream_t fwd_stream_ = nullptr;
+  bool fwd_ahead_ = true;
+  cudaEvent_t ev_upload_ = nullptr, fwd_done_[2] = {nullptr, nullptr}, main_done_[2] = {nullptr, nullptr};
   float* gemm_ws_ = nullptr;          // stream-K partial tiles: [main | side]
   int64_t gemm_ws_floats_ = 0;        // per stream
   std::vector<cudaEvent_t> ovl_events_;
