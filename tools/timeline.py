@@ -48,7 +48,21 @@ def main():
     step_ms = tr.last_step_ms
     tr.set_profile(0)
     print(f"step ms without events {np.mean(plain):.2f}; with timeline events {step_ms:.2f}; tokens {s['ntokens']}")
-    for st, name in ((0, "main"), (1, "side")):
+    def union(iv):
+        tot, cur = 0.0, None
+        for t0, t1 in sorted(iv):
+            if cur is None or t0 > cur[1]:
+                if cur:
+                    tot += cur[1] - cur[0]
+                cur = [t0, t1]
+            else:
+                cur[1] = max(cur[1], t1)
+        return tot + (cur[1] - cur[0] if cur else 0.0)
+    allv = [(float(r[2]), float(r[3])) for r in tl]
+    if allv:
+        span = max(t1 for _, t1 in allv) - min(t0 for t0, _ in allv)
+        print(f"any stream busy {union(allv):.2f} ms of span {span:.2f} ms")
+    for st, name in ((0, "main"), (1, "side"), (2, "comm"), (3, "forward-ahead")):
         rows = tl[tl[:, 0] == st]
         if not len(rows):
             continue
