@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(Args a) {
 // shared memory. Same arithmetic, in the same order, as bwd_dq_k + bwd_dkv_k.
 // R = rows per CTA: 64 (4 warps) for widths <= 64, 32 (2 warps) for widths <= 32
 template <typename T, int DH, int R>
-__global__ void __launch_bounds__(R == 32 ? R * 4 : R * 2, DH <= 64 ? 3 : (R == 32 ? 2 : 1)) bwd_small_k(Args a) {
+__global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_small_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
@@ -593,19 +593,12 @@ __global__ void __launch_bounds__(R == 32 ? R * 4 : R * 2, DH <= 64 ? 3 : (R == 
   }
   stage_wait();
   __syncthreads();
-  // R = 32 (SPLIT): warps [0, R/16) compute dQ (16 query rows each) while
-  // warps [R/16, R/8) compute dK and dV (16 key rows each), concurrently once
-  // D is known. R = 64: every warp does its dQ rows, then its dK/dV rows
-  // (register budget: 3 CTAs of 4 warps per SM).
-  constexpr bool SPLIT = R == 32;
-  const bool dq_warp = SPLIT ? warp < R / 16 : true;
-  const bool kv_warp = SPLIT ? warp >= R / 16 : true;
-  const int r0 = (SPLIT && !dq_warp ? warp - R / 16 : warp) * 16;
+  const int r0 = warp * 16;
   const float l2e = 1.4426950408889634f, c2 = a.sc * l2e;
-  // ---- D = rowsum(dO * O) for the dQ warps' rows, shared through Ds
-  const int row_a = r0 + g, row_b = row_a + 8;
-  float D_a = 0.f, D_b = 0.f;
-  if (dq_warp && r0 < a.qw) {
+  // ---- phase 1: D and dQ for query rows r0..r0+15
+  if (r0 < a.qw) {
+    const int row_a = r0 + g, row_b = row_a + 8;
+    float D_a = 0.f, D_b = 0.f;
     // rows past qw are zero-filled in Gs/Os, so their D is 0; each lane of a
     // quad takes a contiguous quarter of the row (16-byte shared loads)
     if constexpr (DH % 32 == 0) {
@@ -638,10 +631,6 @@ __global__ void __launch_bounds__(R == 32 ? R * 4 : R * 2, DH <= 64 ? 3 : (R == 
       if (row_a < a.qw) Ds[row_a] = D_a;
       if (row_b < a.qw) Ds[row_b] = D_b;
     }
-  }
-  __syncthreads();  // Ds complete
-  // ---- phase 1 (dQ warps): dQ for query rows r0..r0+15
-  if (dq_warp && r0 < a.qw) {
     uint32_t qa[DH / 16][4], ga[DH / 16][4];
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks) {
@@ -711,8 +700,9 @@ __global__ void __launch_bounds__(R == 32 ? R * 4 : R * 2, DH <= 64 ? 3 : (R == 
             MmaT<T>::pack(dq[nt][2] * a.sc, dq[nt][3] * a.sc);
     }
   }
-  // ---- phase 2 (dK/dV warps): dK, dV for key rows r0..r0+15
-  if (!kv_warp || r0 >= a.kw) return;
+  __syncthreads();  // Ds complete
+  // ---- phase 2: dK, dV for key rows r0..r0+15
+  if (r0 >= a.kw) return;
   const int nq = a.qw;
   const int key_a = r0 + g, key_b = key_a + 8;
   float dk[DH / 8][4], dv[DH / 8][4];
@@ -877,7 +867,7 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   if (short32) {
     constexpr int R = 32, QP = R + 32;
     const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
-    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 4 * R, smem_s, st, a);
+    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
     return check_launch("sfk_attention_bwd(small32)");
   }
   if (a.qw <= kRows && a.kw <= kRows) {
