@@ -73,7 +73,9 @@ __global__ void __launch_bounds__(kThreads) beam_topk_k(const T* __restrict__ lo
 
   for (int j = 0; j < kk; ++j) {
     const Best p = prev;
-    Best b{-DBL_MAX, 0x7fffffff};
+    // -inf keys still rank (ties to the lower token), as in the reference's
+    // stable sort of every (hypothesis, token) candidate; only NaN never does
+    Best b{-INFINITY, 0x7fffffff};
     for (int v = threadIdx.x; v < V; v += kThreads) {
       const Best cnd{raw ? double(x(v)) : c + double(x(v) - lse), v};
       if (before(p, cnd) && before(cnd, b)) b = cnd;

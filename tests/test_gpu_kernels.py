@@ -522,6 +522,45 @@ def test_gather_rows_reorders_every_matrix():
                                stream()) != 0
 
 
+@pytest.mark.parametrize("row_elems,copy", [(97, 50), (33, 33), (10, 3)])
+def test_gather_rows_any_row_size(row_elems, copy):
+    """fp32 caches of an odd model width have rows that are not 16-byte
+    multiples: the gather falls back to 4-byte (or byte) copies instead of
+    refusing."""
+    lib = L()
+    rows, nmat = 21, 3
+    src = torch.randn(nmat, rows, row_elems, device="cuda")
+    dst = torch.zeros_like(src)
+    idx = torch.randint(0, rows, (rows,), device="cuda", dtype=torch.int32)
+    lib.check(lib.sfk_gather_rows(ptr(src), ptr(dst), ptr(idx), rows, row_elems * 4, copy * 4, nmat,
+                                  rows * row_elems * 4, stream()), kernel=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dst[..., :copy], src[:, idx.long(), :copy]) and not dst[..., copy:].any()
+
+
+def test_beam_topk_ranks_minus_inf_candidates():
+    """A row with fewer than kk finite log-probs still returns kk distinct
+    tokens: the -inf ones in token order (the reference's stable sort lists
+    them), never padding with repeated eos."""
+    lib = L()
+    V, kk, rows = 50, 8, 2
+    lg = torch.full((rows, V), float("-inf"), device="cuda")
+    lg[0, [3, 7, 11]] = torch.tensor([1.0, 2.0, 0.5], device="cuda")
+    lg[1, :] = torch.randn(V, device="cuda")
+    lse = torch.zeros(rows, device="cuda")
+    eos_lp = torch.zeros(rows, device="cuda")
+    tok = torch.zeros(rows, kk, dtype=torch.int32, device="cuda")
+    lp = torch.zeros(rows, kk, device="cuda")
+    cum = torch.zeros(rows, dtype=torch.float64, device="cuda")
+    lib.check(lib.sfk_beam_topk(0, ptr(lg), V, rows, V, ptr(cum), kk, 2, ptr(lse), ptr(eos_lp), ptr(tok), ptr(lp),
+                                stream()), kernel=True)
+    torch.cuda.synchronize()
+    t0 = tok[0].tolist()
+    assert t0[:3] == [7, 3, 11]
+    assert t0[3:] == [0, 1, 2, 4, 5]  # -inf candidates, lowest token first
+    assert len(set(tok[1].tolist())) == kk
+
+
 @pytest.mark.parametrize("dt,V,kk", [(0, 1000, 8), (1, 32768, 8), (2, 5000, 10), (0, 7, 7)])
 def test_beam_topk_order_and_values(dt, V, kk):
     """sfk_beam_topk against a host ranking of every candidate: key = cum +
