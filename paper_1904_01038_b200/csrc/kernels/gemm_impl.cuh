@@ -834,14 +834,20 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
-template <int BN, bool A_MN, bool B_MN, typename T>
+// FL / tma_store as in gemm_tc2: whole tiles leave through the TMA-store
+// epilogue (compile-time flags where FL >= 0); stream-K parts keep the
+// per-thread epilogue of their fix-up
+template <int BN, bool A_MN, bool B_MN, int FL, typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const Epi e, int M,
-            int N, int K, int vec_ok, const Sk sk) {
+    gemm_tc(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+            const __grid_constant__ CUtensorMap tcm, const Epi e, int M, int N, int K, int vec_ok, int tma_store,
+            const Sk sk) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  // [stages][epilogue staging: 8 warps x 4 KB, 1024-aligned][barriers]
+  uint8_t* stg_region = smem + C::STAGES * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_region + kEpiWarps * kStgFloats * 4);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -957,7 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Epilogue: TMEM gives each thread one row x 32 columns; the 32x32 fp32
     // block bounces through shared memory so a warp then reads/writes 8 rows x
     // 64 contiguous bytes per instruction (coalesced) instead of 32 rows.
-    float* stg = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 2) * kStgFloats;
+    float* stg = reinterpret_cast<float*>(stg_region) + (warp - 2) * kStgFloats;
     volatile int* last_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
     Sched sc(tiles, kblocks, sk.sk_tiles);
     int t = 0, it = 0, tile, kb0, kb1;
@@ -972,7 +978,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[buf], (t >> 1) & 1);
       fence_after();
       if (kb0 == 0 && kb1 == kblocks) {
-        epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
+        if (tma_store)
+          epilogue_tile_tma<BN, FL, T>(e, &tcm, tmem_base + buf * BN, warp, lane, saddr(stg), m0, n0, M, N);
+        else
+          epilogue_tile<BN, T>(e, tmem_base + buf * BN, warp, lane, stg, m0, n0, M, N, vec_ok);
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -1004,6 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++t;
     }
   }
+  if (tma_store && warp >= 2 && lane == 0) bulk_wait0();  // C written before the CTA retires
   fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -1333,10 +1343,10 @@ inline int num_sms_cached() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, typename T>
+template <int BN, bool A_MN, bool B_MN, int FL, typename T>
 int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, int sk_tiles, int sk_grid) {
   using C = Cfg<BN>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tcm;
   // A: K-major [m][k] -> map cols=k rows=m, box rows 128; MN-major [k][m] -> cols=m rows=k, box 64x64
   bool ok = A_MN ? make_map(&ta, g->dtype, g->a, g->m, g->k, g->lda, 64)
                  : make_map(&ta, g->dtype, g->a, g->k, g->m, g->lda, BM);
@@ -1346,9 +1356,11 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
     set_error("sfk_gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
     return SFK_EINVAL;
   }
+  const bool tma_store = vec_ok && make_map(&tcm, g->dtype, g->c, g->n, g->m, g->ldc, 32);
+  if (!tma_store) tcm = ta;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(gemm_tc<BN, A_MN, B_MN, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+    if (cudaFuncSetAttribute(gemm_tc<BN, A_MN, B_MN, FL, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
         cudaSuccess)
       return check_launch("sfk_gemm: smem attribute");
     attr_set = true;
@@ -1356,8 +1368,8 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
   const int grid = sk_tiles > 0 ? sk_grid : (tiles < num_sms_cached() ? tiles : num_sms_cached());
   Sk sk{sk_tiles > 0 ? g->workspace : nullptr, sk_tiles > 0 ? g->counters : nullptr, sk_tiles, g->bias_grad};
-  launch_pdl(gemm_tc<BN, A_MN, B_MN, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, e, g->m, g->n, g->k,
-             vec_ok ? 1 : 0, sk);
+  launch_pdl(gemm_tc<BN, A_MN, B_MN, FL, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, tcm, e, g->m,
+             g->n, g->k, vec_ok ? 1 : 0, tma_store ? 1 : 0, sk);
   return check_launch("sfk_gemm(tcgen05)");
 }
 
@@ -1538,17 +1550,33 @@ int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) 
 #undef SFK_TC2
 #undef SFK_TC2_FL
   }
+  // 1-CTA tiles (small M: the decoder's per-position GEMMs): compile-time
+  // epilogues for the forward combinations, runtime flags otherwise
+  const int f1 = g->flags;
+  constexpr int P1 = SFK_EPI_PREROUND, B1 = SFK_EPI_BIAS, RL1 = SFK_EPI_RELU, RS1 = SFK_EPI_RESIDUAL;
+#define SFK_TC_FWD(BNV)                                                                               \
+  if (f1 == P1) return launch<BNV, false, false, P1, T>(g, e, vec_ok, s, skt, sk_grid);               \
+  if (f1 == (P1 | B1)) return launch<BNV, false, false, P1 | B1, T>(g, e, vec_ok, s, skt, sk_grid);   \
+  if (f1 == (P1 | B1 | RL1)) return launch<BNV, false, false, P1 | B1 | RL1, T>(g, e, vec_ok, s, skt, sk_grid); \
+  if (f1 == (P1 | B1 | RS1)) return launch<BNV, false, false, P1 | B1 | RS1, T>(g, e, vec_ok, s, skt, sk_grid); \
+  return launch<BNV, false, false, -1, T>(g, e, vec_ok, s, skt, sk_grid);
 #define SFK_TC(BNV)                                                         \
   switch (layout) {                                                         \
-    case 0: return launch<BNV, false, false, T>(g, e, vec_ok, s, skt, sk_grid);      \
-    case 1: return launch<BNV, false, true, T>(g, e, vec_ok, s, skt, sk_grid);       \
-    case 3: return launch<BNV, true, true, T>(g, e, vec_ok, s, skt, sk_grid);        \
-    default: return launch<BNV, true, false, T>(g, e, vec_ok, s, skt, sk_grid);      \
+    case 0: SFK_TC_FWD(BNV)                                                 \
+    case 1: return launch<BNV, false, true, -1, T>(g, e, vec_ok, s, skt, sk_grid);       \
+    case 3: return launch<BNV, true, true, -1, T>(g, e, vec_ok, s, skt, sk_grid);        \
+    default: return launch<BNV, true, false, -1, T>(g, e, vec_ok, s, skt, sk_grid);      \
   }
   if (bn == 256) { SFK_TC(256) }
   if (bn == 128) { SFK_TC(128) }
-  SFK_TC(64)
+  switch (layout) {
+    case 0: return launch<64, false, false, -1, T>(g, e, vec_ok, s, skt, sk_grid);
+    case 1: return launch<64, false, true, -1, T>(g, e, vec_ok, s, skt, sk_grid);
+    case 3: return launch<64, true, true, -1, T>(g, e, vec_ok, s, skt, sk_grid);
+    default: return launch<64, true, false, -1, T>(g, e, vec_ok, s, skt, sk_grid);
+  }
 #undef SFK_TC
+#undef SFK_TC_FWD
 }
 // per-dtype entry points (gemm_f16.cu / gemm_bf16.cu)
 int dispatch_f16(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s);
