@@ -120,6 +120,7 @@ __device__ __forceinline__ void stage(T* s, int lds, const T* g, int64_t ldg, in
   const int64_t sstep = int64_t(step) * ldg;
   uint32_t dst = su32(s + r * lds + c);
   const uint32_t dstep = uint32_t(step * lds * int(sizeof(T)));
+#pragma unroll 4
   for (; r < rows_pad; r += step, src += sstep, dst += dstep) {
     const bool ok = cok && r < n;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(ok ? src : g), "r"(ok ? 16 : 0)
@@ -138,6 +139,7 @@ struct Args {
   int64_t ldout, lddq, lddk, lddv;
   float2* stats;
   float* dsum;
+  int vec_dkv;  // dK/dV rows 16-byte aligned (ld % 8 == 0, aligned bases): whole-chunk stores
 };
 
 __device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.causal ? t + 1 : a.klen[b]; }
@@ -778,21 +780,41 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
       }
     }
   }
-  T* dko = static_cast<T*>(a.dk) + h * a.dh;
-  T* dvo = static_cast<T*>(a.dv) + h * a.dh;
+  // this warp's K/V rows are consumed (fragments in registers, phase 1 done
+  // by every warp): stage dK and dV there, then write whole 16-byte chunks
+  T* Ks_w = Ks + r0 * LD;
+  T* Vs_w = Vs + r0 * LD;
 #pragma unroll
   for (int nt = 0; nt < DH / 8; ++nt) {
     const int c = nt * 8 + 2 * tq;
-    if (c >= a.dh) continue;
-    if (key_a < a.kw) {
-      *reinterpret_cast<uint32_t*>(dko + (krow0 + key_a) * a.lddk + c) =
-          MmaT<T>::pack(dk[nt][0] * a.sc, dk[nt][1] * a.sc);
-      *reinterpret_cast<uint32_t*>(dvo + (krow0 + key_a) * a.lddv + c) = MmaT<T>::pack(dv[nt][0], dv[nt][1]);
+    *reinterpret_cast<uint32_t*>(Ks_w + g * LD + c) = MmaT<T>::pack(dk[nt][0] * a.sc, dk[nt][1] * a.sc);
+    *reinterpret_cast<uint32_t*>(Ks_w + (g + 8) * LD + c) = MmaT<T>::pack(dk[nt][2] * a.sc, dk[nt][3] * a.sc);
+    *reinterpret_cast<uint32_t*>(Vs_w + g * LD + c) = MmaT<T>::pack(dv[nt][0], dv[nt][1]);
+    *reinterpret_cast<uint32_t*>(Vs_w + (g + 8) * LD + c) = MmaT<T>::pack(dv[nt][2], dv[nt][3]);
+  }
+  __syncwarp();
+  T* dko = static_cast<T*>(a.dk) + h * a.dh;
+  T* dvo = static_cast<T*>(a.dv) + h * a.dh;
+  if (a.vec_dkv) {
+    constexpr int VPR = DH / 8;
+#pragma unroll
+    for (int q = 0; q < 16 * VPR / 32; ++q) {
+      const int idx = q * 32 + lane, rr = idx / VPR, cc = (idx % VPR) * 8;
+      const int key = r0 + rr;
+      if (key < a.kw && cc < a.dh) {
+        *reinterpret_cast<uint4*>(dko + (krow0 + key) * a.lddk + cc) =
+            *reinterpret_cast<const uint4*>(Ks_w + rr * LD + cc);
+        *reinterpret_cast<uint4*>(dvo + (krow0 + key) * a.lddv + cc) =
+            *reinterpret_cast<const uint4*>(Vs_w + rr * LD + cc);
+      }
     }
-    if (key_b < a.kw) {
-      *reinterpret_cast<uint32_t*>(dko + (krow0 + key_b) * a.lddk + c) =
-          MmaT<T>::pack(dk[nt][2] * a.sc, dk[nt][3] * a.sc);
-      *reinterpret_cast<uint32_t*>(dvo + (krow0 + key_b) * a.lddv + c) = MmaT<T>::pack(dv[nt][2], dv[nt][3]);
+  } else {
+    for (int idx = lane; idx < 16 * a.dh; idx += 32) {
+      const int rr = idx / a.dh, cc = idx % a.dh, key = r0 + rr;
+      if (key < a.kw) {
+        dko[(krow0 + key) * a.lddk + cc] = Ks_w[rr * LD + cc];
+        dvo[(krow0 + key) * a.lddv + cc] = Vs_w[rr * LD + cc];
+      }
     }
   }
 }
@@ -828,6 +850,8 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   a.lddv = s->lddv;
   a.stats = reinterpret_cast<float2*>(s->stats);
   a.dsum = s->scratch;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  a.vec_dkv = (s->lddk % 8 == 0) && (s->lddv % 8 == 0) && (s->dh % 8 == 0) && al16(s->dk) && al16(s->dv) ? 1 : 0;
   constexpr int LD = DH + 8;
   const int kpad = (a.kw + 63) & ~63, qpad = ((a.qw + 63) & ~63) + 64;
   static bool configured = false;
