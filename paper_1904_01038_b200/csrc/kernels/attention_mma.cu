@@ -8,6 +8,8 @@
 //            dS = P (dP - D), dQ = sc dS K;  D = rowsum(dO * O) (per query block)
 //   bwd_dkv  S^T = K Q^T, dP^T = V dO^T, dV = P^T dO, dK = sc dS^T Q (per key block)
 // Spans: query row t of sentence b sees keys j < (causal ? t+1 : len[b]).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sfk {
@@ -561,15 +563,17 @@ __global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(Args a) {
 // once and runs both halves of the backward -- dQ per query warp, then dK/dV
 // per key warp -- with D = rowsum(dO * O) and the saved softmax stats kept in
 // shared memory. Same arithmetic, in the same order, as bwd_dq_k + bwd_dkv_k.
-// R = rows per CTA: 64 (4 warps) for widths <= 64, 32 (2 warps) for widths <= 32
+// R = rows per CTA: 128 (8 warps) for widths <= 128, 64 (4 warps) for widths
+// <= 64, 32 (2 warps) for widths <= 32
 template <typename T, int DH, int R>
-__global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_small_k(Args a) {
+__global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (R == 128 ? (DH <= 64 ? 2 : 1) : (DH <= 64 ? 3 : 1)))
+    bwd_small_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
   constexpr int QP = R + 32;  // staged query rows (zero-padded: dK/dV chunks run up to 31 past qw)
-  constexpr int NC = 32;  // query columns per dK/dV chunk (register budget: 3 CTAs per SM)
+  constexpr int NC = R == 128 ? 16 : 32;  // query columns per dK/dV chunk (register budget: 2-3 CTAs per SM)
   const int b = blockIdx.z, h = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];
@@ -645,9 +649,12 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (DH <= 64 ? 3 : 1)) bwd_s
     float dq[DH / 8][4];
 #pragma unroll
     for (int i = 0; i < DH / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
-    {
-      constexpr int kc = 0;  // all keys fit one R-key chunk
-      constexpr int NT = R / 8;
+    // keys in chunks of up to 64 (dQ accumulates across chunks; the saved
+    // stats make each chunk's probabilities final)
+    constexpr int KC = R == 64 ? 64 : 32;  // 32 at R 128: 2 CTAs/SM without spills
+    constexpr int NT = KC / 8;
+    const int wkeys = a.causal ? min(nk, r0 + 16) : nk;
+    for (int kc = 0; kc < wkeys; kc += KC) {
       float s[NT][4], dp[NT][4];
 #pragma unroll
       for (int i = 0; i < NT; ++i)
@@ -864,9 +871,17 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_small_k<T, DH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_small_k<T, DH, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(fwd_k<T, DH, 128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
   const dim3 gq((a.qw + kRows - 1) / kRows, a.heads, a.batch);
+  // SQF_ATTN_R128=0: widths 65..128 on the split (per 64-row block) kernels
+  static const bool r128 = [] {
+    const char* e = std::getenv("SQF_ATTN_R128");
+    return !(e && std::atoi(e) == 0);
+  }();
+  auto kw128 = [&] { return r128 && a.kw <= 2 * kRows; };
   // sentences of <= 32 positions: 32-row CTAs of 2 warps, so no warp idles
   const bool short32 = a.qw <= 32 && (bwd ? a.kw <= 32 : true);
   if (!bwd) {
@@ -879,6 +894,10 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
         launch_pdl(fwd_k<T, DH, 32, 32>, dim3(1, a.heads, a.batch), 64, smem, st, a);
       else
         launch_pdl(fwd_k<T, DH, 32, 64>, dim3(1, a.heads, a.batch), 64, smem, st, a);
+    } else if (a.qw > kRows && a.qw <= 2 * kRows && kw128()) {
+      // one 8-warp CTA per (sentence, head): K/V staged once
+      const size_t smem = size_t(2 * kRows + 2 * kp) * LD * sizeof(T);
+      launch_pdl(fwd_k<T, DH, 128, 64>, dim3(1, a.heads, a.batch), 256, smem, st, a);
     } else {
       const size_t smem = size_t(kRows + 2 * kp) * LD * sizeof(T);
       if (k32)
@@ -899,6 +918,12 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
     launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
     return check_launch("sfk_attention_bwd(small)");
+  }
+  if (a.qw <= 2 * kRows && kw128()) {
+    constexpr int R = 128, QP = R + 32;
+    const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
+    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
+    return check_launch("sfk_attention_bwd(small128)");
   }
   const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
   launch_pdl(bwd_dq_k<T, DH>, gq, kWarps * 32, smem_q, st, a);

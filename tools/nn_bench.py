@@ -66,12 +66,13 @@ def main():
 
 def attention():
     """Attention fwd / bwd at C4 shapes: self-attention on fused QKV rows
-    (ld 3d), 16 heads of 64; short (width 30) and long (width 120) batches."""
+    (ld 3d), 16 heads of 64; batches of 3584 tokens at widths 16..200."""
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
     H, dh = 16, 64
     d = H * dh
-    for batch, w, causal in ((112, 30, False), (112, 30, True), (28, 120, False), (28, 120, True)):
+    shapes = [(3584 // w, w, c) for w in (16, 30, 48, 64, 96, 120, 200) for c in (False, True)]
+    for batch, w, causal in shapes:
         rows = batch * w
         qkv = (torch.randn(rows, 3 * d, device="cuda") * 0.5).half()
         o = torch.zeros(rows, d, device="cuda").half()
