@@ -71,7 +71,8 @@ typedef struct sfk_gemm_args {
   const void* mask; int64_t ldm;  /* [m x n]        (SFK_EPI_MASK)     */
   int flags;
   int force_simt;                 /* testing: run the SIMT kernel for any dtype */
-  int tile_n;                     /* tuning: force the tcgen05 tile width (64/128/256), 0 = auto */
+  int tile_n;                     /* tuning: force the tcgen05 tile width (64/128/256), 0 = auto,
+                                     < 0 = auto, CTA-pair tiles narrow only past -tile_n % gain */
   int pair;                       /* tuning: 1 = CTA-pair (cta_group::2) 256-row tiles, -1 = single-CTA, 0 = auto */
   /* stream-K (optional): with a workspace of >= 2*SMs*128*256 floats and
    * zeroed counters (>= tiles; re-armed to 0 by the kernel) the 128x256

@@ -339,9 +339,15 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
     const char* e = std::getenv("SQF_PAIR");
     return e ? std::atoi(e) : 1;
   }();
+  // SQF_PAIR_BN: 256 (default) always 256-wide pair tiles; -S picks 128 when its
+  // wave efficiency beats 256's by more than S percent (0: any gain)
+  static const int pair_bn = [] {
+    const char* e = std::getenv("SQF_PAIR_BN");
+    return e ? std::atoi(e) : 256;
+  }();
   if (pair_env && cat != Profiler::GemmWgrad && m >= 512 && dtype_ != SFK_F32) {
     g.pair = 1;
-    g.tile_n = 256;
+    g.tile_n = pair_bn;
   }
   float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
   static const int sk_mode = [] {

@@ -1484,6 +1484,18 @@ inline int pick_bn(int m, int n) {
   return best;
 }
 
+// CTA-pair tile width (256 x BN pair tiles over SMs/2 pairs) by wave
+// efficiency; ties and near-ties (within `slack`) go to the 256-wide tile
+inline int pick_bn2(int m, int n, double slack) {
+  const int pairs = num_sms_cached() / 2;
+  auto eff = [&](int bn) {
+    const long tiles = long((m + 255) / 256) * ((n + bn - 1) / bn);
+    const long waves = (tiles + pairs - 1) / pairs;
+    return double(tiles) / double(waves * pairs);
+  };
+  return eff(128) > eff(256) * (1.0 + slack) ? 128 : 256;
+}
+
 // Stream-K plan for a 128 x 256 1-CTA GEMM: returns the stream-K region size
 // in tiles (0 = plain data-parallel) and the grid through *grid. Measured on
 // B200, the fp32 partial tiles (128 KB each) make the fix-up expensive, so
@@ -1514,7 +1526,9 @@ template <typename T>
 int dispatch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
   int sk_grid = 0;
   const int skt = (g->tile_n == 0 || g->tile_n == 256) && g->pair <= 0 && !g->bias_grad ? pick_stream_k(g, &sk_grid) : 0;
-  const int bn = skt > 0 ? 256 : g->tile_n ? g->tile_n : pick_bn(g->m, g->n);
+  const int bn = skt > 0 ? 256 : g->tile_n > 0 ? g->tile_n
+                               : g->pair > 0 ? pick_bn2(g->m, g->n, g->tile_n < 0 ? -g->tile_n * 0.01 : 0.0)
+                                             : pick_bn(g->m, g->n);
   const int layout = (g->a_kmajor ? 0 : 2) | (g->b_kmajor ? 0 : 1);
   if (g->pair > 0) {
     // compile-time epilogues for the combinations the training step uses:

@@ -3,6 +3,8 @@
 // layer norm forward/backward, bias-grad column partials. Same arithmetic
 // and rounding points as the scalar kernels in nn.cu (which remain the fp32
 // parity-mode path); only the memory access pattern differs.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sfk {
@@ -172,78 +174,79 @@ __global__ void __launch_bounds__(128) embed_bwd_fold_v(const int4* __restrict__
 
 constexpr int kMaxCh = 4;  // d <= 32 lanes * 4 chunks * 8 = 1024
 
-// One warp per two rows (rows w and w + rows_per_block/2 of the block). Every
-// global load of both rows and of gamma/beta is issued up front, so a warp
-// pays one memory round trip, gamma/beta are fetched once per two rows, and
-// the two rows' reductions interleave.
-constexpr int kLnFwdRows = 2;
-template <typename T>
-__global__ void __launch_bounds__(128) ln_fwd_v(const T* __restrict__ x, int rows, int d, const T* __restrict__ g,
-                                               const T* __restrict__ b, T* __restrict__ y,
-                                               float2* __restrict__ stats) {
+// One warp per RW rows (rows w, w + nw, ... of the block). Every global load
+// of the rows and of gamma/beta is issued up front (one memory round trip per
+// warp), x is converted to fp32 once and kept in registers, and the rows'
+// reductions interleave. RW = 1 with 256-thread blocks (default: 24 warps per
+// SM at C4 shapes) or RW = 2 with 128-thread blocks (SQF_LN_FWD_ROWS=2).
+template <typename T, int RW>
+__global__ void __launch_bounds__(RW == 1 ? 256 : 128) ln_fwd_v(const T* __restrict__ x, int rows, int d,
+                                                              const T* __restrict__ g, const T* __restrict__ b,
+                                                              T* __restrict__ y, float2* __restrict__ stats) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-  const int r0 = blockIdx.x * nw * kLnFwdRows + warp;
+  const int r0 = blockIdx.x * nw * RW + warp;
   if (r0 >= rows) return;
-  int rr[kLnFwdRows];
-  bool ok[kLnFwdRows];
+  int rr[RW];
+  bool ok[RW];
 #pragma unroll
-  for (int k = 0; k < kLnFwdRows; ++k) {
+  for (int k = 0; k < RW; ++k) {
     rr[k] = r0 + k * nw;
     ok[k] = rr[k] < rows;
   }
-  uint4 xu[kLnFwdRows][kMaxCh], gu[kMaxCh], bu[kMaxCh];
-#pragma unroll
-  for (int i = 0; i < kMaxCh; ++i) {
-    const int c = (lane + 32 * i) * 8;
-    if (c < d) {
-#pragma unroll
-      for (int k = 0; k < kLnFwdRows; ++k)
-        if (ok[k]) xu[k][i] = *reinterpret_cast<const uint4*>(x + int64_t(rr[k]) * d + c);
-      gu[i] = __ldg(reinterpret_cast<const uint4*>(g + c));
-      bu[i] = __ldg(reinterpret_cast<const uint4*>(b + c));
-    }
-  }
-  float mean[kLnFwdRows], rstd[kLnFwdRows];
+  float xf[RW][kMaxCh][8];
   {
-    float sm[kLnFwdRows];
+    uint4 xu[RW][kMaxCh];
 #pragma unroll
-    for (int k = 0; k < kLnFwdRows; ++k) {
-      sm[k] = 0.f;
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
 #pragma unroll
-      for (int i = 0; i < kMaxCh; ++i) {
-        const int c = (lane + 32 * i) * 8;
-        if (c < d && ok[k]) {
-          float v[8];
-          V8<T>::unpack(xu[k][i], v);
+      for (int k = 0; k < RW; ++k)
+        if (c < d && ok[k]) xu[k][i] = *reinterpret_cast<const uint4*>(x + int64_t(rr[k]) * d + c);
+    }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) sm[k] += v[e];
-        }
+    for (int i = 0; i < kMaxCh; ++i) {
+      const int c = (lane + 32 * i) * 8;
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        if (c < d && ok[k]) V8<T>::unpack(xu[k][i], xf[k][i]);
+        else
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xf[k][i][e] = 0.f;
       }
     }
+  }
+  float mean[RW], rstd[RW];
+  {
+    float sm[RW];
 #pragma unroll
-    for (int k = 0; k < kLnFwdRows; ++k) mean[k] = __fdiv_rn(warp_sum(sm[k]), float(d));
-    float q[kLnFwdRows];
+    for (int k = 0; k < RW; ++k) {
+      sm[k] = 0.f;
 #pragma unroll
-    for (int k = 0; k < kLnFwdRows; ++k) {
+      for (int i = 0; i < kMaxCh; ++i)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sm[k] += xf[k][i][e];
+    }
+#pragma unroll
+    for (int k = 0; k < RW; ++k) mean[k] = __fdiv_rn(warp_sum(sm[k]), float(d));
+    float q[RW];
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
       q[k] = 0.f;
 #pragma unroll
       for (int i = 0; i < kMaxCh; ++i) {
         const int c = (lane + 32 * i) * 8;
-        if (c < d && ok[k]) {
-          float v[8];
-          V8<T>::unpack(xu[k][i], v);
+        if (c < d)
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const float t = __fsub_rn(v[e], mean[k]);
+            const float t = __fsub_rn(xf[k][i][e], mean[k]);
             q[k] = __fadd_rn(q[k], __fmul_rn(t, t));
           }
-        }
       }
     }
 #pragma unroll
-    for (int k = 0; k < kLnFwdRows; ++k) {
+    for (int k = 0; k < RW; ++k) {
       const float var = __fdiv_rn(warp_sum(q[k]), float(d));
       rstd[k] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
     }
@@ -253,23 +256,22 @@ __global__ void __launch_bounds__(128) ln_fwd_v(const T* __restrict__ x, int row
     const int c = (lane + 32 * i) * 8;
     if (c < d) {
       float gg[8], bb[8];
-      V8<T>::unpack(gu[i], gg);
-      V8<T>::unpack(bu[i], bb);
+      V8<T>::unpack(__ldg(reinterpret_cast<const uint4*>(g + c)), gg);
+      V8<T>::unpack(__ldg(reinterpret_cast<const uint4*>(b + c)), bb);
 #pragma unroll
-      for (int k = 0; k < kLnFwdRows; ++k) {
+      for (int k = 0; k < RW; ++k) {
         if (!ok[k]) continue;
-        float v[8], o[8];
-        V8<T>::unpack(xu[k][i], v);
+        float o[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e)
-          o[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v[e], mean[k]), rstd[k]), gg[e]), bb[e]);
+          o[e] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xf[k][i][e], mean[k]), rstd[k]), gg[e]), bb[e]);
         V8<T>::store(y + int64_t(rr[k]) * d + c, o);
       }
     }
   }
   if (lane == 0)
 #pragma unroll
-    for (int k = 0; k < kLnFwdRows; ++k)
+    for (int k = 0; k < RW; ++k)
       if (ok[k]) stats[rr[k]] = make_float2(mean[k], rstd[k]);
 }
 
@@ -1067,15 +1069,22 @@ int embed_bwd_chunked_vec(int dtype, const int32_t* chunks, int nchunks, const i
 int ln_fwd_vec(int dtype, const void* x, int rows, int d, const void* g, const void* b, void* y, float* stats,
                cudaStream_t s) {
   if (dtype == SFK_F32 || d % 8 || d > 1024 || !al16(x) || !al16(y) || !al16(g) || !al16(b)) return SFK_EUNSUP;
-  const int blocks = (rows + 4 * vec::kLnFwdRows - 1) / (4 * vec::kLnFwdRows);
-  if (dtype == SFK_F16)
-    launch_pdl(vec::ln_fwd_v<__half>, blocks, 128, 0, s, static_cast<const __half*>(x), rows, d,
-                                                 static_cast<const __half*>(g), static_cast<const __half*>(b),
-                                                 static_cast<__half*>(y), reinterpret_cast<float2*>(stats));
-  else
-    launch_pdl(vec::ln_fwd_v<__nv_bfloat16>, blocks, 128, 0, s, 
-        static_cast<const __nv_bfloat16*>(x), rows, d, static_cast<const __nv_bfloat16*>(g),
-        static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(y), reinterpret_cast<float2*>(stats));
+  static const int rw = [] {
+    const char* e = std::getenv("SQF_LN_FWD_ROWS");
+    return e && std::atoi(e) == 2 ? 2 : 1;
+  }();
+  auto go = [&](auto tag) {
+    using T = decltype(tag);
+    const T* xt = static_cast<const T*>(x);
+    if (rw == 1)
+      launch_pdl(vec::ln_fwd_v<T, 1>, (rows + 7) / 8, 256, 0, s, xt, rows, d, static_cast<const T*>(g),
+                 static_cast<const T*>(b), static_cast<T*>(y), reinterpret_cast<float2*>(stats));
+    else
+      launch_pdl(vec::ln_fwd_v<T, 2>, (rows + 7) / 8, 128, 0, s, xt, rows, d, static_cast<const T*>(g),
+                 static_cast<const T*>(b), static_cast<T*>(y), reinterpret_cast<float2*>(stats));
+  };
+  if (dtype == SFK_F16) go(__half{});
+  else go(__nv_bfloat16{});
   return check_launch("sfk_layernorm_fwd(vec)");
 }
 
