@@ -9,6 +9,7 @@
 //   bwd_dkv  S^T = K Q^T, dP^T = V dO^T, dV = P^T dO, dK = sc dS^T Q (per key block)
 // Spans: query row t of sentence b sees keys j < (causal ? t+1 : len[b]).
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -564,16 +565,27 @@ __global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(Args a) {
 // per key warp -- with D = rowsum(dO * O) and the saved softmax stats kept in
 // shared memory. Same arithmetic, in the same order, as bwd_dq_k + bwd_dkv_k.
 // R = rows per CTA: 128 (8 warps) for widths <= 128, 64 (4 warps) for widths
-// <= 64, 32 (2 warps) for widths <= 32
-template <typename T, int DH, int R>
-__global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (R == 128 ? (DH <= 64 ? 2 : 1) : (DH <= 64 ? 3 : 1)))
-    bwd_small_k(Args a) {
+// <= 64, 32 (2 warps) for widths <= 32. N16: 16-query dK/dV chunks and 32-key
+// dQ chunks, so the staged query rows need no padding past R and fewer
+// registers buy more resident CTAs per SM (the wave count of a C4 batch is
+// what bounds these launches); otherwise 32-query chunks.
+template <int R, int DH, bool N16>
+struct SmallCfg {
+  static constexpr int NC = N16 || R == 128 ? 16 : 32;  // query columns per dK/dV chunk
+  static constexpr int KC = !N16 && R == 64 ? 64 : 32;  // keys per dQ chunk
+  static constexpr int QP = NC == 16 ? R : R + 32;      // staged query rows (chunks run NC-16 past qw)
+  static constexpr int MINB = R == 32 ? (N16 ? 8 : 6) : R == 64 ? (DH <= 64 ? (N16 ? 4 : 3) : 1)
+                                                                 : (DH <= 64 ? 2 : 1);
+};
+template <typename T, int DH, int R, bool N16>
+__global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
-  constexpr int QP = R + 32;  // staged query rows (zero-padded: dK/dV chunks run up to 31 past qw)
-  constexpr int NC = R == 128 ? 16 : 32;  // query columns per dK/dV chunk (register budget: 2-3 CTAs per SM)
+  using SC = SmallCfg<R, DH, N16>;
+  constexpr int QP = SC::QP;
+  constexpr int NC = SC::NC;
   const int b = blockIdx.z, h = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];
@@ -651,7 +663,7 @@ __global__ void __launch_bounds__(R * 2, R == 32 ? 6 : (R == 128 ? (DH <= 64 ? 2
     for (int i = 0; i < DH / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
     // keys in chunks of up to 64 (dQ accumulates across chunks; the saved
     // stats make each chunk's probabilities final)
-    constexpr int KC = R == 64 ? 64 : 32;  // 32 at R 128: 2 CTAs/SM without spills
+    constexpr int KC = SC::KC;
     constexpr int NT = KC / 8;
     const int wkeys = a.causal ? min(nk, r0 + 16) : nk;
     for (int kc = 0; kc < wkeys; kc += KC) {
@@ -869,9 +881,11 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     cudaFuncSetAttribute(fwd_k<T, DH, 32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dq_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bwd_small_k<T, DH, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(fwd_k<T, DH, 128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
@@ -907,24 +921,29 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     }
     return check_launch("sfk_attention_fwd(mma)");
   }
-  if (short32) {
-    constexpr int R = 32, QP = R + 32;
+  // SQF_ATTN_N16=0: 32-query dK/dV chunks (fewer resident CTAs) for R 32 / 64
+  static const bool n16 = [] {
+    const char* e = std::getenv("SQF_ATTN_N16");
+    return !(e && std::atoi(e) == 0);
+  }();
+  auto small = [&](auto r_tag, auto n16_tag, const char* what) {
+    constexpr int R = decltype(r_tag)::value;
+    constexpr bool N = decltype(n16_tag)::value;
+    constexpr int QP = SmallCfg<R, DH, N>::QP;
     const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
-    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
-    return check_launch("sfk_attention_bwd(small32)");
-  }
-  if (a.qw <= kRows && a.kw <= kRows) {
-    constexpr int R = 64, QP = R + 32;
-    const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
-    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
-    return check_launch("sfk_attention_bwd(small)");
-  }
-  if (a.qw <= 2 * kRows && kw128()) {
-    constexpr int R = 128, QP = R + 32;
-    const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
-    launch_pdl(bwd_small_k<T, DH, R>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
-    return check_launch("sfk_attention_bwd(small128)");
-  }
+    launch_pdl(bwd_small_k<T, DH, R, N>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
+    return check_launch(what);
+  };
+  using I32 = std::integral_constant<int, 32>;
+  using I64 = std::integral_constant<int, 64>;
+  using I128 = std::integral_constant<int, 128>;
+  using On = std::true_type;
+  using Off = std::false_type;
+  if (short32)
+    return n16 ? small(I32{}, On{}, "sfk_attention_bwd(small32)") : small(I32{}, Off{}, "sfk_attention_bwd(small32)");
+  if (a.qw <= kRows && a.kw <= kRows)
+    return n16 ? small(I64{}, On{}, "sfk_attention_bwd(small)") : small(I64{}, Off{}, "sfk_attention_bwd(small)");
+  if (a.qw <= 2 * kRows && kw128()) return small(I128{}, On{}, "sfk_attention_bwd(small128)");
   const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
   launch_pdl(bwd_dq_k<T, DH>, gq, kWarps * 32, smem_q, st, a);
   if (int e = check_launch("sfk_attention_bwd(dq)")) return e;
