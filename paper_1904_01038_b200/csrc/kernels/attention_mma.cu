@@ -149,17 +149,20 @@ __device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.cau
 
 // ------------------------------------------------------------------ forward
 // R = query rows per CTA (64: 4 warps; 32: 2 warps for short sentences)
-// KC = keys per chunk: 32 when every key span fits (short sentences), else 64.
+// KC = keys per chunk: 16 / 32 when every key span fits (short sentences), else 64.
+// HP > 1 (sentences of <= 16 positions): one warp per head, HP heads of one
+// sentence per CTA, staged as one HP*DH-wide tile (R = 16 rows).
 // Scores are kept in log2 units (s * sc * log2 e) so each probability is one
 // subtract and one SFU exp2; the saved max is converted back to natural units.
-template <typename T, int DH, int R, int KC>
-__global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
+template <typename T, int DH, int R, int KC, int HP = 1>
+__global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2) fwd_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int LD = DH + 8;
-  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * R;
+  constexpr int LD = HP * DH + 8;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
+  const int b = blockIdx.z, h0 = blockIdx.y * HP, h = h0 + (HP > 1 ? warp : 0), q0 = blockIdx.x * R;
+  const int co = HP > 1 ? warp * DH : 0;  // this warp's head columns in the staged tiles
   const int len = a.causal ? a.kw : a.klen[b];
   // keys any row of this block can see
   const int nk = a.causal ? min(a.kw, min(q0 + R, a.qw)) : len;
@@ -168,17 +171,17 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   T* Ks = Qs + R * LD;
   T* Vs = Ks + nk_pad * LD;
   const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
-  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0) + q0, min(R, a.qw - q0), R,
-               a.dh);
-  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), nk, nk_pad, a.dh);
-  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), nk, nk_pad, a.dh);
+  stage<T, HP * DH>(Qs, LD, static_cast<const T*>(a.q) + h0 * a.dh, a.ldq, int(qrow0) + q0, min(R, a.qw - q0), R,
+                    HP * a.dh);
+  stage<T, HP * DH>(Ks, LD, static_cast<const T*>(a.k) + h0 * a.dh, a.ldk, int(krow0), nk, nk_pad, HP * a.dh);
+  stage<T, HP * DH>(Vs, LD, static_cast<const T*>(a.v) + h0 * a.dh, a.ldv, int(krow0), nk, nk_pad, HP * a.dh);
   stage_wait();
   __syncthreads();
-  const int r0 = warp * 16;
+  const int r0 = HP > 1 ? 0 : warp * 16;
   if (q0 + r0 >= a.qw) return;
   uint32_t qa[DH / 16][4];
 #pragma unroll
-  for (int ks = 0; ks < DH / 16; ++ks) load_a<T>(qa[ks], Qs, LD, r0, ks * 16, lane);
+  for (int ks = 0; ks < DH / 16; ++ks) load_a<T>(qa[ks], Qs + co, LD, r0, ks * 16, lane);
   const int row_a = q0 + r0 + g, row_b = row_a + 8;  // the two rows this thread holds
   const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 1;
   const int lim_b = row_b < a.qw ? (a.causal ? row_b + 1 : len) : 1;
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
 #pragma unroll
       for (int nt = 0; nt < NT; nt += 2) {
         uint32_t bb[4];
-        load_b_nk<T>(bb, Ks, LD, kc + nt * 8, ks * 16, lane);
+        load_b_nk<T>(bb, Ks + co, LD, kc + nt * 8, ks * 16, lane);
         MmaT<T>::mma(s[nt], qa[ks], bb[0], bb[1]);
         MmaT<T>::mma(s[nt + 1], qa[ks], bb[2], bb[3]);
       }
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
 #pragma unroll
       for (int nt = 0; nt < DH / 8; nt += 2) {
         uint32_t bb[4];
-        load_b_kn<T>(bb, Vs, LD, kc + kk * 16, nt * 8, lane);
+        load_b_kn<T>(bb, Vs + co, LD, kc + kk * 16, nt * 8, lane);
         MmaT<T>::mma(o[nt], pa, bb[0], bb[1]);
         MmaT<T>::mma(o[nt + 1], pa, bb[2], bb[3]);
       }
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(R * 2) fwd_k(Args a) {
   const float ia = 1.0f / l_a, ib = 1.0f / l_b;
   // the warp's Q rows are consumed (fragments are in registers): stage its
   // 16 x DH output there and write whole 16-byte row chunks
-  T* Os = Qs + r0 * LD;
+  T* Os = Qs + co + r0 * LD;
 #pragma unroll
   for (int nt = 0; nt < DH / 8; ++nt) {
     const int c = nt * 8 + 2 * tq;
@@ -569,25 +572,28 @@ __global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(Args a) {
 // dQ chunks, so the staged query rows need no padding past R and fewer
 // registers buy more resident CTAs per SM (the wave count of a C4 batch is
 // what bounds these launches); otherwise 32-query chunks.
+// R = 16 with HP > 1 (sentences of <= 16 positions): one warp per head, HP
+// heads of one sentence per CTA staged as HP*DH-wide tiles.
 template <int R, int DH, bool N16>
 struct SmallCfg {
-  static constexpr int NC = N16 || R == 128 ? 16 : 32;  // query columns per dK/dV chunk
-  static constexpr int KC = !N16 && R == 64 ? 64 : 32;  // keys per dQ chunk
+  static constexpr int NC = N16 || R >= 128 || R == 16 ? 16 : 32;  // query columns per dK/dV chunk
+  static constexpr int KC = R == 16 ? 16 : !N16 && R == 64 ? 64 : 32;  // keys per dQ chunk
   static constexpr int QP = NC == 16 ? R : R + 32;      // staged query rows (chunks run NC-16 past qw)
-  static constexpr int MINB = R == 32 ? (N16 ? 8 : 6) : R == 64 ? (DH <= 64 ? (N16 ? 4 : 3) : 1)
-                                                                 : (DH <= 64 ? 2 : 1);
+  static constexpr int MINB = R == 16 ? 4 : R == 32 ? (N16 ? 8 : 6) : R == 64 ? (DH <= 64 ? (N16 ? 4 : 3) : 1)
+                                                                               : (DH <= 64 ? 2 : 1);
 };
-template <typename T, int DH, int R, bool N16>
-__global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small_k(Args a) {
+template <typename T, int DH, int R, bool N16, int HP = 1>
+__global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small_k(Args a) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
   extern __shared__ __align__(16) uint8_t smem[];
-  constexpr int LD = DH + 8;
+  constexpr int LD = HP * DH + 8;
   using SC = SmallCfg<R, DH, N16>;
   constexpr int QP = SC::QP;
   constexpr int NC = SC::NC;
-  const int b = blockIdx.z, h = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
+  const int b = blockIdx.z, h0 = blockIdx.y * HP, h = h0 + (HP > 1 ? warp : 0);
+  const int co = HP > 1 ? warp * DH : 0;  // this warp's head columns in the staged tiles
   const int len = a.causal ? a.kw : a.klen[b];
   const int nk = a.causal ? min(a.kw, a.qw) : len;
   T* Qs = reinterpret_cast<T*>(smem);
@@ -595,23 +601,28 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
   T* Ks = Gs + QP * LD;
   T* Vs = Ks + R * LD;
   T* Os = Vs + R * LD;  // forward output, for D = rowsum(dO * O)
-  float2* St = reinterpret_cast<float2*>(Os + R * LD);
-  float* Ds = reinterpret_cast<float*>(St + QP);
+  float2* St0 = reinterpret_cast<float2*>(Os + R * LD);  // [HP][QP]
+  float* Ds0 = reinterpret_cast<float*>(St0 + HP * QP);    // [HP][QP]
+  float2* St = St0 + (HP > 1 ? warp * QP : 0);
+  float* Ds = Ds0 + (HP > 1 ? warp * QP : 0);
   const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
-  stage<T, DH>(Qs, LD, static_cast<const T*>(a.q) + h * a.dh, a.ldq, int(qrow0), a.qw, QP, a.dh);
-  stage<T, DH>(Gs, LD, static_cast<const T*>(a.dout) + h * a.dh, a.lddo, int(qrow0), a.qw, QP, a.dh);
+  constexpr int DW = HP * DH;
+  const int dw = HP * a.dh;
+  stage<T, DW>(Qs, LD, static_cast<const T*>(a.q) + h0 * a.dh, a.ldq, int(qrow0), a.qw, QP, dw);
+  stage<T, DW>(Gs, LD, static_cast<const T*>(a.dout) + h0 * a.dh, a.lddo, int(qrow0), a.qw, QP, dw);
   // dQ reads keys < nk; dK/dV rows are all kw key rows (rows >= nk get zero grads)
-  stage<T, DH>(Ks, LD, static_cast<const T*>(a.k) + h * a.dh, a.ldk, int(krow0), a.kw, R, a.dh);
-  stage<T, DH>(Vs, LD, static_cast<const T*>(a.v) + h * a.dh, a.ldv, int(krow0), a.kw, R, a.dh);
-  stage<T, DH>(Os, LD, static_cast<const T*>(a.o) + h * a.dh, a.ldo, int(qrow0), a.qw, R, a.dh);
-  for (int i = threadIdx.x; i < QP; i += blockDim.x) {
-    const float2 sv = i < a.qw ? a.stats[(qrow0 + i) * a.heads + h] : make_float2(0.f, 0.f);
-    St[i] = make_float2(sv.x * 1.4426950408889634f, sv.y);  // max in log2 units
-    Ds[i] = 0.f;
+  stage<T, DW>(Ks, LD, static_cast<const T*>(a.k) + h0 * a.dh, a.ldk, int(krow0), a.kw, R, dw);
+  stage<T, DW>(Vs, LD, static_cast<const T*>(a.v) + h0 * a.dh, a.ldv, int(krow0), a.kw, R, dw);
+  stage<T, DW>(Os, LD, static_cast<const T*>(a.o) + h0 * a.dh, a.ldo, int(qrow0), a.qw, R, dw);
+  for (int j = threadIdx.x; j < HP * QP; j += blockDim.x) {
+    const int i = j % QP, hh = h0 + j / QP;
+    const float2 sv = i < a.qw ? a.stats[(qrow0 + i) * a.heads + hh] : make_float2(0.f, 0.f);
+    St0[j] = make_float2(sv.x * 1.4426950408889634f, sv.y);  // max in log2 units
+    Ds0[j] = 0.f;
   }
   stage_wait();
   __syncthreads();
-  const int r0 = warp * 16;
+  const int r0 = HP > 1 ? 0 : warp * 16;
   const float l2e = 1.4426950408889634f, c2 = a.sc * l2e;
   // ---- phase 1: D and dQ for query rows r0..r0+15
   if (r0 < a.qw) {
@@ -624,10 +635,10 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
 #pragma unroll
       for (int c = tq * QW; c < (tq + 1) * QW; c += 8) {
         float ga[8], oa[8], gb[8], ob[8];
-        vec_ld8<T>(Gs + row_a * LD + c, ga);
-        vec_ld8<T>(Os + row_a * LD + c, oa);
-        vec_ld8<T>(Gs + row_b * LD + c, gb);
-        vec_ld8<T>(Os + row_b * LD + c, ob);
+        vec_ld8<T>(Gs + co + row_a * LD + c, ga);
+        vec_ld8<T>(Os + co + row_a * LD + c, oa);
+        vec_ld8<T>(Gs + co + row_b * LD + c, gb);
+        vec_ld8<T>(Os + co + row_b * LD + c, ob);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           D_a += ga[j] * oa[j];
@@ -637,8 +648,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
     } else {
 #pragma unroll
       for (int c = tq; c < DH; c += 4) {
-        D_a += Num<T>::ld(Gs + row_a * LD + c) * Num<T>::ld(Os + row_a * LD + c);
-        D_b += Num<T>::ld(Gs + row_b * LD + c) * Num<T>::ld(Os + row_b * LD + c);
+        D_a += Num<T>::ld(Gs + co + row_a * LD + c) * Num<T>::ld(Os + co + row_a * LD + c);
+        D_b += Num<T>::ld(Gs + co + row_b * LD + c) * Num<T>::ld(Os + co + row_b * LD + c);
       }
     }
     D_a += __shfl_xor_sync(0xffffffffu, D_a, 1);
@@ -652,8 +663,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
     uint32_t qa[DH / 16][4], ga[DH / 16][4];
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks) {
-      load_a<T>(qa[ks], Qs, LD, r0, ks * 16, lane);
-      load_a<T>(ga[ks], Gs, LD, r0, ks * 16, lane);
+      load_a<T>(qa[ks], Qs + co, LD, r0, ks * 16, lane);
+      load_a<T>(ga[ks], Gs + co, LD, r0, ks * 16, lane);
     }
     const float2 st_a = St[row_a], st_b = St[row_b];
     const int lim_a = row_a < a.qw ? (a.causal ? row_a + 1 : len) : 0;
@@ -677,8 +688,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
 #pragma unroll
         for (int nt = 0; nt < NT; nt += 2) {
           uint32_t bk[4], bv[4];
-          load_b_nk<T>(bk, Ks, LD, kc + nt * 8, ks * 16, lane);
-          load_b_nk<T>(bv, Vs, LD, kc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bk, Ks + co, LD, kc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bv, Vs + co, LD, kc + nt * 8, ks * 16, lane);
           MmaT<T>::mma(s[nt], qa[ks], bk[0], bk[1]);
           MmaT<T>::mma(s[nt + 1], qa[ks], bk[2], bk[3]);
           MmaT<T>::mma(dp[nt], ga[ks], bv[0], bv[1]);
@@ -702,7 +713,7 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
 #pragma unroll
         for (int nt = 0; nt < DH / 8; nt += 2) {
           uint32_t bb[4];
-          load_b_kn<T>(bb, Ks, LD, kc + kk * 16, nt * 8, lane);
+          load_b_kn<T>(bb, Ks + co, LD, kc + kk * 16, nt * 8, lane);
           MmaT<T>::mma(dq[nt], da, bb[0], bb[1]);
           MmaT<T>::mma(dq[nt + 1], da, bb[2], bb[3]);
         }
@@ -736,8 +747,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
     uint32_t ka[DH / 16][4], va[DH / 16][4];
 #pragma unroll
     for (int ks = 0; ks < DH / 16; ++ks) {
-      load_a<T>(ka[ks], Ks, LD, r0, ks * 16, lane);
-      load_a<T>(va[ks], Vs, LD, r0, ks * 16, lane);
+      load_a<T>(ka[ks], Ks + co, LD, r0, ks * 16, lane);
+      load_a<T>(va[ks], Vs + co, LD, r0, ks * 16, lane);
     }
     const int qbeg = a.causal ? (r0 & ~15) : 0;
     const bool ka_ok = key_a < a.kw && (a.causal || key_a < len);
@@ -753,8 +764,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
 #pragma unroll
         for (int nt = 0; nt < NC / 8; nt += 2) {
           uint32_t bq[4], bg[4];
-          load_b_nk<T>(bq, Qs, LD, qc + nt * 8, ks * 16, lane);
-          load_b_nk<T>(bg, Gs, LD, qc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bq, Qs + co, LD, qc + nt * 8, ks * 16, lane);
+          load_b_nk<T>(bg, Gs + co, LD, qc + nt * 8, ks * 16, lane);
           MmaT<T>::mma(s[nt], ka[ks], bq[0], bq[1]);
           MmaT<T>::mma(s[nt + 1], ka[ks], bq[2], bq[3]);
           MmaT<T>::mma(dp[nt], va[ks], bg[0], bg[1]);
@@ -789,8 +800,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
 #pragma unroll
         for (int nt = 0; nt < DH / 8; nt += 2) {
           uint32_t bg[4], bq[4];
-          load_b_kn<T>(bg, Gs, LD, qc + kk * 16, nt * 8, lane);
-          load_b_kn<T>(bq, Qs, LD, qc + kk * 16, nt * 8, lane);
+          load_b_kn<T>(bg, Gs + co, LD, qc + kk * 16, nt * 8, lane);
+          load_b_kn<T>(bq, Qs + co, LD, qc + kk * 16, nt * 8, lane);
           MmaT<T>::mma(dv[nt], pa, bg[0], bg[1]);
           MmaT<T>::mma(dv[nt + 1], pa, bg[2], bg[3]);
           MmaT<T>::mma(dk[nt], da, bq[0], bq[1]);
@@ -801,8 +812,8 @@ __global__ void __launch_bounds__(R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small
   }
   // this warp's K/V rows are consumed (fragments in registers, phase 1 done
   // by every warp): stage dK and dV there, then write whole 16-byte chunks
-  T* Ks_w = Ks + r0 * LD;
-  T* Vs_w = Vs + r0 * LD;
+  T* Ks_w = Ks + co + r0 * LD;
+  T* Vs_w = Vs + co + r0 * LD;
 #pragma unroll
   for (int nt = 0; nt < DH / 8; ++nt) {
     const int c = nt * 8 + 2 * tq;
@@ -886,6 +897,11 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
     cudaFuncSetAttribute(bwd_small_k<T, DH, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_small_k<T, DH, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(bwd_small_k<T, DH, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if constexpr (DH <= 64) {
+      cudaFuncSetAttribute(bwd_small_k<T, DH, 16, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(fwd_k<T, DH, 16, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(fwd_k<T, DH, 16, 32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }
     cudaFuncSetAttribute(fwd_k<T, DH, 128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
@@ -898,11 +914,27 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   auto kw128 = [&] { return r128 && a.kw <= 2 * kRows; };
   // sentences of <= 32 positions: 32-row CTAs of 2 warps, so no warp idles
   const bool short32 = a.qw <= 32 && (bwd ? a.kw <= 32 : true);
+  // SQF_ATTN_HP=0: no multi-head CTAs for sentences of <= 16 positions
+  static const int hp_env = [] {
+    const char* e = std::getenv("SQF_ATTN_HP");
+    return e ? std::atoi(e) : 4;
+  }();
+  constexpr int HP = 4;
+  const bool hp_ok = DH <= 64 && hp_env == HP && a.dh == DH && a.heads % HP == 0 && a.qw <= 16;
   if (!bwd) {
     // every key span within 32: 32-key chunks (no work on a padded half)
     const bool k32 = a.kw <= 32;
     const size_t kp = k32 ? 32 : kpad;
-    if (short32) {
+    if (hp_ok && k32) {
+      if constexpr (DH <= 64) {
+        constexpr int LDW = HP * DH + 8;
+        const dim3 grid(1, a.heads / HP, a.batch);
+        if (a.kw <= 16)
+          launch_pdl(fwd_k<T, DH, 16, 16, HP>, grid, 32 * HP, size_t(16 + 2 * 16) * LDW * sizeof(T), st, a);
+        else
+          launch_pdl(fwd_k<T, DH, 16, 32, HP>, grid, 32 * HP, size_t(16 + 2 * 32) * LDW * sizeof(T), st, a);
+      }
+    } else if (short32) {
       const size_t smem = size_t(32 + 2 * kp) * LD * sizeof(T);
       if (k32)
         launch_pdl(fwd_k<T, DH, 32, 32>, dim3(1, a.heads, a.batch), 64, smem, st, a);
@@ -939,6 +971,14 @@ int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
   using I128 = std::integral_constant<int, 128>;
   using On = std::true_type;
   using Off = std::false_type;
+  if constexpr (DH <= 64) {
+    if (hp_ok && a.kw <= 16) {
+      constexpr int R = 16, QP = SmallCfg<R, DH, true>::QP, LDW = HP * DH + 8;
+      const size_t smem_s = size_t(2 * QP + 3 * R) * LDW * sizeof(T) + size_t(HP * QP) * 12;
+      launch_pdl(bwd_small_k<T, DH, R, true, HP>, dim3(1, a.heads / HP, a.batch), 32 * HP, smem_s, st, a);
+      return check_launch("sfk_attention_bwd(small16x4)");
+    }
+  }
   if (short32)
     return n16 ? small(I32{}, On{}, "sfk_attention_bwd(small32)") : small(I32{}, Off{}, "sfk_attention_bwd(small32)");
   if (a.qw <= kRows && a.kw <= kRows)

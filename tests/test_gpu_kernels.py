@@ -211,6 +211,9 @@ def _spans(batch, qw, kw, lens, causal):
 @pytest.mark.parametrize("batch,qw,kw,heads,dh,causal", [(3, 7, 7, 2, 8, False), (2, 9, 9, 4, 16, True),
                                                         (4, 6, 11, 8, 64, False), (2, 40, 40, 4, 128, True),
                                                         (3, 25, 31, 16, 64, False),
+                                                        # <= 16 wide, heads % 4 == 0: four heads per CTA
+                                                        (5, 16, 16, 8, 64, True), (3, 12, 16, 16, 32, False),
+                                                        (2, 16, 30, 4, 64, False),
                                                         # widths 65..128: one 8-warp CTA per (sentence, head)
                                                         (2, 100, 100, 4, 64, True), (2, 70, 90, 4, 64, False),
                                                         (2, 128, 128, 2, 128, False), (3, 120, 97, 4, 32, False),
