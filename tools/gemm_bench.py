@@ -64,14 +64,14 @@ def run(name, m, n, k, ak, bk, flags, tile_n, iters=20, pair=0):
 
 def main():
     out = {}
+    # GB_VARIANTS="p256,256": subset of {0,128,256,p128,p256} (default all)
+    variants = os.environ.get("GB_VARIANTS", "0,128,256,p128,p256").split(",")
     for sh in SHAPES:
         row = {}
-        for tn in (0, 128, 256):
-            tf, ms = run(*sh, tile_n=tn)
-            row[str(tn)] = (round(tf, 1), round(ms * 1e3, 1))
-        for tn in (128, 256):
-            tf, ms = run(*sh, tile_n=tn, pair=1)
-            row["p" + str(tn)] = (round(tf, 1), round(ms * 1e3, 1))
+        for v in variants:
+            pair = 1 if v.startswith("p") else 0
+            tf, ms = run(*sh, tile_n=int(v.lstrip("p")), pair=pair)
+            row[v] = (round(tf, 1), round(ms * 1e3, 1))
         out[sh[0]] = row
         print(sh[0], json.dumps(row), flush=True)
 
