@@ -1,10 +1,10 @@
 #include "trainer.hpp"
 
-
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
 
 namespace sqf {
 
@@ -123,6 +123,19 @@ void Trainer::init(const Registry& reg) {
   {
     const char* e = std::getenv("SQF_FWD_AHEAD");
     fwd_ahead_ = !(e && std::atoi(e) == 0);
+  }
+  {
+    // SQF_PAIR_SUBBATCH=P (default 10, 16-bit, no dropout): packed
+    // sub-batches of one update whose widths differ by at most P% run two
+    // at a time -- neighbours in width order, rows re-padded to the wider
+    // member -- so those launches cover twice the rows. Same batches, tokens
+    // and per-row arithmetic; only the order of the gradient accumulation
+    // changes (fewer rounded partial sums). fp32 keeps the reference's
+    // sub-batch-by-sub-batch order for its 1e-4 parity, and dropout masks are
+    // drawn per sub-batch, so both run unpaired. 0 = off.
+    const char* e = std::getenv("SQF_PAIR_SUBBATCH");
+    pair_sub_ = e ? std::max(0, std::atoi(e)) : 10;
+    if (dtype_ == SFK_F32 || cfg_.get_real("dropout") != 0.0) pair_sub_ = 0;
   }
   cuda_check(cudaEventCreateWithFlags(&ev_upload_, cudaEventDisableTiming), "event");
   for (auto& e : fwd_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -329,17 +342,73 @@ Trainer::Prefetch Trainer::plan_deal(int epoch, int pos, std::vector<int> order)
   return p;
 }
 
+namespace {
+// Two packed batches of one update as one: rows of `a` then rows of `b`,
+// every row right-padded to the wider widths (make_minibatch's layout,
+// data.cpp:172-219); each row's ids, lengths and corpus index are unchanged.
+MiniBatch merge_minibatches(const MiniBatch& a, const MiniBatch& b) {
+  MiniBatch m;
+  m.rows = a.rows + b.rows;
+  m.src_width = std::max(a.src_width, b.src_width);
+  m.tgt_width = std::max(a.tgt_width, b.tgt_width);
+  const size_t S = size_t(m.src_width), T = size_t(m.tgt_width);
+  m.source.assign(size_t(m.rows) * S, kPad);
+  m.target_in.assign(size_t(m.rows) * T, kPad);
+  m.target_out.assign(size_t(m.rows) * T, kPad);
+  size_t r = 0;
+  for (const MiniBatch* x : {&a, &b}) {
+    for (int i = 0; i < x->rows; ++i, ++r) {
+      const size_t s0 = size_t(i) * size_t(x->src_width), t0 = size_t(i) * size_t(x->tgt_width);
+      std::copy_n(x->source.begin() + ptrdiff_t(s0), x->src_width, m.source.begin() + ptrdiff_t(r * S));
+      std::copy_n(x->target_in.begin() + ptrdiff_t(t0), x->tgt_width, m.target_in.begin() + ptrdiff_t(r * T));
+      std::copy_n(x->target_out.begin() + ptrdiff_t(t0), x->tgt_width, m.target_out.begin() + ptrdiff_t(r * T));
+    }
+    m.src_lens.insert(m.src_lens.end(), x->src_lens.begin(), x->src_lens.end());
+    m.tgt_lens.insert(m.tgt_lens.end(), x->tgt_lens.begin(), x->tgt_lens.end());
+    m.members.insert(m.members.end(), x->members.begin(), x->members.end());
+    m.ntokens += x->ntokens;
+  }
+  return m;
+}
+}  // namespace
+
 void Trainer::pack_local(const std::vector<std::vector<MiniBatch>>& sub, std::vector<PackedBatch>& packs,
                          std::vector<std::pair<int, int>>& which) const {
   packs.clear();
   which.clear();
   for (int lw = 0; lw < local_; ++lw) {
     const int w = rank_ * local_ + lw;
-    for (int a = 0; a < accum_; ++a) {
+    std::vector<int> idx;
+    for (int a = 0; a < accum_; ++a)
+      if (sub[size_t(w)][size_t(a)].rows > 0) idx.push_back(a);
+    if (pair_sub_ <= 0 || idx.size() < 2) {
+      for (int a : idx) {
+        packs.push_back(PackedBatch::pack(sub[size_t(w)][size_t(a)]));
+        which.emplace_back(lw, a);
+      }
+      continue;
+    }
+    // neighbours in width order (least re-padding) pair when the wider one
+    // is at most pair_sub_ % wider; the rest run alone
+    auto width = [&](int a) {
       const MiniBatch& b = sub[size_t(w)][size_t(a)];
-      if (b.rows == 0) continue;
-      packs.push_back(PackedBatch::pack(b));
-      which.emplace_back(lw, a);
+      return std::max(b.src_width, b.tgt_width);
+    };
+    auto key = [&](int a) {
+      const MiniBatch& b = sub[size_t(w)][size_t(a)];
+      return std::make_tuple(width(a), b.src_width, b.tgt_width, a);
+    };
+    std::sort(idx.begin(), idx.end(), [&](int x, int y) { return key(x) < key(y); });
+    for (size_t k = 0; k < idx.size();) {
+      const MiniBatch& b0 = sub[size_t(w)][size_t(idx[k])];
+      if (k + 1 < idx.size() && int64_t(width(idx[k + 1])) * 100 <= int64_t(width(idx[k])) * (100 + pair_sub_)) {
+        packs.push_back(PackedBatch::pack(merge_minibatches(b0, sub[size_t(w)][size_t(idx[k + 1])])));
+        k += 2;
+      } else {
+        packs.push_back(PackedBatch::pack(b0));
+        k += 1;
+      }
+      which.emplace_back(lw, idx[k - 1]);
     }
   }
 }

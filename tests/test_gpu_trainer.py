@@ -271,3 +271,37 @@ def test_bf16_dropout_within_1e2_of_reference_fp32():
         a, b = mine.train_one(), theirs.train_one()
         assert a["ntokens"] == b["ntokens"]
         assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"])
+
+
+@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+def test_paired_subbatches_track_reference(prec, monkeypatch):
+    """SQF_PAIR_SUBBATCH (16-bit, no dropout): an update's sub-batches run two
+    at a time (width-sorted neighbours within the allowed widening, rows
+    re-padded).
+    Same batches and tokens as the reference's sub-batch-by-sub-batch
+    accumulation (deal dispatch, update_freq 5: two pairs and a single);
+    loss within 1e-2 of the reference every step (bf16: of its fp32 run),
+    identical skip decisions, and the paired and unpaired runs agree."""
+    import paper_1904_01038_b200 as sqf
+    V = 1000
+    c = sqf.synthetic_corpus(400, V, V, 1.1, 1)
+    ov = dict(BASE, max_tokens=512, accum=5, dispatch="deal", max_epochs=5, **{prec: True})
+    runs = {}
+    for flag in ("1", "0"):  # "1": pair neighbours up to 100% apart in width (most of them)
+        monkeypatch.setenv("SQF_PAIR_SUBBATCH", "100" if flag == "1" else "0")
+        runs[flag] = sqf.Trainer("transformer_base_defaults", ov, corpus=c, src_vocab=V, tgt_vocab=V)
+    ro = {k: v for k, v in ov.items() if k not in ("bf16", "dispatch")}
+    theirs = ref.RefTrainer("transformer_base_defaults", ro, c, V, V)
+    plan = sqf.make_batches(c, ov["max_tokens"], 0, 1)
+    order = sqf.shuffle_epoch(len(plan), 1, 1)
+    for s in range(4):
+        sub = [[plan[order[s * 5 + a]] for a in range(5)]]
+        a, u, b = runs["1"].train_one(), runs["0"].train_one(), theirs.train_step(sub)
+        assert a["ntokens"] == u["ntokens"] == b["ntokens"]
+        assert a["skipped"] == u["skipped"] == b["skipped"]
+        assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"]), (s, a, b)
+        assert abs(a["loss"] - u["loss"]) <= 1e-2 * abs(u["loss"]), (s, a, u)
+        # paired: fewer (larger) sub-batch passes, so fewer launches
+        assert runs["1"].kernel_launches < runs["0"].kernel_launches
+    p, q = runs["1"].params(), runs["0"].params()
+    assert np.linalg.norm(p - q) <= 1e-2 * np.linalg.norm(q)
