@@ -136,6 +136,8 @@ void Trainer::init(const Registry& reg) {
     const char* e = std::getenv("SQF_PAIR_SUBBATCH");
     pair_sub_ = e ? std::max(0, std::atoi(e)) : 10;
     if (dtype_ == SFK_F32 || cfg_.get_real("dropout") != 0.0) pair_sub_ = 0;
+    const char* g = std::getenv("SQF_PAIR_GROUP");  // sub-batches per pass (default 2)
+    pair_group_ = g ? std::max(1, std::atoi(g)) : 2;
   }
   cuda_check(cudaEventCreateWithFlags(&ev_upload_, cudaEventDisableTiming), "event");
   for (auto& e : fwd_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -343,20 +345,22 @@ Trainer::Prefetch Trainer::plan_deal(int epoch, int pos, std::vector<int> order)
 }
 
 namespace {
-// Two packed batches of one update as one: rows of `a` then rows of `b`,
-// every row right-padded to the wider widths (make_minibatch's layout,
+// Packed batches of one update as one: their rows in order, every row
+// right-padded to the widest member (make_minibatch's layout,
 // data.cpp:172-219); each row's ids, lengths and corpus index are unchanged.
-MiniBatch merge_minibatches(const MiniBatch& a, const MiniBatch& b) {
+MiniBatch merge_minibatches(const std::vector<const MiniBatch*>& parts) {
   MiniBatch m;
-  m.rows = a.rows + b.rows;
-  m.src_width = std::max(a.src_width, b.src_width);
-  m.tgt_width = std::max(a.tgt_width, b.tgt_width);
+  for (const MiniBatch* x : parts) {
+    m.rows += x->rows;
+    m.src_width = std::max(m.src_width, x->src_width);
+    m.tgt_width = std::max(m.tgt_width, x->tgt_width);
+  }
   const size_t S = size_t(m.src_width), T = size_t(m.tgt_width);
   m.source.assign(size_t(m.rows) * S, kPad);
   m.target_in.assign(size_t(m.rows) * T, kPad);
   m.target_out.assign(size_t(m.rows) * T, kPad);
   size_t r = 0;
-  for (const MiniBatch* x : {&a, &b}) {
+  for (const MiniBatch* x : parts) {
     for (int i = 0; i < x->rows; ++i, ++r) {
       const size_t s0 = size_t(i) * size_t(x->src_width), t0 = size_t(i) * size_t(x->tgt_width);
       std::copy_n(x->source.begin() + ptrdiff_t(s0), x->src_width, m.source.begin() + ptrdiff_t(r * S));
@@ -400,15 +404,15 @@ void Trainer::pack_local(const std::vector<std::vector<MiniBatch>>& sub, std::ve
     };
     std::sort(idx.begin(), idx.end(), [&](int x, int y) { return key(x) < key(y); });
     for (size_t k = 0; k < idx.size();) {
-      const MiniBatch& b0 = sub[size_t(w)][size_t(idx[k])];
-      if (k + 1 < idx.size() && int64_t(width(idx[k + 1])) * 100 <= int64_t(width(idx[k])) * (100 + pair_sub_)) {
-        packs.push_back(PackedBatch::pack(merge_minibatches(b0, sub[size_t(w)][size_t(idx[k + 1])])));
-        k += 2;
-      } else {
-        packs.push_back(PackedBatch::pack(b0));
-        k += 1;
-      }
-      which.emplace_back(lw, idx[k - 1]);
+      std::vector<const MiniBatch*> group{&sub[size_t(w)][size_t(idx[k])]};
+      size_t j = k + 1;
+      for (; j < idx.size() && int(group.size()) < pair_group_ &&
+             int64_t(width(idx[j])) * 100 <= int64_t(width(idx[k])) * (100 + pair_sub_);
+           ++j)
+        group.push_back(&sub[size_t(w)][size_t(idx[j])]);
+      packs.push_back(PackedBatch::pack(group.size() == 1 ? *group[0] : merge_minibatches(group)));
+      which.emplace_back(lw, idx[k]);
+      k = j;
     }
   }
 }
