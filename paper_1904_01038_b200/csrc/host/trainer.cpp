@@ -115,11 +115,22 @@ void Trainer::init(const Registry& reg) {
   const char* prio_env = std::getenv("SQF_STREAM_PRIO");
   const int prio = prio_env ? std::atoi(prio_env) : 2;
   const int mid = std::max(hi, lo - 1);
-  const int p_main = prio == 1 ? mid : prio == 2 ? lo : lo, p_side = prio == 2 ? mid : lo, p_comm = hi;
+  int p_main = prio == 1 ? mid : prio == 2 ? lo : lo, p_side = prio == 2 ? mid : lo;
+  const int p_comm = hi;
+  // SQF_FWD_PRIO: the forward-ahead stream's priority -- 0 (default) lowest,
+  // like the main stream; 1 the side stream's; 2 below the main stream, which
+  // then sits between it and the side stream
+  const char* fp_env = std::getenv("SQF_FWD_PRIO");
+  const int fwd_prio = fp_env ? std::atoi(fp_env) : 0;
+  int p_fwd = fwd_prio == 1 ? mid : lo;
+  if (fwd_prio == 2 && prio == 2) {
+    p_main = std::max(hi, lo - 1);
+    p_side = std::max(hi, lo - 2);
+  }
   cuda_check(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, p_main), "stream");
   cuda_check(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, p_side), "side stream");
   cuda_check(cudaStreamCreateWithPriority(&comm_stream_, cudaStreamNonBlocking, p_comm), "comm stream");
-  cuda_check(cudaStreamCreateWithPriority(&fwd_stream_, cudaStreamNonBlocking, lo), "forward stream");
+  cuda_check(cudaStreamCreateWithPriority(&fwd_stream_, cudaStreamNonBlocking, p_fwd), "forward stream");
   {
     const char* e = std::getenv("SQF_FWD_AHEAD");
     fwd_ahead_ = !(e && std::atoi(e) == 0);
