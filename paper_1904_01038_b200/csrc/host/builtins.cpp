@@ -354,15 +354,43 @@ class TransformerModel : public ModelBase {
     return maybe_dropout(t, t.linear(in, w, b, relu), site, x);
   }
 
+  // a pass over several packed batches (DeviceBatch parts): the embedding
+  // and attention run per part, every row-wise op over all rows at once
+  static std::vector<DeviceTape::EmbSpan> emb_spans(const DeviceBatch& b, bool src) {
+    std::vector<DeviceTape::EmbSpan> v;
+    for (int k = 0; k < b.parts(); ++k) {
+      const DeviceBatch::Part pt = b.get_part(k);
+      const int w = src ? pt.src_width : pt.tgt_width;
+      v.push_back({src ? pt.src_pos0 : pt.tgt_pos0, pt.rows * w, w});
+    }
+    return v;
+  }
+  enum class Span { Source, Target, Cross };
+  static std::vector<DeviceTape::AttnPart> attn_parts(const DeviceBatch& b, Span sp) {
+    std::vector<DeviceTape::AttnPart> v;
+    for (int k = 0; k < b.parts(); ++k) {
+      const DeviceBatch::Part pt = b.get_part(k);
+      if (sp == Span::Source)
+        v.push_back({pt.rows, pt.src_width, pt.src_width, pt.src_pos0, pt.src_pos0, pt.src_lens});
+      else if (sp == Span::Target)
+        v.push_back({pt.rows, pt.tgt_width, pt.tgt_width, pt.tgt_pos0, pt.tgt_pos0, nullptr});
+      else
+        v.push_back({pt.rows, pt.tgt_width, pt.src_width, pt.tgt_pos0, pt.src_pos0, pt.src_lens});
+    }
+    return v;
+  }
+
   int encode(DeviceTape& t, const DeviceBatch& b, int& site) const {
-    const int B = b.rows, S = b.src_width;
-    int x = t.embedding(src_embed_, b.source, B * S, S, std::sqrt(float(d_)), pe_dev_, b.src_segs);
+    const auto spans = emb_spans(b, true);
+    const auto parts = attn_parts(b, Span::Source);
+    int x = t.embedding(src_embed_, b.source, int(b.src_positions()), spans, std::sqrt(float(d_)), pe_dev_,
+                        b.src_segs);
     x = maybe_dropout(t, x, site);
     for (const Layer& l : enc_) {
       const int z = t.layer_norm(x, l.ln1g, l.ln1b);
       const ParamRef bqkv = l.self.bqkv();
       const int qkv = t.linear(z, l.self.wqkv(), &bqkv, false);
-      const int a = t.attention(qkv, 0, qkv, d_, 2 * d_, d_, heads_, B, S, S, false, b.src_lens);
+      const int a = t.attention(qkv, 0, qkv, d_, 2 * d_, d_, heads_, parts, false);
       x = residual(t, a, l.self.wo, &l.self.bo, false, x, site);
       const int z2 = t.layer_norm(x, l.ln2g, l.ln2b);
       const int h = t.linear(z2, l.w1, &l.b1, true);
@@ -373,8 +401,10 @@ class TransformerModel : public ModelBase {
 
   // model.cpp:229-275
   int decode(DeviceTape& t, const DeviceBatch& b, int enc, int& site) const {
-    const int B = b.rows, T = b.tgt_width, S = b.src_width;
-    int x = t.embedding(tgt_embed_, b.target_in, B * T, T, std::sqrt(float(d_)), pe_dev_, b.tgt_segs);
+    const auto self_parts = attn_parts(b, Span::Target);
+    const auto cross_parts = attn_parts(b, Span::Cross);
+    int x = t.embedding(tgt_embed_, b.target_in, int(b.tgt_positions()), emb_spans(b, false), std::sqrt(float(d_)),
+                        pe_dev_, b.tgt_segs);
     x = maybe_dropout(t, x, site);
     // cross K/V of every decoder layer from the encoder output in one GEMM
     // (model.cpp:262-263 per layer; same dot products, batched)
@@ -384,12 +414,12 @@ class TransformerModel : public ModelBase {
       const int z = t.layer_norm(x, l.ln1g, l.ln1b);
       const ParamRef bqkv = l.self.bqkv();
       const int qkv = t.linear(z, l.self.wqkv(), &bqkv, false);
-      const int a = t.attention(qkv, 0, qkv, d_, 2 * d_, d_, heads_, B, T, T, true, nullptr);
+      const int a = t.attention(qkv, 0, qkv, d_, 2 * d_, d_, heads_, self_parts, true);
       x = residual(t, a, l.self.wo, &l.self.bo, false, x, site);
       const int z2 = t.layer_norm(x, l.ln2g, l.ln2b);
       const int cq = t.linear(z2, l.cross.wq, &l.cross.bq, false);
       const int kc = 2 * d_ * li++;
-      const int ca = t.attention(cq, 0, ckv_all, kc, kc + d_, d_, heads_, B, T, S, false, b.src_lens);
+      const int ca = t.attention(cq, 0, ckv_all, kc, kc + d_, d_, heads_, cross_parts, false);
       x = residual(t, ca, l.cross.wo, &l.cross.bo, false, x, site);
       const int z3 = t.layer_norm(x, l.ln3g, l.ln3b);
       const int h = t.linear(z3, l.w1, &l.b1, true);

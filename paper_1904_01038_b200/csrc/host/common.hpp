@@ -3,6 +3,7 @@
 // rng.hpp, data.hpp) so code written against the reference reads the same.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <optional>
 #include <stdexcept>
@@ -80,6 +81,10 @@ struct MiniBatch {
   int rows = 0, src_width = 0, tgt_width = 0;
   std::vector<int> source, target_in, target_out, src_lens, tgt_lens, members;
   int64_t ntokens = 0;
+  // several packed batches in one pass (trainer.cpp pack_local): (rows,
+  // src_width, tgt_width) of each, their id arrays concatenated unpadded;
+  // empty: one batch of rows x src_width / tgt_width
+  std::vector<std::array<int, 3>> parts;
 };
 
 struct EpochPlan {

@@ -199,6 +199,7 @@ PackedBatch PackedBatch::pack(const MiniBatch& b) {
   p.src_width = b.src_width;
   p.tgt_width = b.tgt_width;
   p.ntokens = b.ntokens;
+  p.parts = b.parts;
   std::vector<int32_t> su, so, sr, tu, to, tr;
   build_segments(b.source, su, so, sr);
   build_segments(b.target_in, tu, to, tr);
@@ -234,6 +235,18 @@ PackedBatch PackedBatch::pack(const MiniBatch& b) {
   return p;
 }
 
+int64_t DeviceBatch::src_positions() const {
+  int64_t n = 0;
+  for (int k = 0; k < parts(); ++k) n += int64_t(get_part(k).rows) * get_part(k).src_width;
+  return n;
+}
+
+int64_t DeviceBatch::tgt_positions() const {
+  int64_t n = 0;
+  for (int k = 0; k < parts(); ++k) n += int64_t(get_part(k).rows) * get_part(k).tgt_width;
+  return n;
+}
+
 DeviceBatch PackedBatch::bind(const int32_t* d) const {
   DeviceBatch b;
   b.rows = rows;
@@ -246,6 +259,19 @@ DeviceBatch PackedBatch::bind(const int32_t* d) const {
   b.src_lens = d + off_slens;
   b.src_segs = {d + off_su, d + off_so, d + off_sr, n_su, d + off_sc, d + off_sm, n_sc, n_sm, n_ss};
   b.tgt_segs = {d + off_tu, d + off_to, d + off_tr, n_tu, d + off_tc, d + off_tm, n_tc, n_tm, n_ts};
+  if (parts.size() > 1) {
+    if (parts.size() > size_t(DeviceBatch::kMaxParts)) throw ShapeError("packed batch: too many parts");
+    b.nparts = int(parts.size());
+    int row = 0;
+    int64_t sp = 0, tp = 0;
+    for (size_t k = 0; k < parts.size(); ++k) {
+      const auto& [r, sw, tw] = parts[k];
+      b.part[k] = DeviceBatch::Part{r, sw, tw, sp, tp, b.src_lens + row};
+      row += r;
+      sp += int64_t(r) * sw;
+      tp += int64_t(r) * tw;
+    }
+  }
   return b;
 }
 
@@ -255,20 +281,36 @@ DeviceTape::DeviceTape(Arena& arena, const DeviceParams& params, int dtype, cuda
 
 int DeviceTape::embedding(ParamRef table, const int32_t* ids, int rows, int width, float scale, const float* pe,
                           const DeviceBatch::Segs& segs) {
+  return embedding(table, ids, rows, {EmbSpan{0, rows, width}}, scale, pe, segs);
+}
+
+int DeviceTape::embedding(ParamRef table, const int32_t* ids, int rows, const std::vector<EmbSpan>& spans, float scale,
+                          const float* pe, const DeviceBatch::Segs& segs) {
+  int64_t covered = 0;
+  for (const EmbSpan& sp : spans) {
+    if (sp.row0 != covered || sp.width <= 0 || sp.rows % sp.width) throw ShapeError("embedding: span layout mismatch");
+    covered += sp.rows;
+  }
+  if (covered != rows) throw ShapeError("embedding: span layout mismatch");
   Node n;
   n.kind = Kind::Embedding;
   n.p0 = table;
   n.ids = ids;
   n.rows = rows;
   n.cols = table.cols;
-  n.width = width;
+  n.width = spans.size() == 1 ? spans[0].width : 0;
+  n.espans = spans;
   n.scale = scale;
   n.segs = segs;
   n.out = alloc_elems(int64_t(rows) * n.cols);
-  pbegin();
-  sfk_check(sfk_embed_fwd(dtype_, ids, rows, width, n.cols, pptr(table), pe, scale, n.out, cur_), "embed_fwd");
-  pend(Profiler::Embed, 0, double(rows) * n.cols * (2.0 * esize_ + 4));
-  ++launches_;
+  for (const EmbSpan& sp : spans) {
+    pbegin();
+    sfk_check(sfk_embed_fwd(dtype_, ids + sp.row0, sp.rows, sp.width, n.cols, pptr(table), pe, scale,
+                            static_cast<char*>(n.out) + sp.row0 * n.cols * int64_t(esize_), cur_),
+              "embed_fwd");
+    pend(Profiler::Embed, 0, double(sp.rows) * n.cols * (2.0 * esize_ + 4));
+    ++launches_;
+  }
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
 }
@@ -441,10 +483,23 @@ int DeviceTape::external(const void* data, int rows, int cols) {
 
 int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
                           int k_width, bool causal, const int32_t* k_len) {
+  if (nodes_[q].rows != batch * q_width || nodes_[kv].rows != batch * k_width)
+    throw ShapeError("attention: span layout mismatch");
+  return attention(q, q_col, kv, k_col, v_col, d, heads, {AttnPart{batch, q_width, k_width, 0, 0, k_len}}, causal);
+}
+
+int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads,
+                          const std::vector<AttnPart>& parts, bool causal) {
   if (heads <= 0 || d % heads != 0) throw ShapeError("attention: d_model not divisible by heads");
   const Node& qn = nodes_[q];
   const Node& kn = nodes_[kv];
-  if (qn.rows != batch * q_width || kn.rows != batch * k_width) throw ShapeError("attention: span layout mismatch");
+  int64_t qrows = 0;
+  for (const AttnPart& pt : parts) {
+    if (pt.q_row0 != qrows || pt.k_row0 + int64_t(pt.batch) * pt.k_width > kn.rows)
+      throw ShapeError("attention: span layout mismatch");
+    qrows += int64_t(pt.batch) * pt.q_width;
+  }
+  if (parts.empty() || qrows != qn.rows) throw ShapeError("attention: span layout mismatch");
   Node n;
   n.kind = Kind::Attention;
   n.in0 = q;
@@ -453,38 +508,37 @@ int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d,
   n.k_col = k_col;
   n.v_col = v_col;
   n.heads = heads;
-  n.batch = batch;
-  n.q_width = q_width;
-  n.k_width = k_width;
+  n.aparts = parts;
   n.causal = causal;
-  n.k_len = k_len;
   n.rows = qn.rows;
   n.cols = d;
   n.out = alloc_elems(int64_t(n.rows) * d);
   n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * heads * 8));
-  sfk_attn_args a{};
-  a.dtype = dtype_;
-  a.batch = batch;
-  a.q_width = q_width;
-  a.k_width = k_width;
-  a.heads = heads;
-  a.dh = d / heads;
-  a.causal = causal;
-  a.k_len = k_len;
-  a.q = static_cast<const char*>(qn.out) + q_col * esize_;
-  a.ldq = qn.cols;
-  a.k = static_cast<const char*>(kn.out) + k_col * esize_;
-  a.ldk = kn.cols;
-  a.v = static_cast<const char*>(kn.out) + v_col * esize_;
-  a.ldv = kn.cols;
-  a.o = n.out;
-  a.ldo = d;
-  a.stats = n.stats;
-  pbegin();
-  if (!(ablate_mask() & 8)) sfk_check(sfk_attention_fwd(&a, cur_), "attention_fwd");
-  pend(Profiler::AttnFwd, attn_flops(batch, q_width, k_width, k_len, d, causal, false),
-       double(esize_) * d * (2.0 * n.rows + 2.0 * kn.rows));
-  ++launches_;
+  for (const AttnPart& pt : parts) {
+    sfk_attn_args a{};
+    a.dtype = dtype_;
+    a.batch = pt.batch;
+    a.q_width = pt.q_width;
+    a.k_width = pt.k_width;
+    a.heads = heads;
+    a.dh = d / heads;
+    a.causal = causal;
+    a.k_len = pt.k_len;
+    a.q = static_cast<const char*>(qn.out) + (pt.q_row0 * qn.cols + q_col) * int64_t(esize_);
+    a.ldq = qn.cols;
+    a.k = static_cast<const char*>(kn.out) + (pt.k_row0 * kn.cols + k_col) * int64_t(esize_);
+    a.ldk = kn.cols;
+    a.v = static_cast<const char*>(kn.out) + (pt.k_row0 * kn.cols + v_col) * int64_t(esize_);
+    a.ldv = kn.cols;
+    a.o = static_cast<char*>(n.out) + pt.q_row0 * d * int64_t(esize_);
+    a.ldo = d;
+    a.stats = n.stats + pt.q_row0 * heads * 2;
+    pbegin();
+    if (!(ablate_mask() & 8)) sfk_check(sfk_attention_fwd(&a, cur_), "attention_fwd");
+    pend(Profiler::AttnFwd, attn_flops(pt.batch, pt.q_width, pt.k_width, pt.k_len, d, causal, false),
+         double(esize_) * d * (2.0 * pt.batch * pt.q_width + 2.0 * pt.batch * pt.k_width));
+    ++launches_;
+  }
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
 }
@@ -884,38 +938,42 @@ void DeviceTape::backward_node(int id) {
       // layers): each backward writes only its own slice
       if (!fq) throw ShapeError("attention: the query input must not have other consumers");
       (void)fkv;
-      sfk_attn_args a{};
-      a.dtype = dtype_;
-      a.batch = n.batch;
-      a.q_width = n.q_width;
-      a.k_width = n.k_width;
-      a.heads = n.heads;
-      a.dh = n.cols / n.heads;
-      a.causal = n.causal;
-      a.k_len = n.k_len;
-      a.q = static_cast<const char*>(qn.out) + n.q_col * esize_;
-      a.ldq = qn.cols;
-      a.k = static_cast<const char*>(kn.out) + n.k_col * esize_;
-      a.ldk = kn.cols;
-      a.v = static_cast<const char*>(kn.out) + n.v_col * esize_;
-      a.ldv = kn.cols;
-      a.o = n.out;
-      a.ldo = n.cols;
-      a.stats = n.stats;
-      a.dout = n.grad;
-      a.lddo = n.cols;
-      a.dq = static_cast<char*>(dq) + n.q_col * esize_;
-      a.lddq = qn.cols;
-      a.dk = static_cast<char*>(dkv) + n.k_col * esize_;
-      a.lddk = kn.cols;
-      a.dv = static_cast<char*>(dkv) + n.v_col * esize_;
-      a.lddv = kn.cols;
-      a.scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
-      pbegin();
-      if (!(ablate_mask() & 16)) sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
-      pend(Profiler::AttnBwd, attn_flops(n.batch, n.q_width, n.k_width, n.k_len, n.cols, n.causal, true),
-           double(esize_) * n.cols * (4.0 * n.rows + 4.0 * kn.rows));
-      launches_ += 2;
+      float* scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
+      for (const AttnPart& pt : n.aparts) {
+        sfk_attn_args a{};
+        a.dtype = dtype_;
+        a.batch = pt.batch;
+        a.q_width = pt.q_width;
+        a.k_width = pt.k_width;
+        a.heads = n.heads;
+        a.dh = n.cols / n.heads;
+        a.causal = n.causal;
+        a.k_len = pt.k_len;
+        const int64_t qo = pt.q_row0 * qn.cols, ko = pt.k_row0 * kn.cols, oo = pt.q_row0 * n.cols;
+        a.q = static_cast<const char*>(qn.out) + (qo + n.q_col) * int64_t(esize_);
+        a.ldq = qn.cols;
+        a.k = static_cast<const char*>(kn.out) + (ko + n.k_col) * int64_t(esize_);
+        a.ldk = kn.cols;
+        a.v = static_cast<const char*>(kn.out) + (ko + n.v_col) * int64_t(esize_);
+        a.ldv = kn.cols;
+        a.o = static_cast<char*>(n.out) + oo * int64_t(esize_);
+        a.ldo = n.cols;
+        a.stats = n.stats + pt.q_row0 * n.heads * 2;
+        a.dout = static_cast<char*>(n.grad) + oo * int64_t(esize_);
+        a.lddo = n.cols;
+        a.dq = static_cast<char*>(dq) + (qo + n.q_col) * int64_t(esize_);
+        a.lddq = qn.cols;
+        a.dk = static_cast<char*>(dkv) + (ko + n.k_col) * int64_t(esize_);
+        a.lddk = kn.cols;
+        a.dv = static_cast<char*>(dkv) + (ko + n.v_col) * int64_t(esize_);
+        a.lddv = kn.cols;
+        a.scratch = scratch + pt.q_row0 * n.heads;
+        pbegin();
+        if (!(ablate_mask() & 16)) sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
+        pend(Profiler::AttnBwd, attn_flops(pt.batch, pt.q_width, pt.k_width, pt.k_len, n.cols, n.causal, true),
+             double(esize_) * n.cols * (4.0 * pt.batch * pt.q_width + 4.0 * pt.batch * pt.k_width));
+        launches_ += 2;
+      }
       return;
     }
   }

@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../../../include/sqf_kernels.h"
@@ -58,6 +59,24 @@ struct DeviceBatch {
     const int32_t* multi = nullptr;
     int nchunks = 0, nmulti = 0, nslots = 0;
   } src_segs, tgt_segs;
+  // A pass over several packed batches of one update (sub-batch pairing,
+  // trainer.cpp pack_local): part k's sentences keep their own widths; its
+  // source / target positions start at src_pos0 / tgt_pos0 of the
+  // concatenated id arrays. nparts == 0: one part, rows x src_width / tgt_width.
+  struct Part {
+    int rows = 0, src_width = 0, tgt_width = 0;
+    int64_t src_pos0 = 0, tgt_pos0 = 0;
+    const int32_t* src_lens = nullptr;
+  };
+  static constexpr int kMaxParts = 16;
+  int nparts = 0;
+  Part part[kMaxParts];
+  int parts() const { return nparts > 0 ? nparts : 1; }
+  Part get_part(int k) const {
+    return nparts > 0 ? part[k] : Part{rows, src_width, tgt_width, 0, 0, src_lens};
+  }
+  int64_t src_positions() const;
+  int64_t tgt_positions() const;
 };
 
 // Host-side packing of a MiniBatch into one int32 blob (uploaded with a single
@@ -72,6 +91,7 @@ struct PackedBatch {
   size_t off_sc = 0, off_sm = 0, off_tc = 0, off_tm = 0;
   int n_su = 0, n_tu = 0;
   int n_sc = 0, n_sm = 0, n_ss = 0, n_tc = 0, n_tm = 0, n_ts = 0;
+  std::vector<std::array<int, 3>> parts;  // (rows, src_width, tgt_width) per part; empty: one part
   static PackedBatch pack(const MiniBatch& b);
   DeviceBatch bind(const int32_t* dev_blob) const;
 };
@@ -134,6 +154,15 @@ class DeviceTape {
   // a8: out = q(q(E[ids]) * scale) + q(pe[pos]) ; rows = batch*width
   int embedding(ParamRef table, const int32_t* ids, int rows, int width, float scale, const float* pe,
                 const DeviceBatch::Segs& segs);
+  // the same over consecutive spans of positions with their own widths
+  // (a multi-part pass): span k covers rows [row0, row0 + rows), positions
+  // counted from row0
+  struct EmbSpan {
+    int64_t row0;
+    int rows, width;
+  };
+  int embedding(ParamRef table, const int32_t* ids, int rows, const std::vector<EmbSpan>& spans, float scale,
+                const float* pe, const DeviceBatch::Segs& segs);
   // a14
   int layer_norm(int x, ParamRef gamma, ParamRef beta);
   // a9 (+a11 bias, a12 relu, a13 residual add): y = [res +] [relu](x W^T [+ b])
@@ -146,6 +175,16 @@ class DeviceTape {
   // a16: q/k/v are column slices [q_col, q_col+d) of node q and [k_col..), [v_col..) of node kv
   int attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, int batch, int q_width,
                 int k_width, bool causal, const int32_t* k_len);
+  // the same over parts with their own widths (a multi-part pass): part k's
+  // queries are rows q_row0 + [0, batch*q_width) of q, its keys/values rows
+  // k_row0 + [0, batch*k_width) of kv; one launch per part into one output
+  struct AttnPart {
+    int batch, q_width, k_width;
+    int64_t q_row0, k_row0;
+    const int32_t* k_len;
+  };
+  int attention(int q, int q_col, int kv, int k_col, int v_col, int d, int heads, const std::vector<AttnPart>& parts,
+                bool causal);
   // a leaf over caller-owned device memory (rows x cols, row-major, tape
   // dtype): the incremental decoder's K/V caches; never differentiated
   int external(const void* data, int rows, int cols);
@@ -232,9 +271,10 @@ class DeviceTape {
     int width = 0;
     float scale = 1.f;
     DeviceBatch::Segs segs;
+    std::vector<EmbSpan> espans;  // multi-part pass (empty: one span of `width`)
     // attention
-    int q_col = 0, k_col = 0, v_col = 0, heads = 0, batch = 0, q_width = 0, k_width = 0;
-    const int32_t* k_len = nullptr;
+    int q_col = 0, k_col = 0, v_col = 0, heads = 0;
+    std::vector<AttnPart> aparts;
     // xent
     const int32_t* gold = nullptr;
     float eps = 0.f;

@@ -136,19 +136,29 @@ void Trainer::init(const Registry& reg) {
     fwd_ahead_ = !(e && std::atoi(e) == 0);
   }
   {
-    // SQF_PAIR_SUBBATCH=P (default 10, 16-bit, no dropout): packed
-    // sub-batches of one update whose widths differ by at most P% run two
-    // at a time -- neighbours in width order, rows re-padded to the wider
-    // member -- so those launches cover twice the rows. Same batches, tokens
-    // and per-row arithmetic; only the order of the gradient accumulation
-    // changes (fewer rounded partial sums). fp32 keeps the reference's
-    // sub-batch-by-sub-batch order for its 1e-4 parity, and dropout masks are
-    // drawn per sub-batch, so both run unpaired. 0 = off.
+    // Sub-batch grouping (16-bit, no dropout): several packed sub-batches of
+    // one update run as one pass, so every row-wise launch (GEMM, LayerNorm,
+    // xent) covers several times the rows. Same batches, tokens and per-row
+    // arithmetic; only the order of the gradient accumulation changes (fewer
+    // rounded partial sums). fp32 keeps the reference's sub-batch-by-sub-batch
+    // order for its 1e-4 parity, and dropout masks are drawn per sub-batch,
+    // so both run one sub-batch per pass. SQF_PAIR_SUBBATCH=0 turns grouping
+    // off; with SQF_PAIR_PARTS=0 it is the widening bound P (default 10%) for
+    // merging width-sorted neighbours into one re-padded batch.
     const char* e = std::getenv("SQF_PAIR_SUBBATCH");
     pair_sub_ = e ? std::max(0, std::atoi(e)) : 10;
     if (dtype_ == SFK_F32 || cfg_.get_real("dropout") != 0.0) pair_sub_ = 0;
-    const char* g = std::getenv("SQF_PAIR_GROUP");  // sub-batches per pass (default 2)
-    pair_group_ = g ? std::max(1, std::atoi(g)) : 2;
+    // SQF_PAIR_PARTS (default 1): the sub-batches of a pass stay unpadded
+    // parts (MiniBatch::parts; embedding and attention run per part, every
+    // row-wise kernel once over all rows), so any widths can share a pass
+    // and the SQF_PAIR_SUBBATCH widening bound does not apply; 0 merges
+    // width-sorted neighbours within that bound into one re-padded batch.
+    const char* pp = std::getenv("SQF_PAIR_PARTS");
+    pair_parts_ = !(pp && std::atoi(pp) == 0);
+    // SQF_PAIR_GROUP: sub-batches per pass (default 4 with parts, 2 merged;
+    // C4 measured 4 > 3 > 8 > 2 > 16 with parts)
+    const char* g = std::getenv("SQF_PAIR_GROUP");
+    pair_group_ = std::min(g ? std::max(1, std::atoi(g)) : pair_parts_ ? 4 : 2, DeviceBatch::kMaxParts);
   }
   cuda_check(cudaEventCreateWithFlags(&ev_upload_, cudaEventDisableTiming), "event");
   for (auto& e : fwd_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -385,6 +395,26 @@ MiniBatch merge_minibatches(const std::vector<const MiniBatch*>& parts) {
   }
   return m;
 }
+// The same as parts of one pass without re-padding: id arrays concatenated
+// as they are, each part keeping its own widths (MiniBatch::parts); the model
+// runs embedding and attention per part, everything row-wise over all rows.
+MiniBatch join_minibatches(const std::vector<const MiniBatch*>& parts) {
+  MiniBatch m;
+  for (const MiniBatch* x : parts) {
+    m.rows += x->rows;
+    m.src_width = std::max(m.src_width, x->src_width);
+    m.tgt_width = std::max(m.tgt_width, x->tgt_width);
+    m.source.insert(m.source.end(), x->source.begin(), x->source.end());
+    m.target_in.insert(m.target_in.end(), x->target_in.begin(), x->target_in.end());
+    m.target_out.insert(m.target_out.end(), x->target_out.begin(), x->target_out.end());
+    m.src_lens.insert(m.src_lens.end(), x->src_lens.begin(), x->src_lens.end());
+    m.tgt_lens.insert(m.tgt_lens.end(), x->tgt_lens.begin(), x->tgt_lens.end());
+    m.members.insert(m.members.end(), x->members.begin(), x->members.end());
+    m.ntokens += x->ntokens;
+    m.parts.push_back({x->rows, x->src_width, x->tgt_width});
+  }
+  return m;
+}
 }  // namespace
 
 void Trainer::pack_local(const std::vector<std::vector<MiniBatch>>& sub, std::vector<PackedBatch>& packs,
@@ -418,10 +448,12 @@ void Trainer::pack_local(const std::vector<std::vector<MiniBatch>>& sub, std::ve
       std::vector<const MiniBatch*> group{&sub[size_t(w)][size_t(idx[k])]};
       size_t j = k + 1;
       for (; j < idx.size() && int(group.size()) < pair_group_ &&
-             int64_t(width(idx[j])) * 100 <= int64_t(width(idx[k])) * (100 + pair_sub_);
+             (pair_parts_ || int64_t(width(idx[j])) * 100 <= int64_t(width(idx[k])) * (100 + pair_sub_));
            ++j)
         group.push_back(&sub[size_t(w)][size_t(idx[j])]);
-      packs.push_back(PackedBatch::pack(group.size() == 1 ? *group[0] : merge_minibatches(group)));
+      packs.push_back(PackedBatch::pack(group.size() == 1 ? *group[0]
+                                        : pair_parts_ ? join_minibatches(group)
+                                                      : merge_minibatches(group)));
       which.emplace_back(lw, idx[k]);
       k = j;
     }

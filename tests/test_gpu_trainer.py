@@ -273,8 +273,8 @@ def test_bf16_dropout_within_1e2_of_reference_fp32():
         assert abs(a["loss"] - b["loss"]) <= 1e-2 * abs(b["loss"])
 
 
-@pytest.mark.parametrize("prec", ["fp16", "bf16"])
-def test_paired_subbatches_track_reference(prec, monkeypatch):
+@pytest.mark.parametrize("prec,mode", [("fp16", "pad"), ("bf16", "pad"), ("fp16", "parts"), ("bf16", "parts")])
+def test_paired_subbatches_track_reference(prec, mode, monkeypatch):
     """SQF_PAIR_SUBBATCH (16-bit, no dropout): an update's sub-batches run two
     at a time (width-sorted neighbours within the allowed widening, rows
     re-padded).
@@ -287,7 +287,10 @@ def test_paired_subbatches_track_reference(prec, monkeypatch):
     c = sqf.synthetic_corpus(400, V, V, 1.1, 1)
     ov = dict(BASE, max_tokens=512, accum=5, dispatch="deal", max_epochs=5, **{prec: True})
     runs = {}
-    for flag in ("1", "0"):  # "1": pair neighbours up to 100% apart in width (most of them)
+    # "pad": neighbours up to 100% apart in width merged and re-padded (most of
+    # them); "parts": every neighbour pair as two unpadded parts of one pass
+    monkeypatch.setenv("SQF_PAIR_PARTS", "1" if mode == "parts" else "0")
+    for flag in ("1", "0"):
         monkeypatch.setenv("SQF_PAIR_SUBBATCH", "100" if flag == "1" else "0")
         runs[flag] = sqf.Trainer("transformer_base_defaults", ov, corpus=c, src_vocab=V, tgt_vocab=V)
     ro = {k: v for k, v in ov.items() if k not in ("bf16", "dispatch")}
