@@ -242,6 +242,14 @@ int sfk_attention_fwd(const sfk_attn_args* a, void* stream);
 /* dq/dk/dv are written (not accumulated): each is the attention node's sole
  * contribution to its input gradient. */
 int sfk_attention_bwd(const sfk_attn_args* a, void* stream);
+/* n attention problems of one pass (the parts of a multi-part batch, each
+ * with its own widths, lengths and pointers; heads, dh, causality and
+ * strides shared): the same results as n single calls, with the parts of one
+ * width class served by one launch. */
+int sfk_attention_fwd_parts(const sfk_attn_args* a, int n, void* stream);
+int sfk_attention_bwd_parts(const sfk_attn_args* a, int n, void* stream);
+/* kernels launched by the calling thread's last sfk_attention_* call */
+int sfk_attention_last_launches(void);
 
 /* ---------------------------------- fused label-smoothed xent (a18 + a19)
  * tape.cpp:259-290 + 481-502 + criterions.cpp:10-36 in one pass per row:

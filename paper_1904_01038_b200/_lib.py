@@ -93,6 +93,9 @@ sfk_layernorm_bwd_fused = _sig("sfk_layernorm_bwd_fused", C.c_int, C.c_int, vp, 
                                C.c_int, vp, vp, vp, vp, vp)
 sfk_attention_fwd = _sig("sfk_attention_fwd", C.c_int, P(AttnArgs), vp)
 sfk_attention_bwd = _sig("sfk_attention_bwd", C.c_int, P(AttnArgs), vp)
+sfk_attention_fwd_parts = _sig("sfk_attention_fwd_parts", C.c_int, P(AttnArgs), C.c_int, vp)
+sfk_attention_bwd_parts = _sig("sfk_attention_bwd_parts", C.c_int, P(AttnArgs), C.c_int, vp)
+sfk_attention_last_launches = _sig("sfk_attention_last_launches", C.c_int)
 sfk_xent_fwd_bwd = _sig("sfk_xent_fwd_bwd", C.c_int, C.c_int, vp, C.c_int, C.c_int, i64, vp, C.c_int, f32, f32,
                         vp, vp, vp)
 sfk_xent_reduce = _sig("sfk_xent_reduce", C.c_int, vp, C.c_int, vp, vp)

@@ -514,6 +514,9 @@ int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d,
   n.cols = d;
   n.out = alloc_elems(int64_t(n.rows) * d);
   n.stats = static_cast<float*>(arena_.alloc(size_t(n.rows) * heads * 8));
+  // one call for all parts: the parts of one width class share a launch
+  std::vector<sfk_attn_args> args;
+  double flops = 0, bytes = 0;
   for (const AttnPart& pt : parts) {
     sfk_attn_args a{};
     a.dtype = dtype_;
@@ -533,12 +536,15 @@ int DeviceTape::attention(int q, int q_col, int kv, int k_col, int v_col, int d,
     a.o = static_cast<char*>(n.out) + pt.q_row0 * d * int64_t(esize_);
     a.ldo = d;
     a.stats = n.stats + pt.q_row0 * heads * 2;
-    pbegin();
-    if (!(ablate_mask() & 8)) sfk_check(sfk_attention_fwd(&a, cur_), "attention_fwd");
-    pend(Profiler::AttnFwd, attn_flops(pt.batch, pt.q_width, pt.k_width, pt.k_len, d, causal, false),
-         double(esize_) * d * (2.0 * pt.batch * pt.q_width + 2.0 * pt.batch * pt.k_width));
-    ++launches_;
+    args.push_back(a);
+    flops += attn_flops(pt.batch, pt.q_width, pt.k_width, pt.k_len, d, causal, false);
+    bytes += double(esize_) * d * (2.0 * pt.batch * pt.q_width + 2.0 * pt.batch * pt.k_width);
   }
+  pbegin();
+  if (!(ablate_mask() & 8))
+    sfk_check(sfk_attention_fwd_parts(args.data(), int(args.size()), cur_), "attention_fwd");
+  pend(Profiler::AttnFwd, flops, bytes);
+  launches_ += sfk_attention_last_launches();
   nodes_.push_back(n);
   return int(nodes_.size()) - 1;
 }
@@ -939,6 +945,8 @@ void DeviceTape::backward_node(int id) {
       if (!fq) throw ShapeError("attention: the query input must not have other consumers");
       (void)fkv;
       float* scratch = static_cast<float*>(arena_.alloc(size_t(n.rows) * n.heads * 4));
+      std::vector<sfk_attn_args> args;
+      double flops = 0, bytes = 0;
       for (const AttnPart& pt : n.aparts) {
         sfk_attn_args a{};
         a.dtype = dtype_;
@@ -968,12 +976,15 @@ void DeviceTape::backward_node(int id) {
         a.dv = static_cast<char*>(dkv) + (ko + n.v_col) * int64_t(esize_);
         a.lddv = kn.cols;
         a.scratch = scratch + pt.q_row0 * n.heads;
-        pbegin();
-        if (!(ablate_mask() & 16)) sfk_check(sfk_attention_bwd(&a, cur_), "attention_bwd");
-        pend(Profiler::AttnBwd, attn_flops(pt.batch, pt.q_width, pt.k_width, pt.k_len, n.cols, n.causal, true),
-             double(esize_) * n.cols * (4.0 * pt.batch * pt.q_width + 4.0 * pt.batch * pt.k_width));
-        launches_ += 2;
+        args.push_back(a);
+        flops += attn_flops(pt.batch, pt.q_width, pt.k_width, pt.k_len, n.cols, n.causal, true);
+        bytes += double(esize_) * n.cols * (4.0 * pt.batch * pt.q_width + 4.0 * pt.batch * pt.k_width);
       }
+      pbegin();
+      if (!(ablate_mask() & 16))
+        sfk_check(sfk_attention_bwd_parts(args.data(), int(args.size()), cur_), "attention_bwd");
+      pend(Profiler::AttnBwd, flops, bytes);
+      launches_ += sfk_attention_last_launches();
       return;
     }
   }

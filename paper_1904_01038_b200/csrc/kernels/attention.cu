@@ -10,6 +10,8 @@
 // (row, head) so the backward recomputes the reference's exact probabilities
 // p = exp(s - max) * (1/sum) from the same dot products instead of storing
 // the probability matrix.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sfk {
@@ -222,7 +224,8 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_kv_k(P p, const T* __restrict
 }  // namespace sfk
 
 namespace sfk {
-int attention_mma(const sfk_attn_args* s, bool bwd, cudaStream_t st);
+int attention_mma(const sfk_attn_args* s, int n, bool bwd, cudaStream_t st);
+void set_last_launches(int n);
 }
 
 using namespace sfk;
@@ -237,10 +240,12 @@ static int check_attn(const sfk_attn_args* a) {
 }
 
 extern "C" int sfk_attention_fwd(const sfk_attn_args* a, void* stream) {
+  set_last_launches(0);
   if (int e = check_attn(a)) return e;
   if (a->batch * a->q_width == 0) return SFK_OK;
   // fp16/bf16: tensor-core flash kernel; fp32 parity mode: exact SIMT kernel below
-  if (a->dtype != SFK_F32) return attention_mma(a, false, as_stream(stream));
+  if (a->dtype != SFK_F32) return attention_mma(a, 1, false, as_stream(stream));
+  set_last_launches(1);
   attn::P p{a->batch, a->q_width, a->k_width, a->heads, a->dh, a->causal, a->k_len, 1.0f / sqrtf(float(a->dh))};
   const int64_t warps = int64_t(a->batch) * a->q_width * a->heads;
   if (warps == 0) return SFK_OK;
@@ -255,9 +260,11 @@ extern "C" int sfk_attention_fwd(const sfk_attn_args* a, void* stream) {
 }
 
 extern "C" int sfk_attention_bwd(const sfk_attn_args* a, void* stream) {
+  set_last_launches(0);
   if (int e = check_attn(a)) return e;
   if (a->batch * a->q_width == 0) return SFK_OK;
-  if (a->dtype != SFK_F32) return attention_mma(a, true, as_stream(stream));
+  if (a->dtype != SFK_F32) return attention_mma(a, 1, true, as_stream(stream));
+  set_last_launches(2);
   attn::P p{a->batch, a->q_width, a->k_width, a->heads, a->dh, a->causal, a->k_len, 1.0f / sqrtf(float(a->dh))};
   const int64_t qwarps = int64_t(a->batch) * a->q_width * a->heads;
   const int64_t kwarps = int64_t(a->batch) * a->k_width * a->heads;
@@ -275,4 +282,41 @@ extern "C" int sfk_attention_bwd(const sfk_attn_args* a, void* stream) {
         static_cast<T*>(a->dk), a->lddk, static_cast<T*>(a->dv), a->lddv);
   });
   return check_launch("sfk_attention_bwd");
+}
+
+// several attention problems of one pass (the parts of a multi-part batch):
+// the fp16/bf16 kernels serve all parts of one width class in one launch;
+// fp32 runs them one by one
+static int attn_parts(const sfk_attn_args* a, int n, bool bwd, void* stream) {
+  set_last_launches(0);
+  if (!a || n < 0) {
+    set_error("sfk_attention_parts: bad arguments");
+    return SFK_EINVAL;
+  }
+  bool all16 = true;
+  for (int i = 0; i < n; ++i) {
+    if (int e = check_attn(a + i)) return e;
+    all16 = all16 && a[i].dtype != SFK_F32;
+  }
+  // SQF_ATTN_PARTS=0: one launch per part (for A/B measurements)
+  static const bool joint = [] {
+    const char* e = std::getenv("SQF_ATTN_PARTS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (n > 0 && all16 && joint) return attention_mma(a, n, bwd, as_stream(stream));
+  int launched = 0;
+  for (int i = 0; i < n; ++i) {
+    if (int e = bwd ? sfk_attention_bwd(a + i, stream) : sfk_attention_fwd(a + i, stream)) return e;
+    launched += sfk_attention_last_launches();
+  }
+  set_last_launches(launched);
+  return SFK_OK;
+}
+
+extern "C" int sfk_attention_fwd_parts(const sfk_attn_args* a, int n, void* stream) {
+  return attn_parts(a, n, false, stream);
+}
+
+extern "C" int sfk_attention_bwd_parts(const sfk_attn_args* a, int n, void* stream) {
+  return attn_parts(a, n, true, stream);
 }

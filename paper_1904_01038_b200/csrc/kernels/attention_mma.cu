@@ -8,8 +8,10 @@
 //            dS = P (dP - D), dQ = sc dS K;  D = rowsum(dO * O) (per query block)
 //   bwd_dkv  S^T = K Q^T, dP^T = V dO^T, dV = P^T dO, dK = sc dS^T Q (per key block)
 // Spans: query row t of sentence b sees keys j < (causal ? t+1 : len[b]).
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
 
@@ -145,7 +147,49 @@ struct Args {
   int vec_dkv;  // dK/dV rows 16-byte aligned (ld % 8 == 0, aligned bases): whole-chunk stores
 };
 
-__device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.causal ? t + 1 : a.klen[b]; }
+// One launch can serve several parts (sfk_attention_*_parts: the parts of a
+// multi-part pass with the same kernel route): each part's sentences are a
+// consecutive range of blockIdx.z, with their own widths, lengths and base
+// pointers; the remaining fields (heads, dh, strides, scale) are shared.
+struct PartArgs {
+  int begin, qw, kw, vec_dkv;
+  const int32_t* klen;
+  const void *q, *k, *v, *o, *dout;
+  void *dq, *dk, *dv;
+  float2* stats;
+  float* dsum;
+};
+constexpr int kMaxLaunchParts = 16;
+struct LaunchArgs {
+  Args base;
+  int nparts;
+  PartArgs part[kMaxLaunchParts];
+};
+// this CTA's part as a single-part Args; b = the sentence within the part
+__device__ __forceinline__ Args part_view(const LaunchArgs& L, int& b) {
+  int p = 0;
+  for (int i = 1; i < L.nparts; ++i)
+    if (int(blockIdx.z) >= L.part[i].begin) p = i;
+  const PartArgs& pa = L.part[p];
+  Args a = L.base;
+  a.qw = pa.qw;
+  a.kw = pa.kw;
+  a.vec_dkv = pa.vec_dkv;
+  a.klen = pa.klen;
+  a.q = pa.q;
+  a.k = pa.k;
+  a.v = pa.v;
+  a.o = pa.o;
+  a.out = const_cast<void*>(pa.o);
+  a.dout = pa.dout;
+  a.dq = pa.dq;
+  a.dk = pa.dk;
+  a.dv = pa.dv;
+  a.stats = pa.stats;
+  a.dsum = pa.dsum;
+  b = int(blockIdx.z) - pa.begin;
+  return a;
+}
 
 // ------------------------------------------------------------------ forward
 // R = query rows per CTA (64: 4 warps; 32: 2 warps for short sentences)
@@ -155,14 +199,17 @@ __device__ __forceinline__ int nkeys(const Args& a, int b, int t) { return a.cau
 // Scores are kept in log2 units (s * sc * log2 e) so each probability is one
 // subtract and one SFU exp2; the saved max is converted back to natural units.
 template <typename T, int DH, int R, int KC, int HP = 1>
-__global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2) fwd_k(Args a) {
+__global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2) fwd_k(const __grid_constant__ LaunchArgs L) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
+  int b;
+  const Args a = part_view(L, b);
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = HP * DH + 8;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
-  const int b = blockIdx.z, h0 = blockIdx.y * HP, h = h0 + (HP > 1 ? warp : 0), q0 = blockIdx.x * R;
+  const int h0 = blockIdx.y * HP, h = h0 + (HP > 1 ? warp : 0), q0 = blockIdx.x * R;
   const int co = HP > 1 ? warp * DH : 0;  // this warp's head columns in the staged tiles
+  if (q0 >= a.qw) return;  // a grid sized for the widest part of the launch
   const int len = a.causal ? a.kw : a.klen[b];
   // keys any row of this block can see
   const int nk = a.causal ? min(a.kw, min(q0 + R, a.qw)) : len;
@@ -292,12 +339,15 @@ __global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2) fwd_k(Args a) {
 
 // ------------------------------------------------------------------ backward: dQ (+ D)
 template <typename T, int DH>
-__global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
+__global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(const __grid_constant__ LaunchArgs L) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
+  int b;
+  const Args a = part_view(L, b);
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
-  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * kRows;
+  const int h = blockIdx.y, q0 = blockIdx.x * kRows;
+  if (q0 >= a.qw) return;  // a grid sized for the widest part of the launch
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];
   const int nk = a.causal ? min(a.kw, min(q0 + kRows, a.qw)) : len;
@@ -429,13 +479,16 @@ __global__ void __launch_bounds__(kWarps * 32) bwd_dq_k(Args a) {
 
 // ------------------------------------------------------------------ backward: dK, dV
 template <typename T, int DH>
-__global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(Args a) {
+__global__ void __launch_bounds__(kWarps * 32, 3) bwd_dkv_k(const __grid_constant__ LaunchArgs L) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
+  int b;
+  const Args a = part_view(L, b);
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = DH + 8;
   constexpr int NC = DH >= 64 ? 32 : 64;  // query columns per chunk (register budget: 3 CTAs per SM at DH 64)
-  const int b = blockIdx.z, h = blockIdx.y, k0 = blockIdx.x * kRows;
+  const int h = blockIdx.y, k0 = blockIdx.x * kRows;
+  if (k0 >= a.kw) return;  // a grid sized for the widest part of the launch
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
   const int len = a.causal ? a.kw : a.klen[b];
   const int64_t qrow0 = int64_t(b) * a.qw, krow0 = int64_t(b) * a.kw;
@@ -583,16 +636,19 @@ struct SmallCfg {
                                                                                : (DH <= 64 ? 2 : 1);
 };
 template <typename T, int DH, int R, bool N16, int HP = 1>
-__global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2, (SmallCfg<R, DH, N16>::MINB)) bwd_small_k(Args a) {
+__global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2, (SmallCfg<R, DH, N16>::MINB))
+    bwd_small_k(const __grid_constant__ LaunchArgs L) {
   SFK_PDL_WAIT();
   SFK_PDL_LAUNCH();
+  int b;
+  const Args a = part_view(L, b);
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int LD = HP * DH + 8;
   using SC = SmallCfg<R, DH, N16>;
   constexpr int QP = SC::QP;
   constexpr int NC = SC::NC;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane >> 2, tq = lane & 3;
-  const int b = blockIdx.z, h0 = blockIdx.y * HP, h = h0 + (HP > 1 ? warp : 0);
+  const int h0 = blockIdx.y * HP, h = h0 + (HP > 1 ? warp : 0);
   const int co = HP > 1 ? warp * DH : 0;  // this warp's head columns in the staged tiles
   const int len = a.causal ? a.kw : a.klen[b];
   const int nk = a.causal ? min(a.kw, a.qw) : len;
@@ -849,169 +905,265 @@ __global__ void __launch_bounds__(HP > 1 ? 32 * HP : R * 2, (SmallCfg<R, DH, N16
   }
 }
 
+// kernels launched by the calling thread's last attention call
+thread_local int g_last_launches = 0;
+
+// Kernel routes by widths (one instantiation each); parts of a multi-part
+// pass that take the same route share one launch.
+enum Route {
+  F_HP16, F_HP32, F_R32K32, F_R32K64, F_R128, F_R64K32, F_R64K64,
+  B_HP16, B_S32N, B_S32, B_S64N, B_S64, B_S128, B_SPLIT
+};
+struct RoutePlan {
+  int route;
+  size_t smem, smem2;  // smem2: the dK/dV kernel of the split backward
+  int gx, gx2, gy, threads;
+};
+
 template <typename T, int DH>
-int run(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
-  Args a{};
-  a.batch = s->batch;
-  a.qw = s->q_width;
-  a.kw = s->k_width;
-  a.heads = s->heads;
-  a.dh = s->dh;
-  a.causal = s->causal;
-  a.klen = s->k_len;
-  a.sc = 1.0f / sqrtf(float(s->dh));
-  a.q = s->q;
-  a.k = s->k;
-  a.v = s->v;
-  a.o = s->o;
-  a.dout = s->dout;
-  a.ldq = s->ldq;
-  a.ldk = s->ldk;
-  a.ldv = s->ldv;
-  a.ldo = s->ldo;
-  a.lddo = s->lddo;
-  a.out = s->o;
-  a.ldout = s->ldo;
-  a.dq = s->dq;
-  a.lddq = s->lddq;
-  a.dk = s->dk;
-  a.lddk = s->lddk;
-  a.dv = s->dv;
-  a.lddv = s->lddv;
-  a.stats = reinterpret_cast<float2*>(s->stats);
-  a.dsum = s->scratch;
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  a.vec_dkv = (s->lddk % 8 == 0) && (s->lddv % 8 == 0) && (s->dh % 8 == 0) && al16(s->dk) && al16(s->dv) ? 1 : 0;
+RoutePlan plan_route(const sfk_attn_args& s, bool bwd) {
   constexpr int LD = DH + 8;
-  const int kpad = (a.kw + 63) & ~63, qpad = ((a.qw + 63) & ~63) + 64;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(fwd_k<T, DH, 64, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(fwd_k<T, DH, 32, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(fwd_k<T, DH, 64, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(fwd_k<T, DH, 32, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_dq_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_dkv_k<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(bwd_small_k<T, DH, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if constexpr (DH <= 64) {
-      cudaFuncSetAttribute(bwd_small_k<T, DH, 16, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      cudaFuncSetAttribute(fwd_k<T, DH, 16, 16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      cudaFuncSetAttribute(fwd_k<T, DH, 16, 32, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    }
-    cudaFuncSetAttribute(fwd_k<T, DH, 128, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = true;
-  }
-  const dim3 gq((a.qw + kRows - 1) / kRows, a.heads, a.batch);
+  constexpr int HP = 4;
+  const int qw = s.q_width, kw = s.k_width;
+  const int kpad = (kw + 63) & ~63, qpad = ((qw + 63) & ~63) + 64;
   // SQF_ATTN_R128=0: widths 65..128 on the split (per 64-row block) kernels
   static const bool r128 = [] {
     const char* e = std::getenv("SQF_ATTN_R128");
     return !(e && std::atoi(e) == 0);
   }();
-  auto kw128 = [&] { return r128 && a.kw <= 2 * kRows; };
+  const bool kw128 = r128 && kw <= 2 * kRows;
   // sentences of <= 32 positions: 32-row CTAs of 2 warps, so no warp idles
-  const bool short32 = a.qw <= 32 && (bwd ? a.kw <= 32 : true);
+  const bool short32 = qw <= 32 && (bwd ? kw <= 32 : true);
   // SQF_ATTN_HP=0: no multi-head CTAs for sentences of <= 16 positions
   static const int hp_env = [] {
     const char* e = std::getenv("SQF_ATTN_HP");
     return e ? std::atoi(e) : 4;
   }();
-  constexpr int HP = 4;
-  const bool hp_ok = DH <= 64 && hp_env == HP && a.dh == DH && a.heads % HP == 0 && a.qw <= 16;
+  const bool hp_ok = DH <= 64 && hp_env == HP && s.dh == DH && s.heads % HP == 0 && qw <= 16;
+  const size_t es = sizeof(T);
+  RoutePlan r{};
+  r.gx = 1;
+  r.gy = s.heads;
   if (!bwd) {
     // every key span within 32: 32-key chunks (no work on a padded half)
-    const bool k32 = a.kw <= 32;
+    const bool k32 = kw <= 32;
     const size_t kp = k32 ? 32 : kpad;
     if (hp_ok && k32) {
-      if constexpr (DH <= 64) {
-        constexpr int LDW = HP * DH + 8;
-        const dim3 grid(1, a.heads / HP, a.batch);
-        if (a.kw <= 16)
-          launch_pdl(fwd_k<T, DH, 16, 16, HP>, grid, 32 * HP, size_t(16 + 2 * 16) * LDW * sizeof(T), st, a);
-        else
-          launch_pdl(fwd_k<T, DH, 16, 32, HP>, grid, 32 * HP, size_t(16 + 2 * 32) * LDW * sizeof(T), st, a);
-      }
+      constexpr int LDW = HP * DH + 8;
+      r.route = kw <= 16 ? F_HP16 : F_HP32;
+      r.smem = size_t(16 + 2 * (kw <= 16 ? 16 : 32)) * LDW * es;
+      r.gy = s.heads / HP;
+      r.threads = 32 * HP;
     } else if (short32) {
-      const size_t smem = size_t(32 + 2 * kp) * LD * sizeof(T);
-      if (k32)
-        launch_pdl(fwd_k<T, DH, 32, 32>, dim3(1, a.heads, a.batch), 64, smem, st, a);
-      else
-        launch_pdl(fwd_k<T, DH, 32, 64>, dim3(1, a.heads, a.batch), 64, smem, st, a);
-    } else if (a.qw > kRows && a.qw <= 2 * kRows && kw128()) {
+      r.route = k32 ? F_R32K32 : F_R32K64;
+      r.smem = size_t(32 + 2 * kp) * LD * es;
+      r.threads = 64;
+    } else if (qw > kRows && qw <= 2 * kRows && kw128) {
       // one 8-warp CTA per (sentence, head): K/V staged once
-      const size_t smem = size_t(2 * kRows + 2 * kp) * LD * sizeof(T);
-      launch_pdl(fwd_k<T, DH, 128, 64>, dim3(1, a.heads, a.batch), 256, smem, st, a);
+      r.route = F_R128;
+      r.smem = size_t(2 * kRows + 2 * kp) * LD * es;
+      r.threads = 256;
     } else {
-      const size_t smem = size_t(kRows + 2 * kp) * LD * sizeof(T);
-      if (k32)
-        launch_pdl(fwd_k<T, DH, 64, 32>, gq, kWarps * 32, smem, st, a);
-      else
-        launch_pdl(fwd_k<T, DH, 64, 64>, gq, kWarps * 32, smem, st, a);
+      r.route = k32 ? F_R64K32 : F_R64K64;
+      r.smem = size_t(kRows + 2 * kp) * LD * es;
+      r.gx = (qw + kRows - 1) / kRows;
+      r.threads = kWarps * 32;
     }
-    return check_launch("sfk_attention_fwd(mma)");
+    return r;
   }
   // SQF_ATTN_N16=0: 32-query dK/dV chunks (fewer resident CTAs) for R 32 / 64
   static const bool n16 = [] {
     const char* e = std::getenv("SQF_ATTN_N16");
     return !(e && std::atoi(e) == 0);
   }();
-  auto small = [&](auto r_tag, auto n16_tag, const char* what) {
-    constexpr int R = decltype(r_tag)::value;
-    constexpr bool N = decltype(n16_tag)::value;
-    constexpr int QP = SmallCfg<R, DH, N>::QP;
-    const size_t smem_s = size_t(2 * QP + 3 * R) * LD * sizeof(T) + size_t(QP) * 12;
-    launch_pdl(bwd_small_k<T, DH, R, N>, dim3(1, a.heads, a.batch), 2 * R, smem_s, st, a);
-    return check_launch(what);
+  auto small = [&](int route, int R, int QP) {
+    r.route = route;
+    r.smem = size_t(2 * QP + 3 * R) * LD * es + size_t(QP) * 12;
+    r.threads = 2 * R;
   };
-  using I32 = std::integral_constant<int, 32>;
-  using I64 = std::integral_constant<int, 64>;
-  using I128 = std::integral_constant<int, 128>;
-  using On = std::true_type;
-  using Off = std::false_type;
-  if constexpr (DH <= 64) {
-    if (hp_ok && a.kw <= 16) {
-      constexpr int R = 16, QP = SmallCfg<R, DH, true>::QP, LDW = HP * DH + 8;
-      const size_t smem_s = size_t(2 * QP + 3 * R) * LDW * sizeof(T) + size_t(HP * QP) * 12;
-      launch_pdl(bwd_small_k<T, DH, R, true, HP>, dim3(1, a.heads / HP, a.batch), 32 * HP, smem_s, st, a);
-      return check_launch("sfk_attention_bwd(small16x4)");
-    }
+  if (DH <= 64 && hp_ok && kw <= 16) {
+    constexpr int R = 16, QP = SmallCfg<R, DH, true>::QP, LDW = HP * DH + 8;
+    r.route = B_HP16;
+    r.smem = size_t(2 * QP + 3 * R) * LDW * es + size_t(HP * QP) * 12;
+    r.gy = s.heads / HP;
+    r.threads = 32 * HP;
+  } else if (short32) {
+    if (n16) small(B_S32N, 32, SmallCfg<32, DH, true>::QP);
+    else small(B_S32, 32, SmallCfg<32, DH, false>::QP);
+  } else if (qw <= kRows && kw <= kRows) {
+    if (n16) small(B_S64N, 64, SmallCfg<64, DH, true>::QP);
+    else small(B_S64, 64, SmallCfg<64, DH, false>::QP);
+  } else if (qw <= 2 * kRows && kw128) {
+    small(B_S128, 128, SmallCfg<128, DH, true>::QP);
+  } else {
+    r.route = B_SPLIT;
+    r.smem = size_t(2 * kRows + 2 * kpad) * LD * es;
+    r.smem2 = size_t(2 * kRows + 2 * qpad) * LD * es + size_t(qpad) * 12;
+    r.gx = (qw + kRows - 1) / kRows;
+    r.gx2 = (kw + kRows - 1) / kRows;
+    r.threads = kWarps * 32;
   }
-  if (short32)
-    return n16 ? small(I32{}, On{}, "sfk_attention_bwd(small32)") : small(I32{}, Off{}, "sfk_attention_bwd(small32)");
-  if (a.qw <= kRows && a.kw <= kRows)
-    return n16 ? small(I64{}, On{}, "sfk_attention_bwd(small)") : small(I64{}, Off{}, "sfk_attention_bwd(small)");
-  if (a.qw <= 2 * kRows && kw128()) return small(I128{}, On{}, "sfk_attention_bwd(small128)");
-  const size_t smem_q = size_t(2 * kRows + 2 * kpad) * LD * sizeof(T);
-  launch_pdl(bwd_dq_k<T, DH>, gq, kWarps * 32, smem_q, st, a);
-  if (int e = check_launch("sfk_attention_bwd(dq)")) return e;
-  const dim3 gk((a.kw + kRows - 1) / kRows, a.heads, a.batch);
-  const size_t smem_k = size_t(2 * kRows + 2 * qpad) * LD * sizeof(T) + size_t(qpad) * 12;
-  launch_pdl(bwd_dkv_k<T, DH>, gk, kWarps * 32, smem_k, st, a);
-  return check_launch("sfk_attention_bwd(dkv)");
+  return r;
+}
+
+template <typename T, int DH>
+void configure() {
+  static bool configured = false;
+  if (configured) return;
+  auto big = [](auto k) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); };
+  big(fwd_k<T, DH, 64, 64>);
+  big(fwd_k<T, DH, 32, 64>);
+  big(fwd_k<T, DH, 64, 32>);
+  big(fwd_k<T, DH, 32, 32>);
+  big(fwd_k<T, DH, 128, 64>);
+  big(bwd_dq_k<T, DH>);
+  big(bwd_dkv_k<T, DH>);
+  big(bwd_small_k<T, DH, 64, false>);
+  big(bwd_small_k<T, DH, 32, false>);
+  big(bwd_small_k<T, DH, 64, true>);
+  big(bwd_small_k<T, DH, 32, true>);
+  big(bwd_small_k<T, DH, 128, true>);
+  if constexpr (DH <= 64) {
+    big(bwd_small_k<T, DH, 16, true, 4>);
+    big(fwd_k<T, DH, 16, 16, 4>);
+    big(fwd_k<T, DH, 16, 32, 4>);
+  }
+  configured = true;
+}
+
+template <typename T, int DH>
+int launch_route(const RoutePlan& r, int batch, const LaunchArgs& L, cudaStream_t st) {
+  const dim3 g(r.gx, r.gy, batch);
+  const dim3 t(r.threads);
+  switch (r.route) {
+    case F_HP16:
+    case F_HP32:
+    case B_HP16:
+      if constexpr (DH <= 64) {
+        if (r.route == F_HP16) launch_pdl(fwd_k<T, DH, 16, 16, 4>, g, t, r.smem, st, L);
+        else if (r.route == F_HP32) launch_pdl(fwd_k<T, DH, 16, 32, 4>, g, t, r.smem, st, L);
+        else launch_pdl(bwd_small_k<T, DH, 16, true, 4>, g, t, r.smem, st, L);
+      }
+      break;
+    case F_R32K32: launch_pdl(fwd_k<T, DH, 32, 32>, g, t, r.smem, st, L); break;
+    case F_R32K64: launch_pdl(fwd_k<T, DH, 32, 64>, g, t, r.smem, st, L); break;
+    case F_R128: launch_pdl(fwd_k<T, DH, 128, 64>, g, t, r.smem, st, L); break;
+    case F_R64K32: launch_pdl(fwd_k<T, DH, 64, 32>, g, t, r.smem, st, L); break;
+    case F_R64K64: launch_pdl(fwd_k<T, DH, 64, 64>, g, t, r.smem, st, L); break;
+    case B_S32N: launch_pdl(bwd_small_k<T, DH, 32, true>, g, t, r.smem, st, L); break;
+    case B_S32: launch_pdl(bwd_small_k<T, DH, 32, false>, g, t, r.smem, st, L); break;
+    case B_S64N: launch_pdl(bwd_small_k<T, DH, 64, true>, g, t, r.smem, st, L); break;
+    case B_S64: launch_pdl(bwd_small_k<T, DH, 64, false>, g, t, r.smem, st, L); break;
+    case B_S128: launch_pdl(bwd_small_k<T, DH, 128, true>, g, t, r.smem, st, L); break;
+    case B_SPLIT:
+      launch_pdl(bwd_dq_k<T, DH>, g, t, r.smem, st, L);
+      if (int e = check_launch("sfk_attention_bwd(dq)")) return e;
+      launch_pdl(bwd_dkv_k<T, DH>, dim3(r.gx2, r.gy, batch), t, r.smem2, st, L);
+      break;
+  }
+  return check_launch(r.route < B_HP16 ? "sfk_attention_fwd(mma)" : "sfk_attention_bwd(mma)");
+}
+
+// n parts (one for sfk_attention_fwd/bwd): each part's route; the parts of
+// one route (in order) share a launch whose grid covers every part's
+// sentences, sized for its widest part
+template <typename T, int DH>
+int run(const sfk_attn_args* sp, int n, bool bwd, cudaStream_t st) {
+  configure<T, DH>();
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  std::vector<char> done(size_t(n), 0);
+  for (int i = 0; i < n; ++i) {
+    if (done[size_t(i)] || sp[i].batch * sp[i].q_width == 0) continue;
+    const RoutePlan r0 = plan_route<T, DH>(sp[i], bwd);
+    LaunchArgs L{};
+    Args& a = L.base;
+    const sfk_attn_args& s = sp[i];
+    a.heads = s.heads;
+    a.dh = s.dh;
+    a.causal = s.causal;
+    a.sc = 1.0f / sqrtf(float(s.dh));
+    a.ldq = s.ldq;
+    a.ldk = s.ldk;
+    a.ldv = s.ldv;
+    a.ldo = s.ldo;
+    a.lddo = s.lddo;
+    a.ldout = s.ldo;
+    a.lddq = s.lddq;
+    a.lddk = s.lddk;
+    a.lddv = s.lddv;
+    RoutePlan r = r0;
+    int batch = 0;
+    for (int j = i; j < n && L.nparts < kMaxLaunchParts; ++j) {
+      const sfk_attn_args& x = sp[j];
+      if (done[size_t(j)] || x.batch * x.q_width == 0) continue;
+      const RoutePlan rj = plan_route<T, DH>(x, bwd);
+      if (rj.route != r0.route || x.heads != s.heads || x.dh != s.dh || x.causal != s.causal || x.ldq != s.ldq ||
+          x.ldk != s.ldk || x.ldv != s.ldv || x.ldo != s.ldo || x.lddo != s.lddo || x.lddq != s.lddq ||
+          x.lddk != s.lddk || x.lddv != s.lddv)
+        continue;
+      done[size_t(j)] = 1;
+      PartArgs& pa = L.part[L.nparts++];
+      pa.begin = batch;
+      pa.qw = x.q_width;
+      pa.kw = x.k_width;
+      pa.klen = x.k_len;
+      pa.q = x.q;
+      pa.k = x.k;
+      pa.v = x.v;
+      pa.o = x.o;
+      pa.dout = x.dout;
+      pa.dq = x.dq;
+      pa.dk = x.dk;
+      pa.dv = x.dv;
+      pa.stats = reinterpret_cast<float2*>(x.stats);
+      pa.dsum = x.scratch;
+      pa.vec_dkv = (x.lddk % 8 == 0) && (x.lddv % 8 == 0) && (x.dh % 8 == 0) && al16(x.dk) && al16(x.dv) ? 1 : 0;
+      batch += x.batch;
+      r.smem = std::max(r.smem, rj.smem);
+      r.smem2 = std::max(r.smem2, rj.smem2);
+      r.gx = std::max(r.gx, rj.gx);
+      r.gx2 = std::max(r.gx2, rj.gx2);
+    }
+    if (int e = launch_route<T, DH>(r, batch, L, st)) return e;
+    g_last_launches += r.route == B_SPLIT ? 2 : 1;
+  }
+  return SFK_OK;
 }
 
 template <typename T>
-int dispatch_dh(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
-  if (s->dh <= 16) return run<T, 16>(s, bwd, st);
-  if (s->dh <= 32) return run<T, 32>(s, bwd, st);
-  if (s->dh <= 64) return run<T, 64>(s, bwd, st);
-  return run<T, 128>(s, bwd, st);
+int dispatch_dh(const sfk_attn_args* s, int n, bool bwd, cudaStream_t st) {
+  if (s->dh <= 16) return run<T, 16>(s, n, bwd, st);
+  if (s->dh <= 32) return run<T, 32>(s, n, bwd, st);
+  if (s->dh <= 64) return run<T, 64>(s, n, bwd, st);
+  return run<T, 128>(s, n, bwd, st);
 }
 
 }  // namespace fa
 
-// entry used by attention.cu for fp16/bf16
-int attention_mma(const sfk_attn_args* s, bool bwd, cudaStream_t st) {
-  if (s->dh % 8 != 0 || s->dh > 128 || (s->ldq % 8) || (s->ldk % 8) || (s->ldv % 8) || (s->ldo % 8) ||
-      (bwd && ((s->lddo % 8) || (s->lddq % 2) || (s->lddk % 2) || (s->lddv % 2)))) {
-    set_error("sfk_attention(mma): dh must be a multiple of 8 (<= 128) and rows 16-byte aligned");
-    return SFK_EINVAL;
+// entry used by attention.cu for fp16/bf16: n parts sharing heads, dh,
+// causality and strides (one part for sfk_attention_fwd/bwd)
+int attention_mma(const sfk_attn_args* s, int n, bool bwd, cudaStream_t st) {
+  for (int i = 0; i < n; ++i) {
+    const sfk_attn_args& x = s[i];
+    if (x.dh % 8 != 0 || x.dh > 128 || (x.ldq % 8) || (x.ldk % 8) || (x.ldv % 8) || (x.ldo % 8) ||
+        (bwd && ((x.lddo % 8) || (x.lddq % 2) || (x.lddk % 2) || (x.lddv % 2)))) {
+      set_error("sfk_attention(mma): dh must be a multiple of 8 (<= 128) and rows 16-byte aligned");
+      return SFK_EINVAL;
+    }
+    if (x.dh != s->dh || x.dtype != s->dtype) {
+      set_error("sfk_attention(mma): parts must share dtype and head size");
+      return SFK_EINVAL;
+    }
   }
-  if (s->dtype == SFK_F16) return fa::dispatch_dh<__half>(s, bwd, st);
-  return fa::dispatch_dh<__nv_bfloat16>(s, bwd, st);
+  fa::g_last_launches = 0;
+  if (s->dtype == SFK_F16) return fa::dispatch_dh<__half>(s, n, bwd, st);
+  return fa::dispatch_dh<__nv_bfloat16>(s, n, bwd, st);
 }
 
 }  // namespace sfk
+
+namespace sfk {
+void set_last_launches(int n) { fa::g_last_launches = n; }
+}  // namespace sfk
+
+extern "C" int sfk_attention_last_launches(void) { return sfk::fa::g_last_launches; }

@@ -685,3 +685,52 @@ def test_gemm_pair_stream_k(dtype, tile_n, layout, flags, shape):
     assert int(ws[1].abs().sum()) == 0
     again, _ = run_gemm(m, n, k, dtype, *layout, flags=flags, seed=5, stream_k=0, ws=ws, pair=1, tile_n=tile_n)
     assert torch.equal(got, again)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("heads,dh", [(16, 64), (4, 32)])
+def test_attention_parts_match_single_calls(causal, heads, dh):
+    """sfk_attention_{fwd,bwd}_parts (the parts of a multi-part pass, one
+    launch per width class) give bitwise the results of one call per part:
+    parts of 12/16 (four heads per CTA), 30/25 (32-row CTAs), 50, 100 and 150
+    positions, all inside one fused-QKV buffer."""
+    lib = L()
+    rng = np.random.default_rng(7 + heads + int(causal))
+    d = heads * dh
+    shapes = [(6, 12), (5, 16), (4, 30), (3, 25), (2, 50), (2, 100), (1, 150)]  # (sentences, width)
+    rows = sum(b * w for b, w in shapes)
+    qkv = torch.tensor(rng.standard_normal((rows, 3 * d)) * 0.5, device="cuda").half()
+    do = torch.tensor(rng.standard_normal((rows, d)), device="cuda").half()
+    lens = [torch.tensor(rng.integers(1, w + 1, b).astype(np.int32), device="cuda") for b, w in shapes]
+
+    def run(split):
+        o = torch.zeros(rows, d, device="cuda").half()
+        dqkv = torch.zeros(rows, 3 * d, device="cuda").half()
+        st = torch.zeros(rows * heads, 2, device="cuda")
+        sc = torch.zeros(rows * heads, device="cuda")
+        args, r0 = [], 0
+        for (b, w), ln in zip(shapes, lens):
+            q = qkv.data_ptr() + r0 * 3 * d * 2
+            dq = dqkv.data_ptr() + r0 * 3 * d * 2
+            args.append(lib.AttnArgs(dtype=1, batch=b, q_width=w, k_width=w, heads=heads, dh=dh, causal=int(causal),
+                                     k_len=ptr(ln), q=q, ldq=3 * d, k=q + 2 * d, ldk=3 * d, v=q + 4 * d, ldv=3 * d,
+                                     o=o.data_ptr() + r0 * d * 2, ldo=d, stats=st.data_ptr() + r0 * heads * 8,
+                                     dout=do.data_ptr() + r0 * d * 2, lddo=d, dq=dq, lddq=3 * d, dk=dq + 2 * d,
+                                     lddk=3 * d, dv=dq + 4 * d, lddv=3 * d, scratch=sc.data_ptr() + r0 * heads * 4))
+            r0 += b * w
+        if split:
+            for a in args:
+                lib.check(lib.sfk_attention_fwd(C.byref(a), stream()), True)
+            for a in args:
+                lib.check(lib.sfk_attention_bwd(C.byref(a), stream()), True)
+        else:
+            arr = (lib.AttnArgs * len(args))(*args)
+            lib.check(lib.sfk_attention_fwd_parts(arr, len(args), stream()), True)
+            nf = lib.sfk_attention_last_launches()
+            lib.check(lib.sfk_attention_bwd_parts(arr, len(args), stream()), True)
+            assert 0 < nf < len(args)  # width classes share launches
+        torch.cuda.synchronize()
+        return o, dqkv, st
+
+    for x, y in zip(run(True), run(False)):
+        assert torch.equal(x, y)
