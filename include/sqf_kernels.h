@@ -87,6 +87,9 @@ typedef struct sfk_gemm_args {
    * (add_bias backward, tape.cpp:347-358), summed from the A tiles already in
    * shared memory by the epilogue warps -- no second pass over dY. */
   void* bias_grad;
+  /* scheduling: at most this many SMs for the persistent tile loop (0 = all);
+   * leaves SMs to kernels of concurrent streams */
+  int max_sms;
 } sfk_gemm_args;
 
 int sfk_gemm(const sfk_gemm_args* g, void* stream);

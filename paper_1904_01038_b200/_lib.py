@@ -35,7 +35,7 @@ class GemmArgs(C.Structure):
                 ("bias", vp), ("res", vp), ("ldr", i64), ("mask", vp), ("ldm", i64),
                 ("flags", C.c_int), ("force_simt", C.c_int), ("tile_n", C.c_int), ("pair", C.c_int),
                 ("workspace", vp), ("workspace_floats", i64), ("counters", vp), ("n_counters", C.c_int),
-                ("stream_k", C.c_int), ("bias_grad", vp)]
+                ("stream_k", C.c_int), ("bias_grad", vp), ("max_sms", C.c_int)]
 
 
 class AttnArgs(C.Structure):

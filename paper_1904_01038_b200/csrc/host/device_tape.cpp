@@ -391,6 +391,18 @@ void DeviceTape::gemm(int cat, int m, int n, int k, const void* a, int64_t lda, 
     g.pair = 1;
     g.tile_n = pair_bn;
   }
+  // SQF_SIDE_MAX_SMS / SQF_MAIN_MAX_SMS: cap the SMs a GEMM's persistent
+  // tile loop takes on the side stream / on the stream the tape records
+  // on (forward-ahead or main), leaving SMs to the other streams (0 = all)
+  static const int side_max = [] {
+    const char* e = std::getenv("SQF_SIDE_MAX_SMS");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int main_max = [] {
+    const char* e = std::getenv("SQF_MAIN_MAX_SMS");
+    return e ? std::atoi(e) : 0;
+  }();
+  g.max_sms = cur_ == side_ && side_ ? side_max : main_max;
   float* ws = cur_ == stream_ ? ws_main_ : cur_ == side_ ? ws_side_ : nullptr;
   static const int sk_mode = [] {
     const char* v = std::getenv("SQF_GEMM_STREAM_K");  // 0 off (default), 1 auto, 2 force

@@ -1366,7 +1366,8 @@ int launch(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s, in
     attr_set = true;
   }
   const int tiles = ((g->m + BM - 1) / BM) * ((g->n + BN - 1) / BN);
-  const int grid = sk_tiles > 0 ? sk_grid : (tiles < num_sms_cached() ? tiles : num_sms_cached());
+  const int sms = g->max_sms > 0 && g->max_sms < num_sms_cached() ? g->max_sms : num_sms_cached();
+  const int grid = sk_tiles > 0 ? sk_grid : (tiles < sms ? tiles : sms);
   Sk sk{sk_tiles > 0 ? g->workspace : nullptr, sk_tiles > 0 ? g->counters : nullptr, sk_tiles, g->bias_grad};
   launch_pdl(gemm_tc<BN, A_MN, B_MN, FL, T>, dim3(grid), dim3(kThreads), size_t(C::SMEM), s, ta, tb, tcm, e, g->m,
              g->n, g->k, vec_ok ? 1 : 0, tma_store ? 1 : 0, sk);
@@ -1428,7 +1429,8 @@ int launch2(const sfk_gemm_args* g, const Epi& e, bool vec_ok, cudaStream_t s) {
     attr_set = true;
   }
   const int tiles = ((g->m + 255) / 256) * ((g->n + BN - 1) / BN);
-  int pairs = tiles < num_sms_cached() / 2 ? tiles : num_sms_cached() / 2;
+  const int max_pairs = (g->max_sms > 0 && g->max_sms < num_sms_cached() ? g->max_sms : num_sms_cached()) / 2;
+  int pairs = tiles < max_pairs ? tiles : max_pairs > 0 ? max_pairs : 1;
   Sk sk{nullptr, nullptr, 0, g->bias_grad};
   if (tma_store && kSkVariant<BN, A_MN, FL>) {
     const int skt = pick_stream_k2(g, tiles, BN);
