@@ -7,7 +7,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --clock-control none --csv --log-file $O/step_metrics.csv python tools/step_once.py --accum 2 --warmup 1 > $O/ncu_metrics.log 2>&1
 python tools/ncu_classes.py $O/step_metrics.csv > $O/classes.txt 2>&1; cat $O/classes.txt
 for k in gemm_tc2; do
-  timeout 600 ncu --set full --clock-control none -k regex:gemm_tc2 -s 100 -c 12 -o $O/gemm_full python tools/step_once.py --accum 1 --warmup 1 > $O/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none -k regex:gemm_tc2 -s ${GEMM_SKIP:-300} -c ${GEMM_COUNT:-24} -o $O/gemm_full python tools/step_once.py --accum ${GEMM_ACCUM:-4} --warmup 1 > $O/ncu_full.log 2>&1
   ncu -i $O/gemm_full.ncu-rep --page raw --csv > $O/gemm_full.raw.csv 2>/dev/null; rm -f $O/gemm_full.ncu-rep
   python tools/ncu_summary.py $O/gemm_full.raw.csv > $O/gemm_full.txt; cat $O/gemm_full.txt
 done
