@@ -1,5 +1,7 @@
 // sfk_gemm entry point (C ABI): argument checks, the fp32 SIMT path, and the
 // per-dtype tensor-core dispatch (instantiated in gemm_f16.cu / gemm_bf16.cu).
+#include <cstdlib>
+
 #include "gemm_impl.cuh"
 
 extern "C" int sfk_gemm(const sfk_gemm_args* g, void* stream) {
@@ -9,7 +11,14 @@ extern "C" int sfk_gemm(const sfk_gemm_args* g, void* stream) {
     return SFK_EINVAL;
   }
   if (g->m == 0 || g->n == 0) return SFK_OK;
-  Epi e{g->c, g->ldc, g->bias, g->res, g->ldr, g->mask, g->ldm, g->flags};
+  // column blocks fastest when the output has few of them (<= 8 at the
+  // widest tile; SFK_GEMM_RASTER=0 / 1 forces an order)
+  static const int raster_env = [] {
+    const char* v = std::getenv("SFK_GEMM_RASTER");
+    return v ? std::atoi(v) : -1;
+  }();
+  const int raster = raster_env >= 0 ? raster_env : ((g->n + 255) / 256 <= 8 ? 1 : 0);
+  Epi e{g->c, g->ldc, g->bias, g->res, g->ldr, g->mask, g->ldm, g->flags, raster};
   if (((g->flags & SFK_EPI_BIAS) && !g->bias) || ((g->flags & SFK_EPI_RESIDUAL) && !g->res) ||
       ((g->flags & SFK_EPI_MASK) && !g->mask)) {
     set_error("sfk_gemm: epilogue input missing");

@@ -35,7 +35,23 @@ struct Epi {
   const void* mask;
   int64_t ldm;
   int flags;
+  int raster;  // tile order: 0 = row blocks fastest, 1 = column blocks fastest
 };
+
+// Output tile `tile` of a num_m x num_n grid. With few column blocks
+// (raster 1) the column tiles of one row block are consecutive, so the
+// persistent CTAs that share an A row panel run at the same time and read
+// it from DRAM once (the tall activation / gradient operands of the
+// N = 1024 GEMMs); otherwise row blocks run fastest.
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int raster, int& mi, int& ni) {
+  if (raster) {
+    mi = tile / num_n;
+    ni = tile % num_n;
+  } else {
+    mi = tile % num_m;
+    ni = tile / num_m;
+  }
+}
 
 template <typename T>
 __device__ __forceinline__ float epi_value(const Epi& e, int64_t row, int col, float acc) {
@@ -895,7 +911,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0, tile, kb0, kb1;
       uint32_t bias_pend = 0, bias_ph = 0;  // per stage: a bias-tile read outstanding / its bsum phase
       while (sc.next(tile, kb0, kb1)) {
-        const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+        int mi, ni;
+        tile_coords(tile, num_m, num_n, e.raster, mi, ni);
+        const int m0 = mi * BM, n0 = ni * BN;
         const bool btile = A_MN && sk.bias_grad && n0 == 0;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
@@ -969,7 +987,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int t = 0, it = 0, tile, kb0, kb1;
     while (sc.next(tile, kb0, kb1)) {
       const int buf = t & 1;
-      const int m0 = (tile % num_m) * BM, n0 = (tile / num_m) * BN;
+      int mi, ni;
+      tile_coords(tile, num_m, num_n, e.raster, mi, ni);
+      const int m0 = mi * BM, n0 = ni * BN;
       if (A_MN && sk.bias_grad && n0 == 0) {
         bias_grad_tile<T, C::STAGES, C::STAGE>(smem, full, bsum, it, kb1 - kb0, warp, lane, stg,
                                                static_cast<T*>(sk.bias_grad), m0, M);
@@ -1151,9 +1171,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t bias_pend = 0, bias_ph = 0;  // per stage: a bias-tile read outstanding / its bsum phase
       Sched sc(tiles, kblocks, sk_tiles, npairs, pair);
       while (sc.next(tile, kb0, kb1)) {
-        const int m0 = (tile % num_m) * PM + 128 * int(rank);
-        const int n0 = (tile / num_m) * BN + HB * int(rank);
-        const bool btile = A_MN && bias_grad && tile / num_m == 0;
+        int mi, ni;
+        tile_coords(tile, num_m, num_n, e.raster, mi, ni);
+        const int m0 = mi * PM + 128 * int(rank);
+        const int n0 = ni * BN + HB * int(rank);
+        const bool btile = A_MN && bias_grad && ni == 0;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
@@ -1223,7 +1245,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     Sched sc(tiles, kblocks, sk_tiles, npairs, pair);
     for (; sc.next(tile, kb0, kb1); ++t) {
       const int buf = t & 1;
-      const int m0 = (tile % num_m) * PM + 128 * int(rank), n0 = (tile / num_m) * BN;
+      int mi, ni;
+      tile_coords(tile, num_m, num_n, e.raster, mi, ni);
+      const int m0 = mi * PM + 128 * int(rank), n0 = ni * BN;
       // fused bias gradient: each CTA sums its own 128-row half of A; the
       // pair's MMA commit on empty[s] (multicast to both CTAs) says the stage
       // is complete and still unrecycled (never combined with stream-K)
