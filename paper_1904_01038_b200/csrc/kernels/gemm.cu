@@ -12,12 +12,16 @@ extern "C" int sfk_gemm(const sfk_gemm_args* g, void* stream) {
   }
   if (g->m == 0 || g->n == 0) return SFK_OK;
   // column blocks fastest when the output has few of them (<= 8 at the
-  // widest tile; SFK_GEMM_RASTER=0 / 1 forces an order)
+  // widest tile, SFK_GEMM_RASTER_N; SFK_GEMM_RASTER=0 / 1 forces an order)
   static const int raster_env = [] {
     const char* v = std::getenv("SFK_GEMM_RASTER");
     return v ? std::atoi(v) : -1;
   }();
-  const int raster = raster_env >= 0 ? raster_env : ((g->n + 255) / 256 <= 8 ? 1 : 0);
+  static const int raster_n = [] {
+    const char* v = std::getenv("SFK_GEMM_RASTER_N");
+    return v ? std::atoi(v) : 8;
+  }();
+  const int raster = raster_env >= 0 ? raster_env : ((g->n + 255) / 256 <= raster_n ? 1 : 0);
   Epi e{g->c, g->ldc, g->bias, g->res, g->ldr, g->mask, g->ldm, g->flags, raster};
   if (((g->flags & SFK_EPI_BIAS) && !g->bias) || ((g->flags & SFK_EPI_RESIDUAL) && !g->res) ||
       ((g->flags & SFK_EPI_MASK) && !g->mask)) {
