@@ -319,9 +319,9 @@ def run_ours(args, cfg):
                    "skipped_steps": skipped, "loss_scale": tr.scaler()[0] if cfg["prec"] == "fp16" else None,
                    "warmup_steps_run": done,
                    "sub_batch_grouping": ("off" if cfg["prec"] == "fp32" or os.environ.get("SQF_PAIR_SUBBATCH") == "0"
-                                          else "an update's 16 packed sub-batches run %s per pass as unpadded parts "
+                                          else "an update's 16 packed sub-batches run up to %s per pass as unpadded parts "
                                                "(same batches and tokens; embedding/attention per part; "
-                                               "SQF_PAIR_GROUP / SQF_PAIR_PARTS)" % os.environ.get("SQF_PAIR_GROUP", "4")),
+                                               "SQF_PAIR_GROUP / SQF_PAIR_PARTS)" % os.environ.get("SQF_PAIR_GROUP", "6")),
                    "allreduce": ("bucketed NCCL, overlapped with the last backward" if not args.no_overlap
                                  else "bucketed NCCL after backward") if world > 1 else "none (1 GPU)"},
         "e2e": {"value": e2e, "unit": "tgt_tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 36},

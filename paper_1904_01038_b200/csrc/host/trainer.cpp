@@ -155,10 +155,11 @@ void Trainer::init(const Registry& reg) {
     // width-sorted neighbours within that bound into one re-padded batch.
     const char* pp = std::getenv("SQF_PAIR_PARTS");
     pair_parts_ = !(pp && std::atoi(pp) == 0);
-    // SQF_PAIR_GROUP: sub-batches per pass (default 4 with parts, 2 merged;
-    // C4 measured 4 > 3 > 8 > 2 > 16 with parts)
+    // SQF_PAIR_GROUP: sub-batches per pass (default 6 with parts -- an
+    // update of 16 runs as 6 + 6 + 4 -- and 2 merged; C4 with the
+    // column-fastest GEMM tile order measured 6 >= 8 > 4 > 3 > 16)
     const char* g = std::getenv("SQF_PAIR_GROUP");
-    pair_group_ = std::min(g ? std::max(1, std::atoi(g)) : pair_parts_ ? 4 : 2, DeviceBatch::kMaxParts);
+    pair_group_ = std::min(g ? std::max(1, std::atoi(g)) : pair_parts_ ? 6 : 2, DeviceBatch::kMaxParts);
   }
   cuda_check(cudaEventCreateWithFlags(&ev_upload_, cudaEventDisableTiming), "event");
   for (auto& e : fwd_done_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");

@@ -261,7 +261,7 @@ class Trainer {
   cudaStream_t fwd_stream_ = nullptr;
   bool fwd_ahead_ = true;
   int pair_sub_ = 0;    // SQF_PAIR_SUBBATCH: widening (%) allowed when sub-batches share a pass (0 = off)
-  int pair_group_ = 4;       // SQF_PAIR_GROUP: at most this many sub-batches per pass
+  int pair_group_ = 6;       // SQF_PAIR_GROUP: at most this many sub-batches per pass
   bool pair_parts_ = true;   // SQF_PAIR_PARTS: passes of unpadded parts (else re-padded merges)
   cudaEvent_t ev_upload_ = nullptr, fwd_done_[2] = {nullptr, nullptr}, main_done_[2] = {nullptr, nullptr};
   float* gemm_ws_ = nullptr;          // stream-K partial tiles: [main | side]
