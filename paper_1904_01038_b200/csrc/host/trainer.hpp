@@ -263,6 +263,7 @@ class Trainer {
   int pair_sub_ = 0;    // SQF_PAIR_SUBBATCH: widening (%) allowed when sub-batches share a pass (0 = off)
   int pair_group_ = 6;       // SQF_PAIR_GROUP: at most this many sub-batches per pass
   bool pair_parts_ = true;   // SQF_PAIR_PARTS: passes of unpadded parts (else re-padded merges)
+  bool balance_groups_ = true;  // SQF_PAIR_BALANCE: near-equal-sized passes
   cudaEvent_t ev_upload_ = nullptr, fwd_done_[2] = {nullptr, nullptr}, main_done_[2] = {nullptr, nullptr};
   float* gemm_ws_ = nullptr;          // stream-K partial tiles: [main | side]
   int64_t gemm_ws_floats_ = 0;        // per stream
